@@ -1,0 +1,375 @@
+/*
+ * oracle.c -- TEST INFRASTRUCTURE ONLY.  Plain, slow, obviously-correct CPU
+ * max-flow / min-cut for Wu-Chen proper-ordered multi-column graphs.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  The product path
+ * (paper_2601_17026_b200/, libcolgraph.so) never includes, links or calls it,
+ * and this file includes nothing from the product tree.
+ *
+ * What it computes (§1.2-1.3):
+ *   - the s-t graph of a VCE-weight net-surface problem with vertex weights
+ *     only ("The weights on the nodes w(v) are correspondingly
+ *     converted to the costs associated with the edges connecting the node v
+ *     to the source or the sink"), built EXPLICITLY (CSR adjacency lists) with
+ *     the literal Wu-Chen arcs:
+ *         s -> v  capacity -w(v)   if w(v) < 0
+ *         v -> t  capacity  w(v)   if w(v) > 0
+ *         (x,y,z) -> (x,y,z-1)                 capacity INF, z >= 1
+ *         (x,y,z) -> (x',y',max(0, z-Delta))    capacity INF, every z, every
+ *                                              in-range 4-neighbour (x',y')
+ *     with w(x,y,0) = c(x,y,0) - (sum_z c(x,y,z) + 1) and
+ *          w(x,y,z) = c(x,y,z) - c(x,y,z-1), z >= 1     (reading R1)
+ *   - the maximum flow value |f| = sum_v f(v,t) (Eq. 5) by
+ *     Dinitz blocking flows over BFS level graphs (§2) or by
+ *     Edmonds-Karp shortest augmenting paths (§2);
+ *   - the minimal min-cut source set S = vertices reachable from s in the
+ *     residual graph r_f(u,v) = c(u,v) - f(u,v) > 0 (§2.1;
+ *     cut definition Eq. 6-7; Theorem 1);
+ *   - the surface S(x,y) = max { z : (x,y,z) in S }, or -1 and
+ *     status 6 (EMPTY_COLUMN) for a column with no source-side
+ *     vertex;
+ *   - self-checks: capacity (Eq. 2), antisymmetry of each arc pair (Eq. 3),
+ *     conservation at non-terminals (Eq. 4), |f| = net flow out of s,
+ *     t not in S, cut capacity c(S, V-S) = |f| with no INF arc crossing
+ *     (Theorem 1 / Eq. 6).
+ *
+ * All arithmetic is int64; INF = 2^62.  Single-threaded.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OR_INF ((int64_t)1 << 62)
+
+enum { OR_OK = 0, OR_E_INVAL = 1, OR_E_NOMEM = 3, OR_E_EMPTY_COLUMN = 6 };
+
+/* check bits returned in *checks (all set = every invariant holds) */
+enum {
+    CHK_CAPACITY = 1 << 0,     /* 0 <= f <= c on every arc (Eq. 2) */
+    CHK_ANTISYM = 1 << 1,      /* res[a] + res[rev a] == cap[a] + cap[rev a] (Eq. 3) */
+    CHK_CONSERVE = 1 << 2,     /* inflow == outflow at every non-terminal (Eq. 4) */
+    CHK_VALUE = 1 << 3,        /* flow into t == flow out of s (Eq. 5) */
+    CHK_T_NOT_IN_S = 1 << 4,   /* no augmenting path */
+    CHK_CUT_EQ_FLOW = 1 << 5,  /* c(S, V-S) == |f|, no INF arc crosses (Theorem 1) */
+};
+
+typedef struct {
+    int64_t nn;      /* nodes including s, t */
+    int64_t m;       /* half-arcs */
+    int64_t *first;  /* CSR offsets, nn + 1 */
+    int32_t *head;
+    int64_t *rev;
+    int64_t *cap;    /* original capacity */
+    int64_t *res;    /* residual capacity */
+    int64_t *fill;   /* scratch insertion cursor */
+} graph_t;
+
+static void g_free(graph_t *g) {
+    free(g->first); free(g->head); free(g->rev); free(g->cap); free(g->res); free(g->fill);
+    memset(g, 0, sizeof(*g));
+}
+
+/* ---- explicit graph construction: two passes (count, then insert) ---- */
+
+static void add_arc(graph_t *g, int pass, int64_t u, int64_t v, int64_t c) {
+    if (pass == 0) {
+        g->first[u + 1]++;
+        g->first[v + 1]++;
+        return;
+    }
+    int64_t a = g->fill[u]++;
+    int64_t b = g->fill[v]++;
+    g->head[a] = (int32_t)v; g->cap[a] = c; g->res[a] = c; g->rev[a] = b;
+    g->head[b] = (int32_t)u; g->cap[b] = 0; g->res[b] = 0; g->rev[b] = a;
+}
+
+static int g_alloc(graph_t *g, int64_t nn) {
+    memset(g, 0, sizeof(*g));
+    g->nn = nn;
+    g->first = (int64_t *)calloc((size_t)nn + 1, sizeof(int64_t));
+    return g->first ? 0 : -1;
+}
+
+static int g_finish_count(graph_t *g) {
+    for (int64_t i = 0; i < g->nn; i++) g->first[i + 1] += g->first[i];
+    g->m = g->first[g->nn];
+    size_t m = (size_t)(g->m ? g->m : 1);
+    g->head = (int32_t *)malloc(m * sizeof(int32_t));
+    g->rev = (int64_t *)malloc(m * sizeof(int64_t));
+    g->cap = (int64_t *)malloc(m * sizeof(int64_t));
+    g->res = (int64_t *)malloc(m * sizeof(int64_t));
+    g->fill = (int64_t *)malloc((size_t)g->nn * sizeof(int64_t));
+    if (!g->head || !g->rev || !g->cap || !g->res || !g->fill) return -1;
+    memcpy(g->fill, g->first, (size_t)g->nn * sizeof(int64_t));
+    return 0;
+}
+
+/* Vertex weights of the net-surface construction (reading R1). */
+static void column_weights(const int32_t *c, int64_t Z, int64_t col, int64_t *w) {
+    const int32_t *cc = c + col * Z;
+    int64_t sum = 0;
+    for (int64_t z = 0; z < Z; z++) sum += cc[z];
+    w[0] = (int64_t)cc[0] - (sum + 1);
+    for (int64_t z = 1; z < Z; z++) w[z] = (int64_t)cc[z] - (int64_t)cc[z - 1];
+}
+
+static void colgraph_arcs(graph_t *g, int pass, const int32_t *in, int X, int Y, int Z, int delta,
+                          int input_is_weight, int64_t *wbuf) {
+    const int64_t n = (int64_t)X * Y * Z, s = n, t = n + 1;
+    const int dx[4] = {+1, -1, 0, 0}, dy[4] = {0, 0, +1, -1};
+    for (int64_t x = 0; x < X; x++)
+        for (int64_t y = 0; y < Y; y++) {
+            int64_t col = x * Y + y;
+            if (input_is_weight) {
+                for (int64_t z = 0; z < Z; z++) wbuf[z] = in[col * Z + z];
+            } else {
+                column_weights(in, Z, col, wbuf);
+            }
+            for (int64_t z = 0; z < Z; z++) {
+                int64_t v = col * Z + z;
+                if (wbuf[z] < 0) add_arc(g, pass, s, v, -wbuf[z]);
+                if (wbuf[z] > 0) add_arc(g, pass, v, t, wbuf[z]);
+                if (z >= 1) add_arc(g, pass, v, v - 1, OR_INF);
+                int64_t zt = z - delta > 0 ? z - delta : 0;
+                for (int d = 0; d < 4; d++) {
+                    int64_t x2 = x + dx[d], y2 = y + dy[d];
+                    if (x2 < 0 || x2 >= X || y2 < 0 || y2 >= Y) continue;
+                    add_arc(g, pass, v, (x2 * Y + y2) * Z + zt, OR_INF);
+                }
+            }
+        }
+}
+
+/* ---- max-flow algorithms ---- */
+
+static int bfs_levels(const graph_t *g, int64_t s, int64_t t, int32_t *level, int32_t *queue) {
+    for (int64_t i = 0; i < g->nn; i++) level[i] = -1;
+    int64_t qh = 0, qt = 0;
+    level[s] = 0;
+    queue[qt++] = (int32_t)s;
+    while (qh < qt) {
+        int64_t u = queue[qh++];
+        for (int64_t a = g->first[u]; a < g->first[u + 1]; a++) {
+            int64_t v = g->head[a];
+            if (g->res[a] > 0 && level[v] < 0) {
+                level[v] = level[u] + 1;
+                queue[qt++] = (int32_t)v;
+            }
+        }
+    }
+    return level[t] >= 0;
+}
+
+/* Dinitz: blocking flow on the BFS level graph, iterative DFS with current-arc pointers. */
+static int64_t dinic(graph_t *g, int64_t s, int64_t t, int *err) {
+    int32_t *level = (int32_t *)malloc((size_t)g->nn * sizeof(int32_t));
+    int32_t *queue = (int32_t *)malloc((size_t)g->nn * sizeof(int32_t));
+    int64_t *it = (int64_t *)malloc((size_t)g->nn * sizeof(int64_t));
+    int64_t *path = (int64_t *)malloc((size_t)g->nn * sizeof(int64_t));
+    int64_t total = 0;
+    if (!level || !queue || !it || !path) { *err = OR_E_NOMEM; goto done; }
+    while (bfs_levels(g, s, t, level, queue)) {
+        memcpy(it, g->first, (size_t)g->nn * sizeof(int64_t));
+        int64_t depth = 0, v = s;
+        for (;;) {
+            if (v == t) {
+                int64_t f = OR_INF;
+                for (int64_t i = 0; i < depth; i++)
+                    if (g->res[path[i]] < f) f = g->res[path[i]];
+                for (int64_t i = 0; i < depth; i++) {
+                    g->res[path[i]] -= f;
+                    g->res[g->rev[path[i]]] += f;
+                }
+                total += f;
+                int64_t k = 0;
+                while (g->res[path[k]] > 0) k++;
+                depth = k;
+                v = g->head[g->rev[path[k]]]; /* tail of the first saturated arc */
+                continue;
+            }
+            int64_t a = it[v], end = g->first[v + 1];
+            while (a < end && !(g->res[a] > 0 && level[g->head[a]] == level[v] + 1)) a++;
+            it[v] = a;
+            if (a < end) {
+                path[depth++] = a;
+                v = g->head[a];
+            } else {
+                level[v] = -1; /* dead end in this phase */
+                if (v == s) break;
+                depth--;
+                v = g->head[g->rev[path[depth]]];
+                it[v]++;
+            }
+        }
+    }
+done:
+    free(level); free(queue); free(it); free(path);
+    return total;
+}
+
+/* Edmonds-Karp: repeated BFS shortest augmenting path. */
+static int64_t edmonds_karp(graph_t *g, int64_t s, int64_t t, int *err) {
+    int64_t *parent = (int64_t *)malloc((size_t)g->nn * sizeof(int64_t));
+    int32_t *queue = (int32_t *)malloc((size_t)g->nn * sizeof(int32_t));
+    int64_t total = 0;
+    if (!parent || !queue) { *err = OR_E_NOMEM; goto done; }
+    for (;;) {
+        for (int64_t i = 0; i < g->nn; i++) parent[i] = -1;
+        int64_t qh = 0, qt = 0;
+        queue[qt++] = (int32_t)s;
+        parent[s] = -2;
+        while (qh < qt && parent[t] == -1) {
+            int64_t u = queue[qh++];
+            for (int64_t a = g->first[u]; a < g->first[u + 1]; a++) {
+                int64_t v = g->head[a];
+                if (g->res[a] > 0 && parent[v] == -1) {
+                    parent[v] = a;
+                    queue[qt++] = (int32_t)v;
+                }
+            }
+        }
+        if (parent[t] == -1) break;
+        int64_t f = OR_INF;
+        for (int64_t v = t; v != s; v = g->head[g->rev[parent[v]]])
+            if (g->res[parent[v]] < f) f = g->res[parent[v]];
+        for (int64_t v = t; v != s; v = g->head[g->rev[parent[v]]]) {
+            g->res[parent[v]] -= f;
+            g->res[g->rev[parent[v]]] += f;
+        }
+        total += f;
+    }
+done:
+    free(parent); free(queue);
+    return total;
+}
+
+/* Residual BFS from s: the minimal min-cut source set (mark[v] = 1). */
+static int source_set(const graph_t *g, int64_t s, uint8_t *mark) {
+    int32_t *queue = (int32_t *)malloc((size_t)g->nn * sizeof(int32_t));
+    if (!queue) return -1;
+    memset(mark, 0, (size_t)g->nn);
+    int64_t qh = 0, qt = 0;
+    mark[s] = 1;
+    queue[qt++] = (int32_t)s;
+    while (qh < qt) {
+        int64_t u = queue[qh++];
+        for (int64_t a = g->first[u]; a < g->first[u + 1]; a++) {
+            int64_t v = g->head[a];
+            if (g->res[a] > 0 && !mark[v]) { mark[v] = 1; queue[qt++] = (int32_t)v; }
+        }
+    }
+    free(queue);
+    return 0;
+}
+
+static int check_invariants(const graph_t *g, int64_t s, int64_t t, const uint8_t *mark, int64_t flow) {
+    int ok = CHK_CAPACITY | CHK_ANTISYM | CHK_CONSERVE | CHK_VALUE | CHK_T_NOT_IN_S | CHK_CUT_EQ_FLOW;
+    int64_t into_t = 0, out_s = 0, cut = 0;
+    for (int64_t u = 0; u < g->nn; u++) {
+        int64_t net = 0; /* inflow - outflow */
+        for (int64_t a = g->first[u]; a < g->first[u + 1]; a++) {
+            int64_t b = g->rev[a];
+            if (g->res[a] < 0) ok &= ~CHK_CAPACITY;
+            if (g->res[a] + g->res[b] != g->cap[a] + g->cap[b]) ok &= ~CHK_ANTISYM;
+            if (g->cap[a] > 0) { /* forward (original) arc u -> head */
+                int64_t f = g->cap[a] - g->res[a];
+                if (f < 0 || f > g->cap[a]) ok &= ~CHK_CAPACITY;
+                net -= f;
+                if (g->head[a] == t) into_t += f;
+                if (u == s) out_s += f;
+                if (mark[u] && !mark[g->head[a]]) {
+                    if (g->cap[a] >= OR_INF) ok &= ~CHK_CUT_EQ_FLOW;
+                    else cut += g->cap[a];
+                }
+            } else if (g->cap[b] > 0) { /* reverse slot of an arc head -> u */
+                net += g->cap[b] - g->res[b];
+            }
+        }
+        if (u != s && u != t && net != 0) ok &= ~CHK_CONSERVE;
+    }
+    if (into_t != flow || out_s != flow) ok &= ~CHK_VALUE;
+    if (mark[t]) ok &= ~CHK_T_NOT_IN_S;
+    if (cut != flow) ok &= ~CHK_CUT_EQ_FLOW;
+    return ok;
+}
+
+static int64_t run_maxflow(graph_t *g, int64_t s, int64_t t, int algo, int *err) {
+    return algo == 1 ? edmonds_karp(g, s, t, err) : dinic(g, s, t, err);
+}
+
+/*
+ * Column-graph oracle.
+ *   in[X*Y*Z]       int32 costs c[x][y][z] (z fastest), or vertex weights if input_is_weight
+ *   algo            0 = Dinitz, 1 = Edmonds-Karp
+ *   flow_out        |f| (int64)
+ *   surface_out     int32[X*Y], max z in S per column, -1 if none (nullable)
+ *   mask_out        uint8[X*Y*Z], 1 if the vertex is in the minimal source set (nullable)
+ *   checks_out      invariant bits (nullable)
+ *   n_arcs_out      number of explicit arcs built (nullable)
+ * Returns 0, 1 (invalid dims), 3 (out of memory) or 6 (a column has no source-side vertex).
+ */
+int oracle_colgraph_solve(const int32_t *in, int X, int Y, int Z, int delta, int input_is_weight, int algo,
+                          int64_t *flow_out, int32_t *surface_out, uint8_t *mask_out, int32_t *checks_out,
+                          int64_t *n_arcs_out) {
+    if (!in || X < 1 || Y < 1 || Z < 1 || delta < 0) return OR_E_INVAL;
+    if ((int64_t)X * Y * Z + 2 > INT32_MAX) return OR_E_INVAL;
+    const int64_t n = (int64_t)X * Y * Z, s = n, t = n + 1;
+    graph_t g;
+    int err = OR_OK;
+    int64_t *wbuf = (int64_t *)malloc((size_t)Z * sizeof(int64_t));
+    uint8_t *mark = (uint8_t *)malloc((size_t)n + 2);
+    if (!wbuf || !mark || g_alloc(&g, n + 2)) { free(wbuf); free(mark); return OR_E_NOMEM; }
+    colgraph_arcs(&g, 0, in, X, Y, Z, delta, input_is_weight, wbuf);
+    if (g_finish_count(&g)) { g_free(&g); free(wbuf); free(mark); return OR_E_NOMEM; }
+    colgraph_arcs(&g, 1, in, X, Y, Z, delta, input_is_weight, wbuf);
+    if (n_arcs_out) *n_arcs_out = g.m / 2;
+    int64_t flow = run_maxflow(&g, s, t, algo, &err);
+    if (err) { g_free(&g); free(wbuf); free(mark); return err; }
+    if (source_set(&g, s, mark)) { g_free(&g); free(wbuf); free(mark); return OR_E_NOMEM; }
+    if (checks_out) *checks_out = check_invariants(&g, s, t, mark, flow);
+    *flow_out = flow;
+    int status = OR_OK;
+    for (int64_t col = 0; col < (int64_t)X * Y; col++) {
+        int32_t top = -1;
+        for (int64_t z = 0; z < Z; z++)
+            if (mark[col * Z + z]) top = (int32_t)z;
+        if (top < 0) status = OR_E_EMPTY_COLUMN;
+        if (surface_out) surface_out[col] = top;
+    }
+    if (mask_out) memcpy(mask_out, mark, (size_t)n);
+    g_free(&g); free(wbuf); free(mark);
+    return status;
+}
+
+/*
+ * Generic max-flow on an explicit arc list (for pinning the max-flow core
+ * against brute-force minimum cuts on small general graphs).
+ *   tails/heads/caps [m]; nodes 0..nn-1; s, t.
+ *   source_side_out uint8[nn] (nullable): minimal source set.
+ */
+int oracle_graph_maxflow(int nn, int m, const int32_t *tails, const int32_t *heads, const int64_t *caps,
+                         int s, int t, int algo, int64_t *flow_out, uint8_t *source_side_out,
+                         int32_t *checks_out) {
+    if (nn < 2 || m < 0 || s < 0 || t < 0 || s >= nn || t >= nn || s == t) return OR_E_INVAL;
+    graph_t g;
+    int err = OR_OK;
+    if (g_alloc(&g, nn)) return OR_E_NOMEM;
+    for (int i = 0; i < m; i++) {
+        if (tails[i] < 0 || tails[i] >= nn || heads[i] < 0 || heads[i] >= nn || caps[i] < 0) {
+            g_free(&g);
+            return OR_E_INVAL;
+        }
+        add_arc(&g, 0, tails[i], heads[i], caps[i]);
+    }
+    if (g_finish_count(&g)) { g_free(&g); return OR_E_NOMEM; }
+    for (int i = 0; i < m; i++) add_arc(&g, 1, tails[i], heads[i], caps[i]);
+    int64_t flow = run_maxflow(&g, s, t, algo, &err);
+    uint8_t *mark = (uint8_t *)malloc((size_t)nn);
+    if (err || !mark || source_set(&g, s, mark)) { g_free(&g); free(mark); return err ? err : OR_E_NOMEM; }
+    if (checks_out) *checks_out = check_invariants(&g, s, t, mark, flow);
+    *flow_out = flow;
+    if (source_side_out) memcpy(source_side_out, mark, (size_t)nn);
+    g_free(&g); free(mark);
+    return OR_OK;
+}
