@@ -1,0 +1,172 @@
+/*
+ * colgraph.h -- C ABI of the B200-native column-graph max-flow / min-cut library
+ * (hot path of arXiv 2601.17026, "Parallel maxflow for proper-ordered graphs").
+ *
+ * The problem (§1.2, §1.3):
+ *   A proper-ordered multi-column graph of X*Y columns, each of Z vertices
+ *   (x, y, z), z = 0 the bottom ("base").  Vertex weights w(v) are converted to
+ *   terminal arcs ("converted to the costs associated with the
+ *   edges connecting the node v to the source or the sink"):
+ *       w < 0 : arc s -> v of capacity -w        w > 0 : arc v -> t of capacity w
+ *   Intra-column arcs (x,y,z) -> (x,y,z-1) have infinite capacity; inter-column
+ *   arcs to the 4 neighbour columns realise the hard smoothness interval Delta
+ *   ("edge interval").  The library computes the maximum flow value
+ *   |f| (Eq. 5), the minimal minimum-cut source set (Eq. 6-7, Theorem 1
+ *   L86-90) and the optimal net surface S(x,y) = max{z : (x,y,z) in S}
+ *   (SPEC.md:151).
+ *
+ * Vertex weights from a cost volume c[x][y][z] (reading R1):
+ *       w(x,y,0) = c(x,y,0) - (sum_z c(x,y,z) + 1),   w(x,y,z) = c(x,y,z) - c(x,y,z-1)
+ *
+ * Addressing is implicit (§3.2.3): vertex (x,y,z) has index
+ * i = (x*Y + y)*Z + z (z fastest); no adjacency list is stored.
+ *
+ * Conventions for every entry point:
+ *   - Errors are returned as cg_status, never thrown; no C++ exception crosses
+ *     this ABI.
+ *   - "_dev" pointers are CUDA device pointers on cg_dist.device; "_host"
+ *     pointers are host memory (pinned or pageable).
+ *   - All device work is enqueued on cg_dist.stream (NULL = legacy default
+ *     stream).  Calls return after their results are defined (maxflow_solve
+ *     returns with |f| on the host; mincut_extract_surface returns after its
+ *     outputs are written).
+ *   - One handle per thread; a handle is single-solve: build -> solve ->
+ *     extract -> free.
+ *   - Multi-GPU: every rank of a job calls every function collectively with
+ *     its own x-slab (cg_slab_range); results are global on every rank.
+ */
+#ifndef COLGRAPH_H
+#define COLGRAPH_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cg_graph cg_graph; /* opaque, library-owned */
+
+typedef enum {
+    CG_OK = 0,
+    CG_E_INVAL = 1,          /* bad dims (X,Y,Z < 1, n >= 2^31-2), Delta < 0, NULL argument,
+                                nranks > X, unsupported option */
+    CG_E_OVERFLOW = 2,       /* a weight or an excess would exceed INT32_MAX */
+    CG_E_NOMEM = 3,          /* device allocation failed */
+    CG_E_CUDA = 4,           /* a CUDA call or kernel failed */
+    CG_E_NCCL = 5,           /* an NCCL call failed (multi-GPU) */
+    CG_E_EMPTY_COLUMN = 6,   /* some column has no source-side vertex;
+                                outputs are still written, that column's surface is -1 */
+    CG_E_STATE = 7,          /* call out of order (e.g. extract before solve) */
+    CG_E_NOT_CONVERGED = 8   /* max_sweeps reached before termination */
+} cg_status;
+
+/* Full-volume dimensions; Delta >= 0 is the smoothness interval
+ * (Delta >= Z-1: unconstrained columns; Delta = 0: flat surface). */
+typedef struct {
+    int32_t X, Y, Z, delta;
+} cg_dims;
+
+/* Process / device placement.
+ *   rank, nranks : this process's rank and the job size (nranks = 1: single GPU)
+ *   nccl_id      : 128-byte ncclUniqueId shared by all ranks (NULL if nranks == 1)
+ *   device       : CUDA device ordinal the handle lives on
+ *   stream       : cudaStream_t for all work (NULL = legacy default stream) */
+typedef struct {
+    int32_t rank, nranks;
+    const void *nccl_id;
+    int32_t device;
+    void *stream;
+} cg_dist;
+
+/* Solver options (NULL = defaults).
+ *   gr_factor   : global relabel after gr_factor * n units of push/relabel work
+ *                 (factor 1..2); default 1.0
+ *   gap_every   : run the gap heuristic every gap_every sweeps
+ *                 (0 = never); default 0
+ *   check_every : sweeps between host reads of the active-vertex count; default 16
+ *   max_sweeps  : give up with CG_E_NOT_CONVERGED after this many sweeps; default 1<<30
+ *   ops_per_sweep : push/relabel operations a vertex may perform per sweep; default 1 */
+typedef struct {
+    float gr_factor;
+    int32_t gap_every;
+    int32_t check_every;
+    int64_t max_sweeps;
+    int32_t ops_per_sweep;
+} cg_solve_opts;
+
+typedef struct {
+    int64_t sweeps;            /* push-relabel sweep launches */
+    int64_t global_relabels;   /* exact global relabels (incl. initial and final) */
+    int64_t gr_passes;         /* column-scan passes summed over all global relabels */
+    int64_t work;              /* push/relabel operations (active vertex visits) */
+    int64_t gap_runs;          /* gap heuristic invocations */
+    int64_t gap_lifted;        /* vertices lifted to INF by the gap heuristic */
+    int64_t extract_passes;    /* fixpoint passes of the surface extraction */
+    double ms_build, ms_solve, ms_extract, ms_global_relabel, ms_sweeps;
+    double bytes_per_sweep_alg; /* algorithmic bytes of a dense sweep (32 B / vertex) */
+    int64_t source_capacity;   /* N = sum of source-arc capacities (int64) */
+    int64_t kernel_launches;   /* library kernel launches during solve + extract */
+    double ms_sweep_kernels;   /* CUDA-event time of all sweep launches (on the library stream) */
+    double sweep_bytes_alg;    /* algorithmic bytes moved by all sweeps: 4 B per vertex (excess scan)
+                                  + 40 B per active-vertex visit (28 B state read, 12 B push writes) */
+} cg_solve_stats;
+
+/* a1 -- build the int32 structure-of-arrays residual graph.
+ *   cost_dev : device int32[X_r*Y*Z], this rank's x-slab [x][y][z], z fastest;
+ *              costs c (input_is_weight = 0) or vertex weights w (input_is_weight = 1).
+ *              Read during the call only; owned by the caller.
+ *   out      : receives the library-owned handle (free with colgraph_free).
+ * Excess is initialised to the saturated source arcs (Goldberg-Tarjan init,
+ * PAPER.md:134), sink residuals to the sink capacities, all flows to 0.
+ * Errors: CG_E_INVAL, CG_E_OVERFLOW (a weight outside int32), CG_E_NOMEM,
+ *         CG_E_CUDA, CG_E_NCCL. */
+cg_status colgraph_build(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight,
+                         const cg_dist *dist, cg_graph **out);
+
+/* a2-a6 -- lock-free push-relabel to a maximum preflow (§2.1,
+ * Alg. 2) with exact global relabels from the sink (Alg. 3,
+ * §3.2.2), optional gap relabeling (L170-184) and termination decided after an
+ * exact global relabel (§3.2.4).
+ *   flow_value : host int64, receives |f| (Eq. 5) -- global over all ranks.
+ *   stats      : nullable.
+ * Errors: CG_E_STATE (already solved), CG_E_OVERFLOW, CG_E_CUDA, CG_E_NCCL,
+ *         CG_E_NOT_CONVERGED. */
+cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_value, cg_solve_stats *stats);
+
+/* a7 -- minimal min-cut source set and surface (Theorem 1).
+ *   surface_dev : device int32[X_r*Y], S(x,y) = max{z : (x,y,z) in S}, -1 if none.
+ *   mask_dev    : nullable device uint8[X_r*Y*Z], 1 iff the vertex is in S.
+ * Errors: CG_E_STATE (not solved), CG_E_EMPTY_COLUMN (outputs still written),
+ *         CG_E_CUDA, CG_E_NCCL. */
+cg_status mincut_extract_surface(cg_graph *g, int32_t *surface_dev, uint8_t *mask_dev);
+
+/* Convenience end-to-end call on HOST buffers (single GPU): copies cost_host to
+ * the device, builds, solves, extracts and copies surface/mask back.
+ *   surface_host : int32[X*Y];  mask_host : nullable uint8[X*Y*Z].
+ * Same errors as the three calls above. */
+cg_status colgraph_solve_host(const cg_dims *dims, const int32_t *cost_host, int32_t input_is_weight,
+                              const cg_dist *dist, const cg_solve_opts *opts, int64_t *flow_value,
+                              int32_t *surface_host, uint8_t *mask_host, cg_solve_stats *stats);
+
+/* Copy the residual state (8 int32 planes of n_r each: E, H, T, D, L+x, L-x, L+y, L-y)
+ * to device memory out_dev (int32[8*n_r]) -- for certificates and tests. */
+cg_status colgraph_export_state(cg_graph *g, int32_t *out_dev);
+
+/* Copy the handle's accumulated statistics (solve + extract) to *stats (host). */
+cg_status colgraph_stats(const cg_graph *g, cg_solve_stats *stats);
+
+void colgraph_free(cg_graph *g);
+const char *cg_status_str(cg_status s);
+
+/* x-slab of a rank: ceil(X/nranks) planes to the first X mod nranks ranks,
+ * floor to the rest ("larger first"); [x0, x1).
+ * Errors: CG_E_INVAL if nranks < 1, rank out of range or nranks > X. */
+cg_status cg_slab_range(const cg_dims *dims, int32_t rank, int32_t nranks, int32_t *x0, int32_t *x1);
+
+/* Library version string and build flags (for bench provenance). */
+const char *cg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COLGRAPH_H */
