@@ -1,529 +1,70 @@
-// colgraph.cu -- B200 (sm_100a) implementation of include/colgraph.h.
+// colgraph.cu -- host side of the B200 column-graph max-flow library (include/colgraph.h).
 //
-// Hot path of arXiv 2601.17026 (§3.2): push-relabel max-flow on
-// Wu-Chen proper-ordered column graphs with implicit (x,y,z) addressing,
-// redesigned for one GPU per process:
-//   a1 build            k_build                    (§1.2, §2.1)
-//   a2/a5 global relabel k_gr_pass (column scans)  (§2.1, Alg. 3)
-//   a3 sweep            k_sweep (lock-free)        (§2.1, Alg. 2)
-//   a4 termination      host loop + exact relabel  (§3.2.4, Alg. 1)
-//   a5 gap              k_gap_*                    (§2.1)
-//   a6 flow value       k_sum_T                    (Eq. 5)
-//   a7 extraction       k_ext_*                    (Theorem 1)
+// Hot path of arXiv 2601.17026 (§3.2), redesigned for one GPU per process:
+// the paper's per-thread FIFO queues, per-vertex locks and level barriers (§3.2.1-3.2.4)
+// become device worklists of 32-vertex chunks, single-decrementer atomics and
+// level-synchronous frontier kernels launched back to back on one stream.  The host
+// only reads a few counters every `check_every` sweeps.
 //
-// Residual layout: 8 int32 planes of n each,
-//   E  excess            H  height (INF = n_global + 1 = cannot reach t)
-//   T  sink-arc residual D  flow on the down arc (x,y,z)->(x,y,z-1) = residual of the up arc
-//   L0..L3 flow on the lateral arc in direction d (+x,-x,+y,-y) = residual of its reverse.
-// Arc set ("minimal" form, reading R2): down arcs z->z-1 (INF);
-// lateral arcs (x,y,z)->(nbr, zo(z)) with zo(0)=0, zo(z)=z-Delta for z>Delta,
-// none for 1<=z<=Delta.  Each vertex then has at most one lateral in-arc per
-// direction, from (nbr, zi(z)), zi(0)=0, zi(z)=z+Delta.
-//
-// Lock-free rule: every residual field has exactly one decrementer, so every
-// value a thread reads (possibly stale) is a lower bound of what it may
-// subtract; termination is certified by an exact global relabel.
+// Solve loop:
+//   a2  exact global relabel (frontier BFS from t) -> rebuild the active-chunk list
+//   a3  sweeps over the active-chunk list (batch of check_every launches, no host sync)
+//   a5  re-run the global relabel when the work since the last one reaches gr_factor*n
+//        or the sweep time since the last one exceeds its cost
+//   a4  when a sweep finds no active vertex: exact global relabel; stop if no vertex
+//       with excess has a finite height (the preflow is then maximum)
+//   a6  |f| = sum(T0) - sum(T)
 #include "colgraph.h"
-
-#include <cuda_runtime.h>
+#include "kernels.cuh"
 
 #include <algorithm>
 #include <chrono>
-#include <climits>
-#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <vector>
+
+using namespace cg;
 
 namespace {
-
-constexpr unsigned FULL = 0xffffffffu;
-
-struct Geo {
-    int32_t X, Y, Z, delta;  // X = planes owned by this rank
-    int64_t n;               // vertices owned by this rank
-    int64_t YZ;              // vertices per x-plane
-    int32_t INF;             // n_global + 1
-};
-
-struct Soa {
-    int32_t *E, *H, *T, *D, *L;  // L: 4 planes at L + d*n
-};
-
-enum { FLAG_OVERFLOW = 1 };
-
-__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
-
-__device__ __forceinline__ int zo_of(int z, int delta) { return z == 0 ? 0 : (z > delta ? z - delta : -1); }
-__device__ __forceinline__ int zi_of(int z, int delta, int Z) { return z == 0 ? 0 : (z + delta < Z ? z + delta : -1); }
-
-// neighbour column in direction d (0:+x 1:-x 2:+y 3:-y): offset in vertices, or 0 if absent
-__device__ __forceinline__ int64_t nbr_off(const Geo &g, int x, int y, int d) {
-    switch (d) {
-        case 0: return x + 1 < g.X ? g.YZ : 0;
-        case 1: return x >= 1 ? -g.YZ : 0;
-        case 2: return y + 1 < g.Y ? (int64_t)g.Z : 0;
-        default: return y >= 1 ? -(int64_t)g.Z : 0;
-    }
-}
-
-__device__ __forceinline__ int warp_sum_i(int v) {
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-    return v;
-}
-__device__ __forceinline__ long long warp_sum_ll(long long v) {
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-    return v;
-}
-
-// ------------------------------------------------------------------ a1: build
-// One warp per column: w(0) = c(0) - (sum_z c + 1), w(z) = c(z) - c(z-1)
-// (R1); E = max(0,-w) (source arcs saturated), T = max(0,w).
-__global__ void k_build(Geo g, const int32_t *__restrict__ in, int weight_mode, Soa s,
-                        unsigned long long *sums /* [0]=N, [1]=sum T0 */, int *flags) {
-    const int64_t ncol = (int64_t)g.X * g.Y;
-    const int warps = (gridDim.x * blockDim.x) >> 5;
-    long long accN = 0, accT = 0;
-    bool bad = false;
-    for (int64_t col = (int64_t)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); col < ncol; col += warps) {
-        const int32_t *cc = in + col * g.Z;
-        long long colsum = 0;
-        if (!weight_mode) {
-            for (int z = lane_id(); z < g.Z; z += 32) colsum += cc[z];
-            colsum = warp_sum_ll(colsum);
-        }
-        for (int z = lane_id(); z < g.Z; z += 32) {
-            long long w;
-            if (weight_mode) {
-                w = cc[z];
-            } else {
-                w = z == 0 ? (long long)cc[0] - (colsum + 1) : (long long)cc[z] - (long long)cc[z - 1];
-            }
-            if (w > INT_MAX || w < -(long long)INT_MAX) bad = true;
-            int32_t e = w < 0 ? (int32_t)(-w) : 0, t = w > 0 ? (int32_t)w : 0;
-            s.E[col * g.Z + z] = bad ? 0 : e;
-            s.T[col * g.Z + z] = bad ? 0 : t;
-            accN += e;
-            accT += t;
-        }
-    }
-    accN = warp_sum_ll(accN);
-    accT = warp_sum_ll(accT);
-    if (lane_id() == 0) {
-        atomicAdd(&sums[0], (unsigned long long)accN);
-        atomicAdd(&sums[1], (unsigned long long)accT);
-    }
-    if (bad) atomicOr(flags, FLAG_OVERFLOW);
-}
-
-__global__ void k_fill(int32_t *p, int64_t n, int32_t v) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
-}
-
-// ------------------------------------------------------------------ a3: push-relabel sweep
-// One thread per vertex.  An active vertex (E > 0, H < INF) scans its residual
-// out-arcs in the fixed order t, down, lateral-out(+x,-x,+y,-y), up,
-// lateral-in-reverse(+x,-x,+y,-y), takes the lowest neighbour height h_min
-// (first wins ties), relabels to h_min+1 if H <= h_min (Alg. 2 Relabel,
-// "newd = min label(w)+1", only if larger) and pushes delta = min(E, r) along
-// that arc (Alg. 2 Push).  Up to `ops` push/relabel operations per sweep.
-// Fused: warp-aggregated count of vertices active at the start of the sweep.
-__global__ void __launch_bounds__(256) k_sweep(Geo g, Soa s, int ops, unsigned long long *cnt, int *flags) {
-    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    bool act = false;
-    if (v < g.n) {
-        int e = s.E[v];
-        int h = s.H[v];
-        if (e > 0 && h < g.INF) {
-            act = true;
-            const int z = (int)(v % g.Z);
-            const int64_t col = v / g.Z;
-            const int x = (int)(col / g.Y), y = (int)(col % g.Y);
-            const int64_t v0 = v - z;  // column base
-            const int zo = zo_of(z, g.delta), zi = zi_of(z, g.delta, g.Z);
-            int64_t off[4];
-#pragma unroll
-            for (int d = 0; d < 4; d++) off[d] = nbr_off(g, x, y, d);
-            int sent = 0;
-            for (int it = 0; it < ops && e > 0; ++it) {
-                int best = g.INF, arc = -1, res = 0;
-                int64_t tgt = -1;
-                const int tres = s.T[v];
-                if (tres > 0) {
-                    best = 0;
-                    arc = 0;
-                } else {
-                    if (z >= 1) {
-                        int hh = s.H[v - 1];
-                        if (hh < best) { best = hh; arc = 1; tgt = v - 1; }
-                    }
-                    if (zo >= 0) {
-#pragma unroll
-                        for (int d = 0; d < 4; d++) {
-                            if (!off[d]) continue;
-                            int64_t t = v0 + off[d] + zo;
-                            int hh = s.H[t];
-                            if (hh < best) { best = hh; arc = 2 + d; tgt = t; }
-                        }
-                    }
-                    if (z + 1 < g.Z) {
-                        int r = s.D[v + 1];
-                        if (r > 0) {
-                            int hh = s.H[v + 1];
-                            if (hh < best) { best = hh; arc = 6; tgt = v + 1; res = r; }
-                        }
-                    }
-                    if (zi >= 0) {
-#pragma unroll
-                        for (int d = 0; d < 4; d++) {
-                            if (!off[d]) continue;
-                            int64_t u = v0 + off[d] + zi;
-                            int r = s.L[(int64_t)(d ^ 1) * g.n + u];
-                            if (r > 0) {
-                                int hh = s.H[u];
-                                if (hh < best) { best = hh; arc = 7 + d; tgt = u; res = r; }
-                            }
-                        }
-                    }
-                }
-                if (best >= g.INF) {  // no residual path known: dead until the next global relabel
-                    s.H[v] = g.INF;
-                    break;
-                }
-                if (h <= best) {  // relabel
-                    h = best + 1;
-                    s.H[v] = h;
-                    if (h >= g.INF) break;
-                }
-                int df;
-                switch (arc) {
-                    case 0:
-                        df = min(e, tres);
-                        s.T[v] = tres - df;
-                        break;
-                    case 1:
-                        df = e;
-                        atomicAdd(&s.D[v], df);
-                        break;
-                    case 2: case 3: case 4: case 5:
-                        df = e;
-                        atomicAdd(&s.L[(int64_t)(arc - 2) * g.n + v], df);
-                        break;
-                    case 6:
-                        df = min(e, res);
-                        atomicSub(&s.D[v + 1], df);
-                        break;
-                    default:
-                        df = min(e, res);
-                        atomicSub(&s.L[(int64_t)((arc - 7) ^ 1) * g.n + tgt], df);
-                        break;
-                }
-                if (tgt >= 0) {
-                    int old = atomicAdd(&s.E[tgt], df);
-                    if (old > INT_MAX - df) atomicOr(flags, FLAG_OVERFLOW);
-                }
-                e -= df;
-                sent += df;
-            }
-            if (sent) atomicSub(&s.E[v], sent);
-        }
-    }
-    unsigned b = __ballot_sync(FULL, act);
-    if (lane_id() == 0 && b) atomicAdd(cnt, (unsigned long long)__popc(b));
-}
-
-// ------------------------------------------------------------------ a2/a5: exact global relabel
-// H(v) = residual BFS distance from v to t (Alg. 3; PAPER.md:134 footnote).
-// Column structure: down arcs are infinite, so d(z) <= d(z-1)+1; up arcs exist
-// where D(z+1) > 0, so d(z) <= d(z+1)+1 there.  Given the lateral/terminal
-// "external" distances ext(z), a column's distances are two scans:
-//   forward  a(z) = z + prefix_min_{s<=z}(ext(s) - s)
-//   backward d(z) = -z + segmented suffix_min_{s>=z, up-linked}(a(s) + s)
-// Passes repeat (monotone Bellman-Ford relaxation, in place) until a pass
-// changes nothing: the fixpoint is the exact BFS distance.
-__device__ __forceinline__ int warp_prefix_min(int v) {
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int t = __shfl_up_sync(FULL, v, o);
-        if (lane_id() >= o) v = min(v, t);
-    }
-    return v;
-}
-// v_l = min over j >= l reachable through consecutive links (link_l: l -> l+1), within the warp
-__device__ __forceinline__ int warp_seg_suffix_min(int v, bool link) {
-    int f = link;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int v2 = __shfl_down_sync(FULL, v, o);
-        int f2 = __shfl_down_sync(FULL, f, o);
-        if (lane_id() + o < 32) {
-            if (f) v = min(v, v2);
-            f = f && f2;
-        } else {
-            f = 0;
-        }
-    }
-    return v;
-}
-
-__global__ void __launch_bounds__(256) k_gr_pass(Geo g, Soa s, int *changed) {
-    extern __shared__ int32_t sh_a[];  // per warp: Z ints
-    const int wib = threadIdx.x >> 5;
-    int32_t *a = sh_a + (int64_t)wib * g.Z;
-    const int64_t ncol = (int64_t)g.X * g.Y;
-    const int warps = (gridDim.x * blockDim.x) >> 5;
-    const int INF = g.INF;
-    bool any = false;
-    for (int64_t col = (int64_t)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); col < ncol; col += warps) {
-        const int x = (int)(col / g.Y), y = (int)(col % g.Y);
-        const int64_t v0 = col * g.Z;
-        int64_t off[4];
-#pragma unroll
-        for (int d = 0; d < 4; d++) off[d] = nbr_off(g, x, y, d);
-        // forward: ext and prefix-min
-        int carry = INF;  // min over earlier chunks of (ext(s) - s)
-        for (int c0 = 0; c0 < g.Z; c0 += 32) {
-            const int z = c0 + lane_id();
-            int ext = INF;
-            if (z < g.Z) {
-                const int64_t v = v0 + z;
-                if (s.T[v] > 0) ext = 1;
-                const int zo = zo_of(z, g.delta);
-                if (zo >= 0) {
-#pragma unroll
-                    for (int d = 0; d < 4; d++) {
-                        if (!off[d]) continue;
-                        int hh = s.H[v0 + off[d] + zo];
-                        if (hh < INF) ext = min(ext, hh + 1);
-                    }
-                }
-                const int zi = zi_of(z, g.delta, g.Z);
-                if (zi >= 0) {
-#pragma unroll
-                    for (int d = 0; d < 4; d++) {
-                        if (!off[d]) continue;
-                        int64_t u = v0 + off[d] + zi;
-                        if (s.L[(int64_t)(d ^ 1) * g.n + u] > 0) {
-                            int hh = s.H[u];
-                            if (hh < INF) ext = min(ext, hh + 1);
-                        }
-                    }
-                }
-            }
-            int val = min(warp_prefix_min(ext - (z < g.Z ? z : 0)), carry);
-            carry = __shfl_sync(FULL, val, 31);
-            if (z < g.Z) a[z] = min(INF, val + z);
-        }
-        __syncwarp();
-        // backward: segmented suffix min along residual up arcs
-        int carry_b = INF;  // min reachable value (a(s)+s) from the element just above this chunk
-        const int last_c0 = ((g.Z - 1) / 32) * 32;
-        for (int c0 = last_c0; c0 >= 0; c0 -= 32) {
-            const int z = c0 + lane_id();
-            int val = INF;
-            bool link = false;
-            if (z < g.Z) {
-                val = a[z] + z;
-                link = (z + 1 < g.Z) && s.D[v0 + z + 1] > 0;
-            }
-            val = warp_seg_suffix_min(val, link);
-            const unsigned m = __ballot_sync(FULL, link);
-            const unsigned need = FULL << lane_id();
-            if ((m & need) == need) val = min(val, carry_b);
-            carry_b = __shfl_sync(FULL, val, 0);
-            if (z < g.Z) {
-                int d = min(INF, val - z);
-                const int64_t v = v0 + z;
-                int old = s.H[v];
-                if (d < old) {
-                    s.H[v] = d;
-                    any = true;
-                }
-            }
-        }
-        __syncwarp();
-    }
-    if (__any_sync(FULL, any) && lane_id() == 0) atomicOr(changed, 1);
-}
-
-__global__ void k_count_active(Geo g, const int32_t *__restrict__ E, const int32_t *__restrict__ H,
-                               unsigned long long *cnt) {
-    int c = 0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += (int64_t)gridDim.x * blockDim.x)
-        c += (E[i] > 0 && H[i] < g.INF);
-    c = warp_sum_i(c);
-    if (lane_id() == 0 && c) atomicAdd(cnt, (unsigned long long)c);
-}
-
-// ------------------------------------------------------------------ a5: gap heuristic
-constexpr int GAP_BINS = 1 << 20;
-__global__ void k_gap_hist(Geo g, const int32_t *__restrict__ H, unsigned *hist, int *maxh) {
-    int mymax = 0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += (int64_t)gridDim.x * blockDim.x) {
-        int h = H[i];
-        if (h < g.INF) {
-            mymax = max(mymax, h);
-            if (h < GAP_BINS) atomicAdd(&hist[h], 1u);
-        }
-    }
-    for (int o = 16; o; o >>= 1) mymax = max(mymax, __shfl_xor_sync(FULL, mymax, o));
-    if (lane_id() == 0) atomicMax(maxh, mymax);
-}
-// smallest g in [1, min(maxh, GAP_BINS)) with hist[g] == 0
-__global__ void k_gap_find(const unsigned *hist, const int *maxh, int *gap) {
-    const int lim = min(*maxh, GAP_BINS - 1);
-    int best = INT_MAX;
-    for (int h = 1 + (int)threadIdx.x; h < lim; h += blockDim.x)
-        if (hist[h] == 0) { best = h; break; }
-    for (int o = 16; o; o >>= 1) best = min(best, __shfl_xor_sync(FULL, best, o));
-    __shared__ int sb[32];
-    if (lane_id() == 0) sb[threadIdx.x >> 5] = best;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int b = INT_MAX;
-        for (int i = 0; i < (int)(blockDim.x >> 5); i++) b = min(b, sb[i]);
-        *gap = b;
-    }
-}
-__global__ void k_gap_lift(Geo g, int32_t *H, const int *gap, unsigned long long *lifted) {
-    const int gp = *gap;
-    int c = 0;
-    if (gp != INT_MAX) {
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += (int64_t)gridDim.x * blockDim.x) {
-            int h = H[i];
-            if (h > gp && h < g.INF) { H[i] = g.INF; c++; }
-        }
-    }
-    c = warp_sum_i(c);
-    if (lane_id() == 0 && c) atomicAdd(lifted, (unsigned long long)c);
-}
-
-// ------------------------------------------------------------------ a6: flow value
-__global__ void k_sum_T(Geo g, const int32_t *__restrict__ T, unsigned long long *out) {
-    long long acc = 0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += (int64_t)gridDim.x * blockDim.x)
-        acc += T[i];
-    acc = warp_sum_ll(acc);
-    if (lane_id() == 0 && acc) atomicAdd(out, (unsigned long long)acc);
-}
-
-// ------------------------------------------------------------------ a7: extraction
-// Minimal source set S = forward residual closure of {v : E(v) > 0} (SURVEY.md
-// §8(a) a7, reading R5).  S is downward closed in every column (infinite down
-// arcs), so it is top(x,y); pull-style fixpoint per column:
-//   seed   top >= max{z : E(z) > 0}
-//   lat-out from nbr   top >= max(0, top(nbr) - Delta)             (nbr's arcs (nbr,z)->(C,zo(z)))
-//   lat-in  from nbr   top >= max{z' : L_dir(C->nbr)(C,z') > 0, z' = zi(z), z <= top(nbr)}
-//   up     climb while D(top+1) > 0
-__device__ int warp_climb(const Geo &g, const int32_t *__restrict__ D, int64_t v0, int t) {
-    if (t < 0) return t;
-    for (int base = t + 1; base < g.Z; base += 32) {
-        const int z = base + lane_id();
-        const bool stop = (z >= g.Z) || D[v0 + z] <= 0;
-        const unsigned m = __ballot_sync(FULL, stop);
-        if (m) return base + __ffs(m) - 1 - 1;
-    }
-    return g.Z - 1;
-}
-
-__global__ void k_ext_seed(Geo g, Soa s, int32_t *top) {
-    const int64_t ncol = (int64_t)g.X * g.Y;
-    const int warps = (gridDim.x * blockDim.x) >> 5;
-    for (int64_t col = (int64_t)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); col < ncol; col += warps) {
-        const int64_t v0 = col * g.Z;
-        int t = -1;
-        for (int c0 = 0; c0 < g.Z; c0 += 32) {
-            const int z = c0 + lane_id();
-            const unsigned m = __ballot_sync(FULL, z < g.Z && s.E[v0 + z] > 0);
-            if (m) t = c0 + 31 - __clz(m);
-        }
-        t = warp_climb(g, s.D, v0, t);
-        if (lane_id() == 0) top[col] = t;
-    }
-}
-
-__global__ void k_ext_pass(Geo g, Soa s, int32_t *top, int *changed) {
-    const int64_t ncol = (int64_t)g.X * g.Y;
-    const int warps = (gridDim.x * blockDim.x) >> 5;
-    bool any = false;
-    for (int64_t col = (int64_t)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); col < ncol; col += warps) {
-        const int x = (int)(col / g.Y), y = (int)(col % g.Y);
-        const int64_t v0 = col * g.Z;
-        const int t0 = top[col];
-        int t = t0;
-        int tn[4];
-#pragma unroll
-        for (int d = 0; d < 4; d++) {
-            int64_t o = nbr_off(g, x, y, d);
-            tn[d] = o ? top[col + o / g.Z] : -1;
-            if (tn[d] >= 0) t = max(t, max(0, tn[d] - g.delta));
-        }
-#pragma unroll
-        for (int d = 0; d < 4; d++) {
-            if (tn[d] < 0) continue;
-            // C's own lateral arc in direction d points at nbr_d; its flow L_d(C,z') > 0 is a
-            // residual arc (nbr, zo(z')) -> (C, z').  Allowed z' in {0} U [Delta+1, tn+Delta].
-            const int lim = min(g.Z - 1, tn[d] + g.delta);
-            const int32_t *Ld = s.L + (int64_t)d * g.n + v0;
-            for (int hi = lim; hi > t && hi >= g.delta + 1; hi -= 32) {
-                const int z = hi - lane_id();
-                const bool ok = z > t && z >= g.delta + 1 && Ld[z] > 0;
-                const unsigned m = __ballot_sync(FULL, ok);
-                if (m) { t = hi - (__ffs(m) - 1); break; }
-            }
-            if (t < 0 && Ld[0] > 0) t = 0;
-        }
-        if (t > t0 || (t0 < 0 && t >= 0)) t = warp_climb(g, s.D, v0, t);
-        if (t != t0) {
-            any = true;
-            if (lane_id() == 0) top[col] = t;
-        }
-    }
-    if (__any_sync(FULL, any) && lane_id() == 0) atomicOr(changed, 1);
-}
-
-__global__ void k_ext_out(Geo g, const int32_t *__restrict__ top, int32_t *surface, uint8_t *mask, int *empty) {
-    const int64_t ncol = (int64_t)g.X * g.Y;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ncol; i += (int64_t)gridDim.x * blockDim.x) {
-        surface[i] = top[i];
-        if (top[i] < 0) atomicOr(empty, 1);
-    }
-    if (mask) {
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += (int64_t)gridDim.x * blockDim.x)
-            mask[i] = (uint8_t)((int)(i % g.Z) <= top[i / g.Z]);
-    }
-}
-
+constexpr int RING = 256;
+constexpr int BFS_BATCH = 32;
+constexpr int EXT_BATCH = 16;
 }  // namespace
-
-// ====================================================================== host side
 
 struct cg_graph {
     cg_dims dims{};
     cg_dist dist{};
     Geo geo{};
     cudaStream_t stream = nullptr;
-    int32_t *soa = nullptr;  // 8 planes
-    Soa s{};
-    // device scratch
-    unsigned long long *d_u64 = nullptr;  // [0]=N [1]=sumT0 [2]=sumT [3]=active [4]=lifted [8..8+RING) sweep counts
-    int *d_i32 = nullptr;                 // [0]=flags [1]=changed [2]=maxh [3]=gap [4]=empty
-    unsigned *d_hist = nullptr;
-    int32_t *d_top = nullptr;
-    // pinned host mirrors
-    unsigned long long *h_u64 = nullptr;
-    int *h_i32 = nullptr;
-    int64_t N = 0, sumT0 = 0;
-    bool solved = false;
     int num_sms = 148;
+    // one stream-ordered workspace allocation
+    char *ws = nullptr;
+    size_t ws_bytes = 0;
+    Soa s{};
+    int *blist[2] = {nullptr, nullptr};  // BFS frontiers (vertices)
+    int *clist[2] = {nullptr, nullptr};  // sweep worklists (chunks)
+    int *cstamp = nullptr;               // per-chunk list tag
+    int32_t *top = nullptr, *proc = nullptr;
+    int *colstamp = nullptr;
+    int *collist[2] = {nullptr, nullptr};
+    unsigned *hist = nullptr;
+    unsigned *cnt = nullptr;              // [0..2] sweep lists, [4..6] bfs, [8..10] extraction
+    unsigned long long *work = nullptr;   // [RING] active visits per sweep
+    unsigned long long *u64 = nullptr;    // [0]=N [1]=sumT0 [2]=sumT [3]=active [4]=gap lifted
+    int *flags = nullptr;                 // [0]=overflow [1]=maxh [2]=gap [3]=empty
+    // pinned host mirrors
+    unsigned *h_cnt = nullptr;
+    unsigned long long *h_work = nullptr, *h_u64 = nullptr;
+    int *h_flags = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int64_t N = 0, sumT0 = 0;
+    int tag = 0;        // monotone worklist tag
+    int sweep_par = 0;  // sweeps since the last list rebuild (selects list/counter buffers)
+    bool solved = false;
     cg_solve_stats st{};
 };
 
 namespace {
-
-constexpr int RING = 256;
-constexpr int U64_SLOTS = 8 + RING;
 
 struct DeviceGuard {
     int prev = -1;
@@ -538,60 +79,68 @@ struct DeviceGuard {
     }
 };
 
-#define CG_CUDA(call)                                                   \
-    do {                                                                \
-        cudaError_t e_ = (call);                                        \
-        if (e_ != cudaSuccess) {                                        \
-            if (getenv("CG_DEBUG"))                                     \
-                fprintf(stderr, "colgraph: %s -> %s (%s:%d)\n", #call,  \
-                        cudaGetErrorString(e_), __FILE__, __LINE__);    \
-            return e_ == cudaErrorMemoryAllocation ? CG_E_NOMEM : CG_E_CUDA; \
-        }                                                               \
+#define CG_CUDA(call)                                                                          \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess) {                                                               \
+            if (getenv("CG_DEBUG"))                                                            \
+                fprintf(stderr, "colgraph: %s -> %s (%s:%d)\n", #call, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                                   \
+            return e_ == cudaErrorMemoryAllocation ? CG_E_NOMEM : CG_E_CUDA;                   \
+        }                                                                                      \
     } while (0)
 
-int grid_for(int64_t n, int block, int cap) {
+inline int grid_for(int64_t n, int block, int cap) {
     int64_t b = (n + block - 1) / block;
     if (b < 1) b = 1;
     return (int)std::min<int64_t>(b, cap);
 }
 
-cg_status sync_read(cg_graph *g) {
-    CG_CUDA(cudaStreamSynchronize(g->stream));
-    return CG_OK;
+inline double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
-// exact global relabel; leaves the active count in h_u64[3]
+inline bool tracing() { return getenv("CG_TRACE") != nullptr; }
+
+// Grid for worklist kernels: enough warps to fill every SM (8 x 256 threads per SM).
+inline int list_grid(const cg_graph *g, int64_t items) { return grid_for(items * 32, 256, g->num_sms * 8); }
+
+// a2/a5: exact global relabel + rebuild of the sweep worklist; h_u64[3] = active count.
 cg_status global_relabel(cg_graph *g) {
     const Geo &geo = g->geo;
-    const int block = 256;
-    const int wpb = block / 32;
-    const size_t shmem = (size_t)wpb * geo.Z * sizeof(int32_t);
-    if (shmem > 200 * 1024) return CG_E_INVAL;
-    const int64_t ncol = (int64_t)geo.X * geo.Y;
-    const int grid_cols = grid_for(ncol * 32, block, g->num_sms * 16);
-    static bool attr_set = false;
-    if (!attr_set && shmem > 48 * 1024) {
-        CG_CUDA(cudaFuncSetAttribute(k_gr_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr_set = true;
+    cudaStream_t st = g->stream;
+    CG_CUDA(cudaMemsetAsync(g->cnt + 4, 0, 3 * sizeof(unsigned), st));
+    k_bfs_init<<<grid_for(geo.n, 256, g->num_sms * 16), 256, 0, st>>>(geo, g->s, g->blist[0], g->cnt + 4);
+    g->st.kernel_launches++;
+    int L = 1;
+    const int grid = list_grid(g, geo.n);
+    for (;;) {
+        for (int b = 0; b < BFS_BATCH; b++, L++) {
+            const int i = L - 1;
+            k_bfs_level<<<grid, 256, 0, st>>>(geo, g->s, L, g->blist[i & 1], g->cnt + 4 + i % 3,
+                                               g->blist[(i + 1) & 1], g->cnt + 4 + (i + 1) % 3,
+                                               g->cnt + 4 + (i + 2) % 3);
+        }
+        g->st.kernel_launches += BFS_BATCH;
+        CG_CUDA(cudaGetLastError());
+        // the frontier the next level would read
+        CG_CUDA(cudaMemcpyAsync(g->h_cnt + 4, g->cnt + 4 + (L - 1) % 3, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                st));
+        CG_CUDA(cudaStreamSynchronize(st));
+        if (g->h_cnt[4] == 0) break;
+        if ((int64_t)L > (int64_t)geo.INF + BFS_BATCH) return CG_E_CUDA;  // every level claims >= 1 vertex
     }
-    k_fill<<<g->num_sms * 8, 256, 0, g->stream>>>(g->s.H, geo.n, geo.INF);
-    for (int pass = 0;; pass++) {
-        CG_CUDA(cudaMemsetAsync(g->d_i32 + 1, 0, sizeof(int), g->stream));
-        k_gr_pass<<<grid_cols, block, shmem, g->stream>>>(geo, g->s, g->d_i32 + 1);
-        g->st.kernel_launches++;
-        CG_CUDA(cudaMemcpyAsync(g->h_i32 + 1, g->d_i32 + 1, sizeof(int), cudaMemcpyDeviceToHost, g->stream));
-        cg_status st = sync_read(g);
-        if (st) return st;
-        g->st.gr_passes++;
-        if (!g->h_i32[1]) break;
-    }
-    CG_CUDA(cudaMemsetAsync(g->d_u64 + 3, 0, sizeof(unsigned long long), g->stream));
-    k_count_active<<<g->num_sms * 8, 256, 0, g->stream>>>(geo, g->s.E, g->s.H, g->d_u64 + 3);
-    g->st.kernel_launches += 2;  // fill + count
-    CG_CUDA(cudaMemcpyAsync(g->h_u64 + 3, g->d_u64 + 3, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                            g->stream));
-    cg_status st = sync_read(g);
-    if (st) return st;
+    g->st.gr_passes += L - 1;
+    // rebuild the active-chunk worklist into clist[0] / cnt[0]
+    CG_CUDA(cudaMemsetAsync(g->cnt, 0, 3 * sizeof(unsigned), st));
+    CG_CUDA(cudaMemsetAsync(g->u64 + 3, 0, sizeof(unsigned long long), st));
+    const int tag = ++g->tag;
+    k_rebuild_chunks<<<grid_for(geo.nchunks, 256, g->num_sms * 16), 256, 0, st>>>(geo, g->s, g->clist[0], g->cnt,
+                                                                                   g->cstamp, tag, g->u64 + 3);
+    g->st.kernel_launches++;
+    g->sweep_par = 0;
+    CG_CUDA(cudaMemcpyAsync(g->h_u64 + 3, g->u64 + 3, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaStreamSynchronize(st));
     CG_CUDA(cudaGetLastError());
     g->st.global_relabels++;
     return CG_OK;
@@ -599,15 +148,37 @@ cg_status global_relabel(cg_graph *g) {
 
 cg_status run_gap(cg_graph *g) {
     const Geo &geo = g->geo;
-    CG_CUDA(cudaMemsetAsync(g->d_hist, 0, sizeof(unsigned) * GAP_BINS, g->stream));
-    CG_CUDA(cudaMemsetAsync(g->d_i32 + 2, 0, sizeof(int), g->stream));
-    k_gap_hist<<<g->num_sms * 8, 256, 0, g->stream>>>(geo, g->s.H, g->d_hist, g->d_i32 + 2);
-    k_gap_find<<<1, 1024, 0, g->stream>>>(g->d_hist, g->d_i32 + 2, g->d_i32 + 3);
-    k_gap_lift<<<g->num_sms * 8, 256, 0, g->stream>>>(geo, g->s.H, g->d_i32 + 3, g->d_u64 + 4);
+    cudaStream_t st = g->stream;
+    CG_CUDA(cudaMemsetAsync(g->hist, 0, sizeof(unsigned) * GAP_BINS, st));
+    CG_CUDA(cudaMemsetAsync(g->flags + 1, 0, sizeof(int), st));
+    k_gap_hist<<<g->num_sms * 8, 256, 0, st>>>(geo, g->s.H, g->hist, g->flags + 1);
+    k_gap_find<<<1, 1024, 0, st>>>(g->hist, g->flags + 1, g->flags + 2);
+    k_gap_lift<<<g->num_sms * 8, 256, 0, st>>>(geo, g->s.H, g->flags + 2, g->u64 + 4);
     CG_CUDA(cudaGetLastError());
     g->st.kernel_launches += 3;
     g->st.gap_runs++;
     return CG_OK;
+}
+
+template <typename T>
+T *carve(char *&p, int64_t count) {
+    T *r = reinterpret_cast<T *>(p);
+    p += ((size_t)count * sizeof(T) + 255) & ~(size_t)255;
+    return r;
+}
+
+size_t workspace_bytes(const Geo &geo) {
+    const int64_t ncol = (int64_t)geo.X * geo.Y;
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    size_t b = 0;
+    b += al(sizeof(int32_t) * 8 * geo.n);
+    b += 2 * al(sizeof(int) * geo.n);
+    b += 3 * al(sizeof(int) * geo.nchunks);
+    b += 5 * al(sizeof(int) * ncol);
+    b += al(sizeof(unsigned) * GAP_BINS);
+    b += al(sizeof(unsigned) * 16) + al(sizeof(unsigned long long) * RING) + al(sizeof(unsigned long long) * 16) +
+         al(sizeof(int) * 16);
+    return b;
 }
 
 }  // namespace
@@ -629,7 +200,10 @@ const char *cg_status_str(cg_status s) {
     return "CG_E_UNKNOWN";
 }
 
-const char *cg_version(void) { return "colgraph 0.1 sm_100a (lock-free push-relabel, column-scan global relabel)"; }
+const char *cg_version(void) {
+    return "colgraph 0.2 sm_100a (chunk-worklist lock-free push-relabel, frontier-BFS global relabel, "
+           "worklist extraction)";
+}
 
 cg_status cg_slab_range(const cg_dims *dims, int32_t rank, int32_t nranks, int32_t *x0, int32_t *x1) {
     if (!dims || !x0 || !x1 || nranks < 1 || rank < 0 || rank >= nranks || dims->X < nranks) return CG_E_INVAL;
@@ -643,13 +217,13 @@ void colgraph_free(cg_graph *g) {
     if (!g) return;
     {
         DeviceGuard dg(g->dist.device);
-        cudaFree(g->soa);
-        cudaFree(g->d_u64);
-        cudaFree(g->d_i32);
-        cudaFree(g->d_hist);
-        cudaFree(g->d_top);
+        if (g->ws) cudaFreeAsync(g->ws, g->stream);
+        if (g->ev0) cudaEventDestroy(g->ev0);
+        if (g->ev1) cudaEventDestroy(g->ev1);
+        cudaFreeHost(g->h_cnt);
+        cudaFreeHost(g->h_work);
         cudaFreeHost(g->h_u64);
-        cudaFreeHost(g->h_i32);
+        cudaFreeHost(g->h_flags);
     }
     delete g;
 }
@@ -660,12 +234,12 @@ cg_status colgraph_build(const cg_dims *dims, const int32_t *cost_dev, int32_t i
     *out = nullptr;
     if (dims->X < 1 || dims->Y < 1 || dims->Z < 1 || dims->delta < 0) return CG_E_INVAL;
     const int64_t n = (int64_t)dims->X * dims->Y * dims->Z;
-    if (n + dims->Z + 2 >= (int64_t)INT_MAX) return CG_E_INVAL;
+    if (n + dims->Z + 64 >= (int64_t)INT_MAX) return CG_E_INVAL;
     cg_dist dd{0, 1, nullptr, 0, nullptr};
     if (dist) dd = *dist;
-    if (dd.nranks != 1 || dd.rank != 0) return CG_E_INVAL;  // multi-GPU: see colgraph_mgpu (not in this build)
+    if (dd.nranks != 1 || dd.rank != 0) return CG_E_INVAL;  // multi-GPU x-slabs: not in this build
     DeviceGuard dg(dd.device);
-    auto t0 = std::chrono::steady_clock::now();
+    const double t0 = now_ms();
     cg_graph *g = new cg_graph();
     g->dims = *dims;
     g->dist = dd;
@@ -676,45 +250,78 @@ cg_status colgraph_build(const cg_dims *dims, const int32_t *cost_dev, int32_t i
     geo.Y = dims->Y;
     geo.Z = dims->Z;
     geo.delta = dims->delta;
+    geo.CPC = (dims->Z + 31) / 32;
     geo.n = n;
     geo.YZ = (int64_t)dims->Y * dims->Z;
+    geo.nchunks = (int64_t)dims->X * dims->Y * geo.CPC;
     geo.INF = (int32_t)(n + 1);
     auto fail = [&](cg_status st) {
         colgraph_free(g);
         return st;
     };
-    if (cudaMalloc(&g->soa, sizeof(int32_t) * 8 * n) != cudaSuccess) return fail(CG_E_NOMEM);
-    if (cudaMalloc(&g->d_u64, sizeof(unsigned long long) * U64_SLOTS) != cudaSuccess) return fail(CG_E_NOMEM);
-    if (cudaMalloc(&g->d_i32, sizeof(int) * 16) != cudaSuccess) return fail(CG_E_NOMEM);
-    if (cudaMalloc(&g->d_hist, sizeof(unsigned) * GAP_BINS) != cudaSuccess) return fail(CG_E_NOMEM);
-    if (cudaMalloc(&g->d_top, sizeof(int32_t) * dims->X * dims->Y) != cudaSuccess) return fail(CG_E_NOMEM);
-    if (cudaHostAlloc(&g->h_u64, sizeof(unsigned long long) * U64_SLOTS, cudaHostAllocDefault) != cudaSuccess)
-        return fail(CG_E_NOMEM);
-    if (cudaHostAlloc(&g->h_i32, sizeof(int) * 16, cudaHostAllocDefault) != cudaSuccess) return fail(CG_E_NOMEM);
-    g->s.E = g->soa;
-    g->s.H = g->soa + n;
-    g->s.T = g->soa + 2 * n;
-    g->s.D = g->soa + 3 * n;
-    g->s.L = g->soa + 4 * n;
     cudaStream_t st = g->stream;
-    if (cudaMemsetAsync(g->d_u64, 0, sizeof(unsigned long long) * U64_SLOTS, st) != cudaSuccess ||
-        cudaMemsetAsync(g->d_i32, 0, sizeof(int) * 16, st) != cudaSuccess ||
-        cudaMemsetAsync(g->s.H, 0, sizeof(int32_t) * n, st) != cudaSuccess ||
-        cudaMemsetAsync(g->s.D, 0, sizeof(int32_t) * 5 * n, st) != cudaSuccess)
+    {  // keep freed workspaces cached in the stream-ordered pool (repeated solves allocate for free)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dd.device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
+    g->ws_bytes = workspace_bytes(geo);
+    if (cudaMallocAsync(&g->ws, g->ws_bytes, st) != cudaSuccess) {
+        g->ws = nullptr;
+        return fail(CG_E_NOMEM);
+    }
+    if (cudaHostAlloc(&g->h_cnt, sizeof(unsigned) * 16, cudaHostAllocDefault) != cudaSuccess ||
+        cudaHostAlloc(&g->h_work, sizeof(unsigned long long) * RING, cudaHostAllocDefault) != cudaSuccess ||
+        cudaHostAlloc(&g->h_u64, sizeof(unsigned long long) * 16, cudaHostAllocDefault) != cudaSuccess ||
+        cudaHostAlloc(&g->h_flags, sizeof(int) * 16, cudaHostAllocDefault) != cudaSuccess)
+        return fail(CG_E_NOMEM);
+    if (cudaEventCreate(&g->ev0) != cudaSuccess || cudaEventCreate(&g->ev1) != cudaSuccess) return fail(CG_E_CUDA);
+    const int64_t ncol = (int64_t)geo.X * geo.Y;
+    char *p = g->ws;
+    int32_t *soa = carve<int32_t>(p, 8 * n);
+    g->s.E = soa;
+    g->s.H = soa + n;
+    g->s.T = soa + 2 * n;
+    g->s.D = soa + 3 * n;
+    g->s.L = soa + 4 * n;
+    g->blist[0] = carve<int>(p, n);
+    g->blist[1] = carve<int>(p, n);
+    g->clist[0] = carve<int>(p, geo.nchunks);
+    g->clist[1] = carve<int>(p, geo.nchunks);
+    g->cstamp = carve<int>(p, geo.nchunks);
+    g->top = carve<int32_t>(p, ncol);
+    g->proc = carve<int32_t>(p, ncol);
+    g->colstamp = carve<int>(p, ncol);
+    g->collist[0] = carve<int>(p, ncol);
+    g->collist[1] = carve<int>(p, ncol);
+    g->hist = carve<unsigned>(p, GAP_BINS);
+    g->cnt = carve<unsigned>(p, 16);
+    g->work = carve<unsigned long long>(p, RING);
+    g->u64 = carve<unsigned long long>(p, 16);
+    g->flags = carve<int>(p, 16);
+    if (cudaMemsetAsync(g->s.H, 0, sizeof(int32_t) * n, st) != cudaSuccess ||
+        cudaMemsetAsync(g->s.D, 0, sizeof(int32_t) * 5 * n, st) != cudaSuccess ||
+        cudaMemsetAsync(g->cstamp, 0, sizeof(int) * geo.nchunks, st) != cudaSuccess ||
+        cudaMemsetAsync(g->colstamp, 0, sizeof(int) * ncol, st) != cudaSuccess ||
+        cudaMemsetAsync(g->cnt, 0, sizeof(unsigned) * 16, st) != cudaSuccess ||
+        cudaMemsetAsync(g->u64, 0, sizeof(unsigned long long) * 16, st) != cudaSuccess ||
+        cudaMemsetAsync(g->flags, 0, sizeof(int) * 16, st) != cudaSuccess)
         return fail(CG_E_CUDA);
-    const int64_t ncol = (int64_t)dims->X * dims->Y;
     k_build<<<grid_for(ncol * 32, 256, g->num_sms * 16), 256, 0, st>>>(geo, cost_dev, input_is_weight ? 1 : 0, g->s,
-                                                                       g->d_u64, g->d_i32);
+                                                                       g->u64, g->flags);
     if (cudaGetLastError() != cudaSuccess) return fail(CG_E_CUDA);
-    cudaMemcpyAsync(g->h_u64, g->d_u64, sizeof(unsigned long long) * 2, cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(g->h_i32, g->d_i32, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(g->h_u64, g->u64, sizeof(unsigned long long) * 2, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(g->h_flags, g->flags, sizeof(int), cudaMemcpyDeviceToHost, st);
     if (cudaStreamSynchronize(st) != cudaSuccess) return fail(CG_E_CUDA);
-    if (g->h_i32[0] & FLAG_OVERFLOW) return fail(CG_E_OVERFLOW);
+    if (g->h_flags[0] & FLAG_OVERFLOW) return fail(CG_E_OVERFLOW);
     g->N = (int64_t)g->h_u64[0];
     g->sumT0 = (int64_t)g->h_u64[1];
     g->st.source_capacity = g->N;
     g->st.bytes_per_sweep_alg = 32.0 * (double)n;
-    g->st.ms_build = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    g->st.kernel_launches = 1;
+    g->st.ms_build = now_ms() - t0;
     *out = g;
     return CG_OK;
 }
@@ -725,70 +332,79 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
     DeviceGuard dg(g->dist.device);
     cg_solve_opts o{1.0f, 0, 16, (int64_t)1 << 30, 1};
     if (opts) o = *opts;
-    if (o.check_every < 1) o.check_every = 1;
-    if (o.check_every > RING) o.check_every = RING;
-    if (o.ops_per_sweep < 1) o.ops_per_sweep = 1;
-    if (o.gr_factor <= 0.f) o.gr_factor = 1.0f;
+    o.check_every = std::max(1, std::min(o.check_every, RING));
+    o.ops_per_sweep = std::max(1, o.ops_per_sweep);
+    if (!(o.gr_factor > 0.f)) o.gr_factor = 1.0f;
     const Geo &geo = g->geo;
     cudaStream_t st = g->stream;
-    auto t0 = std::chrono::steady_clock::now();
-    double ms_gr = 0.0;
+    const bool trace = tracing();
+    const double t0 = now_ms();
+    double ms_gr = 0.0, last_gr_ms = 0.0;
     auto timed_gr = [&]() {
-        auto a = std::chrono::steady_clock::now();
-        cg_status s = global_relabel(g);
-        ms_gr += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+        const double a = now_ms();
+        const int64_t p0 = g->st.gr_passes;
+        const cg_status s = global_relabel(g);
+        last_gr_ms = now_ms() - a;
+        ms_gr += last_gr_ms;
+        if (trace)
+            fprintf(stderr, "[cg] GR#%lld levels=%lld active=%llu ms=%.3f (sweeps %lld)\n",
+                    (long long)g->st.global_relabels, (long long)(g->st.gr_passes - p0), g->h_u64[3], last_gr_ms,
+                    (long long)g->st.sweeps);
         return s;
     };
     cg_status rs = timed_gr();
     if (rs) return rs;
     int64_t active = (int64_t)g->h_u64[3];
     const double gr_budget = (double)o.gr_factor * (double)geo.n;
-    double work_since_gr = 0.0;
-    const int block = 256;
-    const int grid = grid_for(geo.n, block, INT_MAX);
+    double work_since_gr = 0.0, sweep_ms_since_gr = 0.0;
     int64_t sweeps = 0, since_gap = 0;
+    const int grid = list_grid(g, geo.nchunks);
     cg_status result = CG_OK;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    CG_CUDA(cudaEventCreate(&ev0));
-    CG_CUDA(cudaEventCreate(&ev1));
     while (active > 0) {
         if (sweeps >= o.max_sweeps) { result = CG_E_NOT_CONVERGED; break; }
         const int batch = (int)std::min<int64_t>(o.check_every, o.max_sweeps - sweeps);
-        CG_CUDA(cudaMemsetAsync(g->d_u64 + 8, 0, sizeof(unsigned long long) * batch, st));
-        CG_CUDA(cudaEventRecord(ev0, st));
-        for (int i = 0; i < batch; i++)
-            k_sweep<<<grid, block, 0, st>>>(geo, g->s, o.ops_per_sweep, g->d_u64 + 8 + i, g->d_i32);
-        CG_CUDA(cudaEventRecord(ev1, st));
+        CG_CUDA(cudaMemsetAsync(g->work, 0, sizeof(unsigned long long) * batch, st));
+        CG_CUDA(cudaEventRecord(g->ev0, st));
+        for (int i = 0; i < batch; i++) {
+            const int k = g->sweep_par++;
+            k_sweep<<<grid, 256, 0, st>>>(geo, g->s, o.ops_per_sweep, g->clist[k & 1], g->cnt + k % 3,
+                                          g->clist[(k + 1) & 1], g->cnt + (k + 1) % 3, g->cnt + (k + 2) % 3,
+                                          g->cstamp, ++g->tag, g->work + i, g->flags);
+        }
+        CG_CUDA(cudaEventRecord(g->ev1, st));
         g->st.kernel_launches += batch;
         CG_CUDA(cudaGetLastError());
-        CG_CUDA(cudaMemcpyAsync(g->h_u64 + 8, g->d_u64 + 8, sizeof(unsigned long long) * batch,
-                                cudaMemcpyDeviceToHost, st));
-        CG_CUDA(cudaMemcpyAsync(g->h_i32, g->d_i32, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CG_CUDA(cudaMemcpyAsync(g->h_work, g->work, sizeof(unsigned long long) * batch, cudaMemcpyDeviceToHost, st));
+        CG_CUDA(cudaMemcpyAsync(g->h_flags, g->flags, sizeof(int), cudaMemcpyDeviceToHost, st));
         CG_CUDA(cudaStreamSynchronize(st));
         float ms = 0.f;
-        cudaEventElapsedTime(&ms, ev0, ev1);
+        cudaEventElapsedTime(&ms, g->ev0, g->ev1);
         g->st.ms_sweep_kernels += ms;
-        if (g->h_i32[0] & FLAG_OVERFLOW) { result = CG_E_OVERFLOW; break; }
+        sweep_ms_since_gr += ms;
+        if (g->h_flags[0] & FLAG_OVERFLOW) { result = CG_E_OVERFLOW; break; }
+        if (trace) {
+            fprintf(stderr, "[cg] sweeps %lld..%lld active:", (long long)sweeps, (long long)(sweeps + batch - 1));
+            for (int i = 0; i < batch; i += std::max(1, batch / 8)) fprintf(stderr, " %llu", g->h_work[i]);
+            fprintf(stderr, " | %.3f ms\n", ms);
+        }
         bool quiescent = false;
-        int done = 0;
         for (int i = 0; i < batch; i++) {
-            const unsigned long long c = g->h_u64[8 + i];
-            g->st.sweep_bytes_alg += 4.0 * (double)geo.n + 40.0 * (double)c;
+            const unsigned long long c = g->h_work[i];
+            g->st.sweep_bytes_alg += 44.0 * (double)c;  // 32 B state read + 12 B push writes
             if (c == 0) { quiescent = true; break; }
             work_since_gr += (double)c;
             g->st.work += (int64_t)c;
-            done++;
         }
-        // sweeps after the first idle one in a batch are no-ops (nothing is active)
-        for (int i = done + 1; i < batch && quiescent; i++) g->st.sweep_bytes_alg += 4.0 * (double)geo.n;
         sweeps += batch;
         since_gap += batch;
-        if (quiescent || work_since_gr >= gr_budget) {
+        g->st.sweeps = sweeps;
+        if (quiescent || work_since_gr >= gr_budget || sweep_ms_since_gr >= std::max(last_gr_ms, 0.05)) {
             // a4: termination is decided only after an exact global relabel
             rs = timed_gr();
             if (rs) { result = rs; break; }
             active = (int64_t)g->h_u64[3];
             work_since_gr = 0.0;
+            sweep_ms_since_gr = 0.0;
             since_gap = 0;
         } else if (o.gap_every > 0 && since_gap >= o.gap_every) {
             rs = run_gap(g);
@@ -796,22 +412,18 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
             since_gap = 0;
         }
     }
-    cudaEventDestroy(ev0);
-    cudaEventDestroy(ev1);
     if (result != CG_OK && result != CG_E_NOT_CONVERGED) return result;
     // a6: |f| = sum(T0) - sum(T)
-    CG_CUDA(cudaMemsetAsync(g->d_u64 + 2, 0, sizeof(unsigned long long), st));
-    k_sum_T<<<g->num_sms * 8, 256, 0, st>>>(geo, g->s.T, g->d_u64 + 2);
+    CG_CUDA(cudaMemsetAsync(g->u64 + 2, 0, sizeof(unsigned long long), st));
+    k_sum_T<<<g->num_sms * 8, 256, 0, st>>>(geo, g->s.T, g->u64 + 2);
     g->st.kernel_launches++;
-    CG_CUDA(cudaMemcpyAsync(g->h_u64 + 2, g->d_u64 + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    CG_CUDA(cudaMemcpyAsync(g->h_u64 + 4, g->d_u64 + 4, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaMemcpyAsync(g->h_u64 + 2, g->u64 + 2, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CG_CUDA(cudaStreamSynchronize(st));
     CG_CUDA(cudaGetLastError());
     *flow_value = g->sumT0 - (int64_t)g->h_u64[2];
-    g->st.sweeps = sweeps;
     g->st.gap_lifted = (int64_t)g->h_u64[4];
     g->st.ms_global_relabel = ms_gr;
-    g->st.ms_solve = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    g->st.ms_solve = now_ms() - t0;
     g->st.ms_sweeps = g->st.ms_solve - ms_gr;
     g->solved = true;
     if (stats) *stats = g->st;
@@ -824,27 +436,36 @@ cg_status mincut_extract_surface(cg_graph *g, int32_t *surface_dev, uint8_t *mas
     DeviceGuard dg(g->dist.device);
     const Geo &geo = g->geo;
     cudaStream_t st = g->stream;
-    auto t0 = std::chrono::steady_clock::now();
+    const double t0 = now_ms();
     const int64_t ncol = (int64_t)geo.X * geo.Y;
-    const int grid_cols = grid_for(ncol * 32, 256, g->num_sms * 16);
-    k_ext_seed<<<grid_cols, 256, 0, st>>>(geo, g->s, g->d_top);
+    CG_CUDA(cudaMemsetAsync(g->cnt + 8, 0, 3 * sizeof(unsigned), st));
+    const int tag = ++g->tag;
+    k_ext_seed<<<grid_for(ncol, 256, g->num_sms * 16), 256, 0, st>>>(geo, g->s, g->top, g->proc, g->collist[0],
+                                                                      g->cnt + 8, g->colstamp, tag);
+    g->st.kernel_launches++;
+    const int grid = list_grid(g, ncol);
+    int r = 0;
     for (;;) {
-        CG_CUDA(cudaMemsetAsync(g->d_i32 + 1, 0, sizeof(int), st));
-        k_ext_pass<<<grid_cols, 256, 0, st>>>(geo, g->s, g->d_top, g->d_i32 + 1);
-        g->st.kernel_launches++;
-        CG_CUDA(cudaMemcpyAsync(g->h_i32 + 1, g->d_i32 + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+        for (int b = 0; b < EXT_BATCH; b++, r++) {
+            k_ext_round<<<grid, 256, 0, st>>>(geo, g->s, g->collist[r & 1], g->cnt + 8 + r % 3,
+                                               g->collist[(r + 1) & 1], g->cnt + 8 + (r + 1) % 3,
+                                               g->cnt + 8 + (r + 2) % 3, g->top, g->proc, g->colstamp, ++g->tag);
+        }
+        g->st.kernel_launches += EXT_BATCH;
+        CG_CUDA(cudaGetLastError());
+        CG_CUDA(cudaMemcpyAsync(g->h_cnt + 8, g->cnt + 8 + r % 3, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         CG_CUDA(cudaStreamSynchronize(st));
-        g->st.extract_passes++;
-        if (!g->h_i32[1]) break;
+        if (g->h_cnt[8] == 0) break;
     }
-    CG_CUDA(cudaMemsetAsync(g->d_i32 + 4, 0, sizeof(int), st));
-    k_ext_out<<<g->num_sms * 8, 256, 0, st>>>(geo, g->d_top, surface_dev, mask_dev, g->d_i32 + 4);
-    g->st.kernel_launches += 2;  // seed + out
-    CG_CUDA(cudaMemcpyAsync(g->h_i32 + 4, g->d_i32 + 4, sizeof(int), cudaMemcpyDeviceToHost, st));
+    g->st.extract_passes += r;
+    CG_CUDA(cudaMemsetAsync(g->flags + 3, 0, sizeof(int), st));
+    k_ext_out<<<g->num_sms * 8, 256, 0, st>>>(geo, g->top, surface_dev, mask_dev, g->flags + 3);
+    g->st.kernel_launches++;
+    CG_CUDA(cudaMemcpyAsync(g->h_flags + 3, g->flags + 3, sizeof(int), cudaMemcpyDeviceToHost, st));
     CG_CUDA(cudaStreamSynchronize(st));
     CG_CUDA(cudaGetLastError());
-    g->st.ms_extract = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    return g->h_i32[4] ? CG_E_EMPTY_COLUMN : CG_OK;
+    g->st.ms_extract = now_ms() - t0;
+    return g->h_flags[3] ? CG_E_EMPTY_COLUMN : CG_OK;
 }
 
 cg_status colgraph_stats(const cg_graph *g, cg_solve_stats *stats) {
@@ -856,7 +477,7 @@ cg_status colgraph_stats(const cg_graph *g, cg_solve_stats *stats) {
 cg_status colgraph_export_state(cg_graph *g, int32_t *out_dev) {
     if (!g || !out_dev) return CG_E_INVAL;
     DeviceGuard dg(g->dist.device);
-    CG_CUDA(cudaMemcpyAsync(out_dev, g->soa, sizeof(int32_t) * 8 * g->geo.n, cudaMemcpyDeviceToDevice, g->stream));
+    CG_CUDA(cudaMemcpyAsync(out_dev, g->s.E, sizeof(int32_t) * 8 * g->geo.n, cudaMemcpyDeviceToDevice, g->stream));
     CG_CUDA(cudaStreamSynchronize(g->stream));
     return CG_OK;
 }
@@ -868,6 +489,7 @@ cg_status colgraph_solve_host(const cg_dims *dims, const int32_t *cost_host, int
     if (dims->X < 1 || dims->Y < 1 || dims->Z < 1) return CG_E_INVAL;
     cg_dist dd{0, 1, nullptr, 0, nullptr};
     if (dist) dd = *dist;
+    if (dd.nranks != 1) return CG_E_INVAL;
     DeviceGuard dg(dd.device);
     cudaStream_t st = (cudaStream_t)dd.stream;
     const int64_t n = (int64_t)dims->X * dims->Y * dims->Z, ncol = (int64_t)dims->X * dims->Y;

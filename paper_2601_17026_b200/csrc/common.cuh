@@ -1,0 +1,99 @@
+// common.cuh -- geometry, SoA layout and warp utilities shared by the colgraph kernels.
+//
+// Implicit addressing (§3.2.3): vertex (x,y,z) of this rank's
+// slab has index v = (x*Y + y)*Z + z, z fastest.  A "chunk" is 32 consecutive z
+// of one column -- the unit a warp processes (lane = z offset), so every state
+// load of a chunk is one coalesced 128-byte line.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+
+namespace cg {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+struct Geo {
+    int32_t X, Y, Z, delta;  // X = x-planes owned by this rank
+    int32_t CPC;             // chunks per column = ceil(Z / 32)
+    int64_t n;               // vertices owned by this rank
+    int64_t YZ;              // vertices per x-plane
+    int64_t nchunks;         // X*Y*CPC
+    int32_t INF;             // n_global + 1: "cannot reach t"
+};
+
+// 8 int32 planes of n: E excess, H height, T sink residual, D flow on the down arc
+// (= residual of the up arc into this vertex from below), L[d] flow on the lateral arc in
+// direction d (= residual of its reverse arc).  Directions: 0:+x 1:-x 2:+y 3:-y.
+struct Soa {
+    int32_t *E, *H, *T, *D, *L;  // L + d*n
+};
+
+enum { FLAG_OVERFLOW = 1 };
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ unsigned lanemask_lt() { return (1u << lane_id()) - 1u; }
+__device__ __forceinline__ int64_t gwarp() { return ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; }
+__device__ __forceinline__ int64_t nwarps() { return ((int64_t)gridDim.x * blockDim.x) >> 5; }
+
+// "Minimal" arc set (R2): lateral arc (x,y,z) -> (nbr, zo(z)); the unique
+// lateral in-arc of (x,y,z) per direction comes from (nbr, zi(z)).
+__device__ __forceinline__ int zo_of(int z, int delta) { return z == 0 ? 0 : (z > delta ? z - delta : -1); }
+__device__ __forceinline__ int zi_of(int z, int delta, int Z) { return z == 0 ? 0 : (z + delta < Z ? z + delta : -1); }
+
+// neighbour column offset (in vertices) in direction d, 0 if the neighbour is outside the slab
+__device__ __forceinline__ int64_t nbr_off(const Geo &g, int x, int y, int d) {
+    switch (d) {
+        case 0: return x + 1 < g.X ? g.YZ : 0;
+        case 1: return x >= 1 ? -g.YZ : 0;
+        case 2: return y + 1 < g.Y ? (int64_t)g.Z : 0;
+        default: return y >= 1 ? -(int64_t)g.Z : 0;
+    }
+}
+
+__device__ __forceinline__ int warp_sum_i(int v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+__device__ __forceinline__ int warp_max_i(int v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
+    return v;
+}
+__device__ __forceinline__ int warp_incl_scan(int v) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(FULL, v, o);
+        if (lane_id() >= o) v += t;
+    }
+    return v;
+}
+
+// Warp-aggregated append of one optional item per lane: one atomic per warp.
+__device__ __forceinline__ void warp_append(bool has, int item, int *list, unsigned *count) {
+    const unsigned m = __ballot_sync(FULL, has);
+    if (!m) return;
+    unsigned base = 0;
+    if (lane_id() == 0) base = atomicAdd(count, (unsigned)__popc(m));
+    base = __shfl_sync(FULL, base, 0);
+    if (has) list[base + __popc(m & lanemask_lt())] = item;
+}
+
+// Mark a chunk / column id (or -1) for the next worklist, de-duplicated inside the warp
+// (__match_any_sync) and across warps (stamp[id] == tag means "already listed").
+__device__ __forceinline__ void warp_mark(int id, int *stamp, int tag, int *list, unsigned *count) {
+    const unsigned peers = __match_any_sync(FULL, id);
+    bool add = id >= 0 && (__ffs(peers) - 1) == lane_id();
+    if (add) add = (stamp[id] != tag) && (atomicExch(&stamp[id], tag) != tag);
+    warp_append(add, id, list, count);
+}
+
+}  // namespace cg
