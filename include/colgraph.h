@@ -85,13 +85,16 @@ typedef struct {
  *                 (0 = never); default 0
  *   check_every : sweeps between host reads of the active-vertex count; default 16
  *   max_sweeps  : give up with CG_E_NOT_CONVERGED after this many sweeps; default 1<<30
- *   ops_per_sweep : push/relabel operations a vertex may perform per sweep; default 1 */
+ *   ops_per_sweep : push/relabel operations a vertex may perform per sweep; default 1
+ *   walk_len    : > 0 selects multi-hop sweeps: a vertex's excess follows admissible arcs
+ *                 for up to walk_len hops per launch; 0 = library default, -1 = single hop */
 typedef struct {
     float gr_factor;
     int32_t gap_every;
     int32_t check_every;
     int64_t max_sweeps;
     int32_t ops_per_sweep;
+    int32_t walk_len;
 } cg_solve_opts;
 
 typedef struct {

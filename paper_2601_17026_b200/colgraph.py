@@ -38,7 +38,7 @@ class cg_dist(ctypes.Structure):
 
 class cg_solve_opts(ctypes.Structure):
     _fields_ = [("gr_factor", ctypes.c_float), ("gap_every", ctypes.c_int32), ("check_every", ctypes.c_int32),
-                ("max_sweeps", ctypes.c_int64), ("ops_per_sweep", ctypes.c_int32)]
+                ("max_sweeps", ctypes.c_int64), ("ops_per_sweep", ctypes.c_int32), ("walk_len", ctypes.c_int32)]
 
 
 class cg_solve_stats(ctypes.Structure):
@@ -98,8 +98,10 @@ def version() -> str:
     return _lib.cg_version().decode()
 
 
-def make_opts(gr_factor=1.0, gap_every=0, check_every=16, max_sweeps=1 << 30, ops_per_sweep=1) -> cg_solve_opts:
-    return cg_solve_opts(float(gr_factor), int(gap_every), int(check_every), int(max_sweeps), int(ops_per_sweep))
+def make_opts(gr_factor=1.0, gap_every=0, check_every=16, max_sweeps=1 << 30, ops_per_sweep=1,
+              walk_len=0) -> cg_solve_opts:
+    return cg_solve_opts(float(gr_factor), int(gap_every), int(check_every), int(max_sweeps), int(ops_per_sweep),
+                         int(walk_len))
 
 
 def _dist(device=0, stream=None, rank=0, nranks=1, nccl_id=None) -> cg_dist:

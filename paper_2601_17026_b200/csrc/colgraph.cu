@@ -44,6 +44,8 @@ struct cg_graph {
     int *blist[2] = {nullptr, nullptr};  // BFS frontiers (vertices)
     int *clist[2] = {nullptr, nullptr};  // sweep worklists (chunks)
     int *cstamp = nullptr;               // per-chunk list tag
+    int *vstamp = nullptr;               // per-vertex list tag
+    bool vertex_lists = true;            // sweep worklist granularity (CG_CHUNK_LISTS=1: chunks)
     int32_t *top = nullptr, *proc = nullptr;
     int *colstamp = nullptr;
     int *collist[2] = {nullptr, nullptr};
@@ -135,8 +137,12 @@ cg_status global_relabel(cg_graph *g) {
     CG_CUDA(cudaMemsetAsync(g->cnt, 0, 3 * sizeof(unsigned), st));
     CG_CUDA(cudaMemsetAsync(g->u64 + 3, 0, sizeof(unsigned long long), st));
     const int tag = ++g->tag;
-    k_rebuild_chunks<<<grid_for(geo.nchunks, 256, g->num_sms * 16), 256, 0, st>>>(geo, g->s, g->clist[0], g->cnt,
-                                                                                   g->cstamp, tag, g->u64 + 3);
+    if (g->vertex_lists)
+        k_rebuild_vertices<<<grid_for(geo.n, 256, g->num_sms * 16), 256, 0, st>>>(geo, g->s, g->blist[0], g->cnt,
+                                                                                  g->vstamp, tag, g->u64 + 3);
+    else
+        k_rebuild_chunks<<<grid_for(geo.nchunks, 256, g->num_sms * 16), 256, 0, st>>>(
+            geo, g->s, g->clist[0], g->cnt, g->cstamp, tag, g->u64 + 3);
     g->st.kernel_launches++;
     g->sweep_par = 0;
     CG_CUDA(cudaMemcpyAsync(g->h_u64 + 3, g->u64 + 3, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -174,6 +180,7 @@ size_t workspace_bytes(const Geo &geo) {
     b += al(sizeof(int32_t) * 8 * geo.n);
     b += 2 * al(sizeof(int) * geo.n);
     b += 3 * al(sizeof(int) * geo.nchunks);
+    b += al(sizeof(int) * geo.n);
     b += 5 * al(sizeof(int) * ncol);
     b += al(sizeof(unsigned) * GAP_BINS);
     b += al(sizeof(unsigned) * 16) + al(sizeof(unsigned long long) * RING) + al(sizeof(unsigned long long) * 16) +
@@ -291,6 +298,8 @@ cg_status colgraph_build(const cg_dims *dims, const int32_t *cost_dev, int32_t i
     g->clist[0] = carve<int>(p, geo.nchunks);
     g->clist[1] = carve<int>(p, geo.nchunks);
     g->cstamp = carve<int>(p, geo.nchunks);
+    g->vstamp = carve<int>(p, n);
+    g->vertex_lists = getenv("CG_CHUNK_LISTS") == nullptr;
     g->top = carve<int32_t>(p, ncol);
     g->proc = carve<int32_t>(p, ncol);
     g->colstamp = carve<int>(p, ncol);
@@ -304,6 +313,7 @@ cg_status colgraph_build(const cg_dims *dims, const int32_t *cost_dev, int32_t i
     if (cudaMemsetAsync(g->s.H, 0, sizeof(int32_t) * n, st) != cudaSuccess ||
         cudaMemsetAsync(g->s.D, 0, sizeof(int32_t) * 5 * n, st) != cudaSuccess ||
         cudaMemsetAsync(g->cstamp, 0, sizeof(int) * geo.nchunks, st) != cudaSuccess ||
+        cudaMemsetAsync(g->vstamp, 0, sizeof(int) * n, st) != cudaSuccess ||
         cudaMemsetAsync(g->colstamp, 0, sizeof(int) * ncol, st) != cudaSuccess ||
         cudaMemsetAsync(g->cnt, 0, sizeof(unsigned) * 16, st) != cudaSuccess ||
         cudaMemsetAsync(g->u64, 0, sizeof(unsigned long long) * 16, st) != cudaSuccess ||
@@ -330,8 +340,9 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
     if (!g || !flow_value) return CG_E_INVAL;
     if (g->solved) return CG_E_STATE;
     DeviceGuard dg(g->dist.device);
-    cg_solve_opts o{1.0f, 0, 16, (int64_t)1 << 30, 1};
+    cg_solve_opts o{1.0f, 0, 16, (int64_t)1 << 30, 1, 0};
     if (opts) o = *opts;
+    if (o.walk_len == 0) o.walk_len = getenv("CG_WALK") ? atoi(getenv("CG_WALK")) : 64;  // library default
     o.check_every = std::max(1, std::min(o.check_every, RING));
     o.ops_per_sweep = std::max(1, o.ops_per_sweep);
     if (!(o.gr_factor > 0.f)) o.gr_factor = 1.0f;
@@ -346,10 +357,16 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
         const cg_status s = global_relabel(g);
         last_gr_ms = now_ms() - a;
         ms_gr += last_gr_ms;
-        if (trace)
-            fprintf(stderr, "[cg] GR#%lld levels=%lld active=%llu ms=%.3f (sweeps %lld)\n",
+        if (trace) {
+            // diagnostics only: current flow into t and total excess on active vertices
+            cudaMemsetAsync(g->u64 + 2, 0, sizeof(unsigned long long), st);
+            k_sum_T<<<g->num_sms * 8, 256, 0, st>>>(geo, g->s.T, g->u64 + 2);
+            cudaMemcpyAsync(g->h_u64 + 2, g->u64 + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            fprintf(stderr, "[cg] GR#%lld levels=%lld active=%llu ms=%.3f (sweeps %lld) flow=%lld\n",
                     (long long)g->st.global_relabels, (long long)(g->st.gr_passes - p0), g->h_u64[3], last_gr_ms,
-                    (long long)g->st.sweeps);
+                    (long long)g->st.sweeps, (long long)(g->sumT0 - (int64_t)g->h_u64[2]));
+        }
         return s;
     };
     cg_status rs = timed_gr();
@@ -359,17 +376,33 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
     double work_since_gr = 0.0, sweep_ms_since_gr = 0.0;
     int64_t sweeps = 0, since_gap = 0;
     const int grid = list_grid(g, geo.nchunks);
+    const int gridv = list_grid(g, (geo.n + 31) / 32);
+    const double walk_min = getenv("CG_WALK_MIN") ? atof(getenv("CG_WALK_MIN")) : 1e-3;
+    int64_t last_active = active;
     cg_status result = CG_OK;
     while (active > 0) {
         if (sweeps >= o.max_sweeps) { result = CG_E_NOT_CONVERGED; break; }
         const int batch = (int)std::min<int64_t>(o.check_every, o.max_sweeps - sweeps);
         CG_CUDA(cudaMemsetAsync(g->work, 0, sizeof(unsigned long long) * batch, st));
         CG_CUDA(cudaEventRecord(g->ev0, st));
+        // multi-hop walks while many vertices are active; single hops in the sparse tail
+        const bool walk = o.walk_len > 0 && (double)last_active >= walk_min * (double)geo.n;
+        // size the grid for the current worklist (the kernels stride, so growth is safe)
+        const int gv = std::max(g->num_sms, std::min(gridv, grid_for(2 * last_active, 256, gridv)));
         for (int i = 0; i < batch; i++) {
             const int k = g->sweep_par++;
-            k_sweep<<<grid, 256, 0, st>>>(geo, g->s, o.ops_per_sweep, g->clist[k & 1], g->cnt + k % 3,
-                                          g->clist[(k + 1) & 1], g->cnt + (k + 1) % 3, g->cnt + (k + 2) % 3,
-                                          g->cstamp, ++g->tag, g->work + i, g->flags);
+            if (walk)
+                k_walk<<<gv, 256, 0, st>>>(geo, g->s, o.walk_len, g->blist[k & 1], g->cnt + k % 3,
+                                           g->blist[(k + 1) & 1], g->cnt + (k + 1) % 3, g->cnt + (k + 2) % 3,
+                                           g->vstamp, ++g->tag, g->work + i, g->flags);
+            else if (g->vertex_lists)
+                k_sweep_v<<<gv, 256, 0, st>>>(geo, g->s, o.ops_per_sweep, g->blist[k & 1], g->cnt + k % 3,
+                                              g->blist[(k + 1) & 1], g->cnt + (k + 1) % 3, g->cnt + (k + 2) % 3,
+                                              g->vstamp, ++g->tag, g->work + i, g->flags);
+            else
+                k_sweep<<<grid, 256, 0, st>>>(geo, g->s, o.ops_per_sweep, g->clist[k & 1], g->cnt + k % 3,
+                                              g->clist[(k + 1) & 1], g->cnt + (k + 1) % 3, g->cnt + (k + 2) % 3,
+                                              g->cstamp, ++g->tag, g->work + i, g->flags);
         }
         CG_CUDA(cudaEventRecord(g->ev1, st));
         g->st.kernel_launches += batch;
@@ -388,6 +421,7 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
             fprintf(stderr, " | %.3f ms\n", ms);
         }
         bool quiescent = false;
+        last_active = (int64_t)g->h_work[batch - 1];
         for (int i = 0; i < batch; i++) {
             const unsigned long long c = g->h_work[i];
             g->st.sweep_bytes_alg += 44.0 * (double)c;  // 32 B state read + 12 B push writes
@@ -403,6 +437,7 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
             rs = timed_gr();
             if (rs) { result = rs; break; }
             active = (int64_t)g->h_u64[3];
+            last_active = active;
             work_since_gr = 0.0;
             sweep_ms_since_gr = 0.0;
             since_gap = 0;

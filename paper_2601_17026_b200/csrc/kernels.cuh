@@ -200,6 +200,315 @@ __global__ void __launch_bounds__(256) k_sweep(Geo g, Soa s, int ops, const int 
     if (lane_id() == 0 && mywork) atomicAdd(work, mywork);
 }
 
+// Vertex-granular worklist variant (default): one thread per listed vertex.  Sparse
+// activity (1-2% of the vertices, scattered) would leave 31 of 32 lanes idle in the
+// chunk variant; here every lane carries an active vertex.
+__device__ __forceinline__ void mark_vertex(int64_t id, int *vstamp, int tag, int *list, unsigned *count) {
+    bool add = id >= 0 && vstamp[id] != tag;
+    if (add) add = atomicExch(&vstamp[id], tag) != tag;
+    warp_append(add, (int)id, list, count);
+}
+
+__device__ __forceinline__ int64_t pr_op_v(const Geo &g, const Soa &s, const OpCtx &c, int &e, int &h, int &sent,
+                                           int *flags) {
+    int best = g.INF, arc = -1, res = 0;
+    int64_t tgt = -1;
+    const int tres = s.T[c.v];
+    if (tres > 0) {
+        best = 0;
+        arc = 0;
+    } else {
+        if (c.z >= 1) {
+            const int hh = s.H[c.v - 1];
+            if (hh < best) { best = hh; arc = 1; tgt = c.v - 1; }
+        }
+        if (c.zo >= 0) {
+#pragma unroll
+            for (int d = 0; d < 4; d++) {
+                if (!c.off[d]) continue;
+                const int64_t t = c.v0 + c.off[d] + c.zo;
+                const int hh = s.H[t];
+                if (hh < best) { best = hh; arc = 2 + d; tgt = t; }
+            }
+        }
+        if (c.z + 1 < g.Z) {
+            const int r = s.D[c.v + 1];
+            if (r > 0) {
+                const int hh = s.H[c.v + 1];
+                if (hh < best) { best = hh; arc = 6; tgt = c.v + 1; res = r; }
+            }
+        }
+        if (c.zi >= 0) {
+#pragma unroll
+            for (int d = 0; d < 4; d++) {
+                if (!c.off[d]) continue;
+                const int64_t u = c.v0 + c.off[d] + c.zi;
+                const int r = s.L[(int64_t)(d ^ 1) * g.n + u];
+                if (r > 0) {
+                    const int hh = s.H[u];
+                    if (hh < best) { best = hh; arc = 7 + d; tgt = u; res = r; }
+                }
+            }
+        }
+    }
+    if (best >= g.INF) {
+        h = g.INF;
+        s.H[c.v] = h;
+        return -1;
+    }
+    if (h <= best) {
+        h = best + 1;
+        s.H[c.v] = h;
+        if (h >= g.INF) return -1;
+    }
+    int df;
+    switch (arc) {
+        case 0:
+            df = min(e, tres);
+            s.T[c.v] = tres - df;
+            break;
+        case 1:
+            df = e;
+            atomicAdd(&s.D[c.v], df);
+            break;
+        case 2: case 3: case 4: case 5:
+            df = e;
+            atomicAdd(&s.L[(int64_t)(arc - 2) * g.n + c.v], df);
+            break;
+        case 6:
+            df = min(e, res);
+            atomicSub(&s.D[c.v + 1], df);
+            break;
+        default:
+            df = min(e, res);
+            atomicSub(&s.L[(int64_t)((arc - 7) ^ 1) * g.n + tgt], df);
+            break;
+    }
+    e -= df;
+    sent += df;
+    if (tgt < 0) return -1;
+    const int old = atomicAdd(&s.E[tgt], df);
+    if (old > INT_MAX - df) atomicOr(flags, FLAG_OVERFLOW);
+    return tgt;
+}
+
+__global__ void __launch_bounds__(256) k_sweep_v(Geo g, Soa s, int ops, const int *__restrict__ lin,
+                                                 const unsigned *cin, int *lout, unsigned *cout, unsigned *czero,
+                                                 int *vstamp, int tag, unsigned long long *work, int *flags) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *czero = 0;
+    const int64_t count = *cin;
+    unsigned long long mywork = 0;
+    for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {
+        const int64_t i = base + lane_id();
+        OpCtx c;
+        c.v = i < count ? lin[i] : -1;
+        int e = 0, h = g.INF;
+        if (c.v >= 0) {
+            e = s.E[c.v];
+            h = s.H[c.v];
+        }
+        bool act = e > 0 && h < g.INF;
+        if (!__any_sync(FULL, act)) continue;
+        int sent = 0;
+        if (act) {
+            mywork++;
+            c.col = c.v / g.Z;
+            c.z = (int)(c.v - c.col * g.Z);
+            c.v0 = c.col * g.Z;
+            const int x = (int)(c.col / g.Y), y = (int)(c.col - (int64_t)x * g.Y);
+            c.zo = zo_of(c.z, g.delta);
+            c.zi = zi_of(c.z, g.delta, g.Z);
+#pragma unroll
+            for (int d = 0; d < 4; d++) c.off[d] = nbr_off(g, x, y, d);
+        }
+        for (int it = 0; it < ops; ++it) {
+            int64_t tgt = -1;
+            if (act) {
+                tgt = pr_op_v(g, s, c, e, h, sent, flags);
+                act = e > 0 && h < g.INF;
+            }
+            mark_vertex(tgt, vstamp, tag, lout, cout);
+            if (!__any_sync(FULL, act)) break;
+        }
+        if (sent) atomicSub(&s.E[c.v], sent);
+        mark_vertex(act ? c.v : -1, vstamp, tag, lout, cout);
+    }
+    mywork = warp_sum_ll((long long)mywork);
+    if (lane_id() == 0 && mywork) atomicAdd(work, mywork);
+}
+
+// ------------------------------------------------------------------ a3': multi-hop sweep ("walk")
+// Alg. 2's discharge applied along a path: the owner of an active vertex v takes all
+// of E(v) and carries it down admissible arcs (strictly decreasing labels) for up to K
+// hops, pushing delta = min(carry, r) on each arc.  Finite residuals (T, up, lateral-in
+// reverse) may now be decremented by several walkers, so they are RESERVED with a CAS
+// loop (never negative); infinite arcs only increase the reverse flow (atomicAdd).  A
+// carry that cannot go further is deposited (atomicAdd) on the vertex where it stops,
+// which is listed for the next launch; a stuck vertex is relabelled monotonically
+// (atomicMax, labels never decrease between global relabels).  Excess is decremented
+// only by its owner (the walk start), so conservation is exact.
+struct ArcPick {
+    int best, arc, res;
+    int64_t tgt;
+};
+
+__device__ __forceinline__ ArcPick scan_arcs(const Geo &g, const Soa &s, const OpCtx &c) {
+    ArcPick p{g.INF, -1, 0, -1};
+    const int tres = s.T[c.v];
+    if (tres > 0) {
+        p.best = 0; p.arc = 0; p.res = tres;
+        return p;
+    }
+    if (c.z >= 1) {
+        const int hh = s.H[c.v - 1];
+        if (hh < p.best) { p.best = hh; p.arc = 1; p.tgt = c.v - 1; }
+    }
+    if (c.zo >= 0) {
+#pragma unroll
+        for (int d = 0; d < 4; d++) {
+            if (!c.off[d]) continue;
+            const int64_t t = c.v0 + c.off[d] + c.zo;
+            const int hh = s.H[t];
+            if (hh < p.best) { p.best = hh; p.arc = 2 + d; p.tgt = t; }
+        }
+    }
+    if (c.z + 1 < g.Z) {
+        const int r = s.D[c.v + 1];
+        if (r > 0) {
+            const int hh = s.H[c.v + 1];
+            if (hh < p.best) { p.best = hh; p.arc = 6; p.tgt = c.v + 1; p.res = r; }
+        }
+    }
+    if (c.zi >= 0) {
+#pragma unroll
+        for (int d = 0; d < 4; d++) {
+            if (!c.off[d]) continue;
+            const int64_t u = c.v0 + c.off[d] + c.zi;
+            const int r = s.L[(int64_t)(d ^ 1) * g.n + u];
+            if (r > 0) {
+                const int hh = s.H[u];
+                if (hh < p.best) { p.best = hh; p.arc = 7 + d; p.tgt = u; p.res = r; }
+            }
+        }
+    }
+    return p;
+}
+
+__device__ __forceinline__ void set_ctx(const Geo &g, OpCtx &c, int64_t v) {
+    c.v = v;
+    c.col = v / g.Z;
+    c.z = (int)(v - c.col * g.Z);
+    c.v0 = c.col * g.Z;
+    const int x = (int)(c.col / g.Y), y = (int)(c.col - (int64_t)x * g.Y);
+    c.zo = zo_of(c.z, g.delta);
+    c.zi = zi_of(c.z, g.delta, g.Z);
+#pragma unroll
+    for (int d = 0; d < 4; d++) c.off[d] = nbr_off(g, x, y, d);
+}
+
+// take up to `want` from a residual that several threads may decrement
+__device__ __forceinline__ int reserve(int32_t *p, int want) {
+    int cur = *(volatile int32_t *)p;
+    while (cur > 0) {
+        const int take = min(cur, want);
+        const int old = atomicCAS(p, cur, cur - take);
+        if (old == cur) return take;
+        cur = old;
+    }
+    return 0;
+}
+
+struct BlockQueue {  // block-local append buffer, flushed with one global atomic per block
+    static constexpr int CAP = 2048;
+    int buf[CAP];
+    unsigned n;
+};
+
+__device__ __forceinline__ void deposit(const Geo &g, const Soa &s, int64_t x, int c, int *vstamp, int tag,
+                                        BlockQueue &q, int *lout, unsigned *cout, int *flags) {
+    const int old = atomicAdd(&s.E[x], c);
+    if (old > INT_MAX - c) atomicOr(flags, FLAG_OVERFLOW);
+    if (vstamp[x] != tag && atomicExch(&vstamp[x], tag) != tag) {
+        const unsigned pos = atomicAdd(&q.n, 1u);
+        if (pos < BlockQueue::CAP) q.buf[pos] = (int)x;
+        else lout[atomicAdd(cout, 1u)] = (int)x;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_walk(Geo g, Soa s, int K, const int *__restrict__ lin, const unsigned *cin,
+                                              int *lout, unsigned *cout, unsigned *czero, int *vstamp, int tag,
+                                              unsigned long long *work, int *flags) {
+    __shared__ BlockQueue q;
+    __shared__ unsigned qbase;
+    if (threadIdx.x == 0) q.n = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *czero = 0;
+    __syncthreads();
+    const int64_t count = *cin;
+    unsigned long long mywork = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = lin[i];
+        int c = s.E[v];
+        int hx = s.H[v];
+        if (!(c > 0 && hx < g.INF)) continue;
+        atomicSub(&s.E[v], c);  // the owner takes its whole excess
+        mywork++;
+        OpCtx ctx;
+        set_ctx(g, ctx, v);
+        for (int step = 0; c > 0; ++step) {
+            const ArcPick p = scan_arcs(g, s, ctx);
+            if (p.best >= hx || step >= K) {  // stuck (or hop budget spent): deposit the carry here
+                if (p.best >= hx) atomicMax(&s.H[ctx.v], p.best >= g.INF ? g.INF : p.best + 1);
+                deposit(g, s, ctx.v, c, vstamp, tag, q, lout, cout, flags);
+                break;
+            }
+            int df;
+            switch (p.arc) {
+                case 0: df = reserve(&s.T[ctx.v], c); break;
+                case 1: df = c; atomicAdd(&s.D[ctx.v], df); break;
+                case 2: case 3: case 4: case 5:
+                    df = c;
+                    atomicAdd(&s.L[(int64_t)(p.arc - 2) * g.n + ctx.v], df);
+                    break;
+                case 6: df = reserve(&s.D[ctx.v + 1], c); break;
+                default: df = reserve(&s.L[(int64_t)((p.arc - 7) ^ 1) * g.n + p.tgt], c); break;
+            }
+            if (df == 0) continue;  // lost a reservation race: rescan this vertex
+            if (p.arc == 0) {       // absorbed by t
+                c -= df;
+                continue;
+            }
+            if (df < c) deposit(g, s, ctx.v, c - df, vstamp, tag, q, lout, cout, flags);
+            c = df;
+            hx = p.best;
+            set_ctx(g, ctx, p.tgt);
+        }
+    }
+    __syncthreads();
+    const unsigned nq = min(q.n, (unsigned)BlockQueue::CAP);
+    if (threadIdx.x == 0 && nq) qbase = atomicAdd(cout, nq);
+    __syncthreads();
+    for (unsigned j = threadIdx.x; j < nq; j += blockDim.x) lout[qbase + j] = q.buf[j];
+    mywork = warp_sum_ll((long long)mywork);
+    if (lane_id() == 0 && mywork) atomicAdd(work, mywork);
+}
+
+// After an exact global relabel: list every active vertex (E > 0, H < INF) in index order.
+__global__ void k_rebuild_vertices(Geo g, const Soa s, int *lout, unsigned *cout, int *vstamp, int tag,
+                                   unsigned long long *active) {
+    unsigned long long myact = 0;
+    for (int64_t base = gwarp() * 32; base < g.n; base += nwarps() * 32) {
+        const int64_t v = base + lane_id();
+        bool a = false;
+        if (v < g.n) a = s.E[v] > 0 && s.H[v] < g.INF;
+        if (a) vstamp[v] = tag;
+        myact += a;
+        warp_append(a, (int)v, lout, cout);
+    }
+    myact = warp_sum_ll((long long)myact);
+    if (lane_id() == 0 && myact) atomicAdd(active, myact);
+}
+
 // ------------------------------------------------------------------ a2/a5: exact global relabel
 // H(v) = BFS distance from v to t in the residual graph (Alg. 3: level 1 = vertices
 // with a residual arc into t -- the "{v,s}" of L414 read as t, R6 -- then
