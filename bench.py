@@ -244,13 +244,14 @@ def run_ours(args, spec):
     peak, peak_src = measured_peak()
     achieved = sweep_bytes / (sweep_ms / 1000.0) / 1e9 if sweep_ms > 0 else 0.0
     tr = ncu_traffic()
-    roofline = {"kernel": "k_sweep", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "peak_source": peak_src,
-                "traffic": tr.get("k_sweep_dram_bytes_per_launch") if tr else None,
+    roofline = {"kernel": "push-relabel sweep (k_walk / k_sweep_v)", "bound": "hbm", "achieved": achieved,
+                "peak": peak, "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
+                "traffic": tr.get("sweep_dram_bytes_per_launch") if tr else None,
                 "alg_bytes_per_launch": sweep_bytes / max(sweeps, 1),
                 "avg_launch_us": 1000.0 * sweep_ms / max(sweeps, 1),
-                "alg_bytes_def": "4 B/vertex excess scan + 40 B per active-vertex visit (DESIGN.md)",
-                "share_of_step": sweep_ms / ms_total if ms_total > 0 else None}
+                "alg_bytes_def": "44 B per push/relabel operation: 32 B vertex state read + 12 B push writes "
+                                 "(DESIGN.md 'Algorithmic bytes')",
+                "share_of_step": sweep_ms * args.steps / (ms_total * len(stats)) if ms_total > 0 else None}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "time_to_min_cut_s": ms_step / 1000.0,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",

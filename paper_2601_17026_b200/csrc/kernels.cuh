@@ -452,11 +452,11 @@ __global__ void __launch_bounds__(256) k_walk(Geo g, Soa s, int K, const int *__
         int hx = s.H[v];
         if (!(c > 0 && hx < g.INF)) continue;
         atomicSub(&s.E[v], c);  // the owner takes its whole excess
-        mywork++;
         OpCtx ctx;
         set_ctx(g, ctx, v);
         for (int step = 0; c > 0; ++step) {
             const ArcPick p = scan_arcs(g, s, ctx);
+            mywork++;  // one push or relabel operation per hop
             if (p.best >= hx || step >= K) {  // stuck (or hop budget spent): deposit the carry here
                 if (p.best >= hx) atomicMax(&s.H[ctx.v], p.best >= g.INF ? g.INF : p.best + 1);
                 deposit(g, s, ctx.v, c, vstamp, tag, q, lout, cout, flags);
