@@ -50,6 +50,7 @@ struct cg_graph {
     int *colstamp = nullptr;
     int *collist[2] = {nullptr, nullptr};
     unsigned *hist = nullptr;
+    BfsState *bst = nullptr, *h_bst = nullptr;  // device BFS state + pinned mirror
     unsigned *cnt = nullptr;              // [0..2] sweep lists, [4..6] bfs, [8..10] extraction
     unsigned long long *work = nullptr;   // [RING] active visits per sweep
     unsigned long long *u64 = nullptr;    // [0]=N [1]=sumT0 [2]=sumT [3]=active [4]=gap lifted
@@ -111,26 +112,24 @@ inline int list_grid(const cg_graph *g, int64_t items) { return grid_for(items *
 cg_status global_relabel(cg_graph *g) {
     const Geo &geo = g->geo;
     cudaStream_t st = g->stream;
-    CG_CUDA(cudaMemsetAsync(g->cnt + 4, 0, 3 * sizeof(unsigned), st));
-    k_bfs_init<<<grid_for(geo.n, 256, g->num_sms * 16), 256, 0, st>>>(geo, g->s, g->blist[0], g->cnt + 4);
+    // device-driven levels: state {L = 1, counters 0}; seeds = level 1
+    CG_CUDA(cudaMemsetAsync(g->bst, 0, sizeof(BfsState), st));
+    g->h_bst->L = 1;
+    CG_CUDA(cudaMemcpyAsync(&g->bst->L, &g->h_bst->L, sizeof(int), cudaMemcpyHostToDevice, st));
+    k_bfs_init<<<grid_for(geo.n, 256, g->num_sms * 16), 256, 0, st>>>(geo, g->s, g->blist[0], &g->bst->cnt[0]);
     g->st.kernel_launches++;
     int L = 1;
-    const int grid = list_grid(g, geo.n);
-    for (;;) {
-        for (int b = 0; b < BFS_BATCH; b++, L++) {
-            const int i = L - 1;
-            k_bfs_level<<<grid, 256, 0, st>>>(geo, g->s, L, g->blist[i & 1], g->cnt + 4 + i % 3,
-                                               g->blist[(i + 1) & 1], g->cnt + 4 + (i + 1) % 3,
-                                               g->cnt + 4 + (i + 2) % 3);
-        }
-        g->st.kernel_launches += BFS_BATCH;
+    for (int batch = 0;; batch++) {
+        const int nb = batch == 0 ? 8 : BFS_BATCH;
+        for (int b = 0; b < nb; b++)
+            k_bfs_step<<<g->num_sms * 2, 512, 0, st>>>(geo, g->s, g->blist[0], g->blist[1], g->bst);
+        g->st.kernel_launches += nb;
         CG_CUDA(cudaGetLastError());
-        // the frontier the next level would read
-        CG_CUDA(cudaMemcpyAsync(g->h_cnt + 4, g->cnt + 4 + (L - 1) % 3, sizeof(unsigned), cudaMemcpyDeviceToHost,
-                                st));
+        CG_CUDA(cudaMemcpyAsync(g->h_bst, g->bst, sizeof(BfsState), cudaMemcpyDeviceToHost, st));
         CG_CUDA(cudaStreamSynchronize(st));
-        if (g->h_cnt[4] == 0) break;
-        if ((int64_t)L > (int64_t)geo.INF + BFS_BATCH) return CG_E_CUDA;  // every level claims >= 1 vertex
+        L = g->h_bst->L;
+        if (g->h_bst->cnt[(L - 1) % 3] == 0) break;
+        if ((int64_t)L > (int64_t)geo.INF + 2) return CG_E_CUDA;  // every level claims >= 1 vertex
     }
     g->st.gr_passes += L - 1;
     // rebuild the active-chunk worklist into clist[0] / cnt[0]
@@ -183,6 +182,7 @@ size_t workspace_bytes(const Geo &geo) {
     b += al(sizeof(int) * geo.n);
     b += 5 * al(sizeof(int) * ncol);
     b += al(sizeof(unsigned) * GAP_BINS);
+    b += al(sizeof(BfsState));
     b += al(sizeof(unsigned) * 16) + al(sizeof(unsigned long long) * RING) + al(sizeof(unsigned long long) * 16) +
          al(sizeof(int) * 16);
     return b;
@@ -231,6 +231,7 @@ void colgraph_free(cg_graph *g) {
         cudaFreeHost(g->h_work);
         cudaFreeHost(g->h_u64);
         cudaFreeHost(g->h_flags);
+        cudaFreeHost(g->h_bst);
     }
     delete g;
 }
@@ -282,7 +283,8 @@ cg_status colgraph_build(const cg_dims *dims, const int32_t *cost_dev, int32_t i
     if (cudaHostAlloc(&g->h_cnt, sizeof(unsigned) * 16, cudaHostAllocDefault) != cudaSuccess ||
         cudaHostAlloc(&g->h_work, sizeof(unsigned long long) * RING, cudaHostAllocDefault) != cudaSuccess ||
         cudaHostAlloc(&g->h_u64, sizeof(unsigned long long) * 16, cudaHostAllocDefault) != cudaSuccess ||
-        cudaHostAlloc(&g->h_flags, sizeof(int) * 16, cudaHostAllocDefault) != cudaSuccess)
+        cudaHostAlloc(&g->h_flags, sizeof(int) * 16, cudaHostAllocDefault) != cudaSuccess ||
+        cudaHostAlloc(&g->h_bst, sizeof(BfsState), cudaHostAllocDefault) != cudaSuccess)
         return fail(CG_E_NOMEM);
     if (cudaEventCreate(&g->ev0) != cudaSuccess || cudaEventCreate(&g->ev1) != cudaSuccess) return fail(CG_E_CUDA);
     const int64_t ncol = (int64_t)geo.X * geo.Y;
@@ -306,6 +308,7 @@ cg_status colgraph_build(const cg_dims *dims, const int32_t *cost_dev, int32_t i
     g->collist[0] = carve<int>(p, ncol);
     g->collist[1] = carve<int>(p, ncol);
     g->hist = carve<unsigned>(p, GAP_BINS);
+    g->bst = carve<BfsState>(p, 1);
     g->cnt = carve<unsigned>(p, 16);
     g->work = carve<unsigned long long>(p, RING);
     g->u64 = carve<unsigned long long>(p, 16);
@@ -369,6 +372,16 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
         }
         return s;
     };
+    // a1': exact per-column pre-cancellation (valid initial preflow)
+    const size_t pc_smem = (size_t)8 * (geo.Z + 1) * sizeof(long long);
+    if (getenv("CG_PRECANCEL") && pc_smem <= 200 * 1024) {  // opt-in: measured slower on C4/C5
+        if (pc_smem > 48 * 1024)
+            CG_CUDA(cudaFuncSetAttribute(k_precancel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pc_smem));
+        k_precancel<<<grid_for((int64_t)geo.X * geo.Y * 32, 256, g->num_sms * 16), 256, pc_smem, st>>>(geo, g->s,
+                                                                                                        g->flags);
+        g->st.kernel_launches++;
+        CG_CUDA(cudaGetLastError());
+    }
     cg_status rs = timed_gr();
     if (rs) return rs;
     int64_t active = (int64_t)g->h_u64[3];

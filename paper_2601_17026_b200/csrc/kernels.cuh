@@ -209,48 +209,67 @@ __device__ __forceinline__ void mark_vertex(int64_t id, int *vstamp, int tag, in
     warp_append(add, (int)id, list, count);
 }
 
-__device__ __forceinline__ int64_t pr_op_v(const Geo &g, const Soa &s, const OpCtx &c, int &e, int &h, int &sent,
-                                           int *flags) {
-    int best = g.INF, arc = -1, res = 0;
-    int64_t tgt = -1;
+struct ArcPick {
+    int best, arc, res;
+    int64_t tgt;
+};
+
+// Arc scan in the fixed order t, down, lateral-out(+x,-x,+y,-y), up, lateral-in-reverse.
+// Returns the FIRST admissible arc (neighbour label < hx: Alg. 2 pushes on any admissible
+// arc, and with exact labels every admissible neighbour sits at hx-1); if none is
+// admissible, the lowest residual neighbour (for the relabel "newd = min label(w)+1").
+// Early exit saves most of the scattered loads in the common case.
+__device__ __forceinline__ ArcPick scan_arcs(const Geo &g, const Soa &s, const OpCtx &c, int hx) {
+    ArcPick p{g.INF, -1, 0, -1};
     const int tres = s.T[c.v];
     if (tres > 0) {
-        best = 0;
-        arc = 0;
-    } else {
-        if (c.z >= 1) {
-            const int hh = s.H[c.v - 1];
-            if (hh < best) { best = hh; arc = 1; tgt = c.v - 1; }
-        }
-        if (c.zo >= 0) {
+        p.best = 0; p.arc = 0; p.res = tres;
+        return p;
+    }
+    if (c.z >= 1) {
+        const int hh = s.H[c.v - 1];
+        if (hh < p.best) { p.best = hh; p.arc = 1; p.tgt = c.v - 1; }
+        if (p.best < hx) return p;
+    }
+    if (c.zo >= 0) {
 #pragma unroll
-            for (int d = 0; d < 4; d++) {
-                if (!c.off[d]) continue;
-                const int64_t t = c.v0 + c.off[d] + c.zo;
-                const int hh = s.H[t];
-                if (hh < best) { best = hh; arc = 2 + d; tgt = t; }
-            }
+        for (int d = 0; d < 4; d++) {
+            if (!c.off[d]) continue;
+            const int64_t t = c.v0 + c.off[d] + c.zo;
+            const int hh = s.H[t];
+            if (hh < p.best) { p.best = hh; p.arc = 2 + d; p.tgt = t; }
+            if (p.best < hx) return p;
         }
-        if (c.z + 1 < g.Z) {
-            const int r = s.D[c.v + 1];
+    }
+    if (c.z + 1 < g.Z) {
+        const int r = s.D[c.v + 1];
+        if (r > 0) {
+            const int hh = s.H[c.v + 1];
+            if (hh < p.best) { p.best = hh; p.arc = 6; p.tgt = c.v + 1; p.res = r; }
+            if (p.best < hx) return p;
+        }
+    }
+    if (c.zi >= 0) {
+#pragma unroll
+        for (int d = 0; d < 4; d++) {
+            if (!c.off[d]) continue;
+            const int64_t u = c.v0 + c.off[d] + c.zi;
+            const int r = s.L[(int64_t)(d ^ 1) * g.n + u];
             if (r > 0) {
-                const int hh = s.H[c.v + 1];
-                if (hh < best) { best = hh; arc = 6; tgt = c.v + 1; res = r; }
-            }
-        }
-        if (c.zi >= 0) {
-#pragma unroll
-            for (int d = 0; d < 4; d++) {
-                if (!c.off[d]) continue;
-                const int64_t u = c.v0 + c.off[d] + c.zi;
-                const int r = s.L[(int64_t)(d ^ 1) * g.n + u];
-                if (r > 0) {
-                    const int hh = s.H[u];
-                    if (hh < best) { best = hh; arc = 7 + d; tgt = u; res = r; }
-                }
+                const int hh = s.H[u];
+                if (hh < p.best) { p.best = hh; p.arc = 7 + d; p.tgt = u; p.res = r; }
+                if (p.best < hx) return p;
             }
         }
     }
+    return p;
+}
+
+__device__ __forceinline__ int64_t pr_op_v(const Geo &g, const Soa &s, const OpCtx &c, int &e, int &h, int &sent,
+                                           int *flags) {
+    const ArcPick p = scan_arcs(g, s, c, h);
+    const int best = p.best, arc = p.arc, res = p.res, tres = p.res;
+    const int64_t tgt = p.tgt;
     if (best >= g.INF) {
         h = g.INF;
         s.H[c.v] = h;
@@ -347,53 +366,6 @@ __global__ void __launch_bounds__(256) k_sweep_v(Geo g, Soa s, int ops, const in
 // which is listed for the next launch; a stuck vertex is relabelled monotonically
 // (atomicMax, labels never decrease between global relabels).  Excess is decremented
 // only by its owner (the walk start), so conservation is exact.
-struct ArcPick {
-    int best, arc, res;
-    int64_t tgt;
-};
-
-__device__ __forceinline__ ArcPick scan_arcs(const Geo &g, const Soa &s, const OpCtx &c) {
-    ArcPick p{g.INF, -1, 0, -1};
-    const int tres = s.T[c.v];
-    if (tres > 0) {
-        p.best = 0; p.arc = 0; p.res = tres;
-        return p;
-    }
-    if (c.z >= 1) {
-        const int hh = s.H[c.v - 1];
-        if (hh < p.best) { p.best = hh; p.arc = 1; p.tgt = c.v - 1; }
-    }
-    if (c.zo >= 0) {
-#pragma unroll
-        for (int d = 0; d < 4; d++) {
-            if (!c.off[d]) continue;
-            const int64_t t = c.v0 + c.off[d] + c.zo;
-            const int hh = s.H[t];
-            if (hh < p.best) { p.best = hh; p.arc = 2 + d; p.tgt = t; }
-        }
-    }
-    if (c.z + 1 < g.Z) {
-        const int r = s.D[c.v + 1];
-        if (r > 0) {
-            const int hh = s.H[c.v + 1];
-            if (hh < p.best) { p.best = hh; p.arc = 6; p.tgt = c.v + 1; p.res = r; }
-        }
-    }
-    if (c.zi >= 0) {
-#pragma unroll
-        for (int d = 0; d < 4; d++) {
-            if (!c.off[d]) continue;
-            const int64_t u = c.v0 + c.off[d] + c.zi;
-            const int r = s.L[(int64_t)(d ^ 1) * g.n + u];
-            if (r > 0) {
-                const int hh = s.H[u];
-                if (hh < p.best) { p.best = hh; p.arc = 7 + d; p.tgt = u; p.res = r; }
-            }
-        }
-    }
-    return p;
-}
-
 __device__ __forceinline__ void set_ctx(const Geo &g, OpCtx &c, int64_t v) {
     c.v = v;
     c.col = v / g.Z;
@@ -455,7 +427,7 @@ __global__ void __launch_bounds__(256) k_walk(Geo g, Soa s, int K, const int *__
         OpCtx ctx;
         set_ctx(g, ctx, v);
         for (int step = 0; c > 0; ++step) {
-            const ArcPick p = scan_arcs(g, s, ctx);
+            const ArcPick p = scan_arcs(g, s, ctx, hx);
             mywork++;  // one push or relabel operation per hop
             if (p.best >= hx || step >= K) {  // stuck (or hop budget spent): deposit the carry here
                 if (p.best >= hx) atomicMax(&s.H[ctx.v], p.best >= g.INF ? g.INF : p.best + 1);
@@ -531,51 +503,207 @@ __global__ void k_bfs_init(Geo g, Soa s, int *lout, unsigned *cout) {
     }
 }
 
+// Expand one frontier vertex per lane (v < 0: none): claim every unlabelled residual
+// predecessor with label nl and append the claims with one atomic per warp.
+__device__ __forceinline__ void bfs_expand_warp(const Geo &g, const Soa &s, int nl, int64_t v, int *lout,
+                                                unsigned *cout) {
+    const int INF = g.INF;
+    int u[10];
+    unsigned got = 0;
+    if (v >= 0) {
+        const int64_t col = v / g.Z;
+        const int z = (int)(v - col * g.Z);
+        const int x = (int)(col / g.Y), y = (int)(col - (int64_t)x * g.Y);
+        const int64_t v0 = col * g.Z;
+        const int zo = zo_of(z, g.delta), zi = zi_of(z, g.delta, g.Z);
+        auto claim = [&](int slot, int64_t w) {
+            if (s.H[w] >= INF && atomicCAS(&s.H[w], INF, nl) == INF) {
+                u[slot] = (int)w;
+                got |= 1u << slot;
+            }
+        };
+        if (z + 1 < g.Z) claim(0, v + 1);
+        if (z >= 1 && s.D[v] > 0) claim(1, v - 1);
+#pragma unroll
+        for (int d = 0; d < 4; d++) {
+            const int64_t o = nbr_off(g, x, y, d);
+            if (!o) continue;
+            if (zi >= 0) claim(2 + d, v0 + o + zi);
+            if (zo >= 0 && s.L[(int64_t)d * g.n + v] > 0) claim(6 + d, v0 + o + zo);
+        }
+    }
+    const int k = __popc(got);
+    const int incl = warp_incl_scan(k);
+    const int total = __shfl_sync(FULL, incl, 31);
+    if (total == 0) return;
+    unsigned b = 0;
+    if (lane_id() == 31) b = atomicAdd(cout, (unsigned)total);
+    b = __shfl_sync(FULL, b, 31);
+    unsigned pos = b + incl - k;
+#pragma unroll
+    for (int j = 0; j < 10; j++)
+        if (got >> j & 1u) lout[pos++] = u[j];
+}
+
 __global__ void __launch_bounds__(256) k_bfs_level(Geo g, Soa s, int L, const int *__restrict__ lin,
                                                    const unsigned *cin, int *lout, unsigned *cout,
                                                    unsigned *czero) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *czero = 0;
     const int64_t count = *cin;
-    const int INF = g.INF, nl = L + 1;
     for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {
         const int64_t i = base + lane_id();
-        int u[10];
-        unsigned got = 0;
-        if (i < count) {
-            const int64_t v = lin[i];
-            const int64_t col = v / g.Z;
-            const int z = (int)(v - col * g.Z);
-            const int x = (int)(col / g.Y), y = (int)(col - (int64_t)x * g.Y);
-            const int64_t v0 = col * g.Z;
-            const int zo = zo_of(z, g.delta), zi = zi_of(z, g.delta, g.Z);
-            auto claim = [&](int slot, int64_t w) {
-                if (s.H[w] >= INF && atomicCAS(&s.H[w], INF, nl) == INF) {
-                    u[slot] = (int)w;
-                    got |= 1u << slot;
-                }
-            };
-            if (z + 1 < g.Z) claim(0, v + 1);
-            if (z >= 1 && s.D[v] > 0) claim(1, v - 1);
-#pragma unroll
-            for (int d = 0; d < 4; d++) {
-                const int64_t o = nbr_off(g, x, y, d);
-                if (!o) continue;
-                if (zi >= 0) claim(2 + d, v0 + o + zi);
-                if (zo >= 0 && s.L[(int64_t)d * g.n + v] > 0) claim(6 + d, v0 + o + zo);
-            }
-        }
-        const int k = __popc(got);
-        const int incl = warp_incl_scan(k);
-        const int total = __shfl_sync(FULL, incl, 31);
-        if (total == 0) continue;
-        unsigned b = 0;
-        if (lane_id() == 31) b = atomicAdd(cout, (unsigned)total);
-        b = __shfl_sync(FULL, b, 31);
-        unsigned pos = b + incl - k;
-#pragma unroll
-        for (int j = 0; j < 10; j++)
-            if (got >> j & 1u) lout[pos++] = u[j];
+        bfs_expand_warp(g, s, L + 1, i < count ? (int64_t)lin[i] : -1, lout, cout);
     }
+}
+
+// Device-driven BFS step (the level counter lives on the device, so identical launches
+// can be queued back to back).  Step i = level L = i+1 reads list[i&1] / cnt[i%3],
+// writes list[(i+1)&1] / cnt[(i+1)%3] and zeroes cnt[(i+2)%3].
+//   large frontier: every block expands one level; the last block to finish advances L;
+//   small frontier (<= BFS_SMALL): block 0 alone runs levels back to back separated by
+//   __syncthreads (a level costs ~1-2 us instead of a launch), until the frontier grows
+//   or empties.
+constexpr unsigned BFS_SMALL = 2048;
+struct BfsState {
+    int L;              // current level (1-based)
+    unsigned cnt[3];    // frontier counters
+    unsigned finished;  // blocks done with the current large level
+};
+
+__global__ void __launch_bounds__(512) k_bfs_step(Geo g, Soa s, int *list0, int *list1, BfsState *st) {
+    __shared__ int sL;
+    if (threadIdx.x == 0) sL = *(volatile int *)&st->L;
+    __syncthreads();
+    int L = sL;
+    unsigned count = *(volatile unsigned *)&st->cnt[(L - 1) % 3];
+    if (count == 0) return;
+    if (count <= BFS_SMALL) {
+        if (blockIdx.x != 0) return;
+        for (;;) {
+            const int i = L - 1;
+            int *lin = (i & 1) ? list1 : list0;
+            int *lout = (i & 1) ? list0 : list1;
+            if (threadIdx.x == 0) st->cnt[(i + 2) % 3] = 0;
+            for (unsigned base = (threadIdx.x >> 5) * 32; base < count; base += (blockDim.x >> 5) * 32) {
+                const unsigned j = base + lane_id();
+                bfs_expand_warp(g, s, L + 1, j < count ? (int64_t)lin[j] : -1, lout, &st->cnt[(i + 1) % 3]);
+            }
+            __syncthreads();
+            ++L;
+            count = *(volatile unsigned *)&st->cnt[(L - 1) % 3];
+            __syncthreads();
+            if (count == 0 || count > BFS_SMALL) break;
+        }
+        if (threadIdx.x == 0) st->L = L;
+        return;
+    }
+    const int i = L - 1;
+    const int *lin = (i & 1) ? list1 : list0;
+    int *lout = (i & 1) ? list0 : list1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->cnt[(i + 2) % 3] = 0;
+    for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {
+        const int64_t j = base + lane_id();
+        bfs_expand_warp(g, s, L + 1, j < count ? (int64_t)lin[j] : -1, lout, &st->cnt[(i + 1) % 3]);
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned f = atomicAdd(&st->finished, 1u);
+        if (f == gridDim.x - 1) {
+            st->finished = 0;
+            st->L = L + 1;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ a1': column pre-cancellation
+// Exact max-flow of every column in isolation (ignoring lateral arcs), applied as the
+// initial preflow: source excess may only move DOWN a column (infinite down arcs) into
+// sink arcs below it, and the top-down greedy is optimal because the set of sinks a
+// source can feed is nested.  With a(z) = E(z) - T(z) and S(z) = sum_{j>=z} a(j):
+//   carry leaving z downward    c(z) = S(z) - min_{m in [z, Z]} S(m)       (S(Z) = 0)
+//   absorbed at a sink          ab(z) = min(T(z), c(z+1))
+//   flow on the down arc z->z-1 f(z) = min(c(z), sum_{z'<z} ab(z'))  (only what is absorbed below)
+//   new state  T -= ab,  D = f,  E = f(z+1) + E(z) - ab(z) - f(z) >= 0.
+// Not in the paper: an accelerator whose result is a valid preflow, so the maximum flow
+// and the minimal cut are unchanged.  One warp per column, z in chunks of 32.
+__device__ __forceinline__ long long warp_suffix_sum_ll(long long v) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long t = __shfl_down_sync(FULL, v, o);
+        if (lane_id() + o < 32) v += t;
+    }
+    return v;
+}
+__device__ __forceinline__ long long warp_suffix_min_ll(long long v) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long t = __shfl_down_sync(FULL, v, o);
+        if (lane_id() + o < 32) v = min(v, t);
+    }
+    return v;
+}
+__device__ __forceinline__ long long warp_excl_prefix_sum_ll(long long v) {
+    long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long t = __shfl_up_sync(FULL, x, o);
+        if (lane_id() >= o) x += t;
+    }
+    return x - v;
+}
+
+__global__ void __launch_bounds__(256) k_precancel(Geo g, Soa s, int *flags) {
+    extern __shared__ long long sh_c[];  // per warp: Z+1 carries c(z)
+    long long *cz = sh_c + (int64_t)(threadIdx.x >> 5) * (g.Z + 1);
+    const int64_t ncol = (int64_t)g.X * g.Y;
+    const int last_c0 = ((g.Z - 1) >> 5) << 5;
+    bool bad = false;
+    for (int64_t col = gwarp(); col < ncol; col += nwarps()) {
+        const int64_t v0 = col * g.Z;
+        // pass 1, top-down: suffix sums S(z) and carries c(z)
+        long long sum_above = 0, min_above = 0;  // S over chunks above; min over m above incl. S(Z) = 0
+        if (lane_id() == 0) cz[g.Z] = 0;
+        for (int c0 = last_c0; c0 >= 0; c0 -= 32) {
+            const int z = c0 + lane_id();
+            long long a = 0;
+            if (z < g.Z) a = (long long)s.E[v0 + z] - (long long)s.T[v0 + z];
+            const long long S = warp_suffix_sum_ll(a) + sum_above;
+            const long long m = min(warp_suffix_min_ll(z < g.Z ? S : LLONG_MAX), min_above);
+            if (z < g.Z) cz[z] = S - m;
+            sum_above = __shfl_sync(FULL, S, 0);
+            min_above = __shfl_sync(FULL, m, 0);
+        }
+        __syncwarp();
+        // pass 2, bottom-up: absorption, flows, new state
+        long long ab_below = 0;  // sum of ab(z') for z' below the chunk
+        for (int c0 = 0; c0 < g.Z; c0 += 32) {
+            const int z = c0 + lane_id();
+            const bool ok = z < g.Z;
+            int e = 0, t = 0;
+            long long ab = 0, f = 0;
+            if (ok) {
+                e = s.E[v0 + z];
+                t = s.T[v0 + z];
+                ab = t > 0 ? min((long long)t, cz[z + 1]) : 0;
+            }
+            const long long AB = warp_excl_prefix_sum_ll(ab) + ab_below;
+            if (ok && z >= 1) f = min(cz[z], AB);
+            long long f_up = __shfl_down_sync(FULL, f, 1);
+            const long long ab_total = __shfl_sync(FULL, AB + ab, 31);
+            if (lane_id() == 31) f_up = (z + 1 < g.Z) ? min(cz[z + 1], ab_total) : 0;
+            if (ok) {
+                const long long ne = f_up + (long long)e - ab - f;
+                if (ne < 0 || ne > INT_MAX || f > INT_MAX) bad = true;
+                s.E[v0 + z] = (int32_t)ne;
+                s.T[v0 + z] = t - (int32_t)ab;
+                s.D[v0 + z] = (int32_t)f;
+            }
+            ab_below = ab_total;
+        }
+        __syncwarp();
+    }
+    if (bad) atomicOr(flags, FLAG_OVERFLOW);
 }
 
 // After an exact global relabel: list every chunk holding an active vertex (E > 0,

@@ -239,11 +239,14 @@ def test_determinism(cg):
 
 
 @pytest.mark.parametrize("kw", [dict(gap_every=4), dict(ops_per_sweep=4), dict(gr_factor=0.25),
-                                dict(gr_factor=2.0, check_every=1), dict(gap_every=1, ops_per_sweep=2)])
-def test_options_do_not_change_results(cg, kw):
-    c = V.generate("C1")
-    o = oracle.colgraph_solve(c, 2)
-    assert_same(gpu(cg, c, 2, opts=cg.make_opts(**kw)), o, str(kw))
+                                dict(gr_factor=2.0, check_every=1), dict(gap_every=1, ops_per_sweep=2),
+                                dict(walk_len=-1), dict(walk_len=1), dict(walk_len=7), dict(walk_len=4096)])
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_options_do_not_change_results(cg, kw, name):
+    c = V.generate(name)
+    delta = V.CONFIGS[name].delta
+    o = oracle.colgraph_solve(c, delta)
+    assert_same(gpu(cg, c, delta, opts=cg.make_opts(**kw)), o, str(kw))
 
 
 def test_host_api_matches_device_api(cg):
@@ -286,9 +289,9 @@ def test_error_paths(cg):
 
 
 def test_not_converged_status(cg):
-    c = V.generate("C1")
+    c = V.generate("C2")
     t = torch.from_numpy(c).cuda()
-    h = cg.colgraph_build(t, 2)
+    h = cg.colgraph_build(t, 3)
     try:
         st, _, _ = cg.maxflow_solve(h, cg.make_opts(max_sweeps=1, check_every=1))
         assert st == cg.CG_E_NOT_CONVERGED
