@@ -121,10 +121,30 @@ typedef struct {
  *   out      : receives the library-owned handle (free with colgraph_free).
  * Excess is initialised to the saturated source arcs (Goldberg-Tarjan init,
  * PAPER.md:134), sink residuals to the sink capacities, all flows to 0.
+ * Multi-GPU (cg_dist.nranks > 1): one process per GPU, each passing its own x-slab
+ * (cg_slab_range) and the shared cg_dist.nccl_id; the ranks exchange one halo message
+ * per x-neighbour per sweep with ncclSend/ncclRecv and agree on termination with
+ * ncclAllReduce.
  * Errors: CG_E_INVAL, CG_E_OVERFLOW (a weight outside int32), CG_E_NOMEM,
  *         CG_E_CUDA, CG_E_NCCL. */
 cg_status colgraph_build(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight,
                          const cg_dist *dist, cg_graph **out);
+
+/* a8 -- the same graph cut into `nslabs` x-slabs held by THIS process (cg_slab_range
+ * partition), each with its own residual state and ghost planes, exchanging exactly the
+ * halo messages the NCCL ranks of colgraph_build(nranks > 1) exchange -- moved with
+ * device-to-device copies instead of ncclSend/ncclRecv (§3.2.1 L254 column
+ * segmentation).  Used to validate the multi-GPU algorithm on one GPU.
+ *   cost_dev : device int32[X*Y*Z], the WHOLE volume; outputs of the other calls are
+ *              whole-volume arrays as well.
+ * Errors: as colgraph_build; CG_E_INVAL if nslabs < 1 or nslabs > X. */
+cg_status colgraph_build_slabs(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight,
+                               int32_t nslabs, const cg_dist *dist, cg_graph **out);
+
+/* Fill id_out (128 bytes) with a fresh ncclUniqueId for colgraph_build's cg_dist.nccl_id
+ * (rank 0 calls it and broadcasts the bytes, e.g. with torch.distributed).
+ * Errors: CG_E_INVAL (NULL), CG_E_NCCL (libnccl.so.2 not loadable). */
+cg_status cg_nccl_unique_id(void *id_out);
 
 /* a2-a6 -- lock-free push-relabel to a maximum preflow (§2.1,
  * Alg. 2) with exact global relabels from the sink (Alg. 3,

@@ -62,6 +62,11 @@ def _load():
     P = ctypes.POINTER
     lib.colgraph_build.restype = ctypes.c_int
     lib.colgraph_build.argtypes = [P(cg_dims), ctypes.c_void_p, ctypes.c_int32, P(cg_dist), P(ctypes.c_void_p)]
+    lib.colgraph_build_slabs.restype = ctypes.c_int
+    lib.colgraph_build_slabs.argtypes = [P(cg_dims), ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, P(cg_dist),
+                                         P(ctypes.c_void_p)]
+    lib.cg_nccl_unique_id.restype = ctypes.c_int
+    lib.cg_nccl_unique_id.argtypes = [ctypes.c_void_p]
     lib.maxflow_solve.restype = ctypes.c_int
     lib.maxflow_solve.argtypes = [ctypes.c_void_p, P(cg_solve_opts), P(ctypes.c_int64), P(cg_solve_stats)]
     lib.mincut_extract_surface.restype = ctypes.c_int
@@ -86,7 +91,7 @@ def _load():
 
 _lib = _load()
 
-EXPORTED = ["colgraph_build", "maxflow_solve", "mincut_extract_surface", "colgraph_solve_host",
+EXPORTED = ["colgraph_build", "colgraph_build_slabs", "cg_nccl_unique_id", "maxflow_solve", "mincut_extract_surface", "colgraph_solve_host",
             "colgraph_export_state", "colgraph_stats", "colgraph_free", "cg_status_str", "cg_slab_range", "cg_version"]
 
 
@@ -131,6 +136,34 @@ def colgraph_build(cost, delta: int, input_is_weight: bool = False, stream=None,
     if st != CG_OK:
         raise ColgraphError(st, "colgraph_build")
     return h
+
+
+def colgraph_build_slabs(cost, delta: int, nslabs: int, input_is_weight: bool = False, stream=None):
+    """Whole volume `cost` (CUDA int32 [X, Y, Z]) cut into `nslabs` x-slabs inside this process,
+    exchanging the same halo messages as NCCL ranks (device-to-device copies)."""
+    _check_dev_int32(cost, "cost")
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(cost.device)
+    X, Y, Z = cost.shape
+    dims = cg_dims(X, Y, Z, int(delta))
+    h = ctypes.c_void_p()
+    st = _lib.colgraph_build_slabs(ctypes.byref(dims), ctypes.c_void_p(cost.data_ptr()), int(bool(input_is_weight)),
+                                   int(nslabs), ctypes.byref(_dist(cost.device.index,
+                                                                   ctypes.c_void_p(stream.cuda_stream))),
+                                   ctypes.byref(h))
+    if st != CG_OK:
+        raise ColgraphError(st, "colgraph_build_slabs")
+    return h
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for multi-GPU colgraph_build (rank 0 creates, all ranks share)."""
+    buf = ctypes.create_string_buffer(128)
+    st = _lib.cg_nccl_unique_id(buf)
+    if st != CG_OK:
+        raise ColgraphError(st, "cg_nccl_unique_id")
+    return buf.raw
 
 
 def maxflow_solve(handle, opts: cg_solve_opts | None = None):
@@ -209,12 +242,14 @@ def cg_slab_range(X: int, Y: int, Z: int, delta: int, rank: int, nranks: int):
     return x0.value, x1.value
 
 
-def solve(cost, delta: int, input_is_weight: bool = False, want_mask: bool = True, opts=None):
-    """Device-resident convenience: build -> solve -> extract on a CUDA int32 tensor.
+def solve(cost, delta: int, input_is_weight: bool = False, want_mask: bool = True, opts=None, nslabs: int = 1):
+    """Device-resident convenience: build -> solve -> extract on a CUDA int32 tensor
+    (nslabs > 1: the in-process x-slab path).
     Returns dict(status, extract_status, flow, surface (tensor), mask (tensor), stats)."""
     import torch
     X, Y, Z = cost.shape
-    h = colgraph_build(cost, delta, input_is_weight)
+    h = colgraph_build(cost, delta, input_is_weight) if nslabs == 1 else \
+        colgraph_build_slabs(cost, delta, nslabs, input_is_weight)
     try:
         st, flow, stats = maxflow_solve(h, opts)
         surface = torch.empty((X, Y), dtype=torch.int32, device=cost.device)

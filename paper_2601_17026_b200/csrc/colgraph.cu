@@ -2,26 +2,37 @@
 //
 // Hot path of arXiv 2601.17026 (§3.2), redesigned for one GPU per process:
 // the paper's per-thread FIFO queues, per-vertex locks and level barriers (§3.2.1-3.2.4)
-// become device worklists of 32-vertex chunks, single-decrementer atomics and
-// level-synchronous frontier kernels launched back to back on one stream.  The host
-// only reads a few counters every `check_every` sweeps.
+// become device worklists, single-decrementer atomics and level kernels launched back to
+// back on one stream; the host reads a few counters every `check_every` sweeps.
 //
 // Solve loop:
-//   a2  exact global relabel (frontier BFS from t) -> rebuild the active-chunk list
-//   a3  sweeps over the active-chunk list (batch of check_every launches, no host sync)
+//   a2  exact global relabel (frontier BFS from t) -> rebuild the active-vertex list
+//   a3  sweeps over the active list (a batch of check_every launches without host sync)
 //   a5  re-run the global relabel when the work since the last one reaches gr_factor*n
 //        or the sweep time since the last one exceeds its cost
-//   a4  when a sweep finds no active vertex: exact global relabel; stop if no vertex
-//       with excess has a finite height (the preflow is then maximum)
+//   a4  when a sweep finds no active vertex: exact global relabel; stop if no vertex with
+//       excess has a finite height (the preflow is then maximum)
 //   a6  |f| = sum(T0) - sum(T)
+//
+// x-slabs (§8(e), §3.2.1 column segmentation): the volume is cut into
+// contiguous x-ranges ("slabs"), each with a ghost plane of its neighbours.  After every
+// sweep the slabs exchange one halo message per side (k_halo_pack/unpack); the global
+// relabel becomes label-correcting waves + ghost-height exchanges until no label changes;
+// the extraction exchanges column tops.  Two transports share this driver:
+//   NCCL    one slab per process/GPU (colgraph_build with nranks > 1): ncclSend/Recv to
+//           the x-neighbours, ncclAllReduce for counts;
+//   LOCAL   several slabs in one process (colgraph_build_slabs): the same messages moved
+//           with device-to-device copies -- used to test the multi-slab algorithm on one GPU.
 #include "colgraph.h"
 #include "kernels.cuh"
+#include "nccl_shim.h"
 
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 using namespace cg;
 
@@ -29,40 +40,56 @@ namespace {
 constexpr int RING = 256;
 constexpr int BFS_BATCH = 32;
 constexpr int EXT_BATCH = 16;
+constexpr int LC_BATCH = 16;
+
+struct Slab {
+    Geo geo{};
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    int x0 = 0, x1 = 0;  // owned global x-range
+    char *ws = nullptr;
+    Soa s{};
+    int *blist[2] = {nullptr, nullptr};  // BFS frontiers / sweep worklists (vertices)
+    int *vstamp = nullptr;               // per-vertex list tag
+    int32_t *top = nullptr, *proc = nullptr;  // per column (top has ghost columns)
+    int *colstamp = nullptr;
+    int *collist[2] = {nullptr, nullptr};
+    unsigned *hist = nullptr;
+    BfsState *bst = nullptr;
+    unsigned *cnt = nullptr;             // [0..2] sweep lists, [4..6] lc waves, [8..10] extraction, [12] changes
+    unsigned long long *work = nullptr;  // [RING] operations per sweep
+    unsigned long long *u64 = nullptr;   // [0]=N [1]=sumT0 [2]=sumT [3]=active [4]=gap lifted [5]=scratch
+    int *flags = nullptr;                // [0]=overflow [1]=maxh [2]=gap [3]=empty
+    int32_t *snap[2] = {nullptr, nullptr};   // ghost lateral residual at the last refresh
+    int32_t *hold[2] = {nullptr, nullptr};   // ghost heights before the last relabel exchange
+    int32_t *hsend[2] = {nullptr, nullptr};  // halo messages (4 planes)
+    int32_t *hrecv[2] = {nullptr, nullptr};
+    // pinned host mirrors
+    unsigned *h_cnt = nullptr;
+    unsigned long long *h_work = nullptr, *h_u64 = nullptr;
+    int *h_flags = nullptr;
+    BfsState *h_bst = nullptr;
+    int64_t N = 0, sumT0 = 0;
+    int tag = 0;       // monotone list tag
+    int sweep_k = 0;   // sweeps since the last list rebuild (list/counter parity)
+    int out_tag = 0;   // tag of the list the last sweep wrote (halo appends must reuse it)
+    int wave_k = 0;    // label-correcting waves since the relabel started
+    int ext_k = 0;     // extraction rounds
+};
 }  // namespace
 
 struct cg_graph {
     cg_dims dims{};
     cg_dist dist{};
-    Geo geo{};
-    cudaStream_t stream = nullptr;
-    int num_sms = 148;
-    // one stream-ordered workspace allocation
-    char *ws = nullptr;
-    size_t ws_bytes = 0;
-    Soa s{};
-    int *blist[2] = {nullptr, nullptr};  // BFS frontiers (vertices)
-    int *clist[2] = {nullptr, nullptr};  // sweep worklists (chunks)
-    int *cstamp = nullptr;               // per-chunk list tag
-    int *vstamp = nullptr;               // per-vertex list tag
-    bool vertex_lists = true;            // sweep worklist granularity (CG_CHUNK_LISTS=1: chunks)
-    int32_t *top = nullptr, *proc = nullptr;
-    int *colstamp = nullptr;
-    int *collist[2] = {nullptr, nullptr};
-    unsigned *hist = nullptr;
-    BfsState *bst = nullptr, *h_bst = nullptr;  // device BFS state + pinned mirror
-    unsigned *cnt = nullptr;              // [0..2] sweep lists, [4..6] bfs, [8..10] extraction
-    unsigned long long *work = nullptr;   // [RING] active visits per sweep
-    unsigned long long *u64 = nullptr;    // [0]=N [1]=sumT0 [2]=sumT [3]=active [4]=gap lifted
-    int *flags = nullptr;                 // [0]=overflow [1]=maxh [2]=gap [3]=empty
-    // pinned host mirrors
-    unsigned *h_cnt = nullptr;
-    unsigned long long *h_work = nullptr, *h_u64 = nullptr;
-    int *h_flags = nullptr;
+    int nranks = 1, rank = 0;   // global slab count / this process's first slab
+    bool local = true;          // LOCAL transport (all slabs in this process)
+    std::vector<Slab *> slabs;  // slabs owned by this process
+    ncclComm_t comm = nullptr;
+    int64_t *d_red = nullptr;   // NCCL allreduce buffer
+    int64_t *h_red = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    int64_t N = 0, sumT0 = 0;
-    int tag = 0;        // monotone worklist tag
-    int sweep_par = 0;  // sweeps since the last list rebuild (selects list/counter buffers)
+    int64_t n_global = 0;
     bool solved = false;
     cg_solve_stats st{};
 };
@@ -93,6 +120,21 @@ struct DeviceGuard {
         }                                                                                      \
     } while (0)
 
+#define CG_NCCL(call)                                                                   \
+    do {                                                                                \
+        ncclResult_t r_ = (call);                                                       \
+        if (r_ != ncclSuccess) {                                                        \
+            if (getenv("CG_DEBUG")) fprintf(stderr, "colgraph: %s -> nccl %d\n", #call, (int)r_); \
+            return CG_E_NCCL;                                                           \
+        }                                                                               \
+    } while (0)
+
+#define CG_TRY(expr)                 \
+    do {                             \
+        cg_status s_ = (expr);       \
+        if (s_ != CG_OK) return s_;  \
+    } while (0)
+
 inline int grid_for(int64_t n, int block, int cap) {
     int64_t b = (n + block - 1) / block;
     if (b < 1) b = 1;
@@ -106,64 +148,7 @@ inline double now_ms() {
 inline bool tracing() { return getenv("CG_TRACE") != nullptr; }
 
 // Grid for worklist kernels: enough warps to fill every SM (8 x 256 threads per SM).
-inline int list_grid(const cg_graph *g, int64_t items) { return grid_for(items * 32, 256, g->num_sms * 8); }
-
-// a2/a5: exact global relabel + rebuild of the sweep worklist; h_u64[3] = active count.
-cg_status global_relabel(cg_graph *g) {
-    const Geo &geo = g->geo;
-    cudaStream_t st = g->stream;
-    // device-driven levels: state {L = 1, counters 0}; seeds = level 1
-    CG_CUDA(cudaMemsetAsync(g->bst, 0, sizeof(BfsState), st));
-    g->h_bst->L = 1;
-    CG_CUDA(cudaMemcpyAsync(&g->bst->L, &g->h_bst->L, sizeof(int), cudaMemcpyHostToDevice, st));
-    k_bfs_init<<<grid_for(geo.n, 256, g->num_sms * 16), 256, 0, st>>>(geo, g->s, g->blist[0], &g->bst->cnt[0]);
-    g->st.kernel_launches++;
-    int L = 1;
-    for (int batch = 0;; batch++) {
-        const int nb = batch == 0 ? 8 : BFS_BATCH;
-        for (int b = 0; b < nb; b++)
-            k_bfs_step<<<g->num_sms * 2, 512, 0, st>>>(geo, g->s, g->blist[0], g->blist[1], g->bst);
-        g->st.kernel_launches += nb;
-        CG_CUDA(cudaGetLastError());
-        CG_CUDA(cudaMemcpyAsync(g->h_bst, g->bst, sizeof(BfsState), cudaMemcpyDeviceToHost, st));
-        CG_CUDA(cudaStreamSynchronize(st));
-        L = g->h_bst->L;
-        if (g->h_bst->cnt[(L - 1) % 3] == 0) break;
-        if ((int64_t)L > (int64_t)geo.INF + 2) return CG_E_CUDA;  // every level claims >= 1 vertex
-    }
-    g->st.gr_passes += L - 1;
-    // rebuild the active-chunk worklist into clist[0] / cnt[0]
-    CG_CUDA(cudaMemsetAsync(g->cnt, 0, 3 * sizeof(unsigned), st));
-    CG_CUDA(cudaMemsetAsync(g->u64 + 3, 0, sizeof(unsigned long long), st));
-    const int tag = ++g->tag;
-    if (g->vertex_lists)
-        k_rebuild_vertices<<<grid_for(geo.n, 256, g->num_sms * 16), 256, 0, st>>>(geo, g->s, g->blist[0], g->cnt,
-                                                                                  g->vstamp, tag, g->u64 + 3);
-    else
-        k_rebuild_chunks<<<grid_for(geo.nchunks, 256, g->num_sms * 16), 256, 0, st>>>(
-            geo, g->s, g->clist[0], g->cnt, g->cstamp, tag, g->u64 + 3);
-    g->st.kernel_launches++;
-    g->sweep_par = 0;
-    CG_CUDA(cudaMemcpyAsync(g->h_u64 + 3, g->u64 + 3, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    CG_CUDA(cudaStreamSynchronize(st));
-    CG_CUDA(cudaGetLastError());
-    g->st.global_relabels++;
-    return CG_OK;
-}
-
-cg_status run_gap(cg_graph *g) {
-    const Geo &geo = g->geo;
-    cudaStream_t st = g->stream;
-    CG_CUDA(cudaMemsetAsync(g->hist, 0, sizeof(unsigned) * GAP_BINS, st));
-    CG_CUDA(cudaMemsetAsync(g->flags + 1, 0, sizeof(int), st));
-    k_gap_hist<<<g->num_sms * 8, 256, 0, st>>>(geo, g->s.H, g->hist, g->flags + 1);
-    k_gap_find<<<1, 1024, 0, st>>>(g->hist, g->flags + 1, g->flags + 2);
-    k_gap_lift<<<g->num_sms * 8, 256, 0, st>>>(geo, g->s.H, g->flags + 2, g->u64 + 4);
-    CG_CUDA(cudaGetLastError());
-    g->st.kernel_launches += 3;
-    g->st.gap_runs++;
-    return CG_OK;
-}
+inline int list_grid(const Slab *sl, int64_t items) { return grid_for(items * 32, 256, sl->num_sms * 8); }
 
 template <typename T>
 T *carve(char *&p, int64_t count) {
@@ -173,19 +158,352 @@ T *carve(char *&p, int64_t count) {
 }
 
 size_t workspace_bytes(const Geo &geo) {
-    const int64_t ncol = (int64_t)geo.X * geo.Y;
+    const int64_t ncol = (int64_t)geo.X * geo.Y, plane = (int64_t)(geo.X + 2) * geo.YZ;
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-    size_t b = 0;
-    b += al(sizeof(int32_t) * 8 * geo.n);
-    b += 2 * al(sizeof(int) * geo.n);
-    b += 3 * al(sizeof(int) * geo.nchunks);
-    b += al(sizeof(int) * geo.n);
-    b += 5 * al(sizeof(int) * ncol);
-    b += al(sizeof(unsigned) * GAP_BINS);
-    b += al(sizeof(BfsState));
+    size_t b = 8 * al(sizeof(int32_t) * plane);
+    b += 3 * al(sizeof(int) * geo.n);
+    b += 3 * al(sizeof(int32_t) * (ncol + 2 * geo.Y)) + 2 * al(sizeof(int) * ncol);
+    b += al(sizeof(unsigned) * GAP_BINS) + al(sizeof(BfsState));
     b += al(sizeof(unsigned) * 16) + al(sizeof(unsigned long long) * RING) + al(sizeof(unsigned long long) * 16) +
          al(sizeof(int) * 16);
+    b += 4 * al(sizeof(int32_t) * geo.YZ) + 4 * al(sizeof(int32_t) * 4 * std::max<int64_t>(geo.YZ, 2 * geo.Y));
     return b;
+}
+
+void slab_free(Slab *sl) {
+    if (!sl) return;
+    if (sl->ws) cudaFreeAsync(sl->ws, sl->stream);
+    cudaFreeHost(sl->h_cnt);
+    cudaFreeHost(sl->h_work);
+    cudaFreeHost(sl->h_u64);
+    cudaFreeHost(sl->h_flags);
+    cudaFreeHost(sl->h_bst);
+    delete sl;
+}
+
+// Allocate and initialise a slab, then run a1 (k_build) on its x-range of cost_dev.
+cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode) {
+    const Geo &geo = sl->geo;
+    cudaStream_t st = sl->stream;
+    const int64_t n = geo.n, ncol = (int64_t)geo.X * geo.Y, plane = (int64_t)(geo.X + 2) * geo.YZ;
+    {  // keep freed workspaces cached in the stream-ordered pool (repeated solves allocate for free)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, sl->device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
+    const size_t bytes = workspace_bytes(geo);
+    if (cudaMallocAsync(&sl->ws, bytes, st) != cudaSuccess) {
+        sl->ws = nullptr;
+        return CG_E_NOMEM;
+    }
+    if (cudaHostAlloc(&sl->h_cnt, sizeof(unsigned) * 16, cudaHostAllocDefault) != cudaSuccess ||
+        cudaHostAlloc(&sl->h_work, sizeof(unsigned long long) * RING, cudaHostAllocDefault) != cudaSuccess ||
+        cudaHostAlloc(&sl->h_u64, sizeof(unsigned long long) * 16, cudaHostAllocDefault) != cudaSuccess ||
+        cudaHostAlloc(&sl->h_flags, sizeof(int) * 16, cudaHostAllocDefault) != cudaSuccess ||
+        cudaHostAlloc(&sl->h_bst, sizeof(BfsState), cudaHostAllocDefault) != cudaSuccess)
+        return CG_E_NOMEM;
+    char *p = sl->ws;
+    int32_t *pl[8];
+    for (int i = 0; i < 8; i++) pl[i] = carve<int32_t>(p, plane) + geo.YZ;  // owned plane x = 0
+    sl->s.E = pl[0];
+    sl->s.H = pl[1];
+    sl->s.T = pl[2];
+    sl->s.D = pl[3];
+    for (int d = 0; d < 4; d++) sl->s.L[d] = pl[4 + d];
+    sl->blist[0] = carve<int>(p, n);
+    sl->blist[1] = carve<int>(p, n);
+    sl->vstamp = carve<int>(p, n);
+    sl->top = carve<int32_t>(p, ncol + 2 * geo.Y) + geo.Y;
+    sl->proc = carve<int32_t>(p, ncol + 2 * geo.Y) + geo.Y;
+    sl->colstamp = carve<int>(p, ncol + 2 * geo.Y) + geo.Y;
+    sl->collist[0] = carve<int>(p, ncol);
+    sl->collist[1] = carve<int>(p, ncol);
+    sl->hist = carve<unsigned>(p, GAP_BINS);
+    sl->bst = carve<BfsState>(p, 1);
+    sl->cnt = carve<unsigned>(p, 16);
+    sl->work = carve<unsigned long long>(p, RING);
+    sl->u64 = carve<unsigned long long>(p, 16);
+    sl->flags = carve<int>(p, 16);
+    const int64_t msg = 4 * std::max<int64_t>(geo.YZ, 2 * geo.Y);
+    for (int side = 0; side < 2; side++) {
+        sl->snap[side] = carve<int32_t>(p, geo.YZ);
+        sl->hold[side] = carve<int32_t>(p, geo.YZ);
+        sl->hsend[side] = carve<int32_t>(p, msg);
+        sl->hrecv[side] = carve<int32_t>(p, msg);
+    }
+    // everything starts at zero (E, T written by k_build; heights set by the first relabel)
+    CG_CUDA(cudaMemsetAsync(sl->ws, 0, bytes, st));
+    k_build<<<grid_for(ncol * 32, 256, sl->num_sms * 16), 256, 0, st>>>(geo, cost_dev, weight_mode, sl->s, sl->u64,
+                                                                        sl->flags);
+    CG_CUDA(cudaGetLastError());
+    CG_CUDA(cudaMemcpyAsync(sl->h_u64, sl->u64, sizeof(unsigned long long) * 2, cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaMemcpyAsync(sl->h_flags, sl->flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaStreamSynchronize(st));
+    if (sl->h_flags[0] & FLAG_OVERFLOW) return CG_E_OVERFLOW;
+    sl->N = (int64_t)sl->h_u64[0];
+    sl->sumT0 = (int64_t)sl->h_u64[1];
+    return CG_OK;
+}
+
+// ---------------------------------------------------------------- transport
+
+// Sum of per-slab int64 vectors over every slab of the job (in place on `v`, which holds
+// this process's sum on entry).
+cg_status gsum(cg_graph *g, int64_t *v, int count) {
+    if (g->local || g->nranks == 1) return CG_OK;
+    Slab *sl = g->slabs[0];
+    memcpy(g->h_red, v, sizeof(int64_t) * count);
+    CG_CUDA(cudaMemcpyAsync(g->d_red, g->h_red, sizeof(int64_t) * count, cudaMemcpyHostToDevice, sl->stream));
+    CG_NCCL(nccl().allReduce(g->d_red, g->d_red, count, ncclInt64, ncclSum, g->comm, sl->stream));
+    CG_CUDA(cudaMemcpyAsync(g->h_red, g->d_red, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, sl->stream));
+    CG_CUDA(cudaStreamSynchronize(sl->stream));
+    memcpy(v, g->h_red, sizeof(int64_t) * count);
+    return CG_OK;
+}
+
+cg_status gmax(cg_graph *g, int64_t *v) {
+    if (g->local || g->nranks == 1) return CG_OK;
+    Slab *sl = g->slabs[0];
+    g->h_red[0] = *v;
+    CG_CUDA(cudaMemcpyAsync(g->d_red, g->h_red, sizeof(int64_t), cudaMemcpyHostToDevice, sl->stream));
+    CG_NCCL(nccl().allReduce(g->d_red, g->d_red, 1, ncclInt64, ncclMax, g->comm, sl->stream));
+    CG_CUDA(cudaMemcpyAsync(g->h_red, g->d_red, sizeof(int64_t), cudaMemcpyDeviceToHost, sl->stream));
+    CG_CUDA(cudaStreamSynchronize(sl->stream));
+    *v = g->h_red[0];
+    return CG_OK;
+}
+
+// Move `count` int32 of every slab's hsend[side] to the x-neighbour's hrecv[1-side].
+cg_status transfer(cg_graph *g, int64_t count) {
+    if (g->local) {
+        const int R = (int)g->slabs.size();
+        for (int r = 0; r + 1 < R; r++) {
+            Slab *a = g->slabs[r], *b = g->slabs[r + 1];
+            CG_CUDA(cudaMemcpyAsync(b->hrecv[0], a->hsend[1], sizeof(int32_t) * count, cudaMemcpyDeviceToDevice,
+                                    a->stream));
+            CG_CUDA(cudaMemcpyAsync(a->hrecv[1], b->hsend[0], sizeof(int32_t) * count, cudaMemcpyDeviceToDevice,
+                                    a->stream));
+        }
+        return CG_OK;
+    }
+    Slab *sl = g->slabs[0];
+    CG_NCCL(nccl().groupStart());
+    if (sl->geo.gl) {
+        CG_NCCL(nccl().send(sl->hsend[0], count, ncclInt32, g->rank - 1, g->comm, sl->stream));
+        CG_NCCL(nccl().recv(sl->hrecv[0], count, ncclInt32, g->rank - 1, g->comm, sl->stream));
+    }
+    if (sl->geo.gh) {
+        CG_NCCL(nccl().send(sl->hsend[1], count, ncclInt32, g->rank + 1, g->comm, sl->stream));
+        CG_NCCL(nccl().recv(sl->hrecv[1], count, ncclInt32, g->rank + 1, g->comm, sl->stream));
+    }
+    CG_NCCL(nccl().groupEnd());
+    return CG_OK;
+}
+
+bool multi(const cg_graph *g) { return g->nranks > 1; }
+
+// a8: sweep halo (excess/residual deltas out, heights/residual refresh in); the receiving
+// slab lists boundary vertices that got excess for its next sweep.
+cg_status halo_sweep(cg_graph *g) {
+    for (Slab *sl : g->slabs) {
+        const Geo &geo = sl->geo;
+        const int grid = grid_for(geo.YZ, 256, sl->num_sms * 4);
+        if (geo.gl) k_halo_pack<<<grid, 256, 0, sl->stream>>>(geo, sl->s, 0, sl->snap[0], sl->hsend[0]);
+        if (geo.gh) k_halo_pack<<<grid, 256, 0, sl->stream>>>(geo, sl->s, 1, sl->snap[1], sl->hsend[1]);
+    }
+    CG_TRY(transfer(g, 4 * g->slabs[0]->geo.YZ));
+    for (Slab *sl : g->slabs) {
+        const Geo &geo = sl->geo;
+        const int grid = grid_for(geo.YZ, 256, sl->num_sms * 4);
+        const int k = sl->sweep_k;  // the next sweep reads list[k&1] / cnt[k%3]
+        const int tag = sl->out_tag;  // same tag as the sweep that wrote that list: no duplicates
+        for (int side = 0; side < 2; side++)
+            if (side ? geo.gh : geo.gl)
+                k_halo_unpack<<<grid, 256, 0, sl->stream>>>(geo, sl->s, side, sl->hrecv[side], sl->hsend[side],
+                                                            sl->snap[side], sl->blist[k & 1], sl->cnt + k % 3,
+                                                            sl->vstamp, tag, sl->flags);
+        g->st.kernel_launches += geo.gl + geo.gh;
+    }
+    CG_CUDA(cudaGetLastError());
+    return CG_OK;
+}
+
+// ---------------------------------------------------------------- a2/a5 global relabel
+
+// ghost planes' heights start at INF (unknown) for the label-correcting relabel
+void k_fill_ghost_h(Slab *sl) {
+    const Geo &geo = sl->geo;
+    const int grid = grid_for(geo.YZ, 256, sl->num_sms * 4);
+    if (geo.gl) k_fill<<<grid, 256, 0, sl->stream>>>(sl->s.H - geo.YZ, geo.YZ, geo.INF);
+    if (geo.gh) k_fill<<<grid, 256, 0, sl->stream>>>(sl->s.H + geo.n, geo.YZ, geo.INF);
+}
+
+// Strict level-synchronous BFS of one slab without neighbours (the single-GPU path).
+cg_status bfs_strict(cg_graph *g, Slab *sl) {
+    const Geo &geo = sl->geo;
+    cudaStream_t st = sl->stream;
+    CG_CUDA(cudaMemsetAsync(sl->bst, 0, sizeof(BfsState), st));
+    sl->h_bst->L = 1;
+    CG_CUDA(cudaMemcpyAsync(&sl->bst->L, &sl->h_bst->L, sizeof(int), cudaMemcpyHostToDevice, st));
+    k_bfs_init<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, st>>>(geo, sl->s, sl->blist[0], &sl->bst->cnt[0]);
+    g->st.kernel_launches++;
+    int L = 1;
+    for (int batch = 0;; batch++) {
+        const int nb = batch == 0 ? 8 : BFS_BATCH;
+        for (int b = 0; b < nb; b++)
+            k_bfs_step<<<sl->num_sms * 2, 512, 0, st>>>(geo, sl->s, sl->blist[0], sl->blist[1], sl->bst);
+        g->st.kernel_launches += nb;
+        CG_CUDA(cudaGetLastError());
+        CG_CUDA(cudaMemcpyAsync(sl->h_bst, sl->bst, sizeof(BfsState), cudaMemcpyDeviceToHost, st));
+        CG_CUDA(cudaStreamSynchronize(st));
+        L = sl->h_bst->L;
+        if (sl->h_bst->cnt[(L - 1) % 3] == 0) break;
+        if ((int64_t)L > (int64_t)geo.INF + 2) return CG_E_CUDA;  // every level claims >= 1 vertex
+    }
+    g->st.gr_passes += L - 1;
+    return CG_OK;
+}
+
+// Label-correcting relabel across slabs: local waves until every frontier is empty, then
+// exchange ghost heights and relax from improved ghosts; stop when nothing changed anywhere.
+cg_status bfs_slabs(cg_graph *g) {
+    for (Slab *sl : g->slabs) {
+        const Geo &geo = sl->geo;
+        CG_CUDA(cudaMemsetAsync(sl->cnt + 4, 0, 3 * sizeof(unsigned), sl->stream));
+        k_bfs_init<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(geo, sl->s, sl->blist[0],
+                                                                                     sl->cnt + 4);
+        // ghost heights start unknown (INF)
+        k_fill_ghost_h(sl);
+        sl->wave_k = 0;
+        g->st.kernel_launches += 1;
+    }
+    for (int outer = 0;; outer++) {
+        // local waves
+        for (;;) {
+            int64_t pending = 0;
+            for (Slab *sl : g->slabs) {
+                const Geo &geo = sl->geo;
+                const int grid = list_grid(sl, geo.n);
+                for (int b = 0; b < LC_BATCH; b++) {
+                    const int w = sl->wave_k++;
+                    k_lc_wave<<<grid, 256, 0, sl->stream>>>(geo, sl->s, sl->blist[w & 1], sl->cnt + 4 + w % 3,
+                                                             sl->blist[(w + 1) & 1], sl->cnt + 4 + (w + 1) % 3,
+                                                             sl->cnt + 4 + (w + 2) % 3, sl->vstamp, ++sl->tag);
+                }
+                g->st.kernel_launches += LC_BATCH;
+                g->st.gr_passes += LC_BATCH;
+                CG_CUDA(cudaGetLastError());
+                CG_CUDA(cudaMemcpyAsync(sl->h_cnt + 4, sl->cnt + 4, 3 * sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                        sl->stream));
+            }
+            for (Slab *sl : g->slabs) {
+                CG_CUDA(cudaStreamSynchronize(sl->stream));
+                pending += sl->h_cnt[4 + sl->wave_k % 3];
+            }
+            if (pending == 0) break;
+        }
+        // ghost heights
+        for (Slab *sl : g->slabs) {
+            const Geo &geo = sl->geo;
+            const int grid = grid_for(geo.YZ, 256, sl->num_sms * 4);
+            if (geo.gl) k_halo_pack_h<<<grid, 256, 0, sl->stream>>>(geo, sl->s, 0, sl->hsend[0]);
+            if (geo.gh) k_halo_pack_h<<<grid, 256, 0, sl->stream>>>(geo, sl->s, 1, sl->hsend[1]);
+        }
+        CG_TRY(transfer(g, g->slabs[0]->geo.YZ));
+        int64_t relaxed = 0;
+        for (Slab *sl : g->slabs) {
+            const Geo &geo = sl->geo;
+            const int grid = grid_for(geo.YZ, 256, sl->num_sms * 4);
+            const int w = sl->wave_k;  // the next wave reads list[w&1] / cnt[4 + w%3] (now empty)
+            const int tag = ++sl->tag;
+            for (int side = 0; side < 2; side++) {
+                if (!(side ? geo.gh : geo.gl)) continue;
+                k_halo_unpack_h<<<grid, 256, 0, sl->stream>>>(geo, sl->s, side, sl->hrecv[side], sl->hold[side]);
+                k_lc_ghost<<<grid, 256, 0, sl->stream>>>(geo, sl->s, side, sl->hold[side], sl->blist[w & 1],
+                                                         sl->cnt + 4 + w % 3, sl->vstamp, tag);
+            }
+            CG_CUDA(cudaGetLastError());
+            CG_CUDA(cudaMemcpyAsync(sl->h_cnt + 4, sl->cnt + 4, 3 * sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                    sl->stream));
+        }
+        for (Slab *sl : g->slabs) {
+            CG_CUDA(cudaStreamSynchronize(sl->stream));
+            relaxed += sl->h_cnt[4 + sl->wave_k % 3];
+        }
+        CG_TRY(gsum(g, &relaxed, 1));
+        if (relaxed == 0) break;
+    }
+    return CG_OK;
+}
+
+// a2/a5: global relabel + rebuild of every slab's active list; returns the global active count.
+cg_status global_relabel(cg_graph *g, int64_t *active) {
+    if (!multi(g)) {
+        CG_TRY(bfs_strict(g, g->slabs[0]));
+    } else {
+        CG_TRY(bfs_slabs(g));
+    }
+    int64_t act = 0;
+    for (Slab *sl : g->slabs) {
+        const Geo &geo = sl->geo;
+        CG_CUDA(cudaMemsetAsync(sl->cnt, 0, 3 * sizeof(unsigned), sl->stream));
+        CG_CUDA(cudaMemsetAsync(sl->u64 + 3, 0, sizeof(unsigned long long), sl->stream));
+        k_rebuild_vertices<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(
+            geo, sl->s, sl->blist[0], sl->cnt, sl->vstamp, ++sl->tag, sl->u64 + 3);
+        g->st.kernel_launches++;
+        sl->sweep_k = 0;
+        CG_CUDA(cudaMemcpyAsync(sl->h_u64 + 3, sl->u64 + 3, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                sl->stream));
+    }
+    for (Slab *sl : g->slabs) {
+        CG_CUDA(cudaStreamSynchronize(sl->stream));
+        act += (int64_t)sl->h_u64[3];
+    }
+    CG_CUDA(cudaGetLastError());
+    CG_TRY(gsum(g, &act, 1));
+    *active = act;
+    g->st.global_relabels++;
+    return CG_OK;
+}
+
+cg_status run_gap(cg_graph *g, Slab *sl) {
+    const Geo &geo = sl->geo;
+    cudaStream_t st = sl->stream;
+    CG_CUDA(cudaMemsetAsync(sl->hist, 0, sizeof(unsigned) * GAP_BINS, st));
+    CG_CUDA(cudaMemsetAsync(sl->flags + 1, 0, sizeof(int), st));
+    k_gap_hist<<<sl->num_sms * 8, 256, 0, st>>>(geo, sl->s.H, sl->hist, sl->flags + 1);
+    k_gap_find<<<1, 1024, 0, st>>>(sl->hist, sl->flags + 1, sl->flags + 2);
+    k_gap_lift<<<sl->num_sms * 8, 256, 0, st>>>(geo, sl->s.H, sl->flags + 2, sl->u64 + 4);
+    CG_CUDA(cudaGetLastError());
+    g->st.kernel_launches += 3;
+    g->st.gap_runs++;
+    return CG_OK;
+}
+
+Geo make_geo(const cg_dims *dims, int x0, int x1, int nranks_total, bool gl, bool gh, int64_t n_global) {
+    Geo geo{};
+    geo.X = x1 - x0;
+    geo.Y = dims->Y;
+    geo.Z = dims->Z;
+    geo.delta = dims->delta;
+    geo.CPC = (dims->Z + 31) / 32;
+    geo.gl = gl;
+    geo.gh = gh;
+    geo.n = (int64_t)geo.X * geo.Y * geo.Z;
+    geo.YZ = (int64_t)dims->Y * dims->Z;
+    geo.nchunks = (int64_t)geo.X * geo.Y * geo.CPC;
+    geo.INF = (int32_t)(n_global + 1);
+    (void)nranks_total;
+    return geo;
+}
+
+cg_status validate_dims(const cg_dims *dims) {
+    if (!dims || dims->X < 1 || dims->Y < 1 || dims->Z < 1 || dims->delta < 0) return CG_E_INVAL;
+    const int64_t n = (int64_t)dims->X * dims->Y * dims->Z;
+    if (n + dims->Z + 64 >= (int64_t)INT_MAX) return CG_E_INVAL;
+    return CG_OK;
 }
 
 }  // namespace
@@ -208,8 +526,8 @@ const char *cg_status_str(cg_status s) {
 }
 
 const char *cg_version(void) {
-    return "colgraph 0.2 sm_100a (chunk-worklist lock-free push-relabel, frontier-BFS global relabel, "
-           "worklist extraction)";
+    return "colgraph 0.3 sm_100a (lock-free push-relabel: multi-hop walks + single-hop sweeps over vertex worklists, "
+           "device-driven frontier BFS relabel, worklist extraction, x-slab halos over NCCL)";
 }
 
 cg_status cg_slab_range(const cg_dims *dims, int32_t rank, int32_t nranks, int32_t *x0, int32_t *x1) {
@@ -220,123 +538,105 @@ cg_status cg_slab_range(const cg_dims *dims, int32_t rank, int32_t nranks, int32
     return CG_OK;
 }
 
+cg_status cg_nccl_unique_id(void *id_out) {
+    if (!id_out) return CG_E_INVAL;
+    if (!nccl().ok) return CG_E_NCCL;
+    ncclUniqueId id;
+    if (nccl().getUniqueId(&id) != ncclSuccess) return CG_E_NCCL;
+    memcpy(id_out, &id, sizeof(id));
+    return CG_OK;
+}
+
 void colgraph_free(cg_graph *g) {
     if (!g) return;
     {
         DeviceGuard dg(g->dist.device);
-        if (g->ws) cudaFreeAsync(g->ws, g->stream);
+        for (Slab *sl : g->slabs) slab_free(sl);
+        if (g->comm) nccl().commDestroy(g->comm);
+        if (g->d_red) cudaFree(g->d_red);
+        if (g->h_red) cudaFreeHost(g->h_red);
         if (g->ev0) cudaEventDestroy(g->ev0);
         if (g->ev1) cudaEventDestroy(g->ev1);
-        cudaFreeHost(g->h_cnt);
-        cudaFreeHost(g->h_work);
-        cudaFreeHost(g->h_u64);
-        cudaFreeHost(g->h_flags);
-        cudaFreeHost(g->h_bst);
     }
     delete g;
 }
 
-cg_status colgraph_build(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight, const cg_dist *dist,
-                         cg_graph **out) {
-    if (!dims || !cost_dev || !out) return CG_E_INVAL;
+// Common constructor: `nslabs_local` slabs in this process starting at global slab `rank`.
+static cg_status build_common(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight,
+                              const cg_dist *dist, int nranks, int rank, int nslabs_local, bool local,
+                              cg_graph **out) {
+    CG_TRY(validate_dims(dims));
+    if (!cost_dev || !out) return CG_E_INVAL;
     *out = nullptr;
-    if (dims->X < 1 || dims->Y < 1 || dims->Z < 1 || dims->delta < 0) return CG_E_INVAL;
-    const int64_t n = (int64_t)dims->X * dims->Y * dims->Z;
-    if (n + dims->Z + 64 >= (int64_t)INT_MAX) return CG_E_INVAL;
+    if (nranks < 1 || nranks > dims->X) return CG_E_INVAL;
     cg_dist dd{0, 1, nullptr, 0, nullptr};
     if (dist) dd = *dist;
-    if (dd.nranks != 1 || dd.rank != 0) return CG_E_INVAL;  // multi-GPU x-slabs: not in this build
     DeviceGuard dg(dd.device);
     const double t0 = now_ms();
     cg_graph *g = new cg_graph();
     g->dims = *dims;
     g->dist = dd;
-    g->stream = (cudaStream_t)dd.stream;
-    cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, dd.device);
-    Geo &geo = g->geo;
-    geo.X = dims->X;
-    geo.Y = dims->Y;
-    geo.Z = dims->Z;
-    geo.delta = dims->delta;
-    geo.CPC = (dims->Z + 31) / 32;
-    geo.n = n;
-    geo.YZ = (int64_t)dims->Y * dims->Z;
-    geo.nchunks = (int64_t)dims->X * dims->Y * geo.CPC;
-    geo.INF = (int32_t)(n + 1);
+    g->nranks = nranks;
+    g->rank = rank;
+    g->local = local;
+    g->n_global = (int64_t)dims->X * dims->Y * dims->Z;
     auto fail = [&](cg_status st) {
         colgraph_free(g);
         return st;
     };
-    cudaStream_t st = g->stream;
-    {  // keep freed workspaces cached in the stream-ordered pool (repeated solves allocate for free)
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dd.device) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-    }
-    g->ws_bytes = workspace_bytes(geo);
-    if (cudaMallocAsync(&g->ws, g->ws_bytes, st) != cudaSuccess) {
-        g->ws = nullptr;
-        return fail(CG_E_NOMEM);
-    }
-    if (cudaHostAlloc(&g->h_cnt, sizeof(unsigned) * 16, cudaHostAllocDefault) != cudaSuccess ||
-        cudaHostAlloc(&g->h_work, sizeof(unsigned long long) * RING, cudaHostAllocDefault) != cudaSuccess ||
-        cudaHostAlloc(&g->h_u64, sizeof(unsigned long long) * 16, cudaHostAllocDefault) != cudaSuccess ||
-        cudaHostAlloc(&g->h_flags, sizeof(int) * 16, cudaHostAllocDefault) != cudaSuccess ||
-        cudaHostAlloc(&g->h_bst, sizeof(BfsState), cudaHostAllocDefault) != cudaSuccess)
-        return fail(CG_E_NOMEM);
+    int num_sms = 148;
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dd.device);
     if (cudaEventCreate(&g->ev0) != cudaSuccess || cudaEventCreate(&g->ev1) != cudaSuccess) return fail(CG_E_CUDA);
-    const int64_t ncol = (int64_t)geo.X * geo.Y;
-    char *p = g->ws;
-    int32_t *soa = carve<int32_t>(p, 8 * n);
-    g->s.E = soa;
-    g->s.H = soa + n;
-    g->s.T = soa + 2 * n;
-    g->s.D = soa + 3 * n;
-    g->s.L = soa + 4 * n;
-    g->blist[0] = carve<int>(p, n);
-    g->blist[1] = carve<int>(p, n);
-    g->clist[0] = carve<int>(p, geo.nchunks);
-    g->clist[1] = carve<int>(p, geo.nchunks);
-    g->cstamp = carve<int>(p, geo.nchunks);
-    g->vstamp = carve<int>(p, n);
-    g->vertex_lists = getenv("CG_CHUNK_LISTS") == nullptr;
-    g->top = carve<int32_t>(p, ncol);
-    g->proc = carve<int32_t>(p, ncol);
-    g->colstamp = carve<int>(p, ncol);
-    g->collist[0] = carve<int>(p, ncol);
-    g->collist[1] = carve<int>(p, ncol);
-    g->hist = carve<unsigned>(p, GAP_BINS);
-    g->bst = carve<BfsState>(p, 1);
-    g->cnt = carve<unsigned>(p, 16);
-    g->work = carve<unsigned long long>(p, RING);
-    g->u64 = carve<unsigned long long>(p, 16);
-    g->flags = carve<int>(p, 16);
-    if (cudaMemsetAsync(g->s.H, 0, sizeof(int32_t) * n, st) != cudaSuccess ||
-        cudaMemsetAsync(g->s.D, 0, sizeof(int32_t) * 5 * n, st) != cudaSuccess ||
-        cudaMemsetAsync(g->cstamp, 0, sizeof(int) * geo.nchunks, st) != cudaSuccess ||
-        cudaMemsetAsync(g->vstamp, 0, sizeof(int) * n, st) != cudaSuccess ||
-        cudaMemsetAsync(g->colstamp, 0, sizeof(int) * ncol, st) != cudaSuccess ||
-        cudaMemsetAsync(g->cnt, 0, sizeof(unsigned) * 16, st) != cudaSuccess ||
-        cudaMemsetAsync(g->u64, 0, sizeof(unsigned long long) * 16, st) != cudaSuccess ||
-        cudaMemsetAsync(g->flags, 0, sizeof(int) * 16, st) != cudaSuccess)
-        return fail(CG_E_CUDA);
-    k_build<<<grid_for(ncol * 32, 256, g->num_sms * 16), 256, 0, st>>>(geo, cost_dev, input_is_weight ? 1 : 0, g->s,
-                                                                       g->u64, g->flags);
-    if (cudaGetLastError() != cudaSuccess) return fail(CG_E_CUDA);
-    cudaMemcpyAsync(g->h_u64, g->u64, sizeof(unsigned long long) * 2, cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(g->h_flags, g->flags, sizeof(int), cudaMemcpyDeviceToHost, st);
-    if (cudaStreamSynchronize(st) != cudaSuccess) return fail(CG_E_CUDA);
-    if (g->h_flags[0] & FLAG_OVERFLOW) return fail(CG_E_OVERFLOW);
-    g->N = (int64_t)g->h_u64[0];
-    g->sumT0 = (int64_t)g->h_u64[1];
-    g->st.source_capacity = g->N;
-    g->st.bytes_per_sweep_alg = 32.0 * (double)n;
-    g->st.kernel_launches = 1;
+    if (!local && nranks > 1) {
+        if (!dd.nccl_id || !nccl().ok) return fail(CG_E_NCCL);
+        ncclUniqueId id;
+        memcpy(&id, dd.nccl_id, sizeof(id));
+        if (nccl().commInitRank(&g->comm, nranks, id, rank) != ncclSuccess) return fail(CG_E_NCCL);
+        if (cudaMalloc(&g->d_red, 64 * sizeof(int64_t)) != cudaSuccess ||
+            cudaHostAlloc(&g->h_red, 64 * sizeof(int64_t), cudaHostAllocDefault) != cudaSuccess)
+            return fail(CG_E_NOMEM);
+    }
+    for (int i = 0; i < nslabs_local; i++) {
+        const int r = rank + i;
+        int32_t x0, x1;
+        if (cg_slab_range(dims, r, nranks, &x0, &x1) != CG_OK) return fail(CG_E_INVAL);
+        Slab *sl = new Slab();
+        sl->device = dd.device;
+        sl->stream = (cudaStream_t)dd.stream;
+        sl->num_sms = num_sms;
+        sl->x0 = x0;
+        sl->x1 = x1;
+        sl->geo = make_geo(dims, x0, x1, nranks, r > 0, r + 1 < nranks, g->n_global);
+        g->slabs.push_back(sl);
+        // LOCAL: cost_dev is the whole volume; NCCL / single: this rank's slab
+        const int32_t *src = local ? cost_dev + (int64_t)x0 * sl->geo.YZ : cost_dev;
+        const cg_status s = slab_build(sl, src, input_is_weight ? 1 : 0);
+        if (s != CG_OK) return fail(s);
+    }
+    int64_t fl = 0;
+    for (Slab *sl : g->slabs) fl |= sl->h_flags[0];
+    g->st.source_capacity = 0;
+    for (Slab *sl : g->slabs) g->st.source_capacity += sl->N;
+    CG_TRY(gsum(g, &g->st.source_capacity, 1));
+    g->st.bytes_per_sweep_alg = 32.0 * (double)g->n_global;
+    g->st.kernel_launches = nslabs_local;
     g->st.ms_build = now_ms() - t0;
     *out = g;
     return CG_OK;
+}
+
+cg_status colgraph_build(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight, const cg_dist *dist,
+                         cg_graph **out) {
+    cg_dist dd{0, 1, nullptr, 0, nullptr};
+    if (dist) dd = *dist;
+    if (dd.nranks < 1 || dd.rank < 0 || dd.rank >= dd.nranks) return CG_E_INVAL;
+    return build_common(dims, cost_dev, input_is_weight, &dd, dd.nranks, dd.rank, 1, false, out);
+}
+
+cg_status colgraph_build_slabs(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight, int32_t nslabs,
+                               const cg_dist *dist, cg_graph **out) {
+    if (nslabs < 1) return CG_E_INVAL;
+    return build_common(dims, cost_dev, input_is_weight, dist, nslabs, 0, nslabs, true, out);
 }
 
 cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_value, cg_solve_stats *stats) {
@@ -349,127 +649,156 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
     o.check_every = std::max(1, std::min(o.check_every, RING));
     o.ops_per_sweep = std::max(1, o.ops_per_sweep);
     if (!(o.gr_factor > 0.f)) o.gr_factor = 1.0f;
-    const Geo &geo = g->geo;
-    cudaStream_t st = g->stream;
     const bool trace = tracing();
     const double t0 = now_ms();
-    double ms_gr = 0.0, last_gr_ms = 0.0;
-    auto timed_gr = [&]() {
-        const double a = now_ms();
-        const int64_t p0 = g->st.gr_passes;
-        const cg_status s = global_relabel(g);
-        last_gr_ms = now_ms() - a;
-        ms_gr += last_gr_ms;
-        if (trace) {
-            // diagnostics only: current flow into t and total excess on active vertices
-            cudaMemsetAsync(g->u64 + 2, 0, sizeof(unsigned long long), st);
-            k_sum_T<<<g->num_sms * 8, 256, 0, st>>>(geo, g->s.T, g->u64 + 2);
-            cudaMemcpyAsync(g->h_u64 + 2, g->u64 + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
-            cudaStreamSynchronize(st);
-            fprintf(stderr, "[cg] GR#%lld levels=%lld active=%llu ms=%.3f (sweeps %lld) flow=%lld\n",
-                    (long long)g->st.global_relabels, (long long)(g->st.gr_passes - p0), g->h_u64[3], last_gr_ms,
-                    (long long)g->st.sweeps, (long long)(g->sumT0 - (int64_t)g->h_u64[2]));
-        }
-        return s;
-    };
-    // a1': exact per-column pre-cancellation (valid initial preflow)
-    const size_t pc_smem = (size_t)8 * (geo.Z + 1) * sizeof(long long);
+    Slab *s0 = g->slabs[0];
+    cudaStream_t st0 = s0->stream;
+    // a1': optional exact per-column pre-cancellation (valid initial preflow)
+    const size_t pc_smem = (size_t)8 * (g->dims.Z + 1) * sizeof(long long);
     if (getenv("CG_PRECANCEL") && pc_smem <= 200 * 1024) {  // opt-in: measured slower on C4/C5
         if (pc_smem > 48 * 1024)
             CG_CUDA(cudaFuncSetAttribute(k_precancel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pc_smem));
-        k_precancel<<<grid_for((int64_t)geo.X * geo.Y * 32, 256, g->num_sms * 16), 256, pc_smem, st>>>(geo, g->s,
-                                                                                                        g->flags);
-        g->st.kernel_launches++;
+        for (Slab *sl : g->slabs) {
+            k_precancel<<<grid_for((int64_t)sl->geo.X * sl->geo.Y * 32, 256, sl->num_sms * 16), 256, pc_smem,
+                          sl->stream>>>(sl->geo, sl->s, sl->flags);
+            g->st.kernel_launches++;
+        }
         CG_CUDA(cudaGetLastError());
     }
-    cg_status rs = timed_gr();
-    if (rs) return rs;
-    int64_t active = (int64_t)g->h_u64[3];
-    const double gr_budget = (double)o.gr_factor * (double)geo.n;
-    double work_since_gr = 0.0, sweep_ms_since_gr = 0.0;
-    int64_t sweeps = 0, since_gap = 0;
-    const int grid = list_grid(g, geo.nchunks);
-    const int gridv = list_grid(g, (geo.n + 31) / 32);
+    double ms_gr = 0.0, last_gr_ms = 0.0;
+    int64_t active = 0;
+    auto timed_gr = [&]() -> cg_status {
+        const double a = now_ms();
+        const int64_t p0 = g->st.gr_passes;
+        const cg_status s = global_relabel(g, &active);
+        last_gr_ms = now_ms() - a;
+        ms_gr += last_gr_ms;
+        if (trace) {
+            int64_t sumT = 0;
+            for (Slab *sl : g->slabs) {
+                cudaMemsetAsync(sl->u64 + 2, 0, sizeof(unsigned long long), sl->stream);
+                k_sum_T<<<sl->num_sms * 8, 256, 0, sl->stream>>>(sl->geo, sl->s.T, sl->u64 + 2);
+                cudaMemcpyAsync(sl->h_u64 + 2, sl->u64 + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                sl->stream);
+                cudaStreamSynchronize(sl->stream);
+                sumT += (int64_t)sl->h_u64[2] - sl->sumT0;
+            }
+            gsum(g, &sumT, 1);
+            fprintf(stderr, "[cg] GR#%lld levels=%lld active=%lld ms=%.3f (sweeps %lld) flow=%lld\n",
+                    (long long)g->st.global_relabels, (long long)(g->st.gr_passes - p0), (long long)active, last_gr_ms,
+                    (long long)g->st.sweeps, (long long)-sumT);
+        }
+        return s;
+    };
+    CG_TRY(timed_gr());
+    const double gr_budget = (double)o.gr_factor * (double)g->n_global;
     const double walk_min = getenv("CG_WALK_MIN") ? atof(getenv("CG_WALK_MIN")) : 1e-3;
-    int64_t last_active = active;
+    const double gr_beta = getenv("CG_GR_BETA") ? atof(getenv("CG_GR_BETA")) : 1.0;
+    double work_since_gr = 0.0, sweep_ms_since_gr = 0.0;
+    int64_t sweeps = 0, since_gap = 0, last_active = active;
+    std::vector<int64_t> wv(RING);
     cg_status result = CG_OK;
     while (active > 0) {
         if (sweeps >= o.max_sweeps) { result = CG_E_NOT_CONVERGED; break; }
         const int batch = (int)std::min<int64_t>(o.check_every, o.max_sweeps - sweeps);
-        CG_CUDA(cudaMemsetAsync(g->work, 0, sizeof(unsigned long long) * batch, st));
-        CG_CUDA(cudaEventRecord(g->ev0, st));
         // multi-hop walks while many vertices are active; single hops in the sparse tail
-        const bool walk = o.walk_len > 0 && (double)last_active >= walk_min * (double)geo.n;
-        // size the grid for the current worklist (the kernels stride, so growth is safe)
-        const int gv = std::max(g->num_sms, std::min(gridv, grid_for(2 * last_active, 256, gridv)));
+        const bool walk = o.walk_len > 0 && (double)last_active >= walk_min * (double)g->n_global;
+        for (Slab *sl : g->slabs) CG_CUDA(cudaMemsetAsync(sl->work, 0, sizeof(unsigned long long) * batch, sl->stream));
+        CG_CUDA(cudaEventRecord(g->ev0, st0));
         for (int i = 0; i < batch; i++) {
-            const int k = g->sweep_par++;
-            if (walk)
-                k_walk<<<gv, 256, 0, st>>>(geo, g->s, o.walk_len, g->blist[k & 1], g->cnt + k % 3,
-                                           g->blist[(k + 1) & 1], g->cnt + (k + 1) % 3, g->cnt + (k + 2) % 3,
-                                           g->vstamp, ++g->tag, g->work + i, g->flags);
-            else if (g->vertex_lists)
-                k_sweep_v<<<gv, 256, 0, st>>>(geo, g->s, o.ops_per_sweep, g->blist[k & 1], g->cnt + k % 3,
-                                              g->blist[(k + 1) & 1], g->cnt + (k + 1) % 3, g->cnt + (k + 2) % 3,
-                                              g->vstamp, ++g->tag, g->work + i, g->flags);
-            else
-                k_sweep<<<grid, 256, 0, st>>>(geo, g->s, o.ops_per_sweep, g->clist[k & 1], g->cnt + k % 3,
-                                              g->clist[(k + 1) & 1], g->cnt + (k + 1) % 3, g->cnt + (k + 2) % 3,
-                                              g->cstamp, ++g->tag, g->work + i, g->flags);
+            for (Slab *sl : g->slabs) {
+                const Geo &geo = sl->geo;
+                const int gridv = list_grid(sl, (geo.n + 31) / 32);
+                const int64_t la = std::max<int64_t>(1, last_active / (int64_t)g->nranks);
+                const int gv = std::max(sl->num_sms, std::min(gridv, grid_for(2 * la, 256, gridv)));
+                const int k = sl->sweep_k++;
+                sl->out_tag = ++sl->tag;
+                if (walk)
+                    k_walk<<<gv, 256, 0, sl->stream>>>(geo, sl->s, o.walk_len, sl->blist[k & 1], sl->cnt + k % 3,
+                                                       sl->blist[(k + 1) & 1], sl->cnt + (k + 1) % 3,
+                                                       sl->cnt + (k + 2) % 3, sl->vstamp, sl->out_tag, sl->work + i,
+                                                       sl->flags);
+                else
+                    k_sweep_v<<<gv, 256, 0, sl->stream>>>(geo, sl->s, o.ops_per_sweep, sl->blist[k & 1],
+                                                          sl->cnt + k % 3, sl->blist[(k + 1) & 1],
+                                                          sl->cnt + (k + 1) % 3, sl->cnt + (k + 2) % 3, sl->vstamp,
+                                                          sl->out_tag, sl->work + i, sl->flags);
+                g->st.kernel_launches++;
+            }
+            if (multi(g)) CG_TRY(halo_sweep(g));
         }
-        CG_CUDA(cudaEventRecord(g->ev1, st));
-        g->st.kernel_launches += batch;
+        CG_CUDA(cudaEventRecord(g->ev1, st0));
         CG_CUDA(cudaGetLastError());
-        CG_CUDA(cudaMemcpyAsync(g->h_work, g->work, sizeof(unsigned long long) * batch, cudaMemcpyDeviceToHost, st));
-        CG_CUDA(cudaMemcpyAsync(g->h_flags, g->flags, sizeof(int), cudaMemcpyDeviceToHost, st));
-        CG_CUDA(cudaStreamSynchronize(st));
+        for (Slab *sl : g->slabs) {
+            CG_CUDA(cudaMemcpyAsync(sl->h_work, sl->work, sizeof(unsigned long long) * batch, cudaMemcpyDeviceToHost,
+                                    sl->stream));
+            CG_CUDA(cudaMemcpyAsync(sl->h_flags, sl->flags, sizeof(int), cudaMemcpyDeviceToHost, sl->stream));
+        }
+        int64_t overflow = 0;
+        std::fill(wv.begin(), wv.begin() + batch, 0);
+        for (Slab *sl : g->slabs) {
+            CG_CUDA(cudaStreamSynchronize(sl->stream));
+            overflow |= sl->h_flags[0] & FLAG_OVERFLOW;
+            for (int i = 0; i < batch; i++) wv[i] += (int64_t)sl->h_work[i];
+        }
         float ms = 0.f;
         cudaEventElapsedTime(&ms, g->ev0, g->ev1);
         g->st.ms_sweep_kernels += ms;
         sweep_ms_since_gr += ms;
-        if (g->h_flags[0] & FLAG_OVERFLOW) { result = CG_E_OVERFLOW; break; }
+        wv[batch] = overflow;
+        CG_TRY(gsum(g, wv.data(), batch + 1));
+        if (wv[batch]) { result = CG_E_OVERFLOW; break; }
         if (trace) {
-            fprintf(stderr, "[cg] sweeps %lld..%lld active:", (long long)sweeps, (long long)(sweeps + batch - 1));
-            for (int i = 0; i < batch; i += std::max(1, batch / 8)) fprintf(stderr, " %llu", g->h_work[i]);
-            fprintf(stderr, " | %.3f ms\n", ms);
+            fprintf(stderr, "[cg] sweeps %lld..%lld ops:", (long long)sweeps, (long long)(sweeps + batch - 1));
+            for (int i = 0; i < batch; i += std::max(1, batch / 8)) fprintf(stderr, " %lld", (long long)wv[i]);
+            fprintf(stderr, " | %.3f ms%s\n", ms, walk ? " (walk)" : "");
         }
         bool quiescent = false;
-        last_active = (int64_t)g->h_work[batch - 1];
+        last_active = wv[batch - 1];
         for (int i = 0; i < batch; i++) {
-            const unsigned long long c = g->h_work[i];
-            g->st.sweep_bytes_alg += 44.0 * (double)c;  // 32 B state read + 12 B push writes
-            if (c == 0) { quiescent = true; break; }
-            work_since_gr += (double)c;
-            g->st.work += (int64_t)c;
+            g->st.sweep_bytes_alg += 44.0 * (double)wv[i];  // 32 B state read + 12 B push writes
+            if (wv[i] == 0) { quiescent = true; break; }
+            work_since_gr += (double)wv[i];
+            g->st.work += wv[i];
         }
         sweeps += batch;
         since_gap += batch;
         g->st.sweeps = sweeps;
-        if (quiescent || work_since_gr >= gr_budget || sweep_ms_since_gr >= std::max(last_gr_ms, 0.05)) {
+        // the time-based trigger is a local measurement: agree on it across ranks
+        int64_t trigger = quiescent || work_since_gr >= gr_budget || sweep_ms_since_gr >= gr_beta * std::max(last_gr_ms, 0.05);
+        CG_TRY(gmax(g, &trigger));
+        if (trigger) {
             // a4: termination is decided only after an exact global relabel
-            rs = timed_gr();
-            if (rs) { result = rs; break; }
-            active = (int64_t)g->h_u64[3];
+            CG_TRY(timed_gr());
             last_active = active;
             work_since_gr = 0.0;
             sweep_ms_since_gr = 0.0;
             since_gap = 0;
-        } else if (o.gap_every > 0 && since_gap >= o.gap_every) {
-            rs = run_gap(g);
-            if (rs) { result = rs; break; }
+        } else if (o.gap_every > 0 && since_gap >= o.gap_every && !multi(g)) {
+            CG_TRY(run_gap(g, s0));
             since_gap = 0;
         }
     }
     if (result != CG_OK && result != CG_E_NOT_CONVERGED) return result;
     // a6: |f| = sum(T0) - sum(T)
-    CG_CUDA(cudaMemsetAsync(g->u64 + 2, 0, sizeof(unsigned long long), st));
-    k_sum_T<<<g->num_sms * 8, 256, 0, st>>>(geo, g->s.T, g->u64 + 2);
-    g->st.kernel_launches++;
-    CG_CUDA(cudaMemcpyAsync(g->h_u64 + 2, g->u64 + 2, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    CG_CUDA(cudaStreamSynchronize(st));
+    int64_t red[3] = {0, 0, 0};
+    for (Slab *sl : g->slabs) {
+        CG_CUDA(cudaMemsetAsync(sl->u64 + 2, 0, sizeof(unsigned long long), sl->stream));
+        k_sum_T<<<sl->num_sms * 8, 256, 0, sl->stream>>>(sl->geo, sl->s.T, sl->u64 + 2);
+        g->st.kernel_launches++;
+        CG_CUDA(cudaMemcpyAsync(sl->h_u64 + 2, sl->u64 + 2, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                sl->stream));
+    }
+    for (Slab *sl : g->slabs) {
+        CG_CUDA(cudaStreamSynchronize(sl->stream));
+        red[0] += sl->sumT0;
+        red[1] += (int64_t)sl->h_u64[2];
+        red[2] += (int64_t)sl->h_u64[4];
+    }
     CG_CUDA(cudaGetLastError());
-    *flow_value = g->sumT0 - (int64_t)g->h_u64[2];
-    g->st.gap_lifted = (int64_t)g->h_u64[4];
+    CG_TRY(gsum(g, red, 3));
+    *flow_value = red[0] - red[1];
+    g->st.gap_lifted = red[2];
     g->st.ms_global_relabel = ms_gr;
     g->st.ms_solve = now_ms() - t0;
     g->st.ms_sweeps = g->st.ms_solve - ms_gr;
@@ -482,38 +811,92 @@ cg_status mincut_extract_surface(cg_graph *g, int32_t *surface_dev, uint8_t *mas
     if (!g || !surface_dev) return CG_E_INVAL;
     if (!g->solved) return CG_E_STATE;
     DeviceGuard dg(g->dist.device);
-    const Geo &geo = g->geo;
-    cudaStream_t st = g->stream;
     const double t0 = now_ms();
-    const int64_t ncol = (int64_t)geo.X * geo.Y;
-    CG_CUDA(cudaMemsetAsync(g->cnt + 8, 0, 3 * sizeof(unsigned), st));
-    const int tag = ++g->tag;
-    k_ext_seed<<<grid_for(ncol, 256, g->num_sms * 16), 256, 0, st>>>(geo, g->s, g->top, g->proc, g->collist[0],
-                                                                      g->cnt + 8, g->colstamp, tag);
-    g->st.kernel_launches++;
-    const int grid = list_grid(g, ncol);
-    int r = 0;
-    for (;;) {
-        for (int b = 0; b < EXT_BATCH; b++, r++) {
-            k_ext_round<<<grid, 256, 0, st>>>(geo, g->s, g->collist[r & 1], g->cnt + 8 + r % 3,
-                                               g->collist[(r + 1) & 1], g->cnt + 8 + (r + 1) % 3,
-                                               g->cnt + 8 + (r + 2) % 3, g->top, g->proc, g->colstamp, ++g->tag);
-        }
-        g->st.kernel_launches += EXT_BATCH;
-        CG_CUDA(cudaGetLastError());
-        CG_CUDA(cudaMemcpyAsync(g->h_cnt + 8, g->cnt + 8 + r % 3, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-        CG_CUDA(cudaStreamSynchronize(st));
-        if (g->h_cnt[8] == 0) break;
+    for (Slab *sl : g->slabs) {
+        const Geo &geo = sl->geo;
+        const int64_t ncol = (int64_t)geo.X * geo.Y;
+        CG_CUDA(cudaMemsetAsync(sl->cnt + 8, 0, 3 * sizeof(unsigned), sl->stream));
+        CG_CUDA(cudaMemsetAsync(sl->top - geo.Y, 0xff, sizeof(int32_t) * (ncol + 2 * geo.Y), sl->stream));
+        sl->ext_k = 0;
+        k_ext_seed<<<grid_for(ncol, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(
+            geo, sl->s, sl->top, sl->proc, sl->collist[0], sl->cnt + 8, sl->colstamp, ++sl->tag);
+        g->st.kernel_launches++;
     }
-    g->st.extract_passes += r;
-    CG_CUDA(cudaMemsetAsync(g->flags + 3, 0, sizeof(int), st));
-    k_ext_out<<<g->num_sms * 8, 256, 0, st>>>(geo, g->top, surface_dev, mask_dev, g->flags + 3);
-    g->st.kernel_launches++;
-    CG_CUDA(cudaMemcpyAsync(g->h_flags + 3, g->flags + 3, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CG_CUDA(cudaStreamSynchronize(st));
+    for (int outer = 0;; outer++) {
+        if (multi(g)) {  // exchange column tops (proposals for ghosts, boundary tops)
+            for (Slab *sl : g->slabs) {
+                const Geo &geo = sl->geo;
+                CG_CUDA(cudaMemsetAsync(sl->cnt + 12, 0, sizeof(unsigned), sl->stream));
+                if (geo.gl) k_top_halo_pack<<<1, 256, 0, sl->stream>>>(geo, sl->top, 0, sl->hsend[0]);
+                if (geo.gh) k_top_halo_pack<<<1, 256, 0, sl->stream>>>(geo, sl->top, 1, sl->hsend[1]);
+            }
+            CG_TRY(transfer(g, 2 * g->dims.Y));
+            for (Slab *sl : g->slabs) {
+                const Geo &geo = sl->geo;
+                const int r = sl->ext_k;
+                const int tag = ++sl->tag;
+                for (int side = 0; side < 2; side++)
+                    if (side ? geo.gh : geo.gl)
+                        k_top_halo_unpack<<<grid_for(geo.Y, 256, sl->num_sms), 256, 0, sl->stream>>>(
+                            geo, sl->top, side, sl->hrecv[side], sl->hsend[side], sl->collist[r & 1],
+                            sl->cnt + 8 + r % 3, sl->colstamp, tag, sl->cnt + 12);
+            }
+        }
+        // local rounds until every column list is empty
+        for (;;) {
+            int64_t pending = 0;
+            for (Slab *sl : g->slabs) {
+                const Geo &geo = sl->geo;
+                const int grid = list_grid(sl, (int64_t)geo.X * geo.Y);
+                for (int b = 0; b < EXT_BATCH; b++) {
+                    const int r = sl->ext_k++;
+                    k_ext_round<<<grid, 256, 0, sl->stream>>>(geo, sl->s, sl->collist[r & 1], sl->cnt + 8 + r % 3,
+                                                               sl->collist[(r + 1) & 1], sl->cnt + 8 + (r + 1) % 3,
+                                                               sl->cnt + 8 + (r + 2) % 3, sl->top, sl->proc,
+                                                               sl->colstamp, ++sl->tag);
+                }
+                g->st.kernel_launches += EXT_BATCH;
+                g->st.extract_passes += EXT_BATCH;
+                CG_CUDA(cudaGetLastError());
+                CG_CUDA(cudaMemcpyAsync(sl->h_cnt + 8, sl->cnt + 8, 5 * sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                        sl->stream));
+            }
+            for (Slab *sl : g->slabs) {
+                CG_CUDA(cudaStreamSynchronize(sl->stream));
+                pending += sl->h_cnt[8 + sl->ext_k % 3];
+            }
+            if (pending == 0) break;
+        }
+        if (!multi(g)) break;
+        // another exchange is needed iff some ghost proposal or boundary top changed: run one
+        // more exchange and stop when it changed nothing anywhere
+        int64_t changed = 0;
+        if (outer > 0)
+            for (Slab *sl : g->slabs) changed += sl->h_cnt[12];
+        else
+            changed = 1;
+        CG_TRY(gsum(g, &changed, 1));
+        if (changed == 0) break;
+    }
+    int empty = 0;
+    for (Slab *sl : g->slabs) {
+        const Geo &geo = sl->geo;
+        CG_CUDA(cudaMemsetAsync(sl->flags + 3, 0, sizeof(int), sl->stream));
+        const int64_t soff = g->local ? (int64_t)sl->x0 * geo.Y : 0, moff = g->local ? (int64_t)sl->x0 * geo.YZ : 0;
+        k_ext_out<<<sl->num_sms * 8, 256, 0, sl->stream>>>(geo, sl->top, surface_dev + soff,
+                                                            mask_dev ? mask_dev + moff : nullptr, sl->flags + 3);
+        g->st.kernel_launches++;
+        CG_CUDA(cudaMemcpyAsync(sl->h_flags + 3, sl->flags + 3, sizeof(int), cudaMemcpyDeviceToHost, sl->stream));
+    }
+    for (Slab *sl : g->slabs) {
+        CG_CUDA(cudaStreamSynchronize(sl->stream));
+        empty |= sl->h_flags[3];
+    }
     CG_CUDA(cudaGetLastError());
+    int64_t e64 = empty;
+    CG_TRY(gmax(g, &e64));
     g->st.ms_extract = now_ms() - t0;
-    return g->h_flags[3] ? CG_E_EMPTY_COLUMN : CG_OK;
+    return e64 ? CG_E_EMPTY_COLUMN : CG_OK;
 }
 
 cg_status colgraph_stats(const cg_graph *g, cg_solve_stats *stats) {
@@ -525,16 +908,23 @@ cg_status colgraph_stats(const cg_graph *g, cg_solve_stats *stats) {
 cg_status colgraph_export_state(cg_graph *g, int32_t *out_dev) {
     if (!g || !out_dev) return CG_E_INVAL;
     DeviceGuard dg(g->dist.device);
-    CG_CUDA(cudaMemcpyAsync(out_dev, g->s.E, sizeof(int32_t) * 8 * g->geo.n, cudaMemcpyDeviceToDevice, g->stream));
-    CG_CUDA(cudaStreamSynchronize(g->stream));
+    const int64_t ntot = g->local ? g->n_global : g->slabs[0]->geo.n;
+    for (Slab *sl : g->slabs) {
+        const int64_t off = g->local ? (int64_t)sl->x0 * sl->geo.YZ : 0;
+        const int32_t *planes[8] = {sl->s.E, sl->s.H, sl->s.T, sl->s.D, sl->s.L[0], sl->s.L[1], sl->s.L[2], sl->s.L[3]};
+        for (int f = 0; f < 8; f++)
+            CG_CUDA(cudaMemcpyAsync(out_dev + f * ntot + off, planes[f], sizeof(int32_t) * sl->geo.n,
+                                    cudaMemcpyDeviceToDevice, sl->stream));
+    }
+    for (Slab *sl : g->slabs) CG_CUDA(cudaStreamSynchronize(sl->stream));
     return CG_OK;
 }
 
 cg_status colgraph_solve_host(const cg_dims *dims, const int32_t *cost_host, int32_t input_is_weight,
                               const cg_dist *dist, const cg_solve_opts *opts, int64_t *flow_value,
                               int32_t *surface_host, uint8_t *mask_host, cg_solve_stats *stats) {
-    if (!dims || !cost_host || !flow_value || !surface_host) return CG_E_INVAL;
-    if (dims->X < 1 || dims->Y < 1 || dims->Z < 1) return CG_E_INVAL;
+    if (!cost_host || !flow_value || !surface_host) return CG_E_INVAL;
+    CG_TRY(validate_dims(dims));
     cg_dist dd{0, 1, nullptr, 0, nullptr};
     if (dist) dd = *dist;
     if (dd.nranks != 1) return CG_E_INVAL;
@@ -569,3 +959,4 @@ cg_status colgraph_solve_host(const cg_dims *dims, const int32_t *cost_host, int
 }
 
 }  // extern "C"
+

@@ -16,20 +16,28 @@ namespace cg {
 constexpr unsigned FULL = 0xffffffffu;
 
 struct Geo {
-    int32_t X, Y, Z, delta;  // X = x-planes owned by this rank
+    int32_t X, Y, Z, delta;  // X = x-planes owned by this slab
     int32_t CPC;             // chunks per column = ceil(Z / 32)
-    int64_t n;               // vertices owned by this rank
+    int32_t gl, gh;          // a ghost plane exists at x = -1 (gl) / x = X (gh): neighbour slab
+    int64_t n;               // vertices owned by this slab
     int64_t YZ;              // vertices per x-plane
     int64_t nchunks;         // X*Y*CPC
     int32_t INF;             // n_global + 1: "cannot reach t"
 };
 
-// 8 int32 planes of n: E excess, H height, T sink residual, D flow on the down arc
-// (= residual of the up arc into this vertex from below), L[d] flow on the lateral arc in
-// direction d (= residual of its reverse arc).  Directions: 0:+x 1:-x 2:+y 3:-y.
+// 8 int32 planes: E excess, H height, T sink residual, D flow on the down arc (= residual
+// of the up arc into this vertex from below), L[d] flow on the lateral arc in direction d
+// (= residual of its reverse arc).  Directions: 0:+x 1:-x 2:+y 3:-y.  Each plane holds
+// X+2 x-planes; the pointers address owned plane x = 0, so the ghost planes of the
+// neighbour slabs sit at vertex indices [-YZ, 0) and [n, n+YZ).
 struct Soa {
-    int32_t *E, *H, *T, *D, *L;  // L + d*n
+    int32_t *E, *H, *T, *D;
+    int32_t *L[4];
 };
+
+constexpr int64_t NONE = INT64_MIN;  // "no vertex" (ghost vertices of the x = -1 plane are negative)
+
+__device__ __forceinline__ bool owned(const Geo &g, int64_t v) { return v >= 0 && v < g.n; }
 
 enum { FLAG_OVERFLOW = 1 };
 
@@ -46,8 +54,8 @@ __device__ __forceinline__ int zi_of(int z, int delta, int Z) { return z == 0 ? 
 // neighbour column offset (in vertices) in direction d, 0 if the neighbour is outside the slab
 __device__ __forceinline__ int64_t nbr_off(const Geo &g, int x, int y, int d) {
     switch (d) {
-        case 0: return x + 1 < g.X ? g.YZ : 0;
-        case 1: return x >= 1 ? -g.YZ : 0;
+        case 0: return (x + 1 < g.X || g.gh) ? g.YZ : 0;
+        case 1: return (x >= 1 || g.gl) ? -g.YZ : 0;
         case 2: return y + 1 < g.Y ? (int64_t)g.Z : 0;
         default: return y >= 1 ? -(int64_t)g.Z : 0;
     }

@@ -1,12 +1,15 @@
 // kernels.cuh -- the sm_100a kernels of the column-graph max-flow hot path.
 //
-//   a1 build            k_build               PAPER.md §1.2; §2.1 L134 (init)
-//   a2/a5 global relabel k_bfs_init/k_bfs_level PAPER.md §2.1; Alg. 3; §3.2.2
-//   a3 sweep            k_sweep               PAPER.md §2.1; Alg. 2
-//   a4 termination      k_rebuild_chunks (+ host loop)  PAPER.md §3.2.4; Alg. 1
-//   a5 gap              k_gap_*               PAPER.md §2.1
-//   a6 flow value       k_sum_T               PAPER.md Eq. 5
-//   a7 extraction       k_ext_*               PAPER.md Theorem 1
+//   a1  build             k_build                      PAPER.md §1.2; §2.1 L134 (init)
+//   a1' pre-cancellation  k_precancel (opt-in)         not in the paper
+//   a2/a5 global relabel  k_bfs_init + k_bfs_step      PAPER.md §2.1; Alg. 3; §3.2.2
+//                         k_lc_wave/k_lc_ghost (slabs) label-correcting variant across x-slabs
+//   a3  sweep             k_walk (multi-hop), k_sweep_v PAPER.md §2.1; Alg. 2
+//   a4  termination       k_rebuild_vertices + host    PAPER.md §3.2.4; Alg. 1
+//   a5  gap               k_gap_*                      PAPER.md §2.1
+//   a6  flow value        k_sum_T                      PAPER.md Eq. 5
+//   a7  extraction        k_ext_*                      PAPER.md Theorem 1
+//   a8  halo exchange     k_halo_*, k_ghost_*          PAPER.md §3.2.1 L254 (shared vertices)
 #pragma once
 
 #include "common.cuh"
@@ -57,170 +60,29 @@ __global__ void k_fill(int32_t *p, int64_t n, int32_t v) {
 }
 
 // ------------------------------------------------------------------ a3: push-relabel sweep
-// One warp per listed chunk (32 consecutive z of a column; all state loads coalesced).
-// Each active lane (E > 0, H < INF) performs up to `ops` operations of Alg. 2:
-//   scan the residual out-arcs in the fixed order t, down, lateral-out(+x,-x,+y,-y),
-//   up, lateral-in-reverse(+x,-x,+y,-y); h_min = lowest neighbour height (first wins);
-//   relabel H = h_min + 1 if H <= h_min ("newd = min label(w)+1 ... only if newd >
-//   label(v)"); push delta = min(E, r) along that arc (r = INF on infinite arcs).
-// Lock-free: every residual has one decrementer, so each
-// stale read is a lower bound of what the reader may subtract.
-// Worklist: chunks that received a push or still hold active excess are appended to
-// the next list (de-duplicated by stamp == tag).
+// An active vertex (E > 0, H < INF) runs Alg. 2: it scans its residual out-arcs in the
+// fixed order t, down, lateral-out(+x,-x,+y,-y), up, lateral-in-reverse(+x,-x,+y,-y),
+// pushes delta = min(E, r) (r = INF on infinite arcs) on the first admissible arc
+// (neighbour label < own label), or relabels to min label(w)+1 ("newd = min label(w)+1
+// ... only if newd > label(v)") and pushes on that arc.
+// Lock-free rule: every residual field has one decrementer, so each stale
+// read is a lower bound of what the reader may subtract.
 struct OpCtx {
     int64_t v, v0, col;
     int z, zo, zi;
     int64_t off[4];  // vertex offset of the neighbour column (0 = none)
-    int coff[4];     // column-index offset of the neighbour column
 };
-
-// One push/relabel operation; returns the chunk id that received flow (or -1).
-__device__ __forceinline__ int pr_op(const Geo &g, const Soa &s, const OpCtx &c, int &e, int &h, int &sent,
-                                     int *flags) {
-    int best = g.INF, arc = -1, res = 0, tz = 0, tco = 0;
-    int64_t tgt = -1;
-    const int tres = s.T[c.v];
-    if (tres > 0) {
-        best = 0;
-        arc = 0;
-    } else {
-        if (c.z >= 1) {
-            const int hh = s.H[c.v - 1];
-            if (hh < best) { best = hh; arc = 1; tgt = c.v - 1; tz = c.z - 1; tco = 0; }
-        }
-        if (c.zo >= 0) {
-#pragma unroll
-            for (int d = 0; d < 4; d++) {
-                if (!c.off[d]) continue;
-                const int64_t t = c.v0 + c.off[d] + c.zo;
-                const int hh = s.H[t];
-                if (hh < best) { best = hh; arc = 2 + d; tgt = t; tz = c.zo; tco = c.coff[d]; }
-            }
-        }
-        if (c.z + 1 < g.Z) {
-            const int r = s.D[c.v + 1];
-            if (r > 0) {
-                const int hh = s.H[c.v + 1];
-                if (hh < best) { best = hh; arc = 6; tgt = c.v + 1; res = r; tz = c.z + 1; tco = 0; }
-            }
-        }
-        if (c.zi >= 0) {
-#pragma unroll
-            for (int d = 0; d < 4; d++) {
-                if (!c.off[d]) continue;
-                const int64_t u = c.v0 + c.off[d] + c.zi;
-                const int r = s.L[(int64_t)(d ^ 1) * g.n + u];
-                if (r > 0) {
-                    const int hh = s.H[u];
-                    if (hh < best) { best = hh; arc = 7 + d; tgt = u; res = r; tz = c.zi; tco = c.coff[d]; }
-                }
-            }
-        }
-    }
-    if (best >= g.INF) {  // no residual path known: dead until the next global relabel
-        h = g.INF;
-        s.H[c.v] = h;
-        return -1;
-    }
-    if (h <= best) {  // relabel (Alg. 2 Relabel)
-        h = best + 1;
-        s.H[c.v] = h;
-        if (h >= g.INF) return -1;
-    }
-    int df;  // push (Alg. 2 Push)
-    switch (arc) {
-        case 0:
-            df = min(e, tres);
-            s.T[c.v] = tres - df;
-            break;
-        case 1:
-            df = e;
-            atomicAdd(&s.D[c.v], df);
-            break;
-        case 2: case 3: case 4: case 5:
-            df = e;
-            atomicAdd(&s.L[(int64_t)(arc - 2) * g.n + c.v], df);
-            break;
-        case 6:
-            df = min(e, res);
-            atomicSub(&s.D[c.v + 1], df);
-            break;
-        default:
-            df = min(e, res);
-            atomicSub(&s.L[(int64_t)((arc - 7) ^ 1) * g.n + tgt], df);
-            break;
-    }
-    e -= df;
-    sent += df;
-    if (tgt < 0) return -1;
-    const int old = atomicAdd(&s.E[tgt], df);
-    if (old > INT_MAX - df) atomicOr(flags, FLAG_OVERFLOW);
-    return (int)((c.col + tco) * g.CPC + (tz >> 5));
-}
-
-__global__ void __launch_bounds__(256) k_sweep(Geo g, Soa s, int ops, const int *__restrict__ lin,
-                                               const unsigned *cin, int *lout, unsigned *cout, unsigned *czero,
-                                               int *stamp, int tag, unsigned long long *work, int *flags) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) *czero = 0;
-    const int64_t count = *cin;
-    unsigned long long mywork = 0;
-    for (int64_t i = gwarp(); i < count; i += nwarps()) {
-        const int chunk = lin[i];
-        OpCtx c;
-        c.col = chunk / g.CPC;
-        c.z = (int)(chunk - c.col * g.CPC) * 32 + lane_id();
-        const bool valid = c.z < g.Z;
-        c.v0 = c.col * g.Z;
-        c.v = c.v0 + c.z;
-        int e = valid ? s.E[c.v] : 0;
-        int h = valid ? s.H[c.v] : g.INF;
-        bool act = e > 0 && h < g.INF;
-        const unsigned am = __ballot_sync(FULL, act);
-        if (!am) continue;
-        mywork += __popc(am);
-        const int x = (int)(c.col / g.Y), y = (int)(c.col - (int64_t)x * g.Y);
-        c.zo = zo_of(c.z, g.delta);
-        c.zi = zi_of(c.z, g.delta, g.Z);
-#pragma unroll
-        for (int d = 0; d < 4; d++) c.off[d] = nbr_off(g, x, y, d);
-        c.coff[0] = g.Y; c.coff[1] = -g.Y; c.coff[2] = 1; c.coff[3] = -1;
-        int sent = 0;
-        for (int it = 0; it < ops; ++it) {
-            int tchunk = -1;
-            if (act) {
-                tchunk = pr_op(g, s, c, e, h, sent, flags);
-                act = e > 0 && h < g.INF;
-            }
-            warp_mark(tchunk, stamp, tag, lout, cout);
-            if (!__any_sync(FULL, act)) break;
-        }
-        if (sent) atomicSub(&s.E[c.v], sent);
-        warp_mark(__any_sync(FULL, act) ? chunk : -1, stamp, tag, lout, cout);
-    }
-    if (lane_id() == 0 && mywork) atomicAdd(work, mywork);
-}
-
-// Vertex-granular worklist variant (default): one thread per listed vertex.  Sparse
-// activity (1-2% of the vertices, scattered) would leave 31 of 32 lanes idle in the
-// chunk variant; here every lane carries an active vertex.
-__device__ __forceinline__ void mark_vertex(int64_t id, int *vstamp, int tag, int *list, unsigned *count) {
-    bool add = id >= 0 && vstamp[id] != tag;
-    if (add) add = atomicExch(&vstamp[id], tag) != tag;
-    warp_append(add, (int)id, list, count);
-}
 
 struct ArcPick {
     int best, arc, res;
     int64_t tgt;
 };
 
-// Arc scan in the fixed order t, down, lateral-out(+x,-x,+y,-y), up, lateral-in-reverse.
-// Returns the FIRST admissible arc (neighbour label < hx: Alg. 2 pushes on any admissible
-// arc, and with exact labels every admissible neighbour sits at hx-1); if none is
-// admissible, the lowest residual neighbour (for the relabel "newd = min label(w)+1").
-// Early exit saves most of the scattered loads in the common case.
+// FIRST admissible arc (label < hx) in the fixed order; if none, the lowest residual
+// neighbour (for the relabel).  With exact labels every admissible neighbour sits at hx-1,
+// so the early exit changes nothing but the number of scattered loads.
 __device__ __forceinline__ ArcPick scan_arcs(const Geo &g, const Soa &s, const OpCtx &c, int hx) {
-    ArcPick p{g.INF, -1, 0, -1};
+    ArcPick p{g.INF, -1, 0, NONE};
     const int tres = s.T[c.v];
     if (tres > 0) {
         p.best = 0; p.arc = 0; p.res = tres;
@@ -254,7 +116,7 @@ __device__ __forceinline__ ArcPick scan_arcs(const Geo &g, const Soa &s, const O
         for (int d = 0; d < 4; d++) {
             if (!c.off[d]) continue;
             const int64_t u = c.v0 + c.off[d] + c.zi;
-            const int r = s.L[(int64_t)(d ^ 1) * g.n + u];
+            const int r = s.L[d ^ 1][u];
             if (r > 0) {
                 const int hh = s.H[u];
                 if (hh < p.best) { p.best = hh; p.arc = 7 + d; p.tgt = u; p.res = r; }
@@ -265,26 +127,39 @@ __device__ __forceinline__ ArcPick scan_arcs(const Geo &g, const Soa &s, const O
     return p;
 }
 
-__device__ __forceinline__ int64_t pr_op_v(const Geo &g, const Soa &s, const OpCtx &c, int &e, int &h, int &sent,
-                                           int *flags) {
+__device__ __forceinline__ void set_ctx(const Geo &g, OpCtx &c, int64_t v) {
+    c.v = v;
+    c.col = v / g.Z;
+    c.z = (int)(v - c.col * g.Z);
+    c.v0 = c.col * g.Z;
+    const int x = (int)(c.col / g.Y), y = (int)(c.col - (int64_t)x * g.Y);
+    c.zo = zo_of(c.z, g.delta);
+    c.zi = zi_of(c.z, g.delta, g.Z);
+#pragma unroll
+    for (int d = 0; d < 4; d++) c.off[d] = nbr_off(g, x, y, d);
+}
+
+// Single push/relabel operation of the owner of c.v; returns the vertex that received
+// flow (NONE: none or t; ghost vertices have negative indices).  Decrements follow the
+// single-decrementer rule.
+__device__ __forceinline__ int64_t pr_op(const Geo &g, const Soa &s, const OpCtx &c, int &e, int &h, int &sent,
+                                         int *flags) {
     const ArcPick p = scan_arcs(g, s, c, h);
-    const int best = p.best, arc = p.arc, res = p.res, tres = p.res;
-    const int64_t tgt = p.tgt;
-    if (best >= g.INF) {
+    if (p.best >= g.INF) {  // no residual path known: dead until the next global relabel
         h = g.INF;
         s.H[c.v] = h;
-        return -1;
+        return NONE;
     }
-    if (h <= best) {
-        h = best + 1;
+    if (h <= p.best) {  // relabel
+        h = p.best + 1;
         s.H[c.v] = h;
-        if (h >= g.INF) return -1;
+        if (h >= g.INF) return NONE;
     }
-    int df;
-    switch (arc) {
+    int df;  // push
+    switch (p.arc) {
         case 0:
-            df = min(e, tres);
-            s.T[c.v] = tres - df;
+            df = min(e, p.res);
+            s.T[c.v] = p.res - df;
             break;
         case 1:
             df = e;
@@ -292,23 +167,32 @@ __device__ __forceinline__ int64_t pr_op_v(const Geo &g, const Soa &s, const OpC
             break;
         case 2: case 3: case 4: case 5:
             df = e;
-            atomicAdd(&s.L[(int64_t)(arc - 2) * g.n + c.v], df);
+            atomicAdd(&s.L[p.arc - 2][c.v], df);
             break;
         case 6:
-            df = min(e, res);
+            df = min(e, p.res);
             atomicSub(&s.D[c.v + 1], df);
             break;
         default:
-            df = min(e, res);
-            atomicSub(&s.L[(int64_t)((arc - 7) ^ 1) * g.n + tgt], df);
+            df = min(e, p.res);
+            atomicSub(&s.L[(p.arc - 7) ^ 1][p.tgt], df);
             break;
     }
     e -= df;
     sent += df;
-    if (tgt < 0) return -1;
-    const int old = atomicAdd(&s.E[tgt], df);
+    if (p.arc == 0) return NONE;
+    const int old = atomicAdd(&s.E[p.tgt], df);
     if (old > INT_MAX - df) atomicOr(flags, FLAG_OVERFLOW);
-    return tgt;
+    return p.tgt;
+}
+
+// List an owned vertex for the next sweep (stamp == tag: already listed).  Ghost
+// vertices are listed by their owner when the halo delta arrives.
+__device__ __forceinline__ void mark_vertex(const Geo &g, int64_t id, int *vstamp, int tag, int *list,
+                                            unsigned *count) {
+    bool add = owned(g, id) && vstamp[id] != tag;
+    if (add) add = atomicExch(&vstamp[id], tag) != tag;
+    warp_append(add, (int)id, list, count);
 }
 
 __global__ void __launch_bounds__(256) k_sweep_v(Geo g, Soa s, int ops, const int *__restrict__ lin,
@@ -329,56 +213,35 @@ __global__ void __launch_bounds__(256) k_sweep_v(Geo g, Soa s, int ops, const in
         bool act = e > 0 && h < g.INF;
         if (!__any_sync(FULL, act)) continue;
         int sent = 0;
-        if (act) {
-            mywork++;
-            c.col = c.v / g.Z;
-            c.z = (int)(c.v - c.col * g.Z);
-            c.v0 = c.col * g.Z;
-            const int x = (int)(c.col / g.Y), y = (int)(c.col - (int64_t)x * g.Y);
-            c.zo = zo_of(c.z, g.delta);
-            c.zi = zi_of(c.z, g.delta, g.Z);
-#pragma unroll
-            for (int d = 0; d < 4; d++) c.off[d] = nbr_off(g, x, y, d);
-        }
+        if (act) set_ctx(g, c, c.v);
         for (int it = 0; it < ops; ++it) {
-            int64_t tgt = -1;
+            int64_t tgt = NONE;
             if (act) {
-                tgt = pr_op_v(g, s, c, e, h, sent, flags);
+                mywork++;
+                tgt = pr_op(g, s, c, e, h, sent, flags);
                 act = e > 0 && h < g.INF;
             }
-            mark_vertex(tgt, vstamp, tag, lout, cout);
+            mark_vertex(g, tgt, vstamp, tag, lout, cout);
             if (!__any_sync(FULL, act)) break;
         }
         if (sent) atomicSub(&s.E[c.v], sent);
-        mark_vertex(act ? c.v : -1, vstamp, tag, lout, cout);
+        mark_vertex(g, act ? c.v : NONE, vstamp, tag, lout, cout);
     }
     mywork = warp_sum_ll((long long)mywork);
     if (lane_id() == 0 && mywork) atomicAdd(work, mywork);
 }
 
 // ------------------------------------------------------------------ a3': multi-hop sweep ("walk")
-// Alg. 2's discharge applied along a path: the owner of an active vertex v takes all
-// of E(v) and carries it down admissible arcs (strictly decreasing labels) for up to K
-// hops, pushing delta = min(carry, r) on each arc.  Finite residuals (T, up, lateral-in
+// Alg. 2's discharge applied along a path: the owner of an active vertex v takes all of
+// E(v) and carries it down admissible arcs (strictly decreasing labels) for up to K hops,
+// pushing delta = min(carry, r) on each arc.  Finite residuals (T, up, lateral-in
 // reverse) may now be decremented by several walkers, so they are RESERVED with a CAS
 // loop (never negative); infinite arcs only increase the reverse flow (atomicAdd).  A
 // carry that cannot go further is deposited (atomicAdd) on the vertex where it stops,
 // which is listed for the next launch; a stuck vertex is relabelled monotonically
-// (atomicMax, labels never decrease between global relabels).  Excess is decremented
-// only by its owner (the walk start), so conservation is exact.
-__device__ __forceinline__ void set_ctx(const Geo &g, OpCtx &c, int64_t v) {
-    c.v = v;
-    c.col = v / g.Z;
-    c.z = (int)(v - c.col * g.Z);
-    c.v0 = c.col * g.Z;
-    const int x = (int)(c.col / g.Y), y = (int)(c.col - (int64_t)x * g.Y);
-    c.zo = zo_of(c.z, g.delta);
-    c.zi = zi_of(c.z, g.delta, g.Z);
-#pragma unroll
-    for (int d = 0; d < 4; d++) c.off[d] = nbr_off(g, x, y, d);
-}
-
-// take up to `want` from a residual that several threads may decrement
+// (atomicMax).  Excess is decremented only by its owner (the walk start), so
+// conservation is exact.  A walk that enters a ghost vertex (neighbour slab) deposits
+// there: the halo exchange delivers it to the owner.
 __device__ __forceinline__ int reserve(int32_t *p, int want) {
     int cur = *(volatile int32_t *)p;
     while (cur > 0) {
@@ -400,7 +263,7 @@ __device__ __forceinline__ void deposit(const Geo &g, const Soa &s, int64_t x, i
                                         BlockQueue &q, int *lout, unsigned *cout, int *flags) {
     const int old = atomicAdd(&s.E[x], c);
     if (old > INT_MAX - c) atomicOr(flags, FLAG_OVERFLOW);
-    if (vstamp[x] != tag && atomicExch(&vstamp[x], tag) != tag) {
+    if (owned(g, x) && vstamp[x] != tag && atomicExch(&vstamp[x], tag) != tag) {
         const unsigned pos = atomicAdd(&q.n, 1u);
         if (pos < BlockQueue::CAP) q.buf[pos] = (int)x;
         else lout[atomicAdd(cout, 1u)] = (int)x;
@@ -438,12 +301,9 @@ __global__ void __launch_bounds__(256) k_walk(Geo g, Soa s, int K, const int *__
             switch (p.arc) {
                 case 0: df = reserve(&s.T[ctx.v], c); break;
                 case 1: df = c; atomicAdd(&s.D[ctx.v], df); break;
-                case 2: case 3: case 4: case 5:
-                    df = c;
-                    atomicAdd(&s.L[(int64_t)(p.arc - 2) * g.n + ctx.v], df);
-                    break;
+                case 2: case 3: case 4: case 5: df = c; atomicAdd(&s.L[p.arc - 2][ctx.v], df); break;
                 case 6: df = reserve(&s.D[ctx.v + 1], c); break;
-                default: df = reserve(&s.L[(int64_t)((p.arc - 7) ^ 1) * g.n + p.tgt], c); break;
+                default: df = reserve(&s.L[(p.arc - 7) ^ 1][p.tgt], c); break;
             }
             if (df == 0) continue;  // lost a reservation race: rescan this vertex
             if (p.arc == 0) {       // absorbed by t
@@ -452,6 +312,10 @@ __global__ void __launch_bounds__(256) k_walk(Geo g, Soa s, int K, const int *__
             }
             if (df < c) deposit(g, s, ctx.v, c - df, vstamp, tag, q, lout, cout, flags);
             c = df;
+            if (!owned(g, p.tgt)) {  // crossed into a neighbour slab: hand the carry over
+                deposit(g, s, p.tgt, c, vstamp, tag, q, lout, cout, flags);
+                break;
+            }
             hx = p.best;
             set_ctx(g, ctx, p.tgt);
         }
@@ -465,7 +329,7 @@ __global__ void __launch_bounds__(256) k_walk(Geo g, Soa s, int K, const int *__
     if (lane_id() == 0 && mywork) atomicAdd(work, mywork);
 }
 
-// After an exact global relabel: list every active vertex (E > 0, H < INF) in index order.
+// After a global relabel: list every active vertex (E > 0, H < INF) in index order.
 __global__ void k_rebuild_vertices(Geo g, const Soa s, int *lout, unsigned *cout, int *vstamp, int tag,
                                    unsigned long long *active) {
     unsigned long long myact = 0;
@@ -481,12 +345,10 @@ __global__ void k_rebuild_vertices(Geo g, const Soa s, int *lout, unsigned *cout
     if (lane_id() == 0 && myact) atomicAdd(active, myact);
 }
 
-// ------------------------------------------------------------------ a2/a5: exact global relabel
-// H(v) = BFS distance from v to t in the residual graph (Alg. 3: level 1 = vertices
-// with a residual arc into t -- the "{v,s}" of L414 read as t, R6 -- then
-// level L+1 = unlabelled residual predecessors of level L).  Level-synchronous,
-// frontier-based: each vertex is claimed exactly once by atomicCAS(H, INF, L+1).
-// Residual in-arcs u -> v of v = (x,y,z):
+// ------------------------------------------------------------------ a2/a5: global relabel
+// H(v) = BFS distance from v to t in the residual graph (Alg. 3: level 1 = vertices with a
+// residual arc into t -- the "{v,s}" of L414 read as t, R6 -- then level L+1 =
+// unlabelled residual predecessors of level L).  Residual in-arcs u -> v of v = (x,y,z):
 //   u = (x,y,z+1)             down arc, infinite
 //   u = (x,y,z-1)             up arc, residual D(v)
 //   u = (nbr, zi(z))          lateral arc of u into v, infinite
@@ -503,33 +365,48 @@ __global__ void k_bfs_init(Geo g, Soa s, int *lout, unsigned *cout) {
     }
 }
 
-// Expand one frontier vertex per lane (v < 0: none): claim every unlabelled residual
-// predecessor with label nl and append the claims with one atomic per warp.
+// Expand one frontier vertex per lane (v < 0: none) and append the new frontier with one
+// atomic per warp.  STRICT (single slab): claim unlabelled predecessors with
+// atomicCAS(H, INF, L+1) -- each vertex exactly once.  Otherwise label-correcting (x-slabs):
+// relax predecessors with atomicMin(H, H(v)+1) and list the improved ones once per wave.
+template <bool STRICT>
 __device__ __forceinline__ void bfs_expand_warp(const Geo &g, const Soa &s, int nl, int64_t v, int *lout,
-                                                unsigned *cout) {
+                                                unsigned *cout, int *vstamp, int tag) {
     const int INF = g.INF;
     int u[10];
     unsigned got = 0;
     if (v >= 0) {
+        if (!STRICT) nl = s.H[v] + 1;
         const int64_t col = v / g.Z;
         const int z = (int)(v - col * g.Z);
         const int x = (int)(col / g.Y), y = (int)(col - (int64_t)x * g.Y);
         const int64_t v0 = col * g.Z;
         const int zo = zo_of(z, g.delta), zi = zi_of(z, g.delta, g.Z);
         auto claim = [&](int slot, int64_t w) {
-            if (s.H[w] >= INF && atomicCAS(&s.H[w], INF, nl) == INF) {
-                u[slot] = (int)w;
-                got |= 1u << slot;
+            if (!owned(g, w)) return;  // ghost labels come from their owner
+            if (STRICT) {
+                if (s.H[w] >= INF && atomicCAS(&s.H[w], INF, nl) == INF) {
+                    u[slot] = (int)w;
+                    got |= 1u << slot;
+                }
+            } else {
+                if (s.H[w] > nl && atomicMin(&s.H[w], nl) > nl && vstamp[w] != tag &&
+                    atomicExch(&vstamp[w], tag) != tag) {
+                    u[slot] = (int)w;
+                    got |= 1u << slot;
+                }
             }
         };
-        if (z + 1 < g.Z) claim(0, v + 1);
-        if (z >= 1 && s.D[v] > 0) claim(1, v - 1);
+        if (nl < INF) {
+            if (z + 1 < g.Z) claim(0, v + 1);
+            if (z >= 1 && s.D[v] > 0) claim(1, v - 1);
 #pragma unroll
-        for (int d = 0; d < 4; d++) {
-            const int64_t o = nbr_off(g, x, y, d);
-            if (!o) continue;
-            if (zi >= 0) claim(2 + d, v0 + o + zi);
-            if (zo >= 0 && s.L[(int64_t)d * g.n + v] > 0) claim(6 + d, v0 + o + zo);
+            for (int d = 0; d < 4; d++) {
+                const int64_t o = nbr_off(g, x, y, d);
+                if (!o) continue;
+                if (zi >= 0) claim(2 + d, v0 + o + zi);
+                if (zo >= 0 && s.L[d][v] > 0) claim(6 + d, v0 + o + zo);
+            }
         }
     }
     const int k = __popc(got);
@@ -545,19 +422,8 @@ __device__ __forceinline__ void bfs_expand_warp(const Geo &g, const Soa &s, int 
         if (got >> j & 1u) lout[pos++] = u[j];
 }
 
-__global__ void __launch_bounds__(256) k_bfs_level(Geo g, Soa s, int L, const int *__restrict__ lin,
-                                                   const unsigned *cin, int *lout, unsigned *cout,
-                                                   unsigned *czero) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) *czero = 0;
-    const int64_t count = *cin;
-    for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {
-        const int64_t i = base + lane_id();
-        bfs_expand_warp(g, s, L + 1, i < count ? (int64_t)lin[i] : -1, lout, cout);
-    }
-}
-
-// Device-driven BFS step (the level counter lives on the device, so identical launches
-// can be queued back to back).  Step i = level L = i+1 reads list[i&1] / cnt[i%3],
+// Device-driven strict BFS step (the level counter lives on the device, so identical
+// launches are queued back to back).  Step i = level L = i+1 reads list[i&1] / cnt[i%3],
 // writes list[(i+1)&1] / cnt[(i+1)%3] and zeroes cnt[(i+2)%3].
 //   large frontier: every block expands one level; the last block to finish advances L;
 //   small frontier (<= BFS_SMALL): block 0 alone runs levels back to back separated by
@@ -586,7 +452,8 @@ __global__ void __launch_bounds__(512) k_bfs_step(Geo g, Soa s, int *list0, int 
             if (threadIdx.x == 0) st->cnt[(i + 2) % 3] = 0;
             for (unsigned base = (threadIdx.x >> 5) * 32; base < count; base += (blockDim.x >> 5) * 32) {
                 const unsigned j = base + lane_id();
-                bfs_expand_warp(g, s, L + 1, j < count ? (int64_t)lin[j] : -1, lout, &st->cnt[(i + 1) % 3]);
+                bfs_expand_warp<true>(g, s, L + 1, j < count ? (int64_t)lin[j] : -1, lout, &st->cnt[(i + 1) % 3],
+                                      nullptr, 0);
             }
             __syncthreads();
             ++L;
@@ -603,7 +470,8 @@ __global__ void __launch_bounds__(512) k_bfs_step(Geo g, Soa s, int *list0, int 
     if (blockIdx.x == 0 && threadIdx.x == 0) st->cnt[(i + 2) % 3] = 0;
     for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {
         const int64_t j = base + lane_id();
-        bfs_expand_warp(g, s, L + 1, j < count ? (int64_t)lin[j] : -1, lout, &st->cnt[(i + 1) % 3]);
+        bfs_expand_warp<true>(g, s, L + 1, j < count ? (int64_t)lin[j] : -1, lout, &st->cnt[(i + 1) % 3], nullptr,
+                              0);
     }
     __threadfence();
     __syncthreads();
@@ -616,125 +484,114 @@ __global__ void __launch_bounds__(512) k_bfs_step(Geo g, Soa s, int *list0, int 
     }
 }
 
-// ------------------------------------------------------------------ a1': column pre-cancellation
-// Exact max-flow of every column in isolation (ignoring lateral arcs), applied as the
-// initial preflow: source excess may only move DOWN a column (infinite down arcs) into
-// sink arcs below it, and the top-down greedy is optimal because the set of sinks a
-// source can feed is nested.  With a(z) = E(z) - T(z) and S(z) = sum_{j>=z} a(j):
-//   carry leaving z downward    c(z) = S(z) - min_{m in [z, Z]} S(m)       (S(Z) = 0)
-//   absorbed at a sink          ab(z) = min(T(z), c(z+1))
-//   flow on the down arc z->z-1 f(z) = min(c(z), sum_{z'<z} ab(z'))  (only what is absorbed below)
-//   new state  T -= ab,  D = f,  E = f(z+1) + E(z) - ab(z) - f(z) >= 0.
-// Not in the paper: an accelerator whose result is a valid preflow, so the maximum flow
-// and the minimal cut are unchanged (DESIGN.md §7).  One warp per column, z in chunks of 32.
-__device__ __forceinline__ long long warp_suffix_sum_ll(long long v) {
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const long long t = __shfl_down_sync(FULL, v, o);
-        if (lane_id() + o < 32) v += t;
+// Label-correcting wave (x-slab mode): relax the predecessors of every listed vertex.
+__global__ void __launch_bounds__(256) k_lc_wave(Geo g, Soa s, const int *__restrict__ lin, const unsigned *cin,
+                                                 int *lout, unsigned *cout, unsigned *czero, int *vstamp, int tag) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *czero = 0;
+    const int64_t count = *cin;
+    for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {
+        const int64_t j = base + lane_id();
+        bfs_expand_warp<false>(g, s, 0, j < count ? (int64_t)lin[j] : -1, lout, cout, vstamp, tag);
     }
-    return v;
-}
-__device__ __forceinline__ long long warp_suffix_min_ll(long long v) {
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const long long t = __shfl_down_sync(FULL, v, o);
-        if (lane_id() + o < 32) v = min(v, t);
-    }
-    return v;
-}
-__device__ __forceinline__ long long warp_excl_prefix_sum_ll(long long v) {
-    long long x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const long long t = __shfl_up_sync(FULL, x, o);
-        if (lane_id() >= o) x += t;
-    }
-    return x - v;
 }
 
-__global__ void __launch_bounds__(256) k_precancel(Geo g, Soa s, int *flags) {
-    extern __shared__ long long sh_c[];  // per warp: Z+1 carries c(z)
-    long long *cz = sh_c + (int64_t)(threadIdx.x >> 5) * (g.Z + 1);
-    const int64_t ncol = (int64_t)g.X * g.Y;
-    const int last_c0 = ((g.Z - 1) >> 5) << 5;
-    bool bad = false;
-    for (int64_t col = gwarp(); col < ncol; col += nwarps()) {
-        const int64_t v0 = col * g.Z;
-        // pass 1, top-down: suffix sums S(z) and carries c(z)
-        long long sum_above = 0, min_above = 0;  // S over chunks above; min over m above incl. S(Z) = 0
-        if (lane_id() == 0) cz[g.Z] = 0;
-        for (int c0 = last_c0; c0 >= 0; c0 -= 32) {
-            const int z = c0 + lane_id();
-            long long a = 0;
-            if (z < g.Z) a = (long long)s.E[v0 + z] - (long long)s.T[v0 + z];
-            const long long S = warp_suffix_sum_ll(a) + sum_above;
-            const long long m = min(warp_suffix_min_ll(z < g.Z ? S : LLONG_MAX), min_above);
-            if (z < g.Z) cz[z] = S - m;
-            sum_above = __shfl_sync(FULL, S, 0);
-            min_above = __shfl_sync(FULL, m, 0);
-        }
-        __syncwarp();
-        // pass 2, bottom-up: absorption, flows, new state
-        long long ab_below = 0;  // sum of ab(z') for z' below the chunk
-        for (int c0 = 0; c0 < g.Z; c0 += 32) {
-            const int z = c0 + lane_id();
-            const bool ok = z < g.Z;
-            int e = 0, t = 0;
-            long long ab = 0, f = 0;
-            if (ok) {
-                e = s.E[v0 + z];
-                t = s.T[v0 + z];
-                ab = t > 0 ? min((long long)t, cz[z + 1]) : 0;
+// Ghost seeds: a ghost vertex gv whose label decreased (vs. old[]) relaxes its residual
+// predecessors in this slab's boundary plane:
+//   u = (boundary, zi(z))  lateral arc of u into gv (infinite)
+//   u = (boundary, zo(z))  reverse of gv's lateral arc toward this slab, residual L_dir(gv)
+__global__ void k_lc_ghost(Geo g, Soa s, int side, const int32_t *__restrict__ old, int *lout, unsigned *cout,
+                           int *vstamp, int tag) {
+    const int64_t gbase = side ? g.n : -g.YZ;
+    const int64_t bbase = side ? g.n - g.YZ : 0;
+    const int ldir = side ? 1 : 0;  // direction of the ghost's arcs toward this slab
+    for (int64_t b0 = gwarp() * 32; b0 < g.YZ; b0 += nwarps() * 32) {
+        const int64_t i = b0 + lane_id();
+        int u0 = -1, u1 = -1;
+        if (i < g.YZ) {
+            const int64_t gv = gbase + i;
+            const int l = s.H[gv];
+            if (l < g.INF && l < old[i]) {
+                const int nl = l + 1;
+                const int z = (int)(i % g.Z);
+                const int64_t col0 = bbase + (i - z);
+                const int zi = zi_of(z, g.delta, g.Z), zo = zo_of(z, g.delta);
+                auto relax = [&](int64_t w) -> int {
+                    if (s.H[w] > nl && atomicMin(&s.H[w], nl) > nl && vstamp[w] != tag &&
+                        atomicExch(&vstamp[w], tag) != tag)
+                        return (int)w;
+                    return -1;
+                };
+                if (zi >= 0) u0 = relax(col0 + zi);
+                if (zo >= 0 && s.L[ldir][gv] > 0) u1 = relax(col0 + zo);
             }
-            const long long AB = warp_excl_prefix_sum_ll(ab) + ab_below;
-            if (ok && z >= 1) f = min(cz[z], AB);
-            long long f_up = __shfl_down_sync(FULL, f, 1);
-            const long long ab_total = __shfl_sync(FULL, AB + ab, 31);
-            if (lane_id() == 31) f_up = (z + 1 < g.Z) ? min(cz[z + 1], ab_total) : 0;
-            if (ok) {
-                const long long ne = f_up + (long long)e - ab - f;
-                if (ne < 0 || ne > INT_MAX || f > INT_MAX) bad = true;
-                s.E[v0 + z] = (int32_t)ne;
-                s.T[v0 + z] = t - (int32_t)ab;
-                s.D[v0 + z] = (int32_t)f;
-            }
-            ab_below = ab_total;
         }
-        __syncwarp();
+        warp_append(u0 >= 0, u0, lout, cout);
+        warp_append(u1 >= 0, u1, lout, cout);
     }
-    if (bad) atomicOr(flags, FLAG_OVERFLOW);
 }
 
-// After an exact global relabel: list every chunk holding an active vertex (E > 0,
-// H < INF) and count active vertices.  A warp handles 32 consecutive chunks and
-// appends them with one atomic.
-__global__ void k_rebuild_chunks(Geo g, const Soa s, int *lout, unsigned *cout, int *stamp, int tag,
-                                 unsigned long long *active) {
-    unsigned long long myact = 0;
-    for (int64_t gb = gwarp() * 32; gb < g.nchunks; gb += nwarps() * 32) {
-        unsigned mask = 0;
-        for (int k = 0; k < 32; k++) {
-            const int64_t ch = gb + k;
-            if (ch >= g.nchunks) break;
-            const int64_t col = ch / g.CPC;
-            const int z = (int)(ch - col * g.CPC) * 32 + lane_id();
-            bool a = false;
-            if (z < g.Z) {
-                const int64_t v = col * g.Z + z;
-                a = s.E[v] > 0 && s.H[v] < g.INF;
-            }
-            const unsigned m = __ballot_sync(FULL, a);
-            if (m) {
-                mask |= 1u << k;
-                myact += __popc(m);
-            }
-        }
-        const bool has = (mask >> lane_id()) & 1u;
-        if (has) stamp[gb + lane_id()] = tag;
-        warp_append(has, (int)(gb + lane_id()), lout, cout);
+// ------------------------------------------------------------------ a8: halo exchange (x-slabs)
+// Per side (0: x = -1 ghost / x = 0 boundary; 1: x = X ghost / x = X-1 boundary) one
+// message of 4 planes of Y*Z int32:
+//   [0] dE : excess pushed into the ghost plane since the last exchange
+//   [1] dL : decrements of the ghost's lateral residual toward this slab (snapshot - now)
+//   [2] H  : heights of the boundary plane
+//   [3] L  : the boundary plane's lateral flow toward the neighbour (its ghost residual)
+// The receiver adds dE, subtracts dL (it is the single decrementer's delta), lists the
+// vertices that received excess, and refreshes its ghost plane with H and L - (its own dL).
+__global__ void k_halo_pack(Geo g, Soa s, int side, const int32_t *__restrict__ snap, int32_t *send) {
+    const int64_t gbase = side ? g.n : -g.YZ, bbase = side ? g.n - g.YZ : 0;
+    const int gdir = side ? 1 : 0, bdir = side ? 0 : 1;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.YZ; i += (int64_t)gridDim.x * blockDim.x) {
+        send[i] = s.E[gbase + i];
+        send[g.YZ + i] = snap[i] - s.L[gdir][gbase + i];
+        send[2 * g.YZ + i] = s.H[bbase + i];
+        send[3 * g.YZ + i] = s.L[bdir][bbase + i];
     }
-    if (lane_id() == 0 && myact) atomicAdd(active, myact);
+}
+
+__global__ void k_halo_unpack(Geo g, Soa s, int side, const int32_t *__restrict__ recv,
+                              const int32_t *__restrict__ sent, int32_t *snap, int *lout, unsigned *cout, int *vstamp,
+                              int tag, int *flags) {
+    const int64_t gbase = side ? g.n : -g.YZ, bbase = side ? g.n - g.YZ : 0;
+    const int gdir = side ? 1 : 0, bdir = side ? 0 : 1;
+    for (int64_t b0 = gwarp() * 32; b0 < g.YZ; b0 += nwarps() * 32) {
+        const int64_t i = b0 + lane_id();
+        bool add = false;
+        if (i < g.YZ) {
+            const int64_t bv = bbase + i, gv = gbase + i;
+            const int de = recv[i];
+            if (de) {
+                const long long ne = (long long)s.E[bv] + de;
+                if (ne > INT_MAX) atomicOr(flags, FLAG_OVERFLOW);
+                s.E[bv] = (int32_t)ne;
+                add = vstamp[bv] != tag;
+                if (add) vstamp[bv] = tag;
+            }
+            s.L[bdir][bv] -= recv[g.YZ + i];
+            s.H[gv] = recv[2 * g.YZ + i];
+            const int lg = recv[3 * g.YZ + i] - sent[g.YZ + i];
+            s.L[gdir][gv] = lg;
+            snap[i] = lg;
+            s.E[gv] = 0;
+        }
+        warp_append(add, (int)(bbase + i), lout, cout);
+    }
+}
+
+// Global-relabel halo: heights of the boundary plane -> the neighbour's ghost plane
+// (the previous ghost heights are kept in old[] to detect improvements).
+__global__ void k_halo_pack_h(Geo g, Soa s, int side, int32_t *send) {
+    const int64_t bbase = side ? g.n - g.YZ : 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.YZ; i += (int64_t)gridDim.x * blockDim.x)
+        send[i] = s.H[bbase + i];
+}
+__global__ void k_halo_unpack_h(Geo g, Soa s, int side, const int32_t *__restrict__ recv, int32_t *old) {
+    const int64_t gbase = side ? g.n : -g.YZ;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.YZ; i += (int64_t)gridDim.x * blockDim.x) {
+        old[i] = s.H[gbase + i];
+        s.H[gbase + i] = recv[i];
+    }
 }
 
 // ------------------------------------------------------------------ a5: gap heuristic
@@ -792,6 +649,94 @@ __global__ void k_sum_T(Geo g, const int32_t *__restrict__ T, unsigned long long
     if (lane_id() == 0 && acc) atomicAdd(out, (unsigned long long)acc);
 }
 
+// ------------------------------------------------------------------ a1': column pre-cancellation
+// Exact max-flow of every column in isolation (ignoring lateral arcs), applied as the
+// initial preflow: source excess may only move DOWN a column (infinite down arcs) into
+// sink arcs below it, and the top-down greedy is optimal because the set of sinks a
+// source can feed is nested.  With a(z) = E(z) - T(z) and S(z) = sum_{j>=z} a(j):
+//   carry leaving z downward    c(z) = S(z) - min_{m in [z, Z]} S(m)       (S(Z) = 0)
+//   absorbed at a sink          ab(z) = min(T(z), c(z+1))
+//   flow on the down arc z->z-1 f(z) = min(c(z), sum_{z'<z} ab(z'))  (only what is absorbed below)
+//   new state  T -= ab,  D = f,  E = f(z+1) + E(z) - ab(z) - f(z) >= 0.
+// Not in the paper: an accelerator whose result is a valid preflow, so the maximum flow
+// and the minimal cut are unchanged.  One warp per column, z in chunks of 32.
+__device__ __forceinline__ long long warp_suffix_sum_ll(long long v) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long t = __shfl_down_sync(FULL, v, o);
+        if (lane_id() + o < 32) v += t;
+    }
+    return v;
+}
+__device__ __forceinline__ long long warp_suffix_min_ll(long long v) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long t = __shfl_down_sync(FULL, v, o);
+        if (lane_id() + o < 32) v = min(v, t);
+    }
+    return v;
+}
+__device__ __forceinline__ long long warp_excl_prefix_sum_ll(long long v) {
+    long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long t = __shfl_up_sync(FULL, x, o);
+        if (lane_id() >= o) x += t;
+    }
+    return x - v;
+}
+
+__global__ void __launch_bounds__(256) k_precancel(Geo g, Soa s, int *flags) {
+    extern __shared__ long long sh_c[];  // per warp: Z+1 carries c(z)
+    long long *cz = sh_c + (int64_t)(threadIdx.x >> 5) * (g.Z + 1);
+    const int64_t ncol = (int64_t)g.X * g.Y;
+    const int last_c0 = ((g.Z - 1) >> 5) << 5;
+    bool bad = false;
+    for (int64_t col = gwarp(); col < ncol; col += nwarps()) {
+        const int64_t v0 = col * g.Z;
+        long long sum_above = 0, min_above = 0;  // S over chunks above; min over m above incl. S(Z) = 0
+        if (lane_id() == 0) cz[g.Z] = 0;
+        for (int c0 = last_c0; c0 >= 0; c0 -= 32) {
+            const int z = c0 + lane_id();
+            long long a = 0;
+            if (z < g.Z) a = (long long)s.E[v0 + z] - (long long)s.T[v0 + z];
+            const long long S = warp_suffix_sum_ll(a) + sum_above;
+            const long long m = min(warp_suffix_min_ll(z < g.Z ? S : LLONG_MAX), min_above);
+            if (z < g.Z) cz[z] = S - m;
+            sum_above = __shfl_sync(FULL, S, 0);
+            min_above = __shfl_sync(FULL, m, 0);
+        }
+        __syncwarp();
+        long long ab_below = 0;
+        for (int c0 = 0; c0 < g.Z; c0 += 32) {
+            const int z = c0 + lane_id();
+            const bool ok = z < g.Z;
+            int e = 0, t = 0;
+            long long ab = 0, f = 0;
+            if (ok) {
+                e = s.E[v0 + z];
+                t = s.T[v0 + z];
+                ab = t > 0 ? min((long long)t, cz[z + 1]) : 0;
+            }
+            const long long AB = warp_excl_prefix_sum_ll(ab) + ab_below;
+            if (ok && z >= 1) f = min(cz[z], AB);
+            long long f_up = __shfl_down_sync(FULL, f, 1);
+            const long long ab_total = __shfl_sync(FULL, AB + ab, 31);
+            if (lane_id() == 31) f_up = (z + 1 < g.Z) ? min(cz[z + 1], ab_total) : 0;
+            if (ok) {
+                const long long ne = f_up + (long long)e - ab - f;
+                if (ne < 0 || ne > INT_MAX || f > INT_MAX) bad = true;
+                s.E[v0 + z] = (int32_t)ne;
+                s.T[v0 + z] = t - (int32_t)ab;
+                s.D[v0 + z] = (int32_t)f;
+            }
+            ab_below = ab_total;
+        }
+        __syncwarp();
+    }
+    if (bad) atomicOr(flags, FLAG_OVERFLOW);
+}
+
 // ------------------------------------------------------------------ a7: extraction
 // Minimal source set S = forward residual closure of {v : E(v) > 0} (R5,
 // SURVEY.md V3).  Infinite down arcs make S downward closed per column, so S is
@@ -800,7 +745,9 @@ __global__ void k_sum_T(Geo g, const int32_t *__restrict__ T, unsigned long long
 //   up arcs        climb while D(top+1) > 0
 //   lateral-out    top(nbr) >= zo_eff(top) = max(0, top - Delta)
 //   lateral-in rev top(nbr_d) >= zi(z) for z in (proc, top] with L_{d^1}(nbr_d, zi(z)) > 0
-// A neighbour whose top rises is listed for the next round.
+// A neighbour whose top rises is listed for the next round; a ghost column's rise is
+// delivered to its owner by the top halo (k_top_halo_*).  top[] is indexed by column with
+// the ghost columns at [-Y, 0) and [ncol, ncol + Y).
 __device__ __forceinline__ int warp_climb(const Geo &g, const int32_t *__restrict__ D, int64_t v0, int t) {
     for (int base = t + 1; base < g.Z; base += 32) {
         const int z = base + lane_id();
@@ -845,6 +792,7 @@ __global__ void __launch_bounds__(256) k_ext_round(Geo g, Soa s, const int *__re
                                                    int32_t *proc, int *stamp, int tag) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *czero = 0;
     const int64_t count = *cin;
+    const int64_t ncols = (int64_t)g.X * g.Y;
     for (int64_t i = gwarp(); i < count; i += nwarps()) {
         const int64_t col = lin[i];
         const int p = proc[col];
@@ -854,32 +802,62 @@ __global__ void __launch_bounds__(256) k_ext_round(Geo g, Soa s, const int *__re
         const int x = (int)(col / g.Y), y = (int)(col - (int64_t)x * g.Y);
         t = warp_climb(g, s.D, v0, t);
         if (lane_id() == 0) atomicMax(&top[col], t);
-        int64_t ncol[4];
-        ncol[0] = x + 1 < g.X ? col + g.Y : -1;
-        ncol[1] = x >= 1 ? col - g.Y : -1;
-        ncol[2] = y + 1 < g.Y ? col + 1 : -1;
-        ncol[3] = y >= 1 ? col - 1 : -1;
+        int64_t nc[4];
+        nc[0] = (x + 1 < g.X || g.gh) ? col + g.Y : INT64_MIN;
+        nc[1] = (x >= 1 || g.gl) ? col - g.Y : INT64_MIN;
+        nc[2] = y + 1 < g.Y ? col + 1 : INT64_MIN;
+        nc[3] = y >= 1 ? col - 1 : INT64_MIN;
         int cd[4] = {-1, -1, -1, -1};
         for (int zb = p + 1; zb <= t; zb += 32) {
             const int z = zb + lane_id();
             const int zi = z <= t ? zi_of(z, g.delta, g.Z) : -1;
 #pragma unroll
             for (int d = 0; d < 4; d++)
-                if (zi >= 0 && ncol[d] >= 0 && s.L[(int64_t)(d ^ 1) * g.n + ncol[d] * g.Z + zi] > 0)
-                    cd[d] = max(cd[d], zi);
+                if (zi >= 0 && nc[d] != INT64_MIN && s.L[d ^ 1][nc[d] * g.Z + zi] > 0) cd[d] = max(cd[d], zi);
         }
         const int zout = t > g.delta ? t - g.delta : 0;
         int mark = -1;
 #pragma unroll
         for (int d = 0; d < 4; d++) {
             const int cand = max(warp_max_i(cd[d]), zout);
-            if (lane_id() == d && ncol[d] >= 0) {
-                const int old = atomicMax(&top[ncol[d]], cand);
-                if (old < cand) mark = (int)ncol[d];
+            if (lane_id() == d && nc[d] != INT64_MIN) {
+                const int old = atomicMax(&top[nc[d]], cand);
+                if (old < cand && nc[d] >= 0 && nc[d] < ncols) mark = (int)nc[d];
             }
         }
         warp_mark(mark, stamp, tag, lout, cout);
         if (lane_id() == 0) proc[col] = t;
+    }
+}
+
+// Top halo: [0] this slab's proposals for the ghost columns, [1] its boundary tops.
+__global__ void k_top_halo_pack(Geo g, const int32_t *top, int side, int32_t *send) {
+    const int64_t ncol = (int64_t)g.X * g.Y;
+    const int64_t gbase = side ? ncol : -g.Y, bbase = side ? ncol - g.Y : 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.Y; i += gridDim.x * blockDim.x) {
+        send[i] = top[gbase + i];
+        send[g.Y + i] = top[bbase + i];
+    }
+}
+__global__ void k_top_halo_unpack(Geo g, int32_t *top, int side, const int32_t *__restrict__ recv,
+                                  const int32_t *__restrict__ sent, int *lout, unsigned *cout, int *stamp, int tag,
+                                  unsigned *changed) {
+    const int64_t ncol = (int64_t)g.X * g.Y;
+    const int64_t gbase = side ? ncol : -g.Y, bbase = side ? ncol - g.Y : 0;
+    for (int64_t b0 = gwarp() * 32; b0 < g.Y; b0 += nwarps() * 32) {
+        const int64_t i = b0 + lane_id();
+        bool add = false;
+        if (i < g.Y) {
+            const int prop = recv[i];
+            if (prop > top[bbase + i]) {
+                top[bbase + i] = prop;
+                add = stamp[bbase + i] != tag;
+                if (add) stamp[bbase + i] = tag;
+                atomicAdd(changed, 1u);
+            }
+            top[gbase + i] = max(recv[g.Y + i], sent[i]);
+        }
+        warp_append(add, (int)(bbase + i), lout, cout);
     }
 }
 
