@@ -166,72 +166,93 @@ def run_reference(args, spec):
 def run_ours(args, spec):
     import torch
     rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=dev)
     from paper_2601_17026_b200 import colgraph as cg
-    dev = torch.device("cuda", local)
+    from paper_2601_17026_b200 import dist as cgd
     stream = torch.cuda.current_stream(dev)
-    c_host = V.generate(spec)
-    assert V.sha256_volume(c_host) == V.MANIFEST[spec.name], "synthetic input differs from the pinned manifest"
+    X, Y, Z = spec.X, spec.Y, spec.Z
+    # this rank's x-slab (N = 1: the whole volume), generated directly (same bytes as the slice)
+    x0, x1 = cgd.slab(X, rank, world) if world > 1 else (0, X)
+    c_host = V.generate(spec, x_range=(x0, x1))
+    if world == 1:
+        assert V.sha256_volume(c_host) == V.MANIFEST[spec.name], "synthetic input differs from the pinned manifest"
     c_pin = torch.from_numpy(c_host).pin_memory()
     cost = c_pin.to(dev, non_blocking=False)
-    X, Y, Z = c_host.shape
-    surface = torch.empty((X, Y), dtype=torch.int32, device=dev)
+    nccl_id = cgd.init_nccl_id() if world > 1 else None
     opts = cg.make_opts()
+    surface = torch.empty((x1 - x0, Y), dtype=torch.int32, device=dev)
 
-    def step():
-        h = cg.colgraph_build(cost, spec.delta, stream=stream)
+    def step(cost_dev):
+        if world > 1:
+            r = cgd.solve_slab(cost_dev, (X, Y, Z, spec.delta), rank, world, nccl_id, opts=opts, stream=stream)
+            assert r["status"] == cg.CG_OK and r["extract_status"] == cg.CG_OK, (r["status"], r["extract_status"])
+            return r["flow"], r["stats"], r["surface"]
+        h = cg.colgraph_build(cost_dev, spec.delta, stream=stream)
         try:
             st, flow, _ = cg.maxflow_solve(h, opts)
             assert st == cg.CG_OK, cg.STATUS.get(st)
             est = cg.mincut_extract_surface(h, surface)
             assert est == cg.CG_OK, cg.STATUS.get(est)
-            return flow, cg.colgraph_stats(h)
+            return flow, cg.colgraph_stats(h), surface
         finally:
             cg.colgraph_free(h)
 
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(ms):
+        if world == 1:
+            return ms
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
     for _ in range(max(args.warmup, 0)):
-        flow0, _ = step()
-    torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
+        step(cost)
+    barrier()
     stats = []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            flow, s = step()
+            flow, s, _ = step(cost)
             stats.append(s)
         ev1.record(stream)
         torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    ms_total = ev0.elapsed_time(ev1)
-    if world > 1:
-        t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms_total = float(t.item())
+    barrier()
+    ms_total = max_over_ranks(ev0.elapsed_time(ev1))
     ms_step = ms_total / args.steps
-    nodes_total = spec.n * world  # replicas: every rank solves its own copy
-    value = nodes_total * args.steps / (ms_total / 1000.0) / 1e6
+    value = spec.n * args.steps / (ms_total / 1000.0) / 1e6  # whole volume per step, all ranks together
 
-    # e2e through the host-buffer C-ABI call (H2D of the costs, D2H of the surface + |f|)
+    # e2e through the public API: every step copies this rank's cost slab from pinned host
+    # memory, solves, and reads the surface (+ |f|) back to the host
     e2e_steps = args.e2e_steps or args.steps
-    surf_host = torch.empty((X, Y), dtype=torch.int32).pin_memory()
+    cost_e2e = torch.empty_like(cost)
+    surf_host = torch.empty((x1 - x0, Y), dtype=torch.int32).pin_memory()
+    barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
     e0.record(stream)
     for _ in range(e2e_steps):
-        r = cg.colgraph_solve_host_ptr(c_pin, spec.delta, surf_host, stream=stream)
-        assert r["status"] == 0 and r["flow"] == flow
+        if world == 1:
+            r = cg.colgraph_solve_host_ptr(c_pin, spec.delta, surf_host, stream=stream)
+            assert r["status"] == 0 and r["flow"] == flow
+        else:
+            cost_e2e.copy_(c_pin, non_blocking=True)
+            f2, _, surf_dev = step(cost_e2e)
+            surf_host.copy_(surf_dev)
+            assert f2 == flow
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / e2e_steps
-    e2e_value = nodes_total / (e2e_ms / 1000.0) / 1e6
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / e2e_steps
+    e2e_value = spec.n / (e2e_ms / 1000.0) / 1e6
 
     if rank != 0:
         if world > 1:
@@ -254,13 +275,13 @@ def run_ours(args, spec):
                 "share_of_step": sweep_ms * args.steps / (ms_total * len(stats)) if ms_total > 0 else None}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "time_to_min_cut_s": ms_step / 1000.0,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
-            "data": "synthetic (seeded generator synth/volumes.py, sha256-pinned)",
-            "config": workload_config(spec, {"parallelism": "replicas" if world > 1 else "single-gpu"}),
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "int32", "data": "synthetic (seeded generator synth/volumes.py, sha256-pinned)",
+            "config": workload_config(spec, {"parallelism": f"x-slab{world}" if world > 1 else "single-gpu"}),
             "flow": flow, "roofline": roofline,
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms, "h2d_bytes_per_step": 4 * spec.n,
                     "d2h_bytes_per_step": 4 * X * Y + 8},
-            "gpu_launches": int(sum(s["kernel_launches"] + 1 for s in stats)),
+            "gpu_launches": int(sum(s["kernel_launches"] for s in stats)),
             "solver": {"sweeps_per_step": sweeps / len(stats),
                        "global_relabels_per_step": sum(s["global_relabels"] for s in stats) / len(stats),
                        "gr_passes_per_step": sum(s["gr_passes"] for s in stats) / len(stats),

@@ -121,7 +121,9 @@ def _check_dev_int32(t, name):
 
 def colgraph_build(cost, delta: int, input_is_weight: bool = False, stream=None, rank=0, nranks=1, nccl_id=None,
                    dims=None):
-    """cost: CUDA int32 tensor [X_r, Y, Z] (this rank's slab).  Returns an opaque handle."""
+    """cost: CUDA int32 tensor [X_r, Y, Z] (this rank's slab; dims = full-volume cg_dims when
+    nranks > 1, nccl_id = the 128 bytes from nccl_unique_id() shared by all ranks).
+    Returns an opaque handle."""
     _check_dev_int32(cost, "cost")
     import torch
     if stream is None:
@@ -130,9 +132,11 @@ def colgraph_build(cost, delta: int, input_is_weight: bool = False, stream=None,
         X, Y, Z = cost.shape
         dims = cg_dims(X, Y, Z, int(delta))
     h = ctypes.c_void_p()
+    idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
     st = _lib.colgraph_build(ctypes.byref(dims), ctypes.c_void_p(cost.data_ptr()), int(bool(input_is_weight)),
                              ctypes.byref(_dist(cost.device.index, ctypes.c_void_p(stream.cuda_stream), rank, nranks,
-                                                nccl_id)), ctypes.byref(h))
+                                                ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None)),
+                             ctypes.byref(h))
     if st != CG_OK:
         raise ColgraphError(st, "colgraph_build")
     return h

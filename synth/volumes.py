@@ -172,19 +172,21 @@ def _fault_params(spec: VolumeSpec):
     return (px, py, pz), (nx, ny, nz)
 
 
-def generate(spec: VolumeSpec | str, x_chunk: int = 64) -> np.ndarray:
-    """int32 cost volume c[x][y][z] in 0..255 for a config (z fastest)."""
+def generate(spec: VolumeSpec | str, x_chunk: int = 64, x_range: tuple | None = None) -> np.ndarray:
+    """int32 cost volume c[x][y][z] in 0..255 for a config (z fastest); x_range=(x0, x1)
+    generates only that x-slab (identical bytes to the same slice of the full volume)."""
     if isinstance(spec, str):
         spec = CONFIGS[spec]
     X, Y, Z = spec.X, spec.Y, spec.Z
-    out = np.empty((X, Y, Z), dtype=np.int32)
+    xa, xb = x_range if x_range is not None else (0, X)
+    out = np.empty((xb - xa, Y, Z), dtype=np.int32)
     ys = np.arange(Y, dtype=np.float64).reshape(1, Y, 1)
     zs = np.arange(Z, dtype=np.float64).reshape(1, 1, Z)
     if spec.kind == "fault":
         (px, py, pz), (nx, ny, nz) = _fault_params(spec)
         throw = float(spec.extra["throw"])
-    for x0 in range(0, X, x_chunk):
-        x1 = min(X, x0 + x_chunk)
+    for x0 in range(xa, xb, x_chunk):
+        x1 = min(xb, x0 + x_chunk)
         xs = np.arange(x0, x1, dtype=np.float64).reshape(-1, 1, 1)
         base = _structure(spec, xs, ys, zs)
         if spec.kind == "fault":
@@ -199,7 +201,7 @@ def generate(spec: VolumeSpec | str, x_chunk: int = 64) -> np.ndarray:
         g = np.zeros_like(inten)
         g[:, :, 1:] = inten[:, :, 1:] - inten[:, :, :-1]
         q = np.minimum(255.0, np.floor(np.abs(g) + 0.5))
-        out[x0:x1] = (255.0 - q).astype(np.int32)
+        out[x0 - xa:x1 - xa] = (255.0 - q).astype(np.int32)
     return out
 
 
