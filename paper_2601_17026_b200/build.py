@@ -32,20 +32,24 @@ def _inputs():
     return files
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB):
-        mt = os.path.getmtime(LIB)
+def build(force: bool = False, verbose: bool = False, lib: str = LIB, defines=()) -> str:
+    """Compile the library.  defines: extra -D flags (e.g. ("CG_LAYOUT_AOS=0",) for the
+    plane-layout variant used in A/B measurements, written to another file name)."""
+    if not force and os.path.exists(lib):
+        mt = os.path.getmtime(lib)
         if all(os.path.getmtime(f) <= mt for f in _inputs()):
-            return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
+            return lib
+    tmp = lib + f".tmp{os.getpid()}"
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-I", INCLUDE, "-o", tmp] + [os.path.join(SRC_DIR, s) for s in SOURCES]
+           "-I", INCLUDE, *[f"-D{d}" for d in defines], "-o", tmp] + [os.path.join(SRC_DIR, s) for s in SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv))
+    if "--soa" in sys.argv:
+        print(build(force=True, lib=os.path.join(PKG, "libcolgraph_soa.so"), defines=("CG_LAYOUT_AOS=0",)))

@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libcolgraph.so")
+LIB_PATH = os.environ.get("CG_LIB") or os.path.join(_PKG, "libcolgraph.so")
 
 STATUS = {0: "CG_OK", 1: "CG_E_INVAL", 2: "CG_E_OVERFLOW", 3: "CG_E_NOMEM", 4: "CG_E_CUDA", 5: "CG_E_NCCL",
           6: "CG_E_EMPTY_COLUMN", 7: "CG_E_STATE", 8: "CG_E_NOT_CONVERGED"}

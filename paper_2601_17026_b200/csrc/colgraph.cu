@@ -205,13 +205,19 @@ cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode) {
         cudaHostAlloc(&sl->h_bst, sizeof(BfsState), cudaHostAllocDefault) != cudaSuccess)
         return CG_E_NOMEM;
     char *p = sl->ws;
-    int32_t *pl[8];
-    for (int i = 0; i < 8; i++) pl[i] = carve<int32_t>(p, plane) + geo.YZ;  // owned plane x = 0
-    sl->s.E = pl[0];
-    sl->s.H = pl[1];
-    sl->s.T = pl[2];
-    sl->s.D = pl[3];
-    for (int d = 0; d < 4; d++) sl->s.L[d] = pl[4 + d];
+#if CG_LAYOUT_AOS
+    int32_t *rec = carve<int32_t>(p, 8 * plane) + 8 * geo.YZ;  // owned plane x = 0
+    Field fl[8];
+    for (int i = 0; i < 8; i++) fl[i] = Field{rec + i};
+#else
+    Field fl[8];
+    for (int i = 0; i < 8; i++) fl[i] = Field{carve<int32_t>(p, plane) + geo.YZ};
+#endif
+    sl->s.E = fl[0];
+    sl->s.H = fl[1];
+    sl->s.T = fl[2];
+    sl->s.D = fl[3];
+    for (int d = 0; d < 4; d++) sl->s.L[d] = fl[4 + d];
     sl->blist[0] = carve<int>(p, n);
     sl->blist[1] = carve<int>(p, n);
     sl->vstamp = carve<int>(p, n);
@@ -336,8 +342,8 @@ cg_status halo_sweep(cg_graph *g) {
 void k_fill_ghost_h(Slab *sl) {
     const Geo &geo = sl->geo;
     const int grid = grid_for(geo.YZ, 256, sl->num_sms * 4);
-    if (geo.gl) k_fill<<<grid, 256, 0, sl->stream>>>(sl->s.H - geo.YZ, geo.YZ, geo.INF);
-    if (geo.gh) k_fill<<<grid, 256, 0, sl->stream>>>(sl->s.H + geo.n, geo.YZ, geo.INF);
+    if (geo.gl) k_fill<<<grid, 256, 0, sl->stream>>>(sl->s.H, -geo.YZ, geo.YZ, geo.INF);
+    if (geo.gh) k_fill<<<grid, 256, 0, sl->stream>>>(sl->s.H, geo.n, geo.YZ, geo.INF);
 }
 
 // Strict level-synchronous BFS of one slab without neighbours (the single-GPU path).
@@ -348,7 +354,8 @@ cg_status bfs_strict(cg_graph *g, Slab *sl) {
     sl->h_bst->L = 1;
     CG_CUDA(cudaMemcpyAsync(&sl->bst->L, &sl->h_bst->L, sizeof(int), cudaMemcpyHostToDevice, st));
     k_bfs_init<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, st>>>(geo, sl->s, sl->blist[0], &sl->bst->cnt[0]);
-    g->st.kernel_launches++;
+    k_bfs_seeded<<<1, 1, 0, st>>>(sl->bst);
+    g->st.kernel_launches += 2;
     int L = 1;
     for (int batch = 0;; batch++) {
         const int nb = batch == 0 ? 8 : BFS_BATCH;
@@ -911,10 +918,11 @@ cg_status colgraph_export_state(cg_graph *g, int32_t *out_dev) {
     const int64_t ntot = g->local ? g->n_global : g->slabs[0]->geo.n;
     for (Slab *sl : g->slabs) {
         const int64_t off = g->local ? (int64_t)sl->x0 * sl->geo.YZ : 0;
-        const int32_t *planes[8] = {sl->s.E, sl->s.H, sl->s.T, sl->s.D, sl->s.L[0], sl->s.L[1], sl->s.L[2], sl->s.L[3]};
+        const Field planes[8] = {sl->s.E, sl->s.H, sl->s.T, sl->s.D, sl->s.L[0], sl->s.L[1], sl->s.L[2], sl->s.L[3]};
         for (int f = 0; f < 8; f++)
-            CG_CUDA(cudaMemcpyAsync(out_dev + f * ntot + off, planes[f], sizeof(int32_t) * sl->geo.n,
-                                    cudaMemcpyDeviceToDevice, sl->stream));
+            k_export<<<grid_for(sl->geo.n, 256, sl->num_sms * 8), 256, 0, sl->stream>>>(planes[f], sl->geo.n,
+                                                                                          out_dev + f * ntot + off);
+        CG_CUDA(cudaGetLastError());
     }
     for (Slab *sl : g->slabs) CG_CUDA(cudaStreamSynchronize(sl->stream));
     return CG_OK;

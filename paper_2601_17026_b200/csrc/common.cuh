@@ -25,14 +25,28 @@ struct Geo {
     int32_t INF;             // n_global + 1: "cannot reach t"
 };
 
-// 8 int32 planes: E excess, H height, T sink residual, D flow on the down arc (= residual
-// of the up arc into this vertex from below), L[d] flow on the lateral arc in direction d
-// (= residual of its reverse arc).  Directions: 0:+x 1:-x 2:+y 3:-y.  Each plane holds
-// X+2 x-planes; the pointers address owned plane x = 0, so the ghost planes of the
-// neighbour slabs sit at vertex indices [-YZ, 0) and [n, n+YZ).
+// Residual state: 8 int32 fields per vertex -- E excess, H height, T sink residual, D flow
+// on the down arc (= residual of the up arc into this vertex from below), L[d] flow on the
+// lateral arc in direction d (= residual of its reverse arc); directions 0:+x 1:-x 2:+y 3:-y.
+// Layout: CG_LAYOUT_AOS = 1 (default) stores the 8 fields of a vertex as one
+// 32-byte record (one DRAM sector): the sweep and relabel kernels touch scattered vertices,
+// and one sector then carries all of a vertex's fields.  CG_LAYOUT_AOS = 0 stores 8 planes.
+// Either way z is fastest and each field spans X+2 x-planes: Field::p addresses owned plane
+// x = 0, so the ghost planes of the neighbour slabs sit at vertex indices [-YZ, 0) and
+// [n, n+YZ).
+#ifndef CG_LAYOUT_AOS
+#define CG_LAYOUT_AOS 1
+#endif
+constexpr int FIELD_STRIDE = CG_LAYOUT_AOS ? 8 : 1;
+
+struct Field {
+    int32_t *p;
+    __device__ __forceinline__ int32_t &operator[](int64_t i) const { return p[i * FIELD_STRIDE]; }
+};
+
 struct Soa {
-    int32_t *E, *H, *T, *D;
-    int32_t *L[4];
+    Field E, H, T, D;
+    Field L[4];
 };
 
 constexpr int64_t NONE = INT64_MIN;  // "no vertex" (ghost vertices of the x = -1 plane are negative)
@@ -94,6 +108,39 @@ __device__ __forceinline__ void warp_append(bool has, int item, int *list, unsig
     base = __shfl_sync(FULL, base, 0);
     if (has) list[base + __popc(m & lanemask_lt())] = item;
 }
+
+// Span append: a warp collects up to SPAN lane masks (item j of lane l = base_j + l) and
+// appends all selected items with ONE atomic (dense list builders would otherwise put one
+// atomic per 32 items on a single counter).
+template <int SPAN>
+struct SpanAppender {
+    unsigned m[SPAN];
+    int64_t b[SPAN];
+    int k = 0;
+    __device__ __forceinline__ void add(unsigned mask, int64_t base) {
+        m[k] = mask;
+        b[k] = base;
+        ++k;
+    }
+    __device__ __forceinline__ void flush(int *list, unsigned *count) {
+        int tot = 0;
+#pragma unroll
+        for (int j = 0; j < SPAN; j++)
+            if (j < k) tot += __popc(m[j]);
+        if (tot) {
+            unsigned base = 0;
+            if (lane_id() == 0) base = atomicAdd(count, (unsigned)tot);
+            base = __shfl_sync(FULL, base, 0);
+#pragma unroll
+            for (int j = 0; j < SPAN; j++) {
+                if (j >= k) break;
+                if ((m[j] >> lane_id()) & 1u) list[base + __popc(m[j] & lanemask_lt())] = (int)(b[j] + lane_id());
+                base += __popc(m[j]);
+            }
+        }
+        k = 0;
+    }
+};
 
 // Mark a chunk / column id (or -1) for the next worklist, de-duplicated inside the warp
 // (__match_any_sync) and across warps (stamp[id] == tag means "already listed").

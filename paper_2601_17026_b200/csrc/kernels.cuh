@@ -16,6 +16,14 @@
 
 namespace cg {
 
+// Occupancy targets of the latency-bound worklist kernels (blocks per SM).
+#ifndef CG_SWEEP_MINB
+#define CG_SWEEP_MINB 4
+#endif
+#ifndef CG_BFS_MINB
+#define CG_BFS_MINB 2
+#endif
+
 // ------------------------------------------------------------------ a1: build
 // One warp per column: w(0) = c(0) - (sum_z c + 1), w(z) = c(z) - c(z-1) (R1).
 // E = max(0,-w): source arcs pre-saturated (Goldberg-Tarjan init);
@@ -54,9 +62,16 @@ __global__ void k_build(Geo g, const int32_t *__restrict__ in, int weight_mode, 
     if (bad) atomicOr(flags, FLAG_OVERFLOW);
 }
 
-__global__ void k_fill(int32_t *p, int64_t n, int32_t v) {
+// f[lo .. lo+n) = v
+__global__ void k_fill(Field f, int64_t lo, int64_t n, int32_t v) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        p[i] = v;
+        f[lo + i] = v;
+}
+
+// out[0 .. n) = f[0 .. n)  (state export to plain planes)
+__global__ void k_export(Field f, int64_t n, int32_t *out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = f[i];
 }
 
 // ------------------------------------------------------------------ a3: push-relabel sweep
@@ -195,7 +210,7 @@ __device__ __forceinline__ void mark_vertex(const Geo &g, int64_t id, int *vstam
     warp_append(add, (int)id, list, count);
 }
 
-__global__ void __launch_bounds__(256) k_sweep_v(Geo g, Soa s, int ops, const int *__restrict__ lin,
+__global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_sweep_v(Geo g, Soa s, int ops, const int *__restrict__ lin,
                                                  const unsigned *cin, int *lout, unsigned *cout, unsigned *czero,
                                                  int *vstamp, int tag, unsigned long long *work, int *flags) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *czero = 0;
@@ -270,7 +285,7 @@ __device__ __forceinline__ void deposit(const Geo &g, const Soa &s, int64_t x, i
     }
 }
 
-__global__ void __launch_bounds__(256) k_walk(Geo g, Soa s, int K, const int *__restrict__ lin, const unsigned *cin,
+__global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_walk(Geo g, Soa s, int K, const int *__restrict__ lin, const unsigned *cin,
                                               int *lout, unsigned *cout, unsigned *czero, int *vstamp, int tag,
                                               unsigned long long *work, int *flags) {
     __shared__ BlockQueue q;
@@ -332,14 +347,21 @@ __global__ void __launch_bounds__(256) k_walk(Geo g, Soa s, int K, const int *__
 // After a global relabel: list every active vertex (E > 0, H < INF) in index order.
 __global__ void k_rebuild_vertices(Geo g, const Soa s, int *lout, unsigned *cout, int *vstamp, int tag,
                                    unsigned long long *active) {
+    constexpr int SPAN = 8;
+    SpanAppender<SPAN> ap;
     unsigned long long myact = 0;
-    for (int64_t base = gwarp() * 32; base < g.n; base += nwarps() * 32) {
-        const int64_t v = base + lane_id();
-        bool a = false;
-        if (v < g.n) a = s.E[v] > 0 && s.H[v] < g.INF;
-        if (a) vstamp[v] = tag;
-        myact += a;
-        warp_append(a, (int)v, lout, cout);
+    for (int64_t base = gwarp() * 32 * SPAN; base < g.n; base += nwarps() * 32 * SPAN) {
+#pragma unroll
+        for (int j = 0; j < SPAN; j++) {
+            const int64_t b0 = base + 32 * j;
+            const int64_t v = b0 + lane_id();
+            bool a = false;
+            if (v < g.n) a = s.E[v] > 0 && s.H[v] < g.INF;
+            if (a) vstamp[v] = tag;
+            myact += a;
+            ap.add(__ballot_sync(FULL, a), b0);
+        }
+        ap.flush(lout, cout);
     }
     myact = warp_sum_ll((long long)myact);
     if (lane_id() == 0 && myact) atomicAdd(active, myact);
@@ -354,14 +376,21 @@ __global__ void k_rebuild_vertices(Geo g, const Soa s, int *lout, unsigned *cout
 //   u = (nbr, zi(z))          lateral arc of u into v, infinite
 //   u = (nbr_d, zo(z))        reverse of v's lateral arc in direction d, residual L_d(v)
 __global__ void k_bfs_init(Geo g, Soa s, int *lout, unsigned *cout) {
-    for (int64_t base = gwarp() * 32; base < g.n; base += nwarps() * 32) {
-        const int64_t v = base + lane_id();
-        bool seed = false;
-        if (v < g.n) {
-            seed = s.T[v] > 0;
-            s.H[v] = seed ? 1 : g.INF;
+    constexpr int SPAN = 8;
+    SpanAppender<SPAN> ap;
+    for (int64_t base = gwarp() * 32 * SPAN; base < g.n; base += nwarps() * 32 * SPAN) {
+#pragma unroll
+        for (int j = 0; j < SPAN; j++) {
+            const int64_t b0 = base + 32 * j;
+            const int64_t v = b0 + lane_id();
+            bool seed = false;
+            if (v < g.n) {
+                seed = s.T[v] > 0;
+                s.H[v] = seed ? 1 : g.INF;
+            }
+            ap.add(__ballot_sync(FULL, seed), b0);
         }
-        warp_append(seed, (int)v, lout, cout);
+        ap.flush(lout, cout);
     }
 }
 
@@ -431,12 +460,64 @@ __device__ __forceinline__ void bfs_expand_warp(const Geo &g, const Soa &s, int 
 //   or empties.
 constexpr unsigned BFS_SMALL = 2048;
 struct BfsState {
-    int L;              // current level (1-based)
-    unsigned cnt[3];    // frontier counters
-    unsigned finished;  // blocks done with the current large level
+    int L;                 // current level (1-based)
+    unsigned cnt[3];       // frontier counters
+    unsigned finished;     // blocks done with the current large level
+    unsigned long long claimed;  // vertices labelled so far (direction-optimising switch)
 };
 
-__global__ void __launch_bounds__(512) k_bfs_step(Geo g, Soa s, int *list0, int *list1, BfsState *st) {
+__global__ void k_bfs_seeded(BfsState *st) { st->claimed = st->cnt[0]; }
+
+// Bottom-up (pull) level for large frontiers: every unlabelled vertex u of a 32-z chunk
+// looks for a residual out-arc into level L -- t-arc (L = 0 only), down (u-1), up (u+1 if
+// D(u+1) > 0), lateral-out (nbr, zo), lateral-in reverse (nbr, zi) if L_{d^1}(nbr, zi) > 0 --
+// and takes label L+1.  All loads of a warp are coalesced lines of the chunk or its
+// shifted neighbour chunks, so a level costs ~4 B/vertex plus the unlabelled vertices,
+// instead of ~15 scattered sectors per frontier vertex (Beamer's direction optimisation).
+// Race-free: u is written only by its own lane, and a vertex written L+1 during the level
+// is never read as L by another lane.
+__device__ __forceinline__ void bfs_bottom_up_level(const Geo &g, const Soa &s, int L, int *lout, unsigned *cout) {
+    constexpr int SPAN = 4;
+    SpanAppender<SPAN> ap;
+    const int64_t nchunks = g.nchunks;
+    for (int64_t cb = gwarp() * SPAN; cb < nchunks; cb += nwarps() * SPAN) {
+#pragma unroll
+        for (int j = 0; j < SPAN; j++) {
+            const int64_t ch = cb + j;
+            bool hit = false;
+            int64_t b0 = 0;
+            if (ch < nchunks) {
+                const int64_t col = ch / g.CPC;
+                const int z = (int)(ch - col * g.CPC) * 32 + lane_id();
+                const int64_t v0 = col * g.Z;
+                b0 = v0 + (z - lane_id());
+                const bool valid = z < g.Z;
+                const int64_t u = v0 + z;
+                const bool need = valid && s.H[u] >= g.INF;
+                if (__any_sync(FULL, need) && need) {
+                    if (z >= 1 && s.H[u - 1] == L) hit = true;
+                    if (!hit && z + 1 < g.Z && s.D[u + 1] > 0 && s.H[u + 1] == L) hit = true;
+                    if (!hit) {
+                        const int x = (int)(col / g.Y), y = (int)(col - (int64_t)x * g.Y);
+                        const int zo = zo_of(z, g.delta), zi = zi_of(z, g.delta, g.Z);
+#pragma unroll
+                        for (int d = 0; d < 4 && !hit; d++) {
+                            const int64_t o = nbr_off(g, x, y, d);
+                            if (!o) continue;
+                            if (zo >= 0 && s.H[v0 + o + zo] == L) hit = true;
+                            else if (zi >= 0 && s.L[d ^ 1][v0 + o + zi] > 0 && s.H[v0 + o + zi] == L) hit = true;
+                        }
+                    }
+                    if (hit) s.H[u] = L + 1;
+                }
+            }
+            ap.add(__ballot_sync(FULL, hit), b0);
+        }
+        ap.flush(lout, cout);
+    }
+}
+
+__global__ void __launch_bounds__(512, CG_BFS_MINB) k_bfs_step(Geo g, Soa s, int *list0, int *list1, BfsState *st) {
     __shared__ int sL;
     if (threadIdx.x == 0) sL = *(volatile int *)&st->L;
     __syncthreads();
@@ -458,6 +539,7 @@ __global__ void __launch_bounds__(512) k_bfs_step(Geo g, Soa s, int *list0, int 
             __syncthreads();
             ++L;
             count = *(volatile unsigned *)&st->cnt[(L - 1) % 3];
+            if (threadIdx.x == 0) st->claimed += count;
             __syncthreads();
             if (count == 0 || count > BFS_SMALL) break;
         }
@@ -468,10 +550,19 @@ __global__ void __launch_bounds__(512) k_bfs_step(Geo g, Soa s, int *list0, int 
     const int *lin = (i & 1) ? list1 : list0;
     int *lout = (i & 1) ? list0 : list1;
     if (blockIdx.x == 0 && threadIdx.x == 0) st->cnt[(i + 2) % 3] = 0;
-    for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {
-        const int64_t j = base + lane_id();
-        bfs_expand_warp<true>(g, s, L + 1, j < count ? (int64_t)lin[j] : -1, lout, &st->cnt[(i + 1) % 3], nullptr,
-                              0);
+    // direction optimisation: a top-down expansion touches ~15 scattered sectors per frontier
+    // vertex; a bottom-up level ~4 B per vertex plus ~10 coalesced loads per unlabelled vertex
+    const unsigned long long unvisited = (unsigned long long)g.n - *(volatile unsigned long long *)&st->claimed;
+    // (unreachable vertices stay unvisited and are re-checked every bottom-up level, so only
+    // switch when the frontier is a large share of what is left)
+    if ((unsigned long long)count * 2ull > unvisited && (unsigned long long)count * 64ull > (unsigned long long)g.n) {
+        bfs_bottom_up_level(g, s, L, lout, &st->cnt[(i + 1) % 3]);
+    } else {
+        for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {
+            const int64_t j = base + lane_id();
+            bfs_expand_warp<true>(g, s, L + 1, j < count ? (int64_t)lin[j] : -1, lout, &st->cnt[(i + 1) % 3],
+                                  nullptr, 0);
+        }
     }
     __threadfence();
     __syncthreads();
@@ -479,6 +570,7 @@ __global__ void __launch_bounds__(512) k_bfs_step(Geo g, Soa s, int *list0, int 
         const unsigned f = atomicAdd(&st->finished, 1u);
         if (f == gridDim.x - 1) {
             st->finished = 0;
+            st->claimed += *(volatile unsigned *)&st->cnt[(i + 1) % 3];
             st->L = L + 1;
         }
     }
@@ -598,7 +690,7 @@ __global__ void k_halo_unpack_h(Geo g, Soa s, int side, const int32_t *__restric
 // Cherkassky-Goldberg gap: if no vertex has label g (0 < g < max
 // finite label), every vertex labelled above g cannot reach t: lift it to INF.
 constexpr int GAP_BINS = 1 << 20;
-__global__ void k_gap_hist(Geo g, const int32_t *__restrict__ H, unsigned *hist, int *maxh) {
+__global__ void k_gap_hist(Geo g, const Field H, unsigned *hist, int *maxh) {
     int mymax = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += (int64_t)gridDim.x * blockDim.x) {
         const int h = H[i];
@@ -626,7 +718,7 @@ __global__ void k_gap_find(const unsigned *hist, const int *maxh, int *gap) {
         *gap = b;
     }
 }
-__global__ void k_gap_lift(Geo g, int32_t *H, const int *gap, unsigned long long *lifted) {
+__global__ void k_gap_lift(Geo g, Field H, const int *gap, unsigned long long *lifted) {
     const int gp = *gap;
     int c = 0;
     if (gp != INT_MAX) {
@@ -641,7 +733,7 @@ __global__ void k_gap_lift(Geo g, int32_t *H, const int *gap, unsigned long long
 }
 
 // ------------------------------------------------------------------ a6: flow value
-__global__ void k_sum_T(Geo g, const int32_t *__restrict__ T, unsigned long long *out) {
+__global__ void k_sum_T(Geo g, const Field T, unsigned long long *out) {
     long long acc = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += (int64_t)gridDim.x * blockDim.x)
         acc += T[i];
@@ -748,7 +840,7 @@ __global__ void __launch_bounds__(256) k_precancel(Geo g, Soa s, int *flags) {
 // A neighbour whose top rises is listed for the next round; a ghost column's rise is
 // delivered to its owner by the top halo (k_top_halo_*).  top[] is indexed by column with
 // the ghost columns at [-Y, 0) and [ncol, ncol + Y).
-__device__ __forceinline__ int warp_climb(const Geo &g, const int32_t *__restrict__ D, int64_t v0, int t) {
+__device__ __forceinline__ int warp_climb(const Geo &g, const Field D, int64_t v0, int t) {
     for (int base = t + 1; base < g.Z; base += 32) {
         const int z = base + lane_id();
         const bool stop = (z >= g.Z) || D[v0 + z] <= 0;
