@@ -87,7 +87,15 @@ typedef struct {
  *   max_sweeps  : give up with CG_E_NOT_CONVERGED after this many sweeps; default 1<<30
  *   ops_per_sweep : push/relabel operations a vertex may perform per sweep; default 1
  *   walk_len    : > 0 selects multi-hop sweeps: a vertex's excess follows admissible arcs
- *                 for up to walk_len hops per launch; 0 = library default, -1 = single hop */
+ *                 for up to walk_len hops per launch; 0 = library default, -1 = single hop
+ *                 (vertex-worklist sweep only)
+ *   sweep_kind  : CG_SWEEP_AUTO (0, default) = CG_SWEEP_VERTEX (2): vertex worklists with
+ *                 multi-hop walks; CG_SWEEP_TILES (1): shared-memory column tiles (single
+ *                 slab and Z <= 256, else CG_E_INVAL).
+ *                 A "sweep" of the tile kind is one checkerboard phase (one tile colour).
+ *   tile_steps  : synchronous push steps per tile visit (0 = default 64)
+ *   tile_relabel_every : exact local relabel at the start of a tile visit and every k push
+ *                 steps (0 = default 16, < 0 = never) */
 typedef struct {
     float gr_factor;
     int32_t gap_every;
@@ -95,7 +103,12 @@ typedef struct {
     int64_t max_sweeps;
     int32_t ops_per_sweep;
     int32_t walk_len;
+    int32_t sweep_kind;
+    int32_t tile_steps;
+    int32_t tile_relabel_every;
 } cg_solve_opts;
+
+enum { CG_SWEEP_AUTO = 0, CG_SWEEP_TILES = 1, CG_SWEEP_VERTEX = 2 };
 
 typedef struct {
     int64_t sweeps;            /* push-relabel sweep launches */
@@ -110,8 +123,10 @@ typedef struct {
     int64_t source_capacity;   /* N = sum of source-arc capacities (int64) */
     int64_t kernel_launches;   /* library kernel launches during solve + extract */
     double ms_sweep_kernels;   /* CUDA-event time of all sweep launches (on the library stream) */
-    double sweep_bytes_alg;    /* algorithmic bytes moved by all sweeps: 4 B per vertex (excess scan)
-                                  + 40 B per active-vertex visit (28 B state read, 12 B push writes) */
+    double sweep_bytes_alg;    /* algorithmic bytes moved by all sweeps: vertex worklists 44 B per
+                                  push/relabel operation; tiles (64 B per tile vertex + 8 B per halo
+                                  vertex) per tile visit */
+    int64_t tile_visits;       /* tile visits summed over all phases (tile sweeps only) */
 } cg_solve_stats;
 
 /* a1 -- build the int32 structure-of-arrays residual graph.

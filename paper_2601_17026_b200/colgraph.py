@@ -38,7 +38,8 @@ class cg_dist(ctypes.Structure):
 
 class cg_solve_opts(ctypes.Structure):
     _fields_ = [("gr_factor", ctypes.c_float), ("gap_every", ctypes.c_int32), ("check_every", ctypes.c_int32),
-                ("max_sweeps", ctypes.c_int64), ("ops_per_sweep", ctypes.c_int32), ("walk_len", ctypes.c_int32)]
+                ("max_sweeps", ctypes.c_int64), ("ops_per_sweep", ctypes.c_int32), ("walk_len", ctypes.c_int32),
+                ("sweep_kind", ctypes.c_int32), ("tile_steps", ctypes.c_int32), ("tile_relabel_every", ctypes.c_int32)]
 
 
 class cg_solve_stats(ctypes.Structure):
@@ -48,7 +49,8 @@ class cg_solve_stats(ctypes.Structure):
                 ("ms_extract", ctypes.c_double), ("ms_global_relabel", ctypes.c_double),
                 ("ms_sweeps", ctypes.c_double), ("bytes_per_sweep_alg", ctypes.c_double),
                 ("source_capacity", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
-                ("ms_sweep_kernels", ctypes.c_double), ("sweep_bytes_alg", ctypes.c_double)]
+                ("ms_sweep_kernels", ctypes.c_double), ("sweep_bytes_alg", ctypes.c_double),
+                ("tile_visits", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -103,10 +105,13 @@ def version() -> str:
     return _lib.cg_version().decode()
 
 
+SWEEP_AUTO, SWEEP_TILES, SWEEP_VERTEX = 0, 1, 2
+
+
 def make_opts(gr_factor=1.0, gap_every=0, check_every=16, max_sweeps=1 << 30, ops_per_sweep=1,
-              walk_len=0) -> cg_solve_opts:
+              walk_len=0, sweep_kind=SWEEP_AUTO, tile_steps=0, tile_relabel_every=0) -> cg_solve_opts:
     return cg_solve_opts(float(gr_factor), int(gap_every), int(check_every), int(max_sweeps), int(ops_per_sweep),
-                         int(walk_len))
+                         int(walk_len), int(sweep_kind), int(tile_steps), int(tile_relabel_every))
 
 
 def _dist(device=0, stream=None, rank=0, nranks=1, nccl_id=None) -> cg_dist:

@@ -26,6 +26,7 @@
 #include "colgraph.h"
 #include "kernels.cuh"
 #include "nccl_shim.h"
+#include "tile.cuh"
 
 #include <algorithm>
 #include <chrono>
@@ -59,6 +60,7 @@ struct Slab {
     BfsState *bst = nullptr;
     unsigned *cnt = nullptr;             // [0..2] sweep lists, [4..6] lc waves, [8..10] extraction, [12] changes
     unsigned long long *work = nullptr;  // [RING] operations per sweep
+    unsigned long long *visits = nullptr;  // [RING] tile visits per phase
     unsigned long long *u64 = nullptr;   // [0]=N [1]=sumT0 [2]=sumT [3]=active [4]=gap lifted [5]=scratch
     int *flags = nullptr;                // [0]=overflow [1]=maxh [2]=gap [3]=empty
     int32_t *snap[2] = {nullptr, nullptr};   // ghost lateral residual at the last refresh
@@ -67,7 +69,7 @@ struct Slab {
     int32_t *hrecv[2] = {nullptr, nullptr};
     // pinned host mirrors
     unsigned *h_cnt = nullptr;
-    unsigned long long *h_work = nullptr, *h_u64 = nullptr;
+    unsigned long long *h_work = nullptr, *h_u64 = nullptr, *h_visits = nullptr;
     int *h_flags = nullptr;
     BfsState *h_bst = nullptr;
     int64_t N = 0, sumT0 = 0;
@@ -76,6 +78,14 @@ struct Slab {
     int out_tag = 0;   // tag of the list the last sweep wrote (halo appends must reuse it)
     int wave_k = 0;    // label-correcting waves since the relabel started
     int ext_k = 0;     // extraction rounds
+    // tile discharge (tile.cuh)
+    bool tiles = false;
+    TileGeo tg{};
+    int tS = 0;                 // lane segment length (template instance)
+    int tgrid = 0;              // persistent grid of k_tile_phase
+    size_t tsmem = 0;           // dynamic shared memory per CTA
+    TileLists tl{};
+    int tphase = 0;             // next phase number (colour = phase & 1)
 };
 }  // namespace
 
@@ -167,6 +177,8 @@ size_t workspace_bytes(const Geo &geo) {
     b += al(sizeof(unsigned) * 16) + al(sizeof(unsigned long long) * RING) + al(sizeof(unsigned long long) * 16) +
          al(sizeof(int) * 16);
     b += 4 * al(sizeof(int32_t) * geo.YZ) + 4 * al(sizeof(int32_t) * 4 * std::max<int64_t>(geo.YZ, 2 * geo.Y));
+    b += 5 * al(sizeof(int) * ncol) + al(sizeof(unsigned) * 4) + al(sizeof(unsigned long long) * RING) +
+         al(sizeof(unsigned long long) * 16);
     return b;
 }
 
@@ -178,6 +190,7 @@ void slab_free(Slab *sl) {
     cudaFreeHost(sl->h_u64);
     cudaFreeHost(sl->h_flags);
     cudaFreeHost(sl->h_bst);
+    cudaFreeHost(sl->h_visits);
     delete sl;
 }
 
@@ -202,7 +215,8 @@ cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode) {
         cudaHostAlloc(&sl->h_work, sizeof(unsigned long long) * RING, cudaHostAllocDefault) != cudaSuccess ||
         cudaHostAlloc(&sl->h_u64, sizeof(unsigned long long) * 16, cudaHostAllocDefault) != cudaSuccess ||
         cudaHostAlloc(&sl->h_flags, sizeof(int) * 16, cudaHostAllocDefault) != cudaSuccess ||
-        cudaHostAlloc(&sl->h_bst, sizeof(BfsState), cudaHostAllocDefault) != cudaSuccess)
+        cudaHostAlloc(&sl->h_bst, sizeof(BfsState), cudaHostAllocDefault) != cudaSuccess ||
+        cudaHostAlloc(&sl->h_visits, sizeof(unsigned long long) * RING, cudaHostAllocDefault) != cudaSuccess)
         return CG_E_NOMEM;
     char *p = sl->ws;
 #if CG_LAYOUT_AOS
@@ -233,6 +247,11 @@ cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode) {
     sl->u64 = carve<unsigned long long>(p, 16);
     sl->flags = carve<int>(p, 16);
     const int64_t msg = 4 * std::max<int64_t>(geo.YZ, 2 * geo.Y);
+    for (int k = 0; k < 4; k++) sl->tl.list[k] = carve<int>(p, ncol);
+    sl->tl.stamp = carve<int>(p, ncol);
+    sl->tl.cnt = carve<unsigned>(p, 4);
+    sl->tl.prof = carve<unsigned long long>(p, 16);
+    sl->visits = carve<unsigned long long>(p, RING);
     for (int side = 0; side < 2; side++) {
         sl->snap[side] = carve<int32_t>(p, geo.YZ);
         sl->hold[side] = carve<int32_t>(p, geo.YZ);
@@ -455,10 +474,17 @@ cg_status global_relabel(cg_graph *g, int64_t *active) {
     int64_t act = 0;
     for (Slab *sl : g->slabs) {
         const Geo &geo = sl->geo;
-        CG_CUDA(cudaMemsetAsync(sl->cnt, 0, 3 * sizeof(unsigned), sl->stream));
         CG_CUDA(cudaMemsetAsync(sl->u64 + 3, 0, sizeof(unsigned long long), sl->stream));
-        k_rebuild_vertices<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(
-            geo, sl->s, sl->blist[0], sl->cnt, sl->vstamp, ++sl->tag, sl->u64 + 3);
+        if (sl->tiles) {  // tile worklists: colour 0 tiles for the next even phase, colour 1 for the one after
+            sl->tphase += sl->tphase & 1;
+            CG_CUDA(cudaMemsetAsync(sl->tl.cnt, 0, 4 * sizeof(unsigned), sl->stream));
+            k_tile_rebuild<<<sl->num_sms * 8, 256, 0, sl->stream>>>(geo, sl->tg, sl->s, sl->tl, sl->tphase,
+                                                                    sl->u64 + 3);
+        } else {
+            CG_CUDA(cudaMemsetAsync(sl->cnt, 0, 3 * sizeof(unsigned), sl->stream));
+            k_rebuild_vertices<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(
+                geo, sl->s, sl->blist[0], sl->cnt, sl->vstamp, ++sl->tag, sl->u64 + 3);
+        }
         g->st.kernel_launches++;
         sl->sweep_k = 0;
         CG_CUDA(cudaMemcpyAsync(sl->h_u64 + 3, sl->u64 + 3, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
@@ -487,6 +513,72 @@ cg_status run_gap(cg_graph *g, Slab *sl) {
     g->st.kernel_launches += 3;
     g->st.gap_runs++;
     return CG_OK;
+}
+
+// ---------------------------------------------------------------- a3 on column tiles (tile.cuh)
+
+typedef void (*TileKernel)(Geo, TileGeo, Soa, TileLists, int, unsigned long long *, unsigned long long *, int *);
+
+TileKernel tile_kernel(int S) {
+    switch (S) {
+        case 1: return k_tile_phase<1>;
+        case 2: return k_tile_phase<2>;
+        case 3: return k_tile_phase<3>;
+        case 4: return k_tile_phase<4>;
+        case 6: return k_tile_phase<6>;
+        case 8: return k_tile_phase<8>;
+        default: return nullptr;
+    }
+}
+
+int tile_max_threads_rt(int) { return 512; }
+
+// Choose the lane segment S (>= ceil(Z/32)) and the largest tile shape that fits shared
+// memory; false if Z is too tall for the instantiated sizes (the vertex-worklist sweep is
+// used then).  CG_TILE=TXxTY overrides the shape.
+bool tile_setup(Slab *sl, int steps, int relabel_every) {
+    const Geo &geo = sl->geo;
+    const int need = (geo.Z + 31) / 32;
+    static const int sizes[] = {1, 2, 3, 4, 6, 8};
+    int S = 0;
+    for (int c : sizes)
+        if (c >= need) { S = c; break; }
+    if (!S) return false;
+    int smem_max = 0;
+    cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, sl->device);
+    TileGeo t{};
+    t.P = S | 1;
+    t.CS = 32 * t.P;
+    t.steps = steps;
+    t.relabel_every = relabel_every;
+    static const int shapes[][2] = {{4, 8}, {4, 4}, {2, 4}, {2, 2}, {1, 2}, {1, 1}};
+    bool ok = false;
+    int ox = 0, oy = 0;
+    if (const char *e = getenv("CG_TILE")) sscanf(e, "%dx%d", &ox, &oy);
+    for (auto &sh : shapes) {
+        t.TX = ox > 0 ? ox : sh[0];
+        t.TY = oy > 0 ? oy : sh[1];
+        t.NC = t.TX * t.TY;
+        t.NH = 2 * (t.TX + t.TY);
+        if (t.NC * 32 <= tile_max_threads_rt(S) && tile_smem_bytes(t) <= (size_t)smem_max) { ok = true; break; }
+        if (ox > 0) break;
+    }
+    if (!ok) return false;
+    t.NTX = (geo.X + t.TX - 1) / t.TX;
+    t.NTY = (geo.Y + t.TY - 1) / t.TY;
+    TileKernel k = tile_kernel(S);
+    const size_t bytes = tile_smem_bytes(t);
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) return false;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, t.NC * 32, bytes) != cudaSuccess || per_sm < 1)
+        return false;
+    sl->tg = t;
+    sl->tS = S;
+    sl->tsmem = bytes;
+    sl->tgrid = sl->num_sms * per_sm;
+    sl->tiles = true;
+    if (!getenv("CG_TILE_PROF")) sl->tl.prof = nullptr;
+    return true;
 }
 
 Geo make_geo(const cg_dims *dims, int x0, int x1, int nranks_total, bool gl, bool gh, int64_t n_global) {
@@ -650,8 +742,18 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
     if (!g || !flow_value) return CG_E_INVAL;
     if (g->solved) return CG_E_STATE;
     DeviceGuard dg(g->dist.device);
-    cg_solve_opts o{1.0f, 0, 16, (int64_t)1 << 30, 1, 0};
+    cg_solve_opts o{1.0f, 0, 16, (int64_t)1 << 30, 1, 0, 0, 0, 0};
     if (opts) o = *opts;
+    if (o.sweep_kind == CG_SWEEP_AUTO && getenv("CG_SWEEP")) o.sweep_kind = atoi(getenv("CG_SWEEP"));
+    if (o.tile_steps <= 0) o.tile_steps = getenv("CG_TILE_STEPS") ? atoi(getenv("CG_TILE_STEPS")) : 64;
+    if (o.tile_relabel_every == 0)
+        o.tile_relabel_every = getenv("CG_TILE_RELABEL") ? atoi(getenv("CG_TILE_RELABEL")) : 16;
+    if (o.sweep_kind < CG_SWEEP_AUTO || o.sweep_kind > CG_SWEEP_VERTEX) return CG_E_INVAL;
+    // a3 flavour: the vertex-worklist sweep (AUTO: measured fastest) or
+    // shared-memory column tiles (single slab, Z within the instantiated sizes)
+    bool use_tiles = false;
+    if (o.sweep_kind == CG_SWEEP_TILES && !multi(g)) use_tiles = tile_setup(g->slabs[0], o.tile_steps, o.tile_relabel_every);
+    if (o.sweep_kind == CG_SWEEP_TILES && !use_tiles) return CG_E_INVAL;
     if (o.walk_len == 0) o.walk_len = getenv("CG_WALK") ? atoi(getenv("CG_WALK")) : 64;  // library default
     o.check_every = std::max(1, std::min(o.check_every, RING));
     o.ops_per_sweep = std::max(1, o.ops_per_sweep);
@@ -705,7 +807,67 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
     int64_t sweeps = 0, since_gap = 0, last_active = active;
     std::vector<int64_t> wv(RING);
     cg_status result = CG_OK;
-    while (active > 0) {
+    while (use_tiles && active > 0) {
+        // a3 on tiles: batches of checkerboard phases, no host sync inside a batch
+        if (sweeps >= o.max_sweeps) { result = CG_E_NOT_CONVERGED; break; }
+        const int batch = (int)std::min<int64_t>(o.check_every, o.max_sweeps - sweeps);
+        Slab *sl = s0;
+        const TileKernel tk = tile_kernel(sl->tS);
+        CG_CUDA(cudaMemsetAsync(sl->work, 0, sizeof(unsigned long long) * batch, st0));
+        CG_CUDA(cudaEventRecord(g->ev0, st0));
+        for (int i = 0; i < batch; i++) {
+            tk<<<sl->tgrid, sl->tg.NC * 32, sl->tsmem, st0>>>(sl->geo, sl->tg, sl->s, sl->tl, sl->tphase++,
+                                                               sl->work + i, sl->visits + i, sl->flags);
+            g->st.kernel_launches++;
+        }
+        CG_CUDA(cudaEventRecord(g->ev1, st0));
+        CG_CUDA(cudaGetLastError());
+        CG_CUDA(cudaMemcpyAsync(sl->h_work, sl->work, sizeof(unsigned long long) * batch, cudaMemcpyDeviceToHost, st0));
+        CG_CUDA(cudaMemcpyAsync(sl->h_visits, sl->visits, sizeof(unsigned long long) * batch, cudaMemcpyDeviceToHost,
+                                st0));
+        CG_CUDA(cudaMemcpyAsync(sl->h_cnt, sl->tl.cnt, 4 * sizeof(unsigned), cudaMemcpyDeviceToHost, st0));
+        CG_CUDA(cudaMemcpyAsync(sl->h_flags, sl->flags, sizeof(int), cudaMemcpyDeviceToHost, st0));
+        CG_CUDA(cudaStreamSynchronize(st0));
+        if (sl->h_flags[0] & FLAG_OVERFLOW) { result = CG_E_OVERFLOW; break; }
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, g->ev0, g->ev1);
+        g->st.ms_sweep_kernels += ms;
+        sweep_ms_since_gr += ms;
+        // algorithmic bytes of a tile visit: its state read and written once (2 x 32 B per
+        // vertex) + the halo's height and lateral residual (8 B per halo vertex)
+        const double visit_bytes = (64.0 * sl->tg.NC + 8.0 * sl->tg.NH) * (double)sl->geo.Z;
+        int64_t wsum = 0;
+        for (int i = 0; i < batch; i++) {
+            wsum += (int64_t)sl->h_work[i];
+            g->st.sweep_bytes_alg += visit_bytes * (double)sl->h_visits[i];
+            g->st.tile_visits += (int64_t)sl->h_visits[i];
+        }
+        work_since_gr += (double)wsum;
+        g->st.work += wsum;
+        sweeps += batch;
+        g->st.sweeps = sweeps;
+        const bool quiescent = sl->h_cnt[sl->tphase & 3] == 0 && sl->h_cnt[(sl->tphase + 1) & 3] == 0;
+        if (trace)
+            fprintf(stderr, "[cg] tile phases ..%d ops=%lld visits0=%llu next=%u/%u | %.3f ms\n", sl->tphase,
+                    (long long)wsum, (unsigned long long)sl->h_visits[0], sl->h_cnt[sl->tphase & 3],
+                    sl->h_cnt[(sl->tphase + 1) & 3], ms);
+        if (sl->tl.prof) {
+            unsigned long long pf[16];
+            CG_CUDA(cudaMemcpy(pf, sl->tl.prof, sizeof(pf), cudaMemcpyDeviceToHost));
+            const double v = (double)std::max(1ull, pf[PF_VISITS]);
+            fprintf(stderr, "[cg]   per visit: load %.0f relabel %.0f steps %.0f store %.0f cyc | relabels %.2f lat_it %.1f "
+                    "vert_it %.1f steps %.1f\n", pf[PF_LOAD] / v, pf[PF_RELABEL] / v, pf[PF_STEPS] / v,
+                    pf[PF_STORE] / v, pf[PF_N_RELABEL] / v, pf[PF_LAT_IT] / std::max(1.0, (double)pf[PF_N_RELABEL]),
+                    pf[PF_VERT_IT] / std::max(1.0, (double)pf[PF_LAT_IT]), pf[PF_N_STEPS] / v);
+            CG_CUDA(cudaMemset(sl->tl.prof, 0, sizeof(pf)));
+        }
+        if (quiescent || work_since_gr >= gr_budget || sweep_ms_since_gr >= gr_beta * std::max(last_gr_ms, 0.05)) {
+            CG_TRY(timed_gr());
+            work_since_gr = 0.0;
+            sweep_ms_since_gr = 0.0;
+        }
+    }
+    while (!use_tiles && active > 0) {
         if (sweeps >= o.max_sweeps) { result = CG_E_NOT_CONVERGED; break; }
         const int batch = (int)std::min<int64_t>(o.check_every, o.max_sweeps - sweeps);
         // multi-hop walks while many vertices are active; single hops in the sparse tail
