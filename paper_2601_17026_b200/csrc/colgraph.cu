@@ -61,6 +61,7 @@ struct Slab {
     unsigned *cnt = nullptr;             // [0..2] sweep lists, [4..6] lc waves, [8..10] extraction, [12] changes
     unsigned long long *work = nullptr;  // [RING] operations per sweep
     unsigned long long *visits = nullptr;  // [RING] tile visits per phase
+    unsigned *heads = nullptr;             // [RING] work-fetch cursors of k_walk_ws
     unsigned long long *u64 = nullptr;   // [0]=N [1]=sumT0 [2]=sumT [3]=active [4]=gap lifted [5]=scratch
     int *flags = nullptr;                // [0]=overflow [1]=maxh [2]=gap [3]=empty
     int32_t *snap[2] = {nullptr, nullptr};   // ghost lateral residual at the last refresh
@@ -79,6 +80,7 @@ struct Slab {
     int wave_k = 0;    // label-correcting waves since the relabel started
     int ext_k = 0;     // extraction rounds
     // tile discharge (tile.cuh)
+    int bfs_coop_grid = 0;      // > 0: persistent cooperative BFS (k_bfs_run) with this grid
     bool tiles = false;
     TileGeo tg{};
     int tS = 0;                 // lane segment length (template instance)
@@ -178,7 +180,7 @@ size_t workspace_bytes(const Geo &geo) {
          al(sizeof(int) * 16);
     b += 4 * al(sizeof(int32_t) * geo.YZ) + 4 * al(sizeof(int32_t) * 4 * std::max<int64_t>(geo.YZ, 2 * geo.Y));
     b += 5 * al(sizeof(int) * ncol) + al(sizeof(unsigned) * 4) + al(sizeof(unsigned long long) * RING) +
-         al(sizeof(unsigned long long) * 16);
+         al(sizeof(unsigned long long) * 16) + al(sizeof(unsigned) * RING);
     return b;
 }
 
@@ -252,6 +254,7 @@ cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode) {
     sl->tl.cnt = carve<unsigned>(p, 4);
     sl->tl.prof = carve<unsigned long long>(p, 16);
     sl->visits = carve<unsigned long long>(p, RING);
+    sl->heads = carve<unsigned>(p, RING);
     for (int side = 0; side < 2; side++) {
         sl->snap[side] = carve<int32_t>(p, geo.YZ);
         sl->hold[side] = carve<int32_t>(p, geo.YZ);
@@ -376,6 +379,18 @@ cg_status bfs_strict(cg_graph *g, Slab *sl) {
     k_bfs_seeded<<<1, 1, 0, st>>>(sl->bst);
     g->st.kernel_launches += 2;
     int L = 1;
+    if (sl->bfs_coop_grid > 0) {  // every level in one cooperative launch (k_bfs_run)
+        void *args[] = {(void *)&sl->geo, (void *)&sl->s, (void *)&sl->blist[0], (void *)&sl->blist[1],
+                        (void *)&sl->bst};
+        CG_CUDA(cudaLaunchCooperativeKernel((const void *)k_bfs_run, sl->bfs_coop_grid, 512, args, 0, st));
+        g->st.kernel_launches++;
+        CG_CUDA(cudaMemcpyAsync(sl->h_bst, sl->bst, sizeof(BfsState), cudaMemcpyDeviceToHost, st));
+        CG_CUDA(cudaStreamSynchronize(st));
+        L = sl->h_bst->L;
+        if (sl->h_bst->cnt[(L - 1) % 3] != 0) return CG_E_CUDA;
+        g->st.gr_passes += L - 1;
+        return CG_OK;
+    }
     for (int batch = 0;; batch++) {
         const int nb = batch == 0 ? 8 : BFS_BATCH;
         for (int b = 0; b < nb; b++)
@@ -703,6 +718,13 @@ static cg_status build_common(const cg_dims *dims, const int32_t *cost_dev, int3
         sl->device = dd.device;
         sl->stream = (cudaStream_t)dd.stream;
         sl->num_sms = num_sms;
+        {  // persistent BFS: as many 512-thread blocks as are co-resident (cooperative launch)
+            int per_sm = 0, coop = 0;
+            cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dd.device);
+            if (coop && !getenv("CG_BFS_LEVEL_LAUNCHES") &&
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bfs_run, 512, 0) == cudaSuccess && per_sm > 0)
+                sl->bfs_coop_grid = num_sms * std::min(per_sm, CG_BFS_MINB);
+        }
         sl->x0 = x0;
         sl->x1 = x1;
         sl->geo = make_geo(dims, x0, x1, nranks, r > 0, r + 1 < nranks, g->n_global);
@@ -796,6 +818,9 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
             fprintf(stderr, "[cg] GR#%lld levels=%lld active=%lld ms=%.3f (sweeps %lld) flow=%lld\n",
                     (long long)g->st.global_relabels, (long long)(g->st.gr_passes - p0), (long long)active, last_gr_ms,
                     (long long)g->st.sweeps, (long long)-sumT);
+            const unsigned *h = s0->h_bst->hist;
+            fprintf(stderr, "[cg]   levels by frontier: <=32 %u <=256 %u <=2K %u <=16K %u <=128K %u <=1M %u more %u "
+                    "(bottom-up %u)\n", h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
         }
         return s;
     };
@@ -803,6 +828,8 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
     const double gr_budget = (double)o.gr_factor * (double)g->n_global;
     const double walk_min = getenv("CG_WALK_MIN") ? atof(getenv("CG_WALK_MIN")) : 1e-3;
     const double gr_beta = getenv("CG_GR_BETA") ? atof(getenv("CG_GR_BETA")) : 1.0;
+    // work-fetching walk (k_walk_ws): measured -10 % on C3/C5, +10 % on C4, opt-in
+    const bool walk_ws = getenv("CG_WALK_WS") && atoi(getenv("CG_WALK_WS")) != 0;
     double work_since_gr = 0.0, sweep_ms_since_gr = 0.0;
     int64_t sweeps = 0, since_gap = 0, last_active = active;
     std::vector<int64_t> wv(RING);
@@ -872,7 +899,10 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
         const int batch = (int)std::min<int64_t>(o.check_every, o.max_sweeps - sweeps);
         // multi-hop walks while many vertices are active; single hops in the sparse tail
         const bool walk = o.walk_len > 0 && (double)last_active >= walk_min * (double)g->n_global;
-        for (Slab *sl : g->slabs) CG_CUDA(cudaMemsetAsync(sl->work, 0, sizeof(unsigned long long) * batch, sl->stream));
+        for (Slab *sl : g->slabs) {
+            CG_CUDA(cudaMemsetAsync(sl->work, 0, sizeof(unsigned long long) * batch, sl->stream));
+            if (walk && walk_ws) CG_CUDA(cudaMemsetAsync(sl->heads, 0, sizeof(unsigned) * batch, sl->stream));
+        }
         CG_CUDA(cudaEventRecord(g->ev0, st0));
         for (int i = 0; i < batch; i++) {
             for (Slab *sl : g->slabs) {
@@ -882,7 +912,12 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
                 const int gv = std::max(sl->num_sms, std::min(gridv, grid_for(2 * la, 256, gridv)));
                 const int k = sl->sweep_k++;
                 sl->out_tag = ++sl->tag;
-                if (walk)
+                if (walk && walk_ws)
+                    k_walk_ws<<<gv, 256, 0, sl->stream>>>(geo, sl->s, o.walk_len, sl->blist[k & 1], sl->cnt + k % 3,
+                                                          sl->blist[(k + 1) & 1], sl->cnt + (k + 1) % 3,
+                                                          sl->cnt + (k + 2) % 3, sl->vstamp, sl->out_tag, sl->work + i,
+                                                          sl->flags, sl->heads + i);
+                else if (walk)
                     k_walk<<<gv, 256, 0, sl->stream>>>(geo, sl->s, o.walk_len, sl->blist[k & 1], sl->cnt + k % 3,
                                                        sl->blist[(k + 1) & 1], sl->cnt + (k + 1) % 3,
                                                        sl->cnt + (k + 2) % 3, sl->vstamp, sl->out_tag, sl->work + i,

@@ -344,6 +344,95 @@ __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_walk(Geo g, Soa s, int K
     if (lane_id() == 0 && mywork) atomicAdd(work, mywork);
 }
 
+// Work-fetching variant of k_walk: a lane whose walk has ended takes the next worklist item
+// itself (warp-aggregated atomicAdd on *head), so every iteration of the loop advances 32
+// independent walks by one hop.  In k_walk a warp lasts as long as its longest walk (up to
+// K dependent hops) while the lanes whose walks ended idle.  Same hop semantics as k_walk.
+__global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_walk_ws(Geo g, Soa s, int K, const int *__restrict__ lin,
+                                                     const unsigned *cin, int *lout, unsigned *cout, unsigned *czero,
+                                                     int *vstamp, int tag, unsigned long long *work, int *flags,
+                                                     unsigned *head) {
+    __shared__ BlockQueue q;
+    __shared__ unsigned qbase;
+    if (threadIdx.x == 0) q.n = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *czero = 0;
+    __syncthreads();
+    const unsigned count = *cin;
+    unsigned long long mywork = 0;
+    bool exhausted = false, walking = false;
+    int c = 0, hx = 0, step = 0;
+    OpCtx ctx;
+    ctx.v = NONE;
+    for (;;) {
+        // lanes without a walk fetch the next items (one atomic per warp)
+        const bool need = !walking && !exhausted;
+        const unsigned m = __ballot_sync(FULL, need);
+        if (m) {
+            unsigned base = 0;
+            if (lane_id() == (__ffs(m) - 1)) base = atomicAdd(head, (unsigned)__popc(m));
+            base = __shfl_sync(FULL, base, __ffs(m) - 1);
+            if (need) {
+                const unsigned idx = base + __popc(m & lanemask_lt());
+                if (idx >= count) {
+                    exhausted = true;
+                } else {
+                    const int64_t v = lin[idx];
+                    c = s.E[v];
+                    hx = s.H[v];
+                    if (c > 0 && hx < g.INF) {
+                        atomicSub(&s.E[v], c);  // the owner takes its whole excess
+                        set_ctx(g, ctx, v);
+                        step = 0;
+                        walking = true;
+                    }
+                }
+            }
+        }
+        if (!__any_sync(FULL, walking || !exhausted)) break;
+        if (!walking) continue;
+        // one hop of this lane's walk
+        const ArcPick p = scan_arcs(g, s, ctx, hx);
+        mywork++;
+        if (p.best >= hx || step >= K) {  // stuck (or hop budget spent): deposit the carry here
+            if (p.best >= hx) atomicMax(&s.H[ctx.v], p.best >= g.INF ? g.INF : p.best + 1);
+            deposit(g, s, ctx.v, c, vstamp, tag, q, lout, cout, flags);
+            walking = false;
+            continue;
+        }
+        ++step;
+        int df;
+        switch (p.arc) {
+            case 0: df = reserve(&s.T[ctx.v], c); break;
+            case 1: df = c; atomicAdd(&s.D[ctx.v], df); break;
+            case 2: case 3: case 4: case 5: df = c; atomicAdd(&s.L[p.arc - 2][ctx.v], df); break;
+            case 6: df = reserve(&s.D[ctx.v + 1], c); break;
+            default: df = reserve(&s.L[(p.arc - 7) ^ 1][p.tgt], c); break;
+        }
+        if (df == 0) continue;  // lost a reservation race: rescan this vertex
+        if (p.arc == 0) {       // absorbed by t
+            c -= df;
+            if (c == 0) walking = false;
+            continue;
+        }
+        if (df < c) deposit(g, s, ctx.v, c - df, vstamp, tag, q, lout, cout, flags);
+        c = df;
+        if (!owned(g, p.tgt)) {  // crossed into a neighbour slab: hand the carry over
+            deposit(g, s, p.tgt, c, vstamp, tag, q, lout, cout, flags);
+            walking = false;
+            continue;
+        }
+        hx = p.best;
+        set_ctx(g, ctx, p.tgt);
+    }
+    __syncthreads();
+    const unsigned nq = min(q.n, (unsigned)BlockQueue::CAP);
+    if (threadIdx.x == 0 && nq) qbase = atomicAdd(cout, nq);
+    __syncthreads();
+    for (unsigned j = threadIdx.x; j < nq; j += blockDim.x) lout[qbase + j] = q.buf[j];
+    mywork = warp_sum_ll((long long)mywork);
+    if (lane_id() == 0 && mywork) atomicAdd(work, mywork);
+}
+
 // After a global relabel: list every active vertex (E > 0, H < INF) in index order.
 __global__ void k_rebuild_vertices(Geo g, const Soa s, int *lout, unsigned *cout, int *vstamp, int tag,
                                    unsigned long long *active) {
@@ -414,7 +503,7 @@ __device__ __forceinline__ void bfs_expand_warp(const Geo &g, const Soa &s, int 
         auto claim = [&](int slot, int64_t w) {
             if (!owned(g, w)) return;  // ghost labels come from their owner
             if (STRICT) {
-                if (s.H[w] >= INF && atomicCAS(&s.H[w], INF, nl) == INF) {
+                if (__ldcg(&s.H[w]) >= INF && atomicCAS(&s.H[w], INF, nl) == INF) {
                     u[slot] = (int)w;
                     got |= 1u << slot;
                 }
@@ -464,7 +553,12 @@ struct BfsState {
     unsigned cnt[3];       // frontier counters
     unsigned finished;     // blocks done with the current large level
     unsigned long long claimed;  // vertices labelled so far (direction-optimising switch)
+    unsigned bar[2];       // grid barrier of k_bfs_run (arrivals, generation)
+    unsigned hist[8];      // levels by frontier size: <=32, <=256, <=2048, <=16K, <=128K, <=1M, more; [7] bottom-up
 };
+__device__ __forceinline__ int bfs_bucket(unsigned c) {
+    return c <= 32 ? 0 : c <= 256 ? 1 : c <= 2048 ? 2 : c <= 16384 ? 3 : c <= 131072 ? 4 : c <= 1048576 ? 5 : 6;
+}
 
 __global__ void k_bfs_seeded(BfsState *st) { st->claimed = st->cnt[0]; }
 
@@ -493,10 +587,10 @@ __device__ __forceinline__ void bfs_bottom_up_level(const Geo &g, const Soa &s, 
                 b0 = v0 + (z - lane_id());
                 const bool valid = z < g.Z;
                 const int64_t u = v0 + z;
-                const bool need = valid && s.H[u] >= g.INF;
+                const bool need = valid && __ldcg(&s.H[u]) >= g.INF;
                 if (__any_sync(FULL, need) && need) {
-                    if (z >= 1 && s.H[u - 1] == L) hit = true;
-                    if (!hit && z + 1 < g.Z && s.D[u + 1] > 0 && s.H[u + 1] == L) hit = true;
+                    if (z >= 1 && __ldcg(&s.H[u - 1]) == L) hit = true;
+                    if (!hit && z + 1 < g.Z && s.D[u + 1] > 0 && __ldcg(&s.H[u + 1]) == L) hit = true;
                     if (!hit) {
                         const int x = (int)(col / g.Y), y = (int)(col - (int64_t)x * g.Y);
                         const int zo = zo_of(z, g.delta), zi = zi_of(z, g.delta, g.Z);
@@ -504,8 +598,8 @@ __device__ __forceinline__ void bfs_bottom_up_level(const Geo &g, const Soa &s, 
                         for (int d = 0; d < 4 && !hit; d++) {
                             const int64_t o = nbr_off(g, x, y, d);
                             if (!o) continue;
-                            if (zo >= 0 && s.H[v0 + o + zo] == L) hit = true;
-                            else if (zi >= 0 && s.L[d ^ 1][v0 + o + zi] > 0 && s.H[v0 + o + zi] == L) hit = true;
+                            if (zo >= 0 && __ldcg(&s.H[v0 + o + zo]) == L) hit = true;
+                            else if (zi >= 0 && s.L[d ^ 1][v0 + o + zi] > 0 && __ldcg(&s.H[v0 + o + zi]) == L) hit = true;
                         }
                     }
                     if (hit) s.H[u] = L + 1;
@@ -573,6 +667,100 @@ __global__ void __launch_bounds__(512, CG_BFS_MINB) k_bfs_step(Geo g, Soa s, int
             st->claimed += *(volatile unsigned *)&st->cnt[(i + 1) % 3];
             st->L = L + 1;
         }
+    }
+}
+
+// Persistent strict BFS: ONE cooperative launch runs every level, levels separated by a grid
+// barrier instead of a kernel boundary (a level with a small frontier costs a barrier, ~1-2 us,
+// instead of a launch and a host round trip every BFS batch).  Same level logic as
+// k_bfs_step: small frontiers are run by block 0 alone with block barriers, large ones by
+// the whole grid, top-down or bottom-up.  Must be launched with cudaLaunchCooperativeKernel
+// (all blocks co-resident).
+__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks) {
+    // sense-free counting barrier: bar[0] = arrivals, bar[1] = generation
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned *gen = bar + 1;
+        const unsigned g0 = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            bar[0] = 0;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g0) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(512, CG_BFS_MINB) k_bfs_run(Geo g, Soa s, int *list0, int *list1, BfsState *st) {
+    unsigned *bar = st->bar;
+    int L = *(volatile int *)&st->L;
+    unsigned long long claimed = *(volatile unsigned long long *)&st->claimed;
+    for (int guard = 0; guard <= g.INF + 2; guard++) {
+        const unsigned count = *(volatile unsigned *)&st->cnt[(L - 1) % 3];
+        if (count == 0) break;
+        const int i = L - 1;
+        if (count <= BFS_SMALL) {
+            // everyone has read this level's counter before block 0 starts recycling counters
+            grid_barrier(bar, gridDim.x);
+            if (blockIdx.x == 0) {
+                if (threadIdx.x == 0) st->claimed = claimed;
+                unsigned c = count;
+                for (;;) {
+                    const int j = L - 1;
+                    int *lin = (j & 1) ? list1 : list0;
+                    int *lout = (j & 1) ? list0 : list1;
+                    if (threadIdx.x == 0) {
+                        st->cnt[(j + 2) % 3] = 0;
+                        st->hist[bfs_bucket(c)]++;
+                    }
+                    for (unsigned base = (threadIdx.x >> 5) * 32; base < c; base += (blockDim.x >> 5) * 32) {
+                        const unsigned jj = base + lane_id();
+                        bfs_expand_warp<true>(g, s, L + 1, jj < c ? (int64_t)__ldcg(&lin[jj]) : -1, lout,
+                                              &st->cnt[(j + 1) % 3], nullptr, 0);
+                    }
+                    __syncthreads();
+                    ++L;
+                    c = *(volatile unsigned *)&st->cnt[(L - 1) % 3];
+                    if (threadIdx.x == 0) st->claimed += c;
+                    __syncthreads();
+                    if (c == 0 || c > BFS_SMALL) break;
+                }
+                if (threadIdx.x == 0) st->L = L;
+            }
+            grid_barrier(bar, gridDim.x);
+            L = *(volatile int *)&st->L;
+            claimed = *(volatile unsigned long long *)&st->claimed;
+            continue;
+        }
+        const int *lin = (i & 1) ? list1 : list0;
+        int *lout = (i & 1) ? list0 : list1;
+        // the counter of level L+1 was read by everyone before the previous barrier
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            st->cnt[(i + 2) % 3] = 0;
+            st->hist[bfs_bucket(count)]++;
+        }
+        const unsigned long long unvisited = (unsigned long long)g.n - claimed;
+        if ((unsigned long long)count * 2ull > unvisited && (unsigned long long)count * 64ull > (unsigned long long)g.n) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) st->hist[7]++;
+            bfs_bottom_up_level(g, s, L, lout, &st->cnt[(i + 1) % 3]);
+        } else {
+            for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {
+                const int64_t j = base + lane_id();
+                bfs_expand_warp<true>(g, s, L + 1, j < count ? (int64_t)__ldcg(&lin[j]) : -1, lout, &st->cnt[(i + 1) % 3],
+                                      nullptr, 0);
+            }
+        }
+        grid_barrier(bar, gridDim.x);
+        ++L;
+        claimed += *(volatile unsigned *)&st->cnt[(L - 1) % 3];  // every block: same value
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->L = L;
+        st->claimed = claimed;
     }
 }
 

@@ -1,8 +1,7 @@
-# ad-hoc GPU session (gpurun): stops at the first failing step
 set -x
-timeout 60 python __graft_entry__.py smoke > gpurun_out/t_smoke.log 2>&1 || exit 1
-CG_TILE_PROF=1 CG_TRACE=1 timeout 100 python scripts/diag_solve.py C4 > gpurun_out/t_diag_a.log 2> gpurun_out/t_trace4.log || exit 5
-CG_TILE_PROF=1 CG_TRACE=1 CG_TILE_RELABEL=-1 timeout 100 python scripts/diag_solve.py C4 > gpurun_out/t_diag_b.log 2> gpurun_out/t_trace4_r0.log || exit 5
-CG_TILE_PROF=1 CG_TRACE=1 CG_TILE_STEPS=16 timeout 100 python scripts/diag_solve.py C4 > gpurun_out/t_diag_c.log 2> gpurun_out/t_trace4_s16.log || exit 5
-CG_SWEEP=2 CG_TRACE=1 timeout 100 python scripts/diag_solve.py C4 > gpurun_out/t_diag_d.log 2> gpurun_out/t_trace4_old.log || exit 5
-timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -k "worked or tiny or c1 or c2 or edge or constant" > gpurun_out/t_tests.log 2>&1 || exit 3
+timeout 60 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1 || exit 1
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1 || exit 2
+timeout 400 python bench.py > gpurun_out/bench.log 2>&1 || exit 3
+timeout 120 python scripts/profile_one.py C4 > gpurun_out/plain.log 2>&1 && \
+timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python scripts/profile_one.py C4 > gpurun_out/ncu_list.log 2>&1 || exit 4
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_walk -s 4 -c 3 -o gpurun_out/prof_walk python scripts/profile_one.py C4 > gpurun_out/ncu_full.log 2>&1 || exit 5
