@@ -374,7 +374,13 @@ cg_status bfs_strict(cg_graph *g, Slab *sl) {
     cudaStream_t st = sl->stream;
     CG_CUDA(cudaMemsetAsync(sl->bst, 0, sizeof(BfsState), st));
     sl->h_bst->L = 1;
+    // direction optimisation measured slower than top-down on C3-C5: off unless asked
+    sl->h_bst->bu_alpha = getenv("CG_BU_ALPHA") ? atoi(getenv("CG_BU_ALPHA")) : 0;
+    sl->h_bst->bu_beta = getenv("CG_BU_BETA") ? atoi(getenv("CG_BU_BETA")) : 64;
+    sl->h_bst->small = getenv("CG_BFS_SMALL") ? (unsigned)atoi(getenv("CG_BFS_SMALL")) : BFS_SMALL;
     CG_CUDA(cudaMemcpyAsync(&sl->bst->L, &sl->h_bst->L, sizeof(int), cudaMemcpyHostToDevice, st));
+    CG_CUDA(cudaMemcpyAsync(&sl->bst->bu_alpha, &sl->h_bst->bu_alpha, 2 * sizeof(int) + sizeof(unsigned),
+                            cudaMemcpyHostToDevice, st));
     k_bfs_init<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, st>>>(geo, sl->s, sl->blist[0], &sl->bst->cnt[0]);
     k_bfs_seeded<<<1, 1, 0, st>>>(sl->bst);
     g->st.kernel_launches += 2;
@@ -723,7 +729,7 @@ static cg_status build_common(const cg_dims *dims, const int32_t *cost_dev, int3
             cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dd.device);
             if (coop && !getenv("CG_BFS_LEVEL_LAUNCHES") &&
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bfs_run, 512, 0) == cudaSuccess && per_sm > 0)
-                sl->bfs_coop_grid = num_sms * std::min(per_sm, CG_BFS_MINB);
+                sl->bfs_coop_grid = num_sms * std::min(per_sm, CG_BFS_RUN_MINB);
         }
         sl->x0 = x0;
         sl->x1 = x1;
@@ -821,6 +827,10 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
             const unsigned *h = s0->h_bst->hist;
             fprintf(stderr, "[cg]   levels by frontier: <=32 %u <=256 %u <=2K %u <=16K %u <=128K %u <=1M %u more %u "
                     "(bottom-up %u)\n", h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
+            const unsigned long long *cy = s0->h_bst->cyc;
+            fprintf(stderr, "[cg]   ms by bucket: small %.2f <=16K %.2f <=128K %.2f <=1M %.2f more %.2f bottom-up %.2f\n",
+                    (cy[0] + cy[1] + cy[2]) / 1.965e6, cy[3] / 1.965e6, cy[4] / 1.965e6, cy[5] / 1.965e6,
+                    cy[6] / 1.965e6, cy[7] / 1.965e6);
         }
         return s;
     };

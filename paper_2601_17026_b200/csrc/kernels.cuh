@@ -515,7 +515,33 @@ __device__ __forceinline__ void bfs_expand_warp(const Geo &g, const Soa &s, int 
                 }
             }
         };
-        if (nl < INF) {
+        if (STRICT && nl < INF) {
+            // all candidate predecessors and their labels first (independent loads in flight
+            // together), then CAS only the unlabelled ones: one latency chain per vertex
+            int w[10];  // vertex indices fit int32 (validate_dims: n + ghosts < 2^31)
+            unsigned cand = 0;
+            if (z + 1 < g.Z) { w[0] = (int)(v + 1); cand |= 1u; }
+            if (z >= 1 && s.D[v] > 0) { w[1] = (int)(v - 1); cand |= 2u; }
+#pragma unroll
+            for (int d = 0; d < 4; d++) {
+                const int64_t o = nbr_off(g, x, y, d);
+                if (!o) continue;
+                if (zi >= 0 && owned(g, v0 + o + zi)) { w[2 + d] = (int)(v0 + o + zi); cand |= 1u << (2 + d); }
+                if (zo >= 0 && s.L[d][v] > 0 && owned(g, v0 + o + zo)) {
+                    w[6 + d] = (int)(v0 + o + zo);
+                    cand |= 1u << (6 + d);
+                }
+            }
+            int hw[10];
+#pragma unroll
+            for (int j = 0; j < 10; j++) hw[j] = (cand >> j & 1u) ? __ldcg(&s.H[w[j]]) : 0;
+#pragma unroll
+            for (int j = 0; j < 10; j++)
+                if ((cand >> j & 1u) && hw[j] >= INF && atomicCAS(&s.H[w[j]], INF, nl) == INF) {
+                    u[j] = w[j];
+                    got |= 1u << j;
+                }
+        } else if (nl < INF) {
             if (z + 1 < g.Z) claim(0, v + 1);
             if (z >= 1 && s.D[v] > 0) claim(1, v - 1);
 #pragma unroll
@@ -555,6 +581,9 @@ struct BfsState {
     unsigned long long claimed;  // vertices labelled so far (direction-optimising switch)
     unsigned bar[2];       // grid barrier of k_bfs_run (arrivals, generation)
     unsigned hist[8];      // levels by frontier size: <=32, <=256, <=2048, <=16K, <=128K, <=1M, more; [7] bottom-up
+    unsigned long long cyc[8];  // block-0 clock cycles spent in levels of each bucket ([7]: bottom-up levels)
+    int bu_alpha, bu_beta;      // bottom-up when count*alpha > unvisited and count*beta > n
+    unsigned small;             // k_bfs_run: frontiers <= small are run by block 0 alone
 };
 __device__ __forceinline__ int bfs_bucket(unsigned c) {
     return c <= 32 ? 0 : c <= 256 ? 1 : c <= 2048 ? 2 : c <= 16384 ? 3 : c <= 131072 ? 4 : c <= 1048576 ? 5 : 6;
@@ -688,14 +717,21 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks) {
             __threadfence();
             atomicAdd(bar + 1, 1u);
         } else {
-            while (*gen == g0) __nanosleep(32);
+            unsigned ns = 32;
+            while (*gen == g0) {  // back off: ~300 pollers on one line slow the working blocks
+                __nanosleep(ns);
+                ns = min(ns * 2, 1024u);
+            }
         }
         __threadfence();
     }
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(512, CG_BFS_MINB) k_bfs_run(Geo g, Soa s, int *list0, int *list1, BfsState *st) {
+#ifndef CG_BFS_RUN_MINB
+#define CG_BFS_RUN_MINB 1
+#endif
+__global__ void __launch_bounds__(512, CG_BFS_RUN_MINB) k_bfs_run(Geo g, Soa s, int *list0, int *list1, BfsState *st) {
     unsigned *bar = st->bar;
     int L = *(volatile int *)&st->L;
     unsigned long long claimed = *(volatile unsigned long long *)&st->claimed;
@@ -703,12 +739,13 @@ __global__ void __launch_bounds__(512, CG_BFS_MINB) k_bfs_run(Geo g, Soa s, int 
         const unsigned count = *(volatile unsigned *)&st->cnt[(L - 1) % 3];
         if (count == 0) break;
         const int i = L - 1;
-        if (count <= BFS_SMALL) {
+        if (count <= st->small) {
             // everyone has read this level's counter before block 0 starts recycling counters
             grid_barrier(bar, gridDim.x);
             if (blockIdx.x == 0) {
                 if (threadIdx.x == 0) st->claimed = claimed;
                 unsigned c = count;
+                const long long t0 = clock64();
                 for (;;) {
                     const int j = L - 1;
                     int *lin = (j & 1) ? list1 : list0;
@@ -727,9 +764,12 @@ __global__ void __launch_bounds__(512, CG_BFS_MINB) k_bfs_run(Geo g, Soa s, int 
                     c = *(volatile unsigned *)&st->cnt[(L - 1) % 3];
                     if (threadIdx.x == 0) st->claimed += c;
                     __syncthreads();
-                    if (c == 0 || c > BFS_SMALL) break;
+                    if (c == 0 || c > st->small) break;
                 }
-                if (threadIdx.x == 0) st->L = L;
+                if (threadIdx.x == 0) {
+                    st->L = L;
+                    st->cyc[2] += clock64() - t0;  // small levels, accounted to the <=2K bucket
+                }
             }
             grid_barrier(bar, gridDim.x);
             L = *(volatile int *)&st->L;
@@ -743,8 +783,11 @@ __global__ void __launch_bounds__(512, CG_BFS_MINB) k_bfs_run(Geo g, Soa s, int 
             st->cnt[(i + 2) % 3] = 0;
             st->hist[bfs_bucket(count)]++;
         }
+        const long long t0 = clock64();
         const unsigned long long unvisited = (unsigned long long)g.n - claimed;
-        if ((unsigned long long)count * 2ull > unvisited && (unsigned long long)count * 64ull > (unsigned long long)g.n) {
+        const bool bu = (unsigned long long)count * (unsigned long long)st->bu_alpha > unvisited &&
+                        (unsigned long long)count * (unsigned long long)st->bu_beta > (unsigned long long)g.n;
+        if (bu) {
             if (blockIdx.x == 0 && threadIdx.x == 0) st->hist[7]++;
             bfs_bottom_up_level(g, s, L, lout, &st->cnt[(i + 1) % 3]);
         } else {
@@ -755,6 +798,7 @@ __global__ void __launch_bounds__(512, CG_BFS_MINB) k_bfs_run(Geo g, Soa s, int 
             }
         }
         grid_barrier(bar, gridDim.x);
+        if (blockIdx.x == 0 && threadIdx.x == 0) st->cyc[bu ? 7 : bfs_bucket(count)] += clock64() - t0;
         ++L;
         claimed += *(volatile unsigned *)&st->cnt[(L - 1) % 3];  // every block: same value
     }

@@ -23,9 +23,15 @@ for name in sys.argv[1].split(","):
         torch.cuda.synchronize(); t = time.perf_counter()
         r = cg.solve(c, spec.delta, want_mask=False)
         torch.cuda.synchronize(); dt = time.perf_counter() - t
-        if rep: ts.append(dt * 1000)
+        if rep:
+            ts.append(dt * 1000)
+            st = r["stats"]
+            print(json.dumps({"rep": rep, "ms": round(dt * 1000, 1), "sweeps": st["sweeps"], "grs": st["global_relabels"],
+                              "ms_gr": round(st["ms_global_relabel"], 1), "ms_sw": round(st["ms_sweep_kernels"], 1),
+                              "ms_solve": round(st["ms_solve"], 1), "ms_build": round(st["ms_build"], 1),
+                              "ms_extract": round(st["ms_extract"], 1)}), file=sys.stderr, flush=True)
     s = r["stats"]
-    print(json.dumps({"config": name, "flow": r["flow"], "med_ms": round(statistics.median(ts), 1),
+    print(json.dumps({"config": name, "flow": r["flow"], "med_ms": round(statistics.median(ts), 1), "all": [round(t) for t in ts],
                       "min_ms": round(min(ts), 1), "sweeps": s["sweeps"], "grs": s["global_relabels"],
                       "ms_gr": round(s["ms_global_relabel"], 1), "ms_sw": round(s["ms_sweep_kernels"], 1)}), flush=True)
 '''.replace("ROOT", repr(ROOT))
@@ -41,7 +47,9 @@ for var in sys.argv[3:]:
                          timeout=600)
     for line in out.stdout.splitlines():
         d = json.loads(line)
-        print(f"{name:12s} {d['config']} flow={d['flow']} med={d['med_ms']} min={d['min_ms']} sweeps={d['sweeps']} "
+        print(f"{name:12s} {d['config']} flow={d['flow']} med={d['med_ms']} all={d['all']} sweeps={d['sweeps']} "
               f"grs={d['grs']} gr_ms={d['ms_gr']} sw_ms={d['ms_sw']}", flush=True)
     if out.returncode:
         print(name, "FAILED", out.stderr[-2000:])
+    elif os.environ.get("AB_VERBOSE"):
+        print(out.stderr)
