@@ -33,6 +33,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 using namespace cg;
@@ -73,6 +74,7 @@ struct Slab {
     unsigned long long *h_work = nullptr, *h_u64 = nullptr, *h_visits = nullptr;
     int *h_flags = nullptr;
     BfsState *h_bst = nullptr;
+    char *h_block = nullptr;  // pinned scratch the h_* mirrors are carved from (pinned_acquire)
     int64_t N = 0, sumT0 = 0;
     int tag = 0;       // monotone list tag
     int sweep_k = 0;   // sweeps since the last list rebuild (list/counter parity)
@@ -162,6 +164,33 @@ inline bool tracing() { return getenv("CG_TRACE") != nullptr; }
 // Grid for worklist kernels: enough warps to fill every SM (8 x 256 threads per SM).
 inline int list_grid(const Slab *sl, int64_t items) { return grid_for(items * 32, 256, sl->num_sms * 8); }
 
+// Pinned host scratch blocks, recycled across handles: cudaHostAlloc / cudaFreeHost pin pages
+// and synchronise the device, which made repeated build/free cycles occasionally cost
+// tens of milliseconds.
+constexpr size_t PINNED_BLOCK = 16384;
+std::mutex g_pinned_mu;
+std::vector<char *> g_pinned_free;
+
+char *pinned_acquire() {
+    {
+        std::lock_guard<std::mutex> lk(g_pinned_mu);
+        if (!g_pinned_free.empty()) {
+            char *b = g_pinned_free.back();
+            g_pinned_free.pop_back();
+            return b;
+        }
+    }
+    void *b = nullptr;
+    if (cudaHostAlloc(&b, PINNED_BLOCK, cudaHostAllocPortable) != cudaSuccess) return nullptr;
+    return (char *)b;
+}
+
+void pinned_release(char *b) {
+    if (!b) return;
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    g_pinned_free.push_back(b);
+}
+
 template <typename T>
 T *carve(char *&p, int64_t count) {
     T *r = reinterpret_cast<T *>(p);
@@ -187,12 +216,7 @@ size_t workspace_bytes(const Geo &geo) {
 void slab_free(Slab *sl) {
     if (!sl) return;
     if (sl->ws) cudaFreeAsync(sl->ws, sl->stream);
-    cudaFreeHost(sl->h_cnt);
-    cudaFreeHost(sl->h_work);
-    cudaFreeHost(sl->h_u64);
-    cudaFreeHost(sl->h_flags);
-    cudaFreeHost(sl->h_bst);
-    cudaFreeHost(sl->h_visits);
+    pinned_release(sl->h_block);
     delete sl;
 }
 
@@ -213,13 +237,18 @@ cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode) {
         sl->ws = nullptr;
         return CG_E_NOMEM;
     }
-    if (cudaHostAlloc(&sl->h_cnt, sizeof(unsigned) * 16, cudaHostAllocDefault) != cudaSuccess ||
-        cudaHostAlloc(&sl->h_work, sizeof(unsigned long long) * RING, cudaHostAllocDefault) != cudaSuccess ||
-        cudaHostAlloc(&sl->h_u64, sizeof(unsigned long long) * 16, cudaHostAllocDefault) != cudaSuccess ||
-        cudaHostAlloc(&sl->h_flags, sizeof(int) * 16, cudaHostAllocDefault) != cudaSuccess ||
-        cudaHostAlloc(&sl->h_bst, sizeof(BfsState), cudaHostAllocDefault) != cudaSuccess ||
-        cudaHostAlloc(&sl->h_visits, sizeof(unsigned long long) * RING, cudaHostAllocDefault) != cudaSuccess)
-        return CG_E_NOMEM;
+    sl->h_block = pinned_acquire();
+    if (!sl->h_block) return CG_E_NOMEM;
+    {
+        char *hp = sl->h_block;
+        sl->h_cnt = carve<unsigned>(hp, 16);
+        sl->h_work = carve<unsigned long long>(hp, RING);
+        sl->h_u64 = carve<unsigned long long>(hp, 16);
+        sl->h_flags = carve<int>(hp, 16);
+        sl->h_bst = carve<BfsState>(hp, 1);
+        sl->h_visits = carve<unsigned long long>(hp, RING);
+        if (hp > sl->h_block + PINNED_BLOCK) return CG_E_NOMEM;
+    }
     char *p = sl->ws;
 #if CG_LAYOUT_AOS
     int32_t *rec = carve<int32_t>(p, 8 * plane) + 8 * geo.YZ;  // owned plane x = 0

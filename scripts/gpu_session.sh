@@ -1,2 +1,2 @@
 set -x
-timeout 300 python scripts/phase_timing.py C4 16 > gpurun_out/t_phase.log 2>&1
+timeout 900 python scripts/ab.py C3,C4,C5 3 'aos:' 'soa:CG_LIB=paper_2601_17026_b200/libcolgraph_soa.so' > gpurun_out/t_ab.log 2>&1
