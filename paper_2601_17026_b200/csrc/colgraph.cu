@@ -406,7 +406,7 @@ cg_status bfs_strict(cg_graph *g, Slab *sl) {
     // direction optimisation measured slower than top-down on C3-C5: off unless asked
     sl->h_bst->bu_alpha = getenv("CG_BU_ALPHA") ? atoi(getenv("CG_BU_ALPHA")) : 0;
     sl->h_bst->bu_beta = getenv("CG_BU_BETA") ? atoi(getenv("CG_BU_BETA")) : 64;
-    sl->h_bst->small = getenv("CG_BFS_SMALL") ? (unsigned)atoi(getenv("CG_BFS_SMALL")) : BFS_SMALL;
+    sl->h_bst->small = getenv("CG_BFS_SMALL") ? (unsigned)atoi(getenv("CG_BFS_SMALL")) : BFS_RUN_SMALL;
     CG_CUDA(cudaMemcpyAsync(&sl->bst->L, &sl->h_bst->L, sizeof(int), cudaMemcpyHostToDevice, st));
     CG_CUDA(cudaMemcpyAsync(&sl->bst->bu_alpha, &sl->h_bst->bu_alpha, 2 * sizeof(int) + sizeof(unsigned),
                             cudaMemcpyHostToDevice, st));
@@ -857,9 +857,10 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
             fprintf(stderr, "[cg]   levels by frontier: <=32 %u <=256 %u <=2K %u <=16K %u <=128K %u <=1M %u more %u "
                     "(bottom-up %u)\n", h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
             const unsigned long long *cy = s0->h_bst->cyc;
-            fprintf(stderr, "[cg]   ms by bucket: small %.2f <=16K %.2f <=128K %.2f <=1M %.2f more %.2f bottom-up %.2f\n",
+            fprintf(stderr, "[cg]   ms by bucket: small %.2f <=16K %.2f <=128K %.2f <=1M %.2f more %.2f bottom-up %.2f"
+                    " | small-level vertices %llu\n",
                     (cy[0] + cy[1] + cy[2]) / 1.965e6, cy[3] / 1.965e6, cy[4] / 1.965e6, cy[5] / 1.965e6,
-                    cy[6] / 1.965e6, cy[7] / 1.965e6);
+                    cy[6] / 1.965e6, cy[7] / 1.965e6, (unsigned long long)s0->h_bst->svert);
         }
         return s;
     };

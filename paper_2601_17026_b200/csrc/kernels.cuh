@@ -566,6 +566,78 @@ __device__ __forceinline__ void bfs_expand_warp(const Geo &g, const Soa &s, int 
         if (got >> j & 1u) lout[pos++] = u[j];
 }
 
+// Strict BFS expansion of R frontier vertices per lane at once (vv[r] < 0: none): the R
+// vertex records, then all candidate predecessors' labels are loaded before any CAS, so a
+// lane pays one dependent-load chain per call instead of R; one append atomic per warp.
+__device__ __forceinline__ void load_DL(const Soa &s, int v, int &D, int (&L)[4]) {
+#if CG_LAYOUT_AOS
+    const int4 *rec = reinterpret_cast<const int4 *>(&s.E[v]);  // E H T D | L0 L1 L2 L3
+    const int4 a = rec[0], b = rec[1];
+    D = a.w;
+    L[0] = b.x; L[1] = b.y; L[2] = b.z; L[3] = b.w;
+#else
+    D = s.D[v];
+#pragma unroll
+    for (int d = 0; d < 4; d++) L[d] = s.L[d][v];
+#endif
+}
+
+template <int R>
+__device__ __forceinline__ void bfs_expand_multi(const Geo &g, const Soa &s, int nl, const int (&vv)[R], int *lout,
+                                                 unsigned *cout) {
+    const int INF = g.INF;
+    int w[R][10], hw[R][10];
+    unsigned cand[R], got[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        cand[r] = 0;
+        got[r] = 0;
+        const int v = vv[r];
+        if (v < 0 || nl >= INF) continue;
+        const int col = v / g.Z;
+        const int z = v - col * g.Z;
+        const int x = col / g.Y, y = col - x * g.Y;
+        const int v0 = col * g.Z;
+        const int zo = zo_of(z, g.delta), zi = zi_of(z, g.delta, g.Z);
+        int D, L[4];
+        load_DL(s, v, D, L);
+        if (z + 1 < g.Z) { w[r][0] = v + 1; cand[r] |= 1u; }
+        if (z >= 1 && D > 0) { w[r][1] = v - 1; cand[r] |= 2u; }
+#pragma unroll
+        for (int d = 0; d < 4; d++) {
+            const int o = (int)nbr_off(g, x, y, d);
+            if (!o) continue;
+            if (zi >= 0 && owned(g, v0 + o + zi)) { w[r][2 + d] = v0 + o + zi; cand[r] |= 1u << (2 + d); }
+            if (zo >= 0 && L[d] > 0 && owned(g, v0 + o + zo)) { w[r][6 + d] = v0 + o + zo; cand[r] |= 1u << (6 + d); }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < R; r++)
+#pragma unroll
+        for (int j = 0; j < 10; j++) hw[r][j] = (cand[r] >> j & 1u) ? __ldcg(&s.H[w[r][j]]) : 0;
+    int k = 0;
+#pragma unroll
+    for (int r = 0; r < R; r++)
+#pragma unroll
+        for (int j = 0; j < 10; j++)
+            if ((cand[r] >> j & 1u) && hw[r][j] >= INF && atomicCAS(&s.H[w[r][j]], INF, nl) == INF) {
+                got[r] |= 1u << j;
+                k++;
+            }
+    const int incl = warp_incl_scan(k);
+    const int total = __shfl_sync(FULL, incl, 31);
+    if (total == 0) return;
+    unsigned b = 0;
+    if (lane_id() == 31) b = atomicAdd(cout, (unsigned)total);
+    b = __shfl_sync(FULL, b, 31);
+    unsigned pos = b + incl - k;
+#pragma unroll
+    for (int r = 0; r < R; r++)
+#pragma unroll
+        for (int j = 0; j < 10; j++)
+            if (got[r] >> j & 1u) lout[pos++] = w[r][j];
+}
+
 // Device-driven strict BFS step (the level counter lives on the device, so identical
 // launches are queued back to back).  Step i = level L = i+1 reads list[i&1] / cnt[i%3],
 // writes list[(i+1)&1] / cnt[(i+1)%3] and zeroes cnt[(i+2)%3].
@@ -573,7 +645,8 @@ __device__ __forceinline__ void bfs_expand_warp(const Geo &g, const Soa &s, int 
 //   small frontier (<= BFS_SMALL): block 0 alone runs levels back to back separated by
 //   __syncthreads (a level costs ~1-2 us instead of a launch), until the frontier grows
 //   or empties.
-constexpr unsigned BFS_SMALL = 2048;
+constexpr unsigned BFS_SMALL = 2048;       // k_bfs_step (level-per-launch fallback)
+constexpr unsigned BFS_RUN_SMALL = 64;    // k_bfs_run default (measured)
 struct BfsState {
     int L;                 // current level (1-based)
     unsigned cnt[3];       // frontier counters
@@ -584,6 +657,7 @@ struct BfsState {
     unsigned long long cyc[8];  // block-0 clock cycles spent in levels of each bucket ([7]: bottom-up levels)
     int bu_alpha, bu_beta;      // bottom-up when count*alpha > unvisited and count*beta > n
     unsigned small;             // k_bfs_run: frontiers <= small are run by block 0 alone
+    unsigned long long svert;   // vertices expanded in block-0 (small) levels
 };
 __device__ __forceinline__ int bfs_bucket(unsigned c) {
     return c <= 32 ? 0 : c <= 256 ? 1 : c <= 2048 ? 2 : c <= 16384 ? 3 : c <= 131072 ? 4 : c <= 1048576 ? 5 : 6;
@@ -728,6 +802,9 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks) {
     __syncthreads();
 }
 
+#ifndef BFS_R
+#define BFS_R 2
+#endif
 #ifndef CG_BFS_RUN_MINB
 #define CG_BFS_RUN_MINB 1
 #endif
@@ -753,11 +830,17 @@ __global__ void __launch_bounds__(512, CG_BFS_RUN_MINB) k_bfs_run(Geo g, Soa s, 
                     if (threadIdx.x == 0) {
                         st->cnt[(j + 2) % 3] = 0;
                         st->hist[bfs_bucket(c)]++;
+                        st->svert += c;
                     }
-                    for (unsigned base = (threadIdx.x >> 5) * 32; base < c; base += (blockDim.x >> 5) * 32) {
-                        const unsigned jj = base + lane_id();
-                        bfs_expand_warp<true>(g, s, L + 1, jj < c ? (int64_t)__ldcg(&lin[jj]) : -1, lout,
-                                              &st->cnt[(j + 1) % 3], nullptr, 0);
+                    for (unsigned base = (threadIdx.x >> 5) * 32 * BFS_R; base < c;
+                         base += (blockDim.x >> 5) * 32 * BFS_R) {
+                        int vv[BFS_R];
+#pragma unroll
+                        for (int r = 0; r < BFS_R; r++) {
+                            const unsigned jj = base + r * 32 + lane_id();
+                            vv[r] = jj < c ? __ldcg(&lin[jj]) : -1;
+                        }
+                        bfs_expand_multi<BFS_R>(g, s, L + 1, vv, lout, &st->cnt[(j + 1) % 3]);
                     }
                     __syncthreads();
                     ++L;
@@ -791,10 +874,23 @@ __global__ void __launch_bounds__(512, CG_BFS_RUN_MINB) k_bfs_run(Geo g, Soa s, 
             if (blockIdx.x == 0 && threadIdx.x == 0) st->hist[7]++;
             bfs_bottom_up_level(g, s, L, lout, &st->cnt[(i + 1) % 3]);
         } else {
-            for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {
-                const int64_t j = base + lane_id();
-                bfs_expand_warp<true>(g, s, L + 1, j < count ? (int64_t)__ldcg(&lin[j]) : -1, lout, &st->cnt[(i + 1) % 3],
-                                      nullptr, 0);
+            // few vertices per warp: spread them (R = 1); many: R per lane for load-level parallelism
+            if ((int64_t)count < nwarps() * 32 * BFS_R) {
+                for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {
+                    const int64_t j = base + lane_id();
+                    int vv[1] = {j < count ? __ldcg(&lin[j]) : -1};
+                    bfs_expand_multi<1>(g, s, L + 1, vv, lout, &st->cnt[(i + 1) % 3]);
+                }
+            } else {
+                for (int64_t base = gwarp() * 32 * BFS_R; base < count; base += nwarps() * 32 * BFS_R) {
+                    int vv[BFS_R];
+#pragma unroll
+                    for (int r = 0; r < BFS_R; r++) {
+                        const int64_t j = base + r * 32 + lane_id();
+                        vv[r] = j < count ? __ldcg(&lin[j]) : -1;
+                    }
+                    bfs_expand_multi<BFS_R>(g, s, L + 1, vv, lout, &st->cnt[(i + 1) % 3]);
+                }
             }
         }
         grid_barrier(bar, gridDim.x);

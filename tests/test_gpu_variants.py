@@ -83,7 +83,8 @@ def test_tiles_rejects_tall_columns(cg):
 
 
 @pytest.mark.parametrize("var", [{"CG_WALK_WS": "1"}, {"CG_BFS_LEVEL_LAUNCHES": "1"},
-                                 {"CG_WALK_WS": "1", "CG_WALK_MIN": "0"}])
+                                 {"CG_WALK_WS": "1", "CG_WALK_MIN": "0"}, {"CG_BFS_SMALL": "2048"},
+                                 {"CG_BFS_SMALL": "0"}, {"CG_BU_ALPHA": "2"}])
 def test_schedule_variants(cg, env, var):
     for k, v in var.items():
         env.setenv(k, v)
