@@ -870,6 +870,7 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
     const double gr_beta = getenv("CG_GR_BETA") ? atof(getenv("CG_GR_BETA")) : 1.0;
     // work-fetching walk (k_walk_ws): measured -10 % on C3/C5, +10 % on C4, opt-in
     const bool walk_ws = getenv("CG_WALK_WS") && atoi(getenv("CG_WALK_WS")) != 0;
+    const int walk_park = getenv("CG_WALK_PARK") ? atoi(getenv("CG_WALK_PARK")) : 0;
     double work_since_gr = 0.0, sweep_ms_since_gr = 0.0;
     int64_t sweeps = 0, since_gap = 0, last_active = active;
     std::vector<int64_t> wv(RING);
@@ -961,7 +962,7 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
                     k_walk<<<gv, 256, 0, sl->stream>>>(geo, sl->s, o.walk_len, sl->blist[k & 1], sl->cnt + k % 3,
                                                        sl->blist[(k + 1) & 1], sl->cnt + (k + 1) % 3,
                                                        sl->cnt + (k + 2) % 3, sl->vstamp, sl->out_tag, sl->work + i,
-                                                       sl->flags);
+                                                       sl->flags, walk_park);
                 else
                     k_sweep_v<<<gv, 256, 0, sl->stream>>>(geo, sl->s, o.ops_per_sweep, sl->blist[k & 1],
                                                           sl->cnt + k % 3, sl->blist[(k + 1) & 1],

@@ -287,7 +287,7 @@ __device__ __forceinline__ void deposit(const Geo &g, const Soa &s, int64_t x, i
 
 __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_walk(Geo g, Soa s, int K, const int *__restrict__ lin, const unsigned *cin,
                                               int *lout, unsigned *cout, unsigned *czero, int *vstamp, int tag,
-                                              unsigned long long *work, int *flags) {
+                                              unsigned long long *work, int *flags, int park) {
     __shared__ BlockQueue q;
     __shared__ unsigned qbase;
     if (threadIdx.x == 0) q.n = 0;
@@ -308,7 +308,14 @@ __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_walk(Geo g, Soa s, int K
             const ArcPick p = scan_arcs(g, s, ctx, hx);
             mywork++;  // one push or relabel operation per hop
             if (p.best >= hx || step >= K) {  // stuck (or hop budget spent): deposit the carry here
-                if (p.best >= hx) atomicMax(&s.H[ctx.v], p.best >= g.INF ? g.INF : p.best + 1);
+                if (p.best >= hx) {
+                    atomicMax(&s.H[ctx.v], p.best >= g.INF ? g.INF : p.best + 1);
+                    if (park) {  // parked until the next global relabel (not re-listed)
+                        const int old = atomicAdd(&s.E[ctx.v], c);
+                        if (old > INT_MAX - c) atomicOr(flags, FLAG_OVERFLOW);
+                        break;
+                    }
+                }
                 deposit(g, s, ctx.v, c, vstamp, tag, q, lout, cout, flags);
                 break;
             }
