@@ -178,6 +178,25 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
  *         CG_E_CUDA, CG_E_NCCL. */
 cg_status mincut_extract_surface(cg_graph *g, int32_t *surface_dev, uint8_t *mask_dev);
 
+/* NEXT-2 -- phase 2 and flow export: turn the maximum preflow left by
+ * maxflow_solve into a maximum FLOW by returning every unit of stranded excess to s (the
+ * paper's Alg. 2 runs until excess returns to s; §2.1, Eq. 2-4),
+ * and write the flow on every arc.  The same push-relabel runs with s as its terminal
+ * (terminal residual = flow on s->v); flows into t do not change, so |f| is unchanged.
+ *   cost_dev : the SAME device input and mode passed to colgraph_build (the source / sink
+ *              capacities are recomputed from it; the handle does not keep them).
+ *   opts     : solver options for phase 2 (nullable; sweep_kind is forced to the vertex kind).
+ *   flow_dev : device int32[7 * n], planes of n = X*Y*Z in index order (x*Y + y)*Z + z:
+ *              [0] s->v   [1] v->t   [2] down arc v -> (x,y,z-1)
+ *              [3..6] lateral arc of v in direction +x, -x, +y, -y, i.e. v -> (nbr, zo(z))
+ *              with zo(0) = 0, zo(z) = z - Delta for z > Delta (reading R2).
+ * Single-slab handles only.  Call mincut_extract_surface BEFORE this (afterwards it returns
+ * CG_E_STATE: the handle then holds a flow, not a preflow).
+ * Errors: CG_E_INVAL (NULL, multi-slab handle), CG_E_STATE (not solved / already exported),
+ *         CG_E_NOT_CONVERGED (max_sweeps hit, or excess left), CG_E_CUDA. */
+cg_status maxflow_export_flow(cg_graph *g, const int32_t *cost_dev, int32_t input_is_weight, const cg_solve_opts *opts,
+                              int32_t *flow_dev);
+
 /* Convenience end-to-end call on HOST buffers (single GPU): copies cost_host to
  * the device, builds, solves, extracts and copies surface/mask back.
  *   surface_host : int32[X*Y];  mask_host : nullable uint8[X*Y*Z].

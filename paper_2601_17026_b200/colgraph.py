@@ -76,6 +76,9 @@ def _load():
     lib.colgraph_solve_host.restype = ctypes.c_int
     lib.colgraph_solve_host.argtypes = [P(cg_dims), ctypes.c_void_p, ctypes.c_int32, P(cg_dist), P(cg_solve_opts),
                                         P(ctypes.c_int64), ctypes.c_void_p, ctypes.c_void_p, P(cg_solve_stats)]
+    lib.maxflow_export_flow.restype = ctypes.c_int
+    lib.maxflow_export_flow.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, P(cg_solve_opts),
+                                        ctypes.c_void_p]
     lib.colgraph_export_state.restype = ctypes.c_int
     lib.colgraph_export_state.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
     lib.colgraph_stats.restype = ctypes.c_int
@@ -93,7 +96,8 @@ def _load():
 
 _lib = _load()
 
-EXPORTED = ["colgraph_build", "colgraph_build_slabs", "cg_nccl_unique_id", "maxflow_solve", "mincut_extract_surface", "colgraph_solve_host",
+EXPORTED = ["colgraph_build", "colgraph_build_slabs", "cg_nccl_unique_id", "maxflow_solve", "mincut_extract_surface",
+            "maxflow_export_flow", "colgraph_solve_host",
             "colgraph_export_state", "colgraph_stats", "colgraph_free", "cg_status_str", "cg_slab_range", "cg_version"]
 
 
@@ -201,6 +205,20 @@ def colgraph_stats(handle) -> dict:
     if st != CG_OK:
         raise ColgraphError(st, "colgraph_stats")
     return stats.as_dict()
+
+
+def maxflow_export_flow(handle, cost, input_is_weight: bool = False, flow=None, opts: cg_solve_opts | None = None):
+    """Phase 2 + flow export (include/colgraph.h).  cost: the CUDA int32 input given to
+    colgraph_build.  Returns (status, flow) with flow a CUDA int32 tensor [7, X, Y, Z]:
+    s->v, v->t, down, lateral +x, -x, +y, -y."""
+    import torch
+    _check_dev_int32(cost, "cost")
+    if flow is None:
+        flow = torch.empty((7,) + tuple(cost.shape), dtype=torch.int32, device=cost.device)
+    _check_dev_int32(flow, "flow")
+    st = _lib.maxflow_export_flow(handle, ctypes.c_void_p(cost.data_ptr()), int(bool(input_is_weight)),
+                                  ctypes.byref(opts) if opts is not None else None, ctypes.c_void_p(flow.data_ptr()))
+    return st, flow
 
 
 def colgraph_free(handle) -> None:

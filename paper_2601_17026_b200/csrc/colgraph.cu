@@ -105,6 +105,7 @@ struct cg_graph {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int64_t n_global = 0;
     bool solved = false;
+    bool exported = false;      // phase 2 ran (maxflow_export_flow): the preflow is now a flow
     cg_solve_stats st{};
 };
 
@@ -657,150 +658,13 @@ cg_status validate_dims(const cg_dims *dims) {
 
 }  // namespace
 
-extern "C" {
-
-const char *cg_status_str(cg_status s) {
-    switch (s) {
-        case CG_OK: return "CG_OK";
-        case CG_E_INVAL: return "CG_E_INVAL";
-        case CG_E_OVERFLOW: return "CG_E_OVERFLOW";
-        case CG_E_NOMEM: return "CG_E_NOMEM";
-        case CG_E_CUDA: return "CG_E_CUDA";
-        case CG_E_NCCL: return "CG_E_NCCL";
-        case CG_E_EMPTY_COLUMN: return "CG_E_EMPTY_COLUMN";
-        case CG_E_STATE: return "CG_E_STATE";
-        case CG_E_NOT_CONVERGED: return "CG_E_NOT_CONVERGED";
-    }
-    return "CG_E_UNKNOWN";
-}
-
-const char *cg_version(void) {
-    return "colgraph 0.3 sm_100a (lock-free push-relabel: multi-hop walks + single-hop sweeps over vertex worklists, "
-           "device-driven frontier BFS relabel, worklist extraction, x-slab halos over NCCL)";
-}
-
-cg_status cg_slab_range(const cg_dims *dims, int32_t rank, int32_t nranks, int32_t *x0, int32_t *x1) {
-    if (!dims || !x0 || !x1 || nranks < 1 || rank < 0 || rank >= nranks || dims->X < nranks) return CG_E_INVAL;
-    const int32_t q = dims->X / nranks, r = dims->X % nranks;
-    *x0 = rank * q + std::min(rank, r);
-    *x1 = *x0 + q + (rank < r ? 1 : 0);
-    return CG_OK;
-}
-
-cg_status cg_nccl_unique_id(void *id_out) {
-    if (!id_out) return CG_E_INVAL;
-    if (!nccl().ok) return CG_E_NCCL;
-    ncclUniqueId id;
-    if (nccl().getUniqueId(&id) != ncclSuccess) return CG_E_NCCL;
-    memcpy(id_out, &id, sizeof(id));
-    return CG_OK;
-}
-
-void colgraph_free(cg_graph *g) {
-    if (!g) return;
-    {
-        DeviceGuard dg(g->dist.device);
-        for (Slab *sl : g->slabs) slab_free(sl);
-        if (g->comm) nccl().commDestroy(g->comm);
-        if (g->d_red) cudaFree(g->d_red);
-        if (g->h_red) cudaFreeHost(g->h_red);
-        if (g->ev0) cudaEventDestroy(g->ev0);
-        if (g->ev1) cudaEventDestroy(g->ev1);
-    }
-    delete g;
-}
-
-// Common constructor: `nslabs_local` slabs in this process starting at global slab `rank`.
-static cg_status build_common(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight,
-                              const cg_dist *dist, int nranks, int rank, int nslabs_local, bool local,
-                              cg_graph **out) {
-    CG_TRY(validate_dims(dims));
-    if (!cost_dev || !out) return CG_E_INVAL;
-    *out = nullptr;
-    if (nranks < 1 || nranks > dims->X) return CG_E_INVAL;
-    cg_dist dd{0, 1, nullptr, 0, nullptr};
-    if (dist) dd = *dist;
-    DeviceGuard dg(dd.device);
-    const double t0 = now_ms();
-    cg_graph *g = new cg_graph();
-    g->dims = *dims;
-    g->dist = dd;
-    g->nranks = nranks;
-    g->rank = rank;
-    g->local = local;
-    g->n_global = (int64_t)dims->X * dims->Y * dims->Z;
-    auto fail = [&](cg_status st) {
-        colgraph_free(g);
-        return st;
-    };
-    int num_sms = 148;
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dd.device);
-    if (cudaEventCreate(&g->ev0) != cudaSuccess || cudaEventCreate(&g->ev1) != cudaSuccess) return fail(CG_E_CUDA);
-    if (!local && nranks > 1) {
-        if (!dd.nccl_id || !nccl().ok) return fail(CG_E_NCCL);
-        ncclUniqueId id;
-        memcpy(&id, dd.nccl_id, sizeof(id));
-        if (nccl().commInitRank(&g->comm, nranks, id, rank) != ncclSuccess) return fail(CG_E_NCCL);
-        if (cudaMalloc(&g->d_red, 64 * sizeof(int64_t)) != cudaSuccess ||
-            cudaHostAlloc(&g->h_red, 64 * sizeof(int64_t), cudaHostAllocDefault) != cudaSuccess)
-            return fail(CG_E_NOMEM);
-    }
-    for (int i = 0; i < nslabs_local; i++) {
-        const int r = rank + i;
-        int32_t x0, x1;
-        if (cg_slab_range(dims, r, nranks, &x0, &x1) != CG_OK) return fail(CG_E_INVAL);
-        Slab *sl = new Slab();
-        sl->device = dd.device;
-        sl->stream = (cudaStream_t)dd.stream;
-        sl->num_sms = num_sms;
-        {  // persistent BFS: as many 512-thread blocks as are co-resident (cooperative launch)
-            int per_sm = 0, coop = 0;
-            cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dd.device);
-            if (coop && !getenv("CG_BFS_LEVEL_LAUNCHES") &&
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bfs_run, 512, 0) == cudaSuccess && per_sm > 0)
-                sl->bfs_coop_grid = num_sms * std::min(per_sm, CG_BFS_RUN_MINB);
-        }
-        sl->x0 = x0;
-        sl->x1 = x1;
-        sl->geo = make_geo(dims, x0, x1, nranks, r > 0, r + 1 < nranks, g->n_global);
-        g->slabs.push_back(sl);
-        // LOCAL: cost_dev is the whole volume; NCCL / single: this rank's slab
-        const int32_t *src = local ? cost_dev + (int64_t)x0 * sl->geo.YZ : cost_dev;
-        const cg_status s = slab_build(sl, src, input_is_weight ? 1 : 0);
-        if (s != CG_OK) return fail(s);
-    }
-    int64_t fl = 0;
-    for (Slab *sl : g->slabs) fl |= sl->h_flags[0];
-    g->st.source_capacity = 0;
-    for (Slab *sl : g->slabs) g->st.source_capacity += sl->N;
-    CG_TRY(gsum(g, &g->st.source_capacity, 1));
-    g->st.bytes_per_sweep_alg = 32.0 * (double)g->n_global;
-    g->st.kernel_launches = nslabs_local;
-    g->st.ms_build = now_ms() - t0;
-    *out = g;
-    return CG_OK;
-}
-
-cg_status colgraph_build(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight, const cg_dist *dist,
-                         cg_graph **out) {
-    cg_dist dd{0, 1, nullptr, 0, nullptr};
-    if (dist) dd = *dist;
-    if (dd.nranks < 1 || dd.rank < 0 || dd.rank >= dd.nranks) return CG_E_INVAL;
-    return build_common(dims, cost_dev, input_is_weight, &dd, dd.nranks, dd.rank, 1, false, out);
-}
-
-cg_status colgraph_build_slabs(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight, int32_t nslabs,
-                               const cg_dist *dist, cg_graph **out) {
-    if (nslabs < 1) return CG_E_INVAL;
-    return build_common(dims, cost_dev, input_is_weight, dist, nslabs, 0, nslabs, true, out);
-}
-
-cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_value, cg_solve_stats *stats) {
-    if (!g || !flow_value) return CG_E_INVAL;
-    if (g->solved) return CG_E_STATE;
-    DeviceGuard dg(g->dist.device);
-    cg_solve_opts o{1.0f, 0, 16, (int64_t)1 << 30, 1, 0, 0, 0, 0};
+// Solver options with library defaults (NULL = defaults; 0 fields = defaults); use_tiles = the
+// tile sweep was requested and set up.
+cg_status normalize_opts(cg_graph *g, const cg_solve_opts *opts, cg_solve_opts &o, bool &use_tiles) {
+    o = cg_solve_opts{1.0f, 0, 16, (int64_t)1 << 30, 1, 0, 0, 0, 0};
     if (opts) o = *opts;
+    if (o.check_every <= 0) o.check_every = 16;
+    if (o.max_sweeps <= 0) o.max_sweeps = (int64_t)1 << 30;
     if (o.sweep_kind == CG_SWEEP_AUTO && getenv("CG_SWEEP")) o.sweep_kind = atoi(getenv("CG_SWEEP"));
     if (o.tile_steps <= 0) o.tile_steps = getenv("CG_TILE_STEPS") ? atoi(getenv("CG_TILE_STEPS")) : 64;
     if (o.tile_relabel_every == 0)
@@ -808,30 +672,24 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
     if (o.sweep_kind < CG_SWEEP_AUTO || o.sweep_kind > CG_SWEEP_VERTEX) return CG_E_INVAL;
     // a3 flavour: the vertex-worklist sweep (AUTO: measured fastest) or
     // shared-memory column tiles (single slab, Z within the instantiated sizes)
-    bool use_tiles = false;
+    use_tiles = false;
     if (o.sweep_kind == CG_SWEEP_TILES && !multi(g)) use_tiles = tile_setup(g->slabs[0], o.tile_steps, o.tile_relabel_every);
     if (o.sweep_kind == CG_SWEEP_TILES && !use_tiles) return CG_E_INVAL;
     if (o.walk_len == 0) o.walk_len = getenv("CG_WALK") ? atoi(getenv("CG_WALK")) : 64;  // library default
     o.check_every = std::max(1, std::min(o.check_every, RING));
     o.ops_per_sweep = std::max(1, o.ops_per_sweep);
     if (!(o.gr_factor > 0.f)) o.gr_factor = 1.0f;
+    for (Slab *sl : g->slabs) sl->tiles = sl->tiles && use_tiles;
+    return CG_OK;
+}
+
+// a2-a5: exact global relabel, then sweeps until a global relabel finds no active vertex
+// (a maximum preflow).  Shared by maxflow_solve (phase 1) and maxflow_export_flow (phase 2).
+cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &ms_gr) {
     const bool trace = tracing();
-    const double t0 = now_ms();
     Slab *s0 = g->slabs[0];
     cudaStream_t st0 = s0->stream;
-    // a1': optional exact per-column pre-cancellation (valid initial preflow; DESIGN.md §7)
-    const size_t pc_smem = (size_t)8 * (g->dims.Z + 1) * sizeof(long long);
-    if (getenv("CG_PRECANCEL") && pc_smem <= 200 * 1024) {  // opt-in: measured slower on C4/C5
-        if (pc_smem > 48 * 1024)
-            CG_CUDA(cudaFuncSetAttribute(k_precancel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pc_smem));
-        for (Slab *sl : g->slabs) {
-            k_precancel<<<grid_for((int64_t)sl->geo.X * sl->geo.Y * 32, 256, sl->num_sms * 16), 256, pc_smem,
-                          sl->stream>>>(sl->geo, sl->s, sl->flags);
-            g->st.kernel_launches++;
-        }
-        CG_CUDA(cudaGetLastError());
-    }
-    double ms_gr = 0.0, last_gr_ms = 0.0;
+    double last_gr_ms = 0.0;
     int64_t active = 0;
     auto timed_gr = [&]() -> cg_status {
         const double a = now_ms();
@@ -872,7 +730,7 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
     const bool walk_ws = getenv("CG_WALK_WS") && atoi(getenv("CG_WALK_WS")) != 0;
     const int walk_park = getenv("CG_WALK_PARK") ? atoi(getenv("CG_WALK_PARK")) : 0;
     double work_since_gr = 0.0, sweep_ms_since_gr = 0.0;
-    int64_t sweeps = 0, since_gap = 0, last_active = active;
+    int64_t sweeps = g->st.sweeps, since_gap = 0, last_active = active;
     std::vector<int64_t> wv(RING);
     cg_status result = CG_OK;
     while (use_tiles && active > 0) {
@@ -1024,6 +882,171 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
             since_gap = 0;
         }
     }
+    return result;
+}
+
+extern "C" {
+
+const char *cg_status_str(cg_status s) {
+    switch (s) {
+        case CG_OK: return "CG_OK";
+        case CG_E_INVAL: return "CG_E_INVAL";
+        case CG_E_OVERFLOW: return "CG_E_OVERFLOW";
+        case CG_E_NOMEM: return "CG_E_NOMEM";
+        case CG_E_CUDA: return "CG_E_CUDA";
+        case CG_E_NCCL: return "CG_E_NCCL";
+        case CG_E_EMPTY_COLUMN: return "CG_E_EMPTY_COLUMN";
+        case CG_E_STATE: return "CG_E_STATE";
+        case CG_E_NOT_CONVERGED: return "CG_E_NOT_CONVERGED";
+    }
+    return "CG_E_UNKNOWN";
+}
+
+const char *cg_version(void) {
+    return "colgraph 0.3 sm_100a (lock-free push-relabel: multi-hop walks + single-hop sweeps over vertex worklists, "
+           "device-driven frontier BFS relabel, worklist extraction, x-slab halos over NCCL)";
+}
+
+cg_status cg_slab_range(const cg_dims *dims, int32_t rank, int32_t nranks, int32_t *x0, int32_t *x1) {
+    if (!dims || !x0 || !x1 || nranks < 1 || rank < 0 || rank >= nranks || dims->X < nranks) return CG_E_INVAL;
+    const int32_t q = dims->X / nranks, r = dims->X % nranks;
+    *x0 = rank * q + std::min(rank, r);
+    *x1 = *x0 + q + (rank < r ? 1 : 0);
+    return CG_OK;
+}
+
+cg_status cg_nccl_unique_id(void *id_out) {
+    if (!id_out) return CG_E_INVAL;
+    if (!nccl().ok) return CG_E_NCCL;
+    ncclUniqueId id;
+    if (nccl().getUniqueId(&id) != ncclSuccess) return CG_E_NCCL;
+    memcpy(id_out, &id, sizeof(id));
+    return CG_OK;
+}
+
+void colgraph_free(cg_graph *g) {
+    if (!g) return;
+    {
+        DeviceGuard dg(g->dist.device);
+        for (Slab *sl : g->slabs) slab_free(sl);
+        if (g->comm) nccl().commDestroy(g->comm);
+        if (g->d_red) cudaFree(g->d_red);
+        if (g->h_red) cudaFreeHost(g->h_red);
+        if (g->ev0) cudaEventDestroy(g->ev0);
+        if (g->ev1) cudaEventDestroy(g->ev1);
+    }
+    delete g;
+}
+
+// Common constructor: `nslabs_local` slabs in this process starting at global slab `rank`.
+static cg_status build_common(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight,
+                              const cg_dist *dist, int nranks, int rank, int nslabs_local, bool local,
+                              cg_graph **out) {
+    CG_TRY(validate_dims(dims));
+    if (!cost_dev || !out) return CG_E_INVAL;
+    *out = nullptr;
+    if (nranks < 1 || nranks > dims->X) return CG_E_INVAL;
+    cg_dist dd{0, 1, nullptr, 0, nullptr};
+    if (dist) dd = *dist;
+    DeviceGuard dg(dd.device);
+    const double t0 = now_ms();
+    cg_graph *g = new cg_graph();
+    g->dims = *dims;
+    g->dist = dd;
+    g->nranks = nranks;
+    g->rank = rank;
+    g->local = local;
+    g->n_global = (int64_t)dims->X * dims->Y * dims->Z;
+    auto fail = [&](cg_status st) {
+        colgraph_free(g);
+        return st;
+    };
+    int num_sms = 148;
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dd.device);
+    if (cudaEventCreate(&g->ev0) != cudaSuccess || cudaEventCreate(&g->ev1) != cudaSuccess) return fail(CG_E_CUDA);
+    if (!local && nranks > 1) {
+        if (!dd.nccl_id || !nccl().ok) return fail(CG_E_NCCL);
+        ncclUniqueId id;
+        memcpy(&id, dd.nccl_id, sizeof(id));
+        if (nccl().commInitRank(&g->comm, nranks, id, rank) != ncclSuccess) return fail(CG_E_NCCL);
+        if (cudaMalloc(&g->d_red, 64 * sizeof(int64_t)) != cudaSuccess ||
+            cudaHostAlloc(&g->h_red, 64 * sizeof(int64_t), cudaHostAllocDefault) != cudaSuccess)
+            return fail(CG_E_NOMEM);
+    }
+    for (int i = 0; i < nslabs_local; i++) {
+        const int r = rank + i;
+        int32_t x0, x1;
+        if (cg_slab_range(dims, r, nranks, &x0, &x1) != CG_OK) return fail(CG_E_INVAL);
+        Slab *sl = new Slab();
+        sl->device = dd.device;
+        sl->stream = (cudaStream_t)dd.stream;
+        sl->num_sms = num_sms;
+        {  // persistent BFS: as many 512-thread blocks as are co-resident (cooperative launch)
+            int per_sm = 0, coop = 0;
+            cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dd.device);
+            if (coop && !getenv("CG_BFS_LEVEL_LAUNCHES") &&
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bfs_run, 512, 0) == cudaSuccess && per_sm > 0)
+                sl->bfs_coop_grid = num_sms * std::min(per_sm, CG_BFS_RUN_MINB);
+        }
+        sl->x0 = x0;
+        sl->x1 = x1;
+        sl->geo = make_geo(dims, x0, x1, nranks, r > 0, r + 1 < nranks, g->n_global);
+        g->slabs.push_back(sl);
+        // LOCAL: cost_dev is the whole volume; NCCL / single: this rank's slab
+        const int32_t *src = local ? cost_dev + (int64_t)x0 * sl->geo.YZ : cost_dev;
+        const cg_status s = slab_build(sl, src, input_is_weight ? 1 : 0);
+        if (s != CG_OK) return fail(s);
+    }
+    int64_t fl = 0;
+    for (Slab *sl : g->slabs) fl |= sl->h_flags[0];
+    g->st.source_capacity = 0;
+    for (Slab *sl : g->slabs) g->st.source_capacity += sl->N;
+    CG_TRY(gsum(g, &g->st.source_capacity, 1));
+    g->st.bytes_per_sweep_alg = 32.0 * (double)g->n_global;
+    g->st.kernel_launches = nslabs_local;
+    g->st.ms_build = now_ms() - t0;
+    *out = g;
+    return CG_OK;
+}
+
+cg_status colgraph_build(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight, const cg_dist *dist,
+                         cg_graph **out) {
+    cg_dist dd{0, 1, nullptr, 0, nullptr};
+    if (dist) dd = *dist;
+    if (dd.nranks < 1 || dd.rank < 0 || dd.rank >= dd.nranks) return CG_E_INVAL;
+    return build_common(dims, cost_dev, input_is_weight, &dd, dd.nranks, dd.rank, 1, false, out);
+}
+
+cg_status colgraph_build_slabs(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight, int32_t nslabs,
+                               const cg_dist *dist, cg_graph **out) {
+    if (nslabs < 1) return CG_E_INVAL;
+    return build_common(dims, cost_dev, input_is_weight, dist, nslabs, 0, nslabs, true, out);
+}
+
+cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_value, cg_solve_stats *stats) {
+    if (!g || !flow_value) return CG_E_INVAL;
+    if (g->solved) return CG_E_STATE;
+    DeviceGuard dg(g->dist.device);
+    cg_solve_opts o{};
+    bool use_tiles = false;
+    CG_TRY(normalize_opts(g, opts, o, use_tiles));
+    const bool trace = tracing();
+    const double t0 = now_ms();
+    Slab *s0 = g->slabs[0];
+    // a1': optional exact per-column pre-cancellation (valid initial preflow; DESIGN.md §7)
+    const size_t pc_smem = (size_t)8 * (g->dims.Z + 1) * sizeof(long long);
+    if (getenv("CG_PRECANCEL") && pc_smem <= 200 * 1024) {  // opt-in: measured slower on C4/C5
+        if (pc_smem > 48 * 1024)
+            CG_CUDA(cudaFuncSetAttribute(k_precancel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pc_smem));
+        for (Slab *sl : g->slabs) {
+            k_precancel<<<grid_for((int64_t)sl->geo.X * sl->geo.Y * 32, 256, sl->num_sms * 16), 256, pc_smem,
+                          sl->stream>>>(sl->geo, sl->s, sl->flags);
+            g->st.kernel_launches++;
+        }
+        CG_CUDA(cudaGetLastError());
+    }
+    double ms_gr = 0.0;
+    const cg_status result = pr_loop(g, o, use_tiles, ms_gr);
     if (result != CG_OK && result != CG_E_NOT_CONVERGED) return result;
     // a6: |f| = sum(T0) - sum(T)
     int64_t red[3] = {0, 0, 0};
@@ -1054,7 +1077,7 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
 
 cg_status mincut_extract_surface(cg_graph *g, int32_t *surface_dev, uint8_t *mask_dev) {
     if (!g || !surface_dev) return CG_E_INVAL;
-    if (!g->solved) return CG_E_STATE;
+    if (!g->solved || g->exported) return CG_E_STATE;
     DeviceGuard dg(g->dist.device);
     const double t0 = now_ms();
     for (Slab *sl : g->slabs) {
@@ -1142,6 +1165,48 @@ cg_status mincut_extract_surface(cg_graph *g, int32_t *surface_dev, uint8_t *mas
     CG_TRY(gmax(g, &e64));
     g->st.ms_extract = now_ms() - t0;
     return e64 ? CG_E_EMPTY_COLUMN : CG_OK;
+}
+
+cg_status maxflow_export_flow(cg_graph *g, const int32_t *cost_dev, int32_t input_is_weight, const cg_solve_opts *opts,
+                              int32_t *flow_dev) {
+    if (!g || !cost_dev || !flow_dev) return CG_E_INVAL;
+    if (!g->solved || g->exported) return CG_E_STATE;
+    if (multi(g) || g->slabs.size() != 1) return CG_E_INVAL;
+    DeviceGuard dg(g->dist.device);
+    cg_solve_opts o{};
+    bool use_tiles = false;
+    cg_solve_opts oo = opts ? *opts : cg_solve_opts{};
+    oo.sweep_kind = CG_SWEEP_VERTEX;  // phase 2 runs on the vertex worklists
+    CG_TRY(normalize_opts(g, &oo, o, use_tiles));
+    Slab *sl = g->slabs[0];
+    const Geo &geo = sl->geo;
+    const int64_t ncol = (int64_t)geo.X * geo.Y;
+    int32_t *tmp = nullptr;
+    CG_CUDA(cudaMallocAsync(&tmp, sizeof(int32_t) * geo.n, sl->stream));
+    // phase 2 (NEXT-2): the terminal of the push-relabel becomes s -- T(v) := flow on s->v,
+    // the phase-1 sink residuals are parked in tmp -- and the same solver returns every unit of
+    // stranded excess to s.  Vertices with excess cannot reach t (maximum preflow), so no
+    // flow into t changes.
+    k_phase2_setup<<<grid_for(ncol * 32, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(geo, cost_dev,
+                                                                                       input_is_weight ? 1 : 0,
+                                                                                       sl->s, tmp);
+    g->st.kernel_launches++;
+    CG_CUDA(cudaGetLastError());
+    double ms_gr = 0.0;
+    cg_status r = pr_loop(g, o, false, ms_gr);
+    if (r == CG_OK) {
+        CG_CUDA(cudaMemsetAsync(sl->flags + 3, 0, sizeof(int), sl->stream));
+        k_flow_export<<<grid_for(ncol * 32, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(
+            geo, cost_dev, input_is_weight ? 1 : 0, sl->s, tmp, flow_dev, sl->flags + 3);
+        g->st.kernel_launches++;
+        CG_CUDA(cudaMemcpyAsync(sl->h_flags + 3, sl->flags + 3, sizeof(int), cudaMemcpyDeviceToHost, sl->stream));
+        CG_CUDA(cudaStreamSynchronize(sl->stream));
+        if (sl->h_flags[3]) r = CG_E_NOT_CONVERGED;  // some vertex kept excess: not a flow
+    }
+    cudaFreeAsync(tmp, sl->stream);
+    CG_CUDA(cudaStreamSynchronize(sl->stream));
+    g->exported = true;
+    return r;
 }
 
 cg_status colgraph_stats(const cg_graph *g, cg_solve_stats *stats) {

@@ -62,6 +62,59 @@ __global__ void k_build(Geo g, const int32_t *__restrict__ in, int weight_mode, 
     if (bad) atomicOr(flags, FLAG_OVERFLOW);
 }
 
+// ------------------------------------------------------------------ NEXT-2: phase 2 + flow export
+// Vertex weights are recomputed from the caller's input exactly as k_build does (one warp
+// per column) to recover the source / sink capacities E0 = max(0,-w), T0 = max(0,w).
+__device__ __forceinline__ long long column_sum(const int32_t *cc, int Z) {
+    long long colsum = 0;
+    for (int z = lane_id(); z < Z; z += 32) colsum += cc[z];
+    return warp_sum_ll(colsum);
+}
+
+__device__ __forceinline__ long long weight_of(const int32_t *cc, int z, long long colsum, int weight_mode) {
+    if (weight_mode) return cc[z];
+    return z == 0 ? (long long)cc[0] - (colsum + 1) : (long long)cc[z] - (long long)cc[z - 1];
+}
+
+// tmp = phase-1 sink residual T; T := E0 (flow on the saturated source arc s->v)
+__global__ void k_phase2_setup(Geo g, const int32_t *__restrict__ in, int weight_mode, Soa s, int32_t *tmp) {
+    const int64_t ncol = (int64_t)g.X * g.Y;
+    for (int64_t col = gwarp(); col < ncol; col += nwarps()) {
+        const int32_t *cc = in + col * g.Z;
+        const long long colsum = weight_mode ? 0 : column_sum(cc, g.Z);
+        for (int z = lane_id(); z < g.Z; z += 32) {
+            const int64_t v = col * g.Z + z;
+            const long long w = weight_of(cc, z, colsum, weight_mode);
+            tmp[v] = s.T[v];
+            s.T[v] = w < 0 ? (int32_t)(-w) : 0;
+        }
+    }
+}
+
+// out planes (int32[7][n]): s->v, v->t, down v->v-1, lateral +x, -x, +y, -y.  Any vertex left
+// with excess sets *bad (the result would not be a flow).
+__global__ void k_flow_export(Geo g, const int32_t *__restrict__ in, int weight_mode, Soa s,
+                              const int32_t *__restrict__ tmp, int32_t *out, int *bad) {
+    const int64_t ncol = (int64_t)g.X * g.Y, n = g.n;
+    bool b = false;
+    for (int64_t col = gwarp(); col < ncol; col += nwarps()) {
+        const int32_t *cc = in + col * g.Z;
+        const long long colsum = weight_mode ? 0 : column_sum(cc, g.Z);
+        for (int z = lane_id(); z < g.Z; z += 32) {
+            const int64_t v = col * g.Z + z;
+            const long long w = weight_of(cc, z, colsum, weight_mode);
+            const int32_t t0 = w > 0 ? (int32_t)w : 0;
+            out[v] = s.T[v];
+            out[n + v] = t0 - tmp[v];
+            out[2 * n + v] = s.D[v];
+#pragma unroll
+            for (int d = 0; d < 4; d++) out[(3 + d) * n + v] = s.L[d][v];
+            b |= s.E[v] != 0;
+        }
+    }
+    if (b) atomicOr(bad, 1);
+}
+
 // f[lo .. lo+n) = v
 __global__ void k_fill(Field f, int64_t lo, int64_t n, int32_t v) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

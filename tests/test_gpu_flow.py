@@ -1,0 +1,169 @@
+"""NEXT-2: phase 2 + flow export.  maxflow_export_flow must return a
+maximum FLOW on the Wu-Chen arcs.  Checked against the definitions, independently of the
+CUDA path: capacity (Eq. 2), conservation at every vertex (Eq. 4), value
+= the oracle's |f| (Eq. 5), and the cut read off the flow's residual graph (BFS from s,
+Theorem 1) = the oracle's minimal source set."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+from scipy.sparse.csgraph import breadth_first_order
+
+import oracle
+from synth import volumes as V
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+DIRS = [(1, 0), (-1, 0), (0, 1), (0, -1)]
+
+
+@pytest.fixture(scope="module")
+def cg():
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a CUDA device")
+    from paper_2601_17026_b200 import colgraph
+    return colgraph
+
+
+def weights(c, weight):
+    cc = c.astype(np.int64)
+    if weight:
+        return cc
+    w = np.empty_like(cc)
+    w[:, :, 0] = cc[:, :, 0] - (cc.sum(axis=2) + 1)
+    w[:, :, 1:] = cc[:, :, 1:] - cc[:, :, :-1]
+    return w
+
+
+def sl(dx, X):  # (source slice, target slice) along one axis for a shift dx
+    return slice(max(0, -dx), X - max(0, dx)), slice(max(0, dx), X - max(0, -dx))
+
+
+def check_flow(c, delta, F, weight=False):
+    X, Y, Z = c.shape
+    n = X * Y * Z
+    fs, ft, fd, *L = [F[i].astype(np.int64) for i in range(7)]
+    w = weights(c, weight)
+    E0, T0 = np.maximum(-w, 0), np.maximum(w, 0)
+    zs = np.arange(Z)
+    zo = np.where(zs == 0, 0, np.where(zs > delta, zs - delta, -1))
+    valid = zo >= 0
+    # Eq. 2: capacities (infinite arcs: non-negative); arcs that do not exist carry nothing
+    assert (fs >= 0).all() and (fs <= E0).all()
+    assert (ft >= 0).all() and (ft <= T0).all()
+    assert (fd >= 0).all() and (fd[:, :, 0] == 0).all()
+    for d, (dx, dy) in enumerate(DIRS):
+        assert (L[d] >= 0).all() and (L[d][:, :, ~valid] == 0).all()
+        if dx == 1: assert (L[d][X - 1] == 0).all()
+        if dx == -1: assert (L[d][0] == 0).all()
+        if dy == 1: assert (L[d][:, Y - 1] == 0).all()
+        if dy == -1: assert (L[d][:, 0] == 0).all()
+    # Eq. 4: conservation at every vertex
+    net = fs - ft - fd
+    net[:, :, :-1] += fd[:, :, 1:]
+    for d, (dx, dy) in enumerate(DIRS):
+        net -= L[d]
+        xs, xt = sl(dx, X)
+        ys, yt = sl(dy, Y)
+        src = L[d][xs, ys][:, :, valid]
+        tgt = net[xt, yt]
+        for k, z in enumerate(zs[valid]):
+            tgt[:, :, zo[z]] += src[:, :, k]
+    assert not net.any(), "conservation violated"
+    assert ft.sum() == fs.sum()
+    # residual graph of the flow; BFS from s
+    idx = np.arange(n).reshape(X, Y, Z)
+    s_node, t_node = n, n + 1
+    rows, cols = [], []
+    m = fs < E0
+    rows.append(np.full(m.sum(), s_node)); cols.append(idx[m])
+    m = ft < T0
+    rows.append(idx[m]); cols.append(np.full(m.sum(), t_node))
+    rows.append(idx[:, :, 1:].ravel()); cols.append(idx[:, :, :-1].ravel())
+    m = fd[:, :, 1:] > 0
+    rows.append(idx[:, :, :-1][m]); cols.append(idx[:, :, 1:][m])
+    for d, (dx, dy) in enumerate(DIRS):
+        xs, xt = sl(dx, X)
+        ys, yt = sl(dy, Y)
+        vz = np.flatnonzero(valid)
+        tail = idx[xs, ys][:, :, vz]
+        head = idx[xt, yt][:, :, zo[vz]]
+        rows.append(tail.ravel()); cols.append(head.ravel())
+        m = L[d][xs, ys][:, :, vz] > 0
+        rows.append(head[m]); cols.append(tail[m])
+    r = np.concatenate(rows); cl = np.concatenate(cols)
+    g = sp.csr_matrix((np.ones(len(r), np.int8), (r, cl)), shape=(n + 2, n + 2))
+    reach = breadth_first_order(g, s_node, directed=True, return_predecessors=False)
+    assert t_node not in set(reach.tolist()), "augmenting path left"
+    mask = np.zeros(n, np.uint8)
+    mask[reach[reach < n]] = 1
+    return int(ft.sum()), mask.reshape(X, Y, Z)
+
+
+def export(cg, c, delta, weight=False, opts=None, extract_first=True):
+    t = torch.from_numpy(np.ascontiguousarray(c, np.int32)).cuda()
+    h = cg.colgraph_build(t, delta, weight)
+    try:
+        st, flow, _ = cg.maxflow_solve(h, None)
+        assert st == 0
+        if extract_first:
+            surf = torch.empty(c.shape[:2], dtype=torch.int32, device="cuda")
+            assert cg.mincut_extract_surface(h, surf) in (0, 6)
+        st, F = cg.maxflow_export_flow(h, t, weight, opts=opts)
+        assert st == 0, cg.STATUS.get(st)
+        if extract_first:
+            surf2 = torch.empty(c.shape[:2], dtype=torch.int32, device="cuda")
+            assert cg.mincut_extract_surface(h, surf2) == cg.CG_E_STATE
+            assert cg.maxflow_export_flow(h, t, weight)[0] == cg.CG_E_STATE
+        return flow, F.cpu().numpy()
+    finally:
+        cg.colgraph_free(h)
+
+
+def test_flow_random_tiny(cg):
+    for seed in range(1000, 1300):
+        c, delta = V.tiny_case(seed)
+        o = oracle.colgraph_solve(c, delta)
+        flow, F = export(cg, c, delta)
+        val, mask = check_flow(c, delta, F)
+        assert flow == val == o["flow"], seed
+        assert np.array_equal(mask, o["mask"]), seed
+
+
+def test_flow_weight_mode(cg):
+    rng = np.random.default_rng(5)
+    for trial in range(100):
+        X, Y, Z = (int(v) for v in rng.integers(1, 7, 3))
+        delta = int(rng.integers(0, 4))
+        w = rng.integers(-20, 21, size=(X, Y, Z)).astype(np.int32)
+        o = oracle.colgraph_solve(w, delta, input_is_weight=True)
+        flow, F = export(cg, w, delta, weight=True)
+        val, mask = check_flow(w, delta, F, weight=True)
+        assert flow == val == o["flow"], trial
+        assert np.array_equal(mask, o["mask"]), trial
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_flow_configs(cg, name):
+    c = V.generate(name)
+    delta = V.CONFIGS[name].delta
+    o = oracle.colgraph_solve(c, delta)
+    flow, F = export(cg, c, delta, extract_first=False)
+    val, mask = check_flow(c, delta, F)
+    assert flow == val == o["flow"]
+    assert np.array_equal(mask, o["mask"])
+
+
+def test_flow_errors(cg):
+    t = torch.zeros((2, 2, 3), dtype=torch.int32, device="cuda")
+    h = cg.colgraph_build(t, 1)
+    try:
+        assert cg.maxflow_export_flow(h, t)[0] == cg.CG_E_STATE  # not solved yet
+    finally:
+        cg.colgraph_free(h)
+    h = cg.colgraph_build_slabs(torch.zeros((4, 2, 3), dtype=torch.int32, device="cuda"), 1, 2)
+    try:
+        assert cg.maxflow_solve(h, None)[0] == 0
+        assert cg.maxflow_export_flow(h, torch.zeros((4, 2, 3), dtype=torch.int32, device="cuda"))[0] == cg.CG_E_INVAL
+    finally:
+        cg.colgraph_free(h)
