@@ -59,7 +59,7 @@ def _load():
         u8p = ctypes.POINTER(ctypes.c_uint8)
         lib.oracle_colgraph_solve.restype = ctypes.c_int
         lib.oracle_colgraph_solve.argtypes = [i32p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                              ctypes.c_int, ctypes.c_int, i64p, i32p, u8p, i32p, i64p]
+                                              ctypes.c_int, ctypes.c_int, ctypes.c_int, i64p, i32p, u8p, i32p, i64p]
         lib.oracle_graph_maxflow.restype = ctypes.c_int
         lib.oracle_graph_maxflow.argtypes = [ctypes.c_int, ctypes.c_int, i32p, i32p, i64p, ctypes.c_int,
                                              ctypes.c_int, ctypes.c_int, i64p, u8p, i32p]
@@ -71,9 +71,10 @@ def _ptr(a, ct):
     return a.ctypes.data_as(ctypes.POINTER(ct))
 
 
-def colgraph_solve(c: np.ndarray, delta: int, input_is_weight: bool = False, algo: str = "dinic",
+def colgraph_solve(c: np.ndarray, delta, input_is_weight: bool = False, algo: str = "dinic",
                    want_mask: bool = True) -> dict:
-    """Solve the column graph of cost (or weight) volume c[X][Y][Z].
+    """Solve the column graph of cost (or weight) volume c[X][Y][Z].  delta: int (isotropic)
+    or (delta_x, delta_y).
 
     Returns dict(status, flow, surface[X,Y] int32, mask[X,Y,Z] uint8 or None,
     checks (bit set), n_arcs).
@@ -86,7 +87,8 @@ def colgraph_solve(c: np.ndarray, delta: int, input_is_weight: bool = False, alg
     mask = np.zeros((X, Y, Z), np.uint8) if want_mask else None
     checks = np.zeros(1, np.int32)
     n_arcs = np.zeros(1, np.int64)
-    st = lib.oracle_colgraph_solve(_ptr(c, ctypes.c_int32), X, Y, Z, int(delta), int(bool(input_is_weight)),
+    dx, dy = (int(delta[0]), int(delta[1])) if isinstance(delta, (tuple, list)) else (int(delta), -1)
+    st = lib.oracle_colgraph_solve(_ptr(c, ctypes.c_int32), X, Y, Z, dx, dy, int(bool(input_is_weight)),
                                    ALGOS[algo], _ptr(flow, ctypes.c_int64), _ptr(surface, ctypes.c_int32),
                                    _ptr(mask, ctypes.c_uint8) if want_mask else None,
                                    _ptr(checks, ctypes.c_int32), _ptr(n_arcs, ctypes.c_int64))

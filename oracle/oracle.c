@@ -114,7 +114,10 @@ static void column_weights(const int32_t *c, int64_t Z, int64_t col, int64_t *w)
     for (int64_t z = 1; z < Z; z++) w[z] = (int64_t)cc[z] - (int64_t)cc[z - 1];
 }
 
-static void colgraph_arcs(graph_t *g, int pass, const int32_t *in, int X, int Y, int Z, int delta,
+/* Inter-column arcs (x,y,z) -> (x',y',max(0,z-Delta_d)): the edge interval toward the
+ * adjacent column in direction d, Delta_x for the x-neighbours and Delta_y for
+ * the y-neighbours (Delta_x = Delta_y is the paper's isotropic case). */
+static void colgraph_arcs(graph_t *g, int pass, const int32_t *in, int X, int Y, int Z, int delta, int delta_y,
                           int input_is_weight, int64_t *wbuf) {
     const int64_t n = (int64_t)X * Y * Z, s = n, t = n + 1;
     const int dx[4] = {+1, -1, 0, 0}, dy[4] = {0, 0, +1, -1};
@@ -131,10 +134,11 @@ static void colgraph_arcs(graph_t *g, int pass, const int32_t *in, int X, int Y,
                 if (wbuf[z] < 0) add_arc(g, pass, s, v, -wbuf[z]);
                 if (wbuf[z] > 0) add_arc(g, pass, v, t, wbuf[z]);
                 if (z >= 1) add_arc(g, pass, v, v - 1, OR_INF);
-                int64_t zt = z - delta > 0 ? z - delta : 0;
                 for (int d = 0; d < 4; d++) {
                     int64_t x2 = x + dx[d], y2 = y + dy[d];
                     if (x2 < 0 || x2 >= X || y2 < 0 || y2 >= Y) continue;
+                    const int64_t dl = d < 2 ? delta : delta_y;
+                    const int64_t zt = z - dl > 0 ? z - dl : 0;
                     add_arc(g, pass, v, (x2 * Y + y2) * Z + zt, OR_INF);
                 }
             }
@@ -301,6 +305,7 @@ static int64_t run_maxflow(graph_t *g, int64_t s, int64_t t, int algo, int *err)
 /*
  * Column-graph oracle.
  *   in[X*Y*Z]       int32 costs c[x][y][z] (z fastest), or vertex weights if input_is_weight
+ *   delta, delta_y  smoothness toward x- / y-neighbours (delta_y = -1: same as delta)
  *   algo            0 = Dinitz, 1 = Edmonds-Karp
  *   flow_out        |f| (int64)
  *   surface_out     int32[X*Y], max z in S per column, -1 if none (nullable)
@@ -309,10 +314,11 @@ static int64_t run_maxflow(graph_t *g, int64_t s, int64_t t, int algo, int *err)
  *   n_arcs_out      number of explicit arcs built (nullable)
  * Returns 0, 1 (invalid dims), 3 (out of memory) or 6 (a column has no source-side vertex).
  */
-int oracle_colgraph_solve(const int32_t *in, int X, int Y, int Z, int delta, int input_is_weight, int algo,
-                          int64_t *flow_out, int32_t *surface_out, uint8_t *mask_out, int32_t *checks_out,
+int oracle_colgraph_solve(const int32_t *in, int X, int Y, int Z, int delta, int delta_y, int input_is_weight,
+                          int algo, int64_t *flow_out, int32_t *surface_out, uint8_t *mask_out, int32_t *checks_out,
                           int64_t *n_arcs_out) {
-    if (!in || X < 1 || Y < 1 || Z < 1 || delta < 0) return OR_E_INVAL;
+    if (delta_y == -1) delta_y = delta; /* isotropic */
+    if (!in || X < 1 || Y < 1 || Z < 1 || delta < 0 || delta_y < 0) return OR_E_INVAL;
     if ((int64_t)X * Y * Z + 2 > INT32_MAX) return OR_E_INVAL;
     const int64_t n = (int64_t)X * Y * Z, s = n, t = n + 1;
     graph_t g;
@@ -320,9 +326,9 @@ int oracle_colgraph_solve(const int32_t *in, int X, int Y, int Z, int delta, int
     int64_t *wbuf = (int64_t *)malloc((size_t)Z * sizeof(int64_t));
     uint8_t *mark = (uint8_t *)malloc((size_t)n + 2);
     if (!wbuf || !mark || g_alloc(&g, n + 2)) { free(wbuf); free(mark); return OR_E_NOMEM; }
-    colgraph_arcs(&g, 0, in, X, Y, Z, delta, input_is_weight, wbuf);
+    colgraph_arcs(&g, 0, in, X, Y, Z, delta, delta_y, input_is_weight, wbuf);
     if (g_finish_count(&g)) { g_free(&g); free(wbuf); free(mark); return OR_E_NOMEM; }
-    colgraph_arcs(&g, 1, in, X, Y, Z, delta, input_is_weight, wbuf);
+    colgraph_arcs(&g, 1, in, X, Y, Z, delta, delta_y, input_is_weight, wbuf);
     if (n_arcs_out) *n_arcs_out = g.m / 2;
     int64_t flow = run_maxflow(&g, s, t, algo, &err);
     if (err) { g_free(&g); free(wbuf); free(mark); return err; }

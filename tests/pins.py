@@ -31,11 +31,19 @@ def _pair_ok(a, b, delta, allow_empty):
     return ok
 
 
-def enumerate_surfaces(X: int, Y: int, Z: int, delta: int, allow_empty: bool = False) -> np.ndarray:
-    """All feasible top-assignments, shape (K, X*Y), column index x*Y + y.
+def _dxy(delta):
+    """delta: int (isotropic) or (delta_x, delta_y) -- the edge interval toward x- and
+    y-neighbours."""
+    return (int(delta[0]), int(delta[1])) if isinstance(delta, (tuple, list)) else (int(delta), int(delta))
+
+
+def enumerate_surfaces(X: int, Y: int, Z: int, delta, allow_empty: bool = False) -> np.ndarray:
+    """All feasible top-assignments, shape (K, X*Y), column index x*Y + y:
+    |S(x,y) - S(x-1,y)| <= delta_x and |S(x,y) - S(x,y-1)| <= delta_y.
 
     allow_empty adds top = -1 (empty column) for the weight-mode closure pin.
     """
+    dx, dy = _dxy(delta)
     vals = np.arange(-1 if allow_empty else 0, Z, dtype=np.int16)
     cur = np.zeros((1, 0), dtype=np.int16)
     for col in range(X * Y):
@@ -45,14 +53,14 @@ def enumerate_surfaces(X: int, Y: int, Z: int, delta: int, allow_empty: bool = F
         v = np.tile(vals, K)
         ok = np.ones(len(v), dtype=bool)
         if x > 0:
-            ok &= _pair_ok(v, new[:, (x - 1) * Y + y], delta, allow_empty)
+            ok &= _pair_ok(v, new[:, (x - 1) * Y + y], dx, allow_empty)
         if y > 0:
-            ok &= _pair_ok(v, new[:, x * Y + y - 1], delta, allow_empty)
+            ok &= _pair_ok(v, new[:, x * Y + y - 1], dy, allow_empty)
         cur = np.concatenate([new[ok], v[ok, None]], axis=1)
     return cur
 
 
-def brute_force_surfaces(c: np.ndarray, delta: int):
+def brute_force_surfaces(c: np.ndarray, delta):
     """(min cost, lowest optimal surface (X,Y), number of optima, number of feasible surfaces)."""
     X, Y, Z = c.shape
     S = enumerate_surfaces(X, Y, Z, delta)
@@ -63,7 +71,7 @@ def brute_force_surfaces(c: np.ndarray, delta: int):
     return int(best), opt.min(axis=0).reshape(X, Y).astype(np.int32), int(len(opt)), int(len(S))
 
 
-def brute_force_weight_closure(w: np.ndarray, delta: int):
+def brute_force_weight_closure(w: np.ndarray, delta):
     """Weight mode: min over closed sets S of sum_{v in S} w(v) (plus sum max(-w,0) = min cut),
     and the pointwise-lowest optimal top assignment (-1 = empty column)."""
     X, Y, Z = w.shape

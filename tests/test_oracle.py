@@ -188,3 +188,62 @@ def test_c1_full_value_identity():
 def test_invalid_inputs():
     assert oracle.colgraph_solve(np.zeros((1, 1, 1), np.int32), -1)["status"] == 1
     assert oracle.graph_maxflow(2, [(0, 1, 1)], 0, 0)["status"] == 1
+
+
+# ---------------------------------------------------------------- NEXT-3: anisotropic smoothness (Delta_x != Delta_y)
+# The edge interval is defined per adjacent column; SURVEY.md §8(f) NEXT-3.
+
+def test_aniso_random_tiny_bruteforce():
+    """Every (Delta_x, Delta_y)-feasible surface enumerated: |f| = min cost + K0 and the
+    surface is the pointwise-lowest optimum."""
+    rng = np.random.default_rng(31)
+    for trial in range(120):
+        X, Y, Z = int(rng.integers(1, 4)), int(rng.integers(1, 4)), int(rng.integers(1, 8))
+        dx, dy = (int(v) for v in rng.integers(0, 4, 2))
+        c = rng.integers(0, (4, 10, 256)[trial % 3], size=(X, Y, Z)).astype(np.int32)
+        _check_vs_bruteforce(c, (dx, dy), "dinic" if trial % 2 else "ek")
+
+
+def test_aniso_weight_mode_bruteforce():
+    rng = np.random.default_rng(32)
+    for trial in range(60):
+        X, Y, Z = int(rng.integers(1, 4)), int(rng.integers(1, 3)), int(rng.integers(1, 6))
+        dx, dy = (int(v) for v in rng.integers(0, 3, 2))
+        w = rng.integers(-9, 10, size=(X, Y, Z)).astype(np.int32)
+        val, lowest = pins.brute_force_weight_closure(w, (dx, dy))
+        r = oracle.colgraph_solve(w, (dx, dy), input_is_weight=True)
+        assert r["checks"] == oracle.ALL_CHECKS
+        assert r["flow"] == val and np.array_equal(r["surface"], lowest)
+
+
+@pytest.mark.parametrize("dx,dy", [(1, 0), (2, 5), (0, 3)])
+def test_aniso_lines(dx, dy):
+    """Y = 1: only Delta_x constrains the line; X = 1: only Delta_y (Viterbi DP)."""
+    c = V.tiny(90 + dx, 30, 1, 14, 255)
+    opt, surf = pins.dp_line(c.reshape(-1, 14), dx)
+    r = solve(c, (dx, dy))
+    assert r["flow"] == opt + pins.k0(c) and np.array_equal(r["surface"].ravel(), surf)
+    c = V.tiny(95 + dy, 1, 27, 12, 9)
+    opt, surf = pins.dp_line(c.reshape(-1, 12), dy)
+    r = solve(c, (dx, dy))
+    assert r["flow"] == opt + pins.k0(c) and np.array_equal(r["surface"].ravel(), surf)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_aniso_closed_form_rows(seed):
+    """Delta_x >= Z-1, Delta_y = 0: every x-slice is one flat row, independently of the
+    others -- S(x, .) = lowest argmin_z sum_y c(x,y,z)."""
+    c = V.tiny(500 + seed, 5, 4, 9, (3, 255)[seed % 2])
+    tot = c.astype(np.int64).sum(axis=1)  # [x][z]
+    z = tot.argmin(axis=1)
+    r = solve(c, (8, 0))
+    assert r["flow"] == int(tot.min(axis=1).sum()) + pins.k0(c)
+    assert np.array_equal(r["surface"], np.repeat(z[:, None], 4, axis=1).astype(np.int32))
+
+
+def test_aniso_transpose_swaps_deltas():
+    c = V.generate("C1")[:7, :5, :]
+    a = solve(c, (1, 3))
+    b = solve(np.ascontiguousarray(c.transpose(1, 0, 2)), (3, 1))
+    assert a["flow"] == b["flow"] and np.array_equal(a["surface"], b["surface"].T)
+    assert solve(c, (2, 2))["flow"] == solve(c, 2)["flow"]
