@@ -61,9 +61,15 @@ typedef enum {
 } cg_status;
 
 /* Full-volume dimensions; Delta >= 0 is the smoothness interval
- * (Delta >= Z-1: unconstrained columns; Delta = 0: flat surface). */
+ * (Delta >= Z-1: unconstrained columns; Delta = 0: flat surface).
+ *   delta   : edge interval toward the x-neighbour columns (Delta_x)
+ *   delta_y : edge interval toward the y-neighbour columns (Delta_y); -1 = same as delta.
+ *             Anisotropic smoothness is SURVEY.md §8(f) NEXT-3 (the paper defines the edge
+ *             interval per adjacent column).  Callers must set it (-1 for the
+ *             isotropic case); values < -1 are CG_E_INVAL. */
 typedef struct {
     int32_t X, Y, Z, delta;
+    int32_t delta_y;
 } cg_dims;
 
 /* Process / device placement.

@@ -28,7 +28,15 @@ class ColgraphError(RuntimeError):
 
 
 class cg_dims(ctypes.Structure):
-    _fields_ = [("X", ctypes.c_int32), ("Y", ctypes.c_int32), ("Z", ctypes.c_int32), ("delta", ctypes.c_int32)]
+    """delta: Delta_x; delta_y: Delta_y (-1 = isotropic).  Python callers may pass delta as an
+    int or as a (delta_x, delta_y) pair."""
+    _fields_ = [("X", ctypes.c_int32), ("Y", ctypes.c_int32), ("Z", ctypes.c_int32), ("delta", ctypes.c_int32),
+                ("delta_y", ctypes.c_int32)]
+
+    def __init__(self, X=0, Y=0, Z=0, delta=0, delta_y=None):
+        if isinstance(delta, (tuple, list)):
+            delta, delta_y = delta
+        super().__init__(int(X), int(Y), int(Z), int(delta), -1 if delta_y is None else int(delta_y))
 
 
 class cg_dist(ctypes.Structure):
@@ -139,7 +147,7 @@ def colgraph_build(cost, delta: int, input_is_weight: bool = False, stream=None,
         stream = torch.cuda.current_stream(cost.device)
     if dims is None:
         X, Y, Z = cost.shape
-        dims = cg_dims(X, Y, Z, int(delta))
+        dims = cg_dims(X, Y, Z, delta)
     h = ctypes.c_void_p()
     idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
     st = _lib.colgraph_build(ctypes.byref(dims), ctypes.c_void_p(cost.data_ptr()), int(bool(input_is_weight)),
@@ -159,7 +167,7 @@ def colgraph_build_slabs(cost, delta: int, nslabs: int, input_is_weight: bool = 
     if stream is None:
         stream = torch.cuda.current_stream(cost.device)
     X, Y, Z = cost.shape
-    dims = cg_dims(X, Y, Z, int(delta))
+    dims = cg_dims(X, Y, Z, delta)
     h = ctypes.c_void_p()
     st = _lib.colgraph_build_slabs(ctypes.byref(dims), ctypes.c_void_p(cost.data_ptr()), int(bool(input_is_weight)),
                                    int(nslabs), ctypes.byref(_dist(cost.device.index,
@@ -230,7 +238,7 @@ def colgraph_solve_host(cost: np.ndarray, delta: int, input_is_weight: bool = Fa
     """End-to-end on host buffers (H2D, build, solve, extract, D2H inside the library)."""
     cost = np.ascontiguousarray(cost, dtype=np.int32)
     X, Y, Z = cost.shape
-    dims = cg_dims(X, Y, Z, int(delta))
+    dims = cg_dims(X, Y, Z, delta)
     surface = np.empty((X, Y), np.int32)
     mask = np.empty((X, Y, Z), np.uint8) if want_mask else None
     flow = ctypes.c_int64(0)
@@ -246,7 +254,7 @@ def colgraph_solve_host_ptr(cost_host, delta: int, surface_host, mask_host=None,
                             opts: cg_solve_opts | None = None, stream=None):
     """colgraph_solve_host on (pinned) host torch tensors, without extra host copies."""
     X, Y, Z = cost_host.shape
-    dims = cg_dims(X, Y, Z, int(delta))
+    dims = cg_dims(X, Y, Z, delta)
     flow = ctypes.c_int64(0)
     stats = cg_solve_stats()
     sh = ctypes.c_void_p(stream.cuda_stream) if stream is not None else None

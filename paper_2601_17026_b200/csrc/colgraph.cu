@@ -638,6 +638,7 @@ Geo make_geo(const cg_dims *dims, int x0, int x1, int nranks_total, bool gl, boo
     geo.Y = dims->Y;
     geo.Z = dims->Z;
     geo.delta = dims->delta;
+    geo.delta_y = dims->delta_y < 0 ? dims->delta : dims->delta_y;
     geo.CPC = (dims->Z + 31) / 32;
     geo.gl = gl;
     geo.gh = gh;
@@ -650,7 +651,7 @@ Geo make_geo(const cg_dims *dims, int x0, int x1, int nranks_total, bool gl, boo
 }
 
 cg_status validate_dims(const cg_dims *dims) {
-    if (!dims || dims->X < 1 || dims->Y < 1 || dims->Z < 1 || dims->delta < 0) return CG_E_INVAL;
+    if (!dims || dims->X < 1 || dims->Y < 1 || dims->Z < 1 || dims->delta < 0 || dims->delta_y < -1) return CG_E_INVAL;
     const int64_t n = (int64_t)dims->X * dims->Y * dims->Z;
     if (n + dims->Z + 64 >= (int64_t)INT_MAX) return CG_E_INVAL;
     return CG_OK;
@@ -903,7 +904,7 @@ const char *cg_status_str(cg_status s) {
 }
 
 const char *cg_version(void) {
-    return "colgraph 0.3 sm_100a (lock-free push-relabel: multi-hop walks + single-hop sweeps over vertex worklists, "
+    return "colgraph 0.4 sm_100a (lock-free push-relabel: multi-hop walks + single-hop sweeps over vertex worklists, "
            "device-driven frontier BFS relabel, worklist extraction, x-slab halos over NCCL)";
 }
 

@@ -16,7 +16,8 @@ namespace cg {
 constexpr unsigned FULL = 0xffffffffu;
 
 struct Geo {
-    int32_t X, Y, Z, delta;  // X = x-planes owned by this slab
+    int32_t X, Y, Z, delta;  // X = x-planes owned by this slab; delta = Delta_x (toward x-neighbours)
+    int32_t delta_y;         // Delta_y (toward y-neighbours); = delta in the isotropic case
     int32_t CPC;             // chunks per column = ceil(Z / 32)
     int32_t gl, gh;          // a ghost plane exists at x = -1 (gl) / x = X (gh): neighbour slab
     int64_t n;               // vertices owned by this slab
@@ -64,6 +65,8 @@ __device__ __forceinline__ int64_t nwarps() { return ((int64_t)gridDim.x * block
 // lateral in-arc of (x,y,z) per direction comes from (nbr, zi(z)).
 __device__ __forceinline__ int zo_of(int z, int delta) { return z == 0 ? 0 : (z > delta ? z - delta : -1); }
 __device__ __forceinline__ int zi_of(int z, int delta, int Z) { return z == 0 ? 0 : (z + delta < Z ? z + delta : -1); }
+// edge interval toward direction d (0:+x 1:-x 2:+y 3:-y): Delta_x or Delta_y (NEXT-3)
+__device__ __forceinline__ int delta_d(const Geo &g, int d) { return d < 2 ? g.delta : g.delta_y; }
 
 // neighbour column offset (in vertices) in direction d, 0 if the neighbour is outside the slab
 __device__ __forceinline__ int64_t nbr_off(const Geo &g, int x, int y, int d) {

@@ -137,7 +137,7 @@ __global__ void k_export(Field f, int64_t n, int32_t *out) {
 // read is a lower bound of what the reader may subtract.
 struct OpCtx {
     int64_t v, v0, col;
-    int z, zo, zi;
+    int z, zo[2], zi[2];  // [0]: toward x-neighbours (Delta_x), [1]: y-neighbours (Delta_y)
     int64_t off[4];  // vertex offset of the neighbour column (0 = none)
 };
 
@@ -161,11 +161,11 @@ __device__ __forceinline__ ArcPick scan_arcs(const Geo &g, const Soa &s, const O
         if (hh < p.best) { p.best = hh; p.arc = 1; p.tgt = c.v - 1; }
         if (p.best < hx) return p;
     }
-    if (c.zo >= 0) {
+    if (c.zo[0] >= 0 || c.zo[1] >= 0) {
 #pragma unroll
         for (int d = 0; d < 4; d++) {
-            if (!c.off[d]) continue;
-            const int64_t t = c.v0 + c.off[d] + c.zo;
+            if (!c.off[d] || c.zo[d >> 1] < 0) continue;
+            const int64_t t = c.v0 + c.off[d] + c.zo[d >> 1];
             const int hh = s.H[t];
             if (hh < p.best) { p.best = hh; p.arc = 2 + d; p.tgt = t; }
             if (p.best < hx) return p;
@@ -179,11 +179,11 @@ __device__ __forceinline__ ArcPick scan_arcs(const Geo &g, const Soa &s, const O
             if (p.best < hx) return p;
         }
     }
-    if (c.zi >= 0) {
+    if (c.zi[0] >= 0 || c.zi[1] >= 0) {
 #pragma unroll
         for (int d = 0; d < 4; d++) {
-            if (!c.off[d]) continue;
-            const int64_t u = c.v0 + c.off[d] + c.zi;
+            if (!c.off[d] || c.zi[d >> 1] < 0) continue;
+            const int64_t u = c.v0 + c.off[d] + c.zi[d >> 1];
             const int r = s.L[d ^ 1][u];
             if (r > 0) {
                 const int hh = s.H[u];
@@ -201,8 +201,10 @@ __device__ __forceinline__ void set_ctx(const Geo &g, OpCtx &c, int64_t v) {
     c.z = (int)(v - c.col * g.Z);
     c.v0 = c.col * g.Z;
     const int x = (int)(c.col / g.Y), y = (int)(c.col - (int64_t)x * g.Y);
-    c.zo = zo_of(c.z, g.delta);
-    c.zi = zi_of(c.z, g.delta, g.Z);
+    c.zo[0] = zo_of(c.z, g.delta);
+    c.zo[1] = zo_of(c.z, g.delta_y);
+    c.zi[0] = zi_of(c.z, g.delta, g.Z);
+    c.zi[1] = zi_of(c.z, g.delta_y, g.Z);
 #pragma unroll
     for (int d = 0; d < 4; d++) c.off[d] = nbr_off(g, x, y, d);
 }
@@ -559,7 +561,8 @@ __device__ __forceinline__ void bfs_expand_warp(const Geo &g, const Soa &s, int 
         const int z = (int)(v - col * g.Z);
         const int x = (int)(col / g.Y), y = (int)(col - (int64_t)x * g.Y);
         const int64_t v0 = col * g.Z;
-        const int zo = zo_of(z, g.delta), zi = zi_of(z, g.delta, g.Z);
+        const int zox = zo_of(z, g.delta), zix = zi_of(z, g.delta, g.Z);
+        const int zoy = zo_of(z, g.delta_y), ziy = zi_of(z, g.delta_y, g.Z);
         auto claim = [&](int slot, int64_t w) {
             if (!owned(g, w)) return;  // ghost labels come from their owner
             if (STRICT) {
@@ -586,6 +589,7 @@ __device__ __forceinline__ void bfs_expand_warp(const Geo &g, const Soa &s, int 
             for (int d = 0; d < 4; d++) {
                 const int64_t o = nbr_off(g, x, y, d);
                 if (!o) continue;
+                const int zi = d < 2 ? zix : ziy, zo = d < 2 ? zox : zoy;
                 if (zi >= 0 && owned(g, v0 + o + zi)) { w[2 + d] = (int)(v0 + o + zi); cand |= 1u << (2 + d); }
                 if (zo >= 0 && s.L[d][v] > 0 && owned(g, v0 + o + zo)) {
                     w[6 + d] = (int)(v0 + o + zo);
@@ -608,6 +612,7 @@ __device__ __forceinline__ void bfs_expand_warp(const Geo &g, const Soa &s, int 
             for (int d = 0; d < 4; d++) {
                 const int64_t o = nbr_off(g, x, y, d);
                 if (!o) continue;
+                const int zi = d < 2 ? zix : ziy, zo = d < 2 ? zox : zoy;
                 if (zi >= 0) claim(2 + d, v0 + o + zi);
                 if (zo >= 0 && s.L[d][v] > 0) claim(6 + d, v0 + o + zo);
             }
@@ -658,7 +663,8 @@ __device__ __forceinline__ void bfs_expand_multi(const Geo &g, const Soa &s, int
         const int z = v - col * g.Z;
         const int x = col / g.Y, y = col - x * g.Y;
         const int v0 = col * g.Z;
-        const int zo = zo_of(z, g.delta), zi = zi_of(z, g.delta, g.Z);
+        const int zox = zo_of(z, g.delta), zix = zi_of(z, g.delta, g.Z);
+        const int zoy = zo_of(z, g.delta_y), ziy = zi_of(z, g.delta_y, g.Z);
         int D, L[4];
         load_DL(s, v, D, L);
         if (z + 1 < g.Z) { w[r][0] = v + 1; cand[r] |= 1u; }
@@ -667,6 +673,7 @@ __device__ __forceinline__ void bfs_expand_multi(const Geo &g, const Soa &s, int
         for (int d = 0; d < 4; d++) {
             const int o = (int)nbr_off(g, x, y, d);
             if (!o) continue;
+            const int zi = d < 2 ? zix : ziy, zo = d < 2 ? zox : zoy;
             if (zi >= 0 && owned(g, v0 + o + zi)) { w[r][2 + d] = v0 + o + zi; cand[r] |= 1u << (2 + d); }
             if (zo >= 0 && L[d] > 0 && owned(g, v0 + o + zo)) { w[r][6 + d] = v0 + o + zo; cand[r] |= 1u << (6 + d); }
         }
@@ -756,11 +763,11 @@ __device__ __forceinline__ void bfs_bottom_up_level(const Geo &g, const Soa &s, 
                     if (!hit && z + 1 < g.Z && s.D[u + 1] > 0 && __ldcg(&s.H[u + 1]) == L) hit = true;
                     if (!hit) {
                         const int x = (int)(col / g.Y), y = (int)(col - (int64_t)x * g.Y);
-                        const int zo = zo_of(z, g.delta), zi = zi_of(z, g.delta, g.Z);
 #pragma unroll
                         for (int d = 0; d < 4 && !hit; d++) {
                             const int64_t o = nbr_off(g, x, y, d);
                             if (!o) continue;
+                            const int zo = zo_of(z, delta_d(g, d)), zi = zi_of(z, delta_d(g, d), g.Z);
                             if (zo >= 0 && __ldcg(&s.H[v0 + o + zo]) == L) hit = true;
                             else if (zi >= 0 && s.L[d ^ 1][v0 + o + zi] > 0 && __ldcg(&s.H[v0 + o + zi]) == L) hit = true;
                         }
@@ -1290,15 +1297,16 @@ __global__ void __launch_bounds__(256) k_ext_round(Geo g, Soa s, const int *__re
         int cd[4] = {-1, -1, -1, -1};
         for (int zb = p + 1; zb <= t; zb += 32) {
             const int z = zb + lane_id();
-            const int zi = z <= t ? zi_of(z, g.delta, g.Z) : -1;
 #pragma unroll
-            for (int d = 0; d < 4; d++)
+            for (int d = 0; d < 4; d++) {
+                const int zi = z <= t ? zi_of(z, delta_d(g, d), g.Z) : -1;
                 if (zi >= 0 && nc[d] != INT64_MIN && s.L[d ^ 1][nc[d] * g.Z + zi] > 0) cd[d] = max(cd[d], zi);
+            }
         }
-        const int zout = t > g.delta ? t - g.delta : 0;
         int mark = -1;
 #pragma unroll
         for (int d = 0; d < 4; d++) {
+            const int zout = t > delta_d(g, d) ? t - delta_d(g, d) : 0;
             const int cand = max(warp_max_i(cd[d]), zout);
             if (lane_id() == d && nc[d] != INT64_MIN) {
                 const int old = atomicMax(&top[nc[d]], cand);

@@ -210,11 +210,11 @@ __device__ __forceinline__ void local_relabel(const Geo &g, const TileGeo &t, co
             if (hold[k] >= g.INF) frozen |= 1u << k;
             if (hold[k] < g.INF) {
                 int b = tsm[m.T + (a)] > 0 ? 1 : LINF;
-                const int zo = zo_of(z, g.delta), zi = zi_of(z, g.delta, Z);
 #pragma unroll
                 for (int dd = 0; dd < 4; dd++) {
                     const int nb = cc.nb[dd];
                     if (nb == NB_NONE || nb >= 0) continue;  // halo exits only
+                    const int zo = zo_of(z, delta_d(g, dd)), zi = zi_of(z, delta_d(g, dd), Z);
                     if (zo >= 0) {
                         const int hh = op.nH(nb, zo);
                         if (hh < g.INF) b = min(b, hh + 1);
@@ -251,12 +251,12 @@ __device__ __forceinline__ void local_relabel(const Geo &g, const TileGeo &t, co
             for (int k = 0; k < S; k++) {
                 const int z = lane * S + k;
                 if (z >= Z || hold[k] >= g.INF) continue;
-                const int zo = zo_of(z, g.delta), zi = zi_of(z, g.delta, Z);
                 int b = d[k];
 #pragma unroll
                 for (int dd = 0; dd < 4; dd++) {
                     const int nb = cc.nb[dd];
                     if (nb < 0) continue;  // tile neighbours only (halo exits are in base)
+                    const int zo = zo_of(z, delta_d(g, dd)), zi = zi_of(z, delta_d(g, dd), Z);
                     if (zo >= 0) b = min(b, tsm[m.H + (nb * t.CS + tpos<S>(zo, t.P))] + 1);
                     if (zi >= 0 && tsm[m.L0 + (dd ^ 1) * m.ncs + (nb * t.CS + tpos<S>(zi, t.P))] > 0)
                         b = min(b, tsm[m.H + (nb * t.CS + tpos<S>(zi, t.P))] + 1);
@@ -292,11 +292,11 @@ __device__ __forceinline__ int min_nbr_label(const Geo &g, const TileOps<S> &op,
     if (tsm[m.T + (a)] > 0) return 0;
     int b = g.INF;
     if (z >= 1) b = min(b, tsm[m.H + (op.at(z - 1))]);
-    const int zo = zo_of(z, g.delta), zi = zi_of(z, g.delta, g.Z);
 #pragma unroll
     for (int d = 0; d < 4; d++) {
         const int nb = cc.nb[d];
         if (nb == NB_NONE) continue;
+        const int zo = zo_of(z, delta_d(g, d)), zi = zi_of(z, delta_d(g, d), g.Z);
         if (zo >= 0) b = min(b, op.nH(nb, zo));
         if (zi >= 0 && op.nLres(nb, d, zi) > 0) b = min(b, op.nH(nb, zi));
     }
@@ -405,12 +405,12 @@ __device__ __forceinline__ bool push_step(const Geo &g, const TileGeo &t, const 
             tsm[m.T + a] -= df;
         } else {
             bool done = false;
-            const int zo = zo_of(z, g.delta);
-            if (zo >= 0) {
+            {
 #pragma unroll
                 for (int d = 0; d < 4; d++) {
                     const int nb = cc.nb[d];
-                    if (done || nb == NB_NONE) continue;
+                    const int zo = zo_of(z, delta_d(g, d));
+                    if (done || nb == NB_NONE || zo < 0) continue;
                     if (op.nH(nb, zo) < hk) {  // lateral-out (infinite)
                         df = e[k];
                         atomicAdd(&tsm[m.L0 + d * m.ncs + a], df);
@@ -434,12 +434,12 @@ __device__ __forceinline__ bool push_step(const Geo &g, const TileGeo &t, const 
                     done = true;
                 }
             }
-            const int zi = zi_of(z, g.delta, Z);
-            if (!done && zi >= 0) {
+            if (!done) {
 #pragma unroll
                 for (int d = 0; d < 4; d++) {
                     const int nb = cc.nb[d];
-                    if (done || nb == NB_NONE) continue;
+                    const int zi = zi_of(z, delta_d(g, d), Z);
+                    if (done || nb == NB_NONE || zi < 0) continue;
                     const int r = op.nLres(nb, d, zi);
                     if (r > 0 && op.nH(nb, zi) < hk) {  // lateral-in reverse
                         df = min(e[k], r);

@@ -46,13 +46,14 @@ def check_flow(c, delta, F, weight=False):
     w = weights(c, weight)
     E0, T0 = np.maximum(-w, 0), np.maximum(w, 0)
     zs = np.arange(Z)
-    zo = np.where(zs == 0, 0, np.where(zs > delta, zs - delta, -1))
-    valid = zo >= 0
+    dxy = tuple(delta) if isinstance(delta, (tuple, list)) else (delta, delta)
+    ZO = [np.where(zs == 0, 0, np.where(zs > dl, zs - dl, -1)) for dl in dxy]  # x-, y-neighbours
     # Eq. 2: capacities (infinite arcs: non-negative); arcs that do not exist carry nothing
     assert (fs >= 0).all() and (fs <= E0).all()
     assert (ft >= 0).all() and (ft <= T0).all()
     assert (fd >= 0).all() and (fd[:, :, 0] == 0).all()
     for d, (dx, dy) in enumerate(DIRS):
+        valid = ZO[d >> 1] >= 0
         assert (L[d] >= 0).all() and (L[d][:, :, ~valid] == 0).all()
         if dx == 1: assert (L[d][X - 1] == 0).all()
         if dx == -1: assert (L[d][0] == 0).all()
@@ -62,6 +63,8 @@ def check_flow(c, delta, F, weight=False):
     net = fs - ft - fd
     net[:, :, :-1] += fd[:, :, 1:]
     for d, (dx, dy) in enumerate(DIRS):
+        zo = ZO[d >> 1]
+        valid = zo >= 0
         net -= L[d]
         xs, xt = sl(dx, X)
         ys, yt = sl(dy, Y)
@@ -83,9 +86,10 @@ def check_flow(c, delta, F, weight=False):
     m = fd[:, :, 1:] > 0
     rows.append(idx[:, :, :-1][m]); cols.append(idx[:, :, 1:][m])
     for d, (dx, dy) in enumerate(DIRS):
+        zo = ZO[d >> 1]
         xs, xt = sl(dx, X)
         ys, yt = sl(dy, Y)
-        vz = np.flatnonzero(valid)
+        vz = np.flatnonzero(zo >= 0)
         tail = idx[xs, ys][:, :, vz]
         head = idx[xt, yt][:, :, zo[vz]]
         rows.append(tail.ravel()); cols.append(head.ravel())
