@@ -1193,8 +1193,46 @@ cg_status maxflow_export_flow(cg_graph *g, const int32_t *cost_dev, int32_t inpu
                                                                                        sl->s, tmp);
     g->st.kernel_launches++;
     CG_CUDA(cudaGetLastError());
-    double ms_gr = 0.0;
-    cg_status r = pr_loop(g, o, false, ms_gr);
+    cg_status r = CG_OK;
+    const bool pr_only = getenv("CG_PHASE2_PR") != nullptr;  // the generic alternative (slow tail)
+    if (!pr_only) {
+        // level-ordered cancellation (k_return_level): one launch per level; levels whose
+        // lateral arcs stay on the level (z = 0, Delta_d = 0) first net antiparallel flows,
+        // then repeat until a pass sees no excess there (at most SAME_LEVEL_PASSES)
+        constexpr int SAME_LEVEL_PASSES = 64;
+        const bool flat = geo.delta == 0 || geo.delta_y == 0;
+        const int grid = grid_for(ncol, 256, sl->num_sms * 8);
+        for (int z = 0; z < geo.Z; z++) {
+            const bool same_level = z == 0 || flat;
+            if (same_level) {
+                k_net_level<<<grid, 256, 0, sl->stream>>>(geo, sl->s, z);
+                g->st.kernel_launches++;
+            }
+            for (int it = 0; it < (same_level ? SAME_LEVEL_PASSES : 1); it++) {
+                if (same_level) CG_CUDA(cudaMemsetAsync(sl->cnt + 13, 0, sizeof(unsigned), sl->stream));
+                k_return_level<<<grid, 256, 0, sl->stream>>>(geo, sl->s, z, sl->cnt + 13);
+                g->st.kernel_launches++;
+                if (!same_level) break;
+                CG_CUDA(cudaMemcpyAsync(sl->h_cnt + 13, sl->cnt + 13, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                        sl->stream));
+                CG_CUDA(cudaStreamSynchronize(sl->stream));
+                if (sl->h_cnt[13] == 0) break;
+            }
+        }
+        CG_CUDA(cudaGetLastError());
+    }
+    {
+        // whatever a capped same-level level left (cycles longer than 2) goes back to s by the
+        // generic phase-2 push-relabel (exact; rarely needed)
+        CG_CUDA(cudaMemsetAsync(sl->cnt + 14, 0, sizeof(unsigned), sl->stream));
+        k_count_excess<<<grid_for(geo.n, 256, sl->num_sms * 8), 256, 0, sl->stream>>>(geo, sl->s, sl->cnt + 14);
+        CG_CUDA(cudaMemcpyAsync(sl->h_cnt + 14, sl->cnt + 14, sizeof(unsigned), cudaMemcpyDeviceToHost, sl->stream));
+        CG_CUDA(cudaStreamSynchronize(sl->stream));
+        if (pr_only || sl->h_cnt[14]) {
+            double ms_gr = 0.0;
+            r = pr_loop(g, o, false, ms_gr);
+        }
+    }
     if (r == CG_OK) {
         CG_CUDA(cudaMemsetAsync(sl->flags + 3, 0, sizeof(int), sl->stream));
         k_flow_export<<<grid_for(ncol * 32, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(

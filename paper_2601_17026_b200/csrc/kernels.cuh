@@ -91,6 +91,85 @@ __global__ void k_phase2_setup(Geo g, const int32_t *__restrict__ in, int weight
     }
 }
 
+// Phase 2 by level-ordered flow cancellation.  Every arc that carries flow goes down in z
+// (down arcs, lateral arcs to z - Delta) except the lateral arcs on the same level (z = 0, or
+// Delta_d = 0), so the excess of a vertex at level z is returned by cancelling its inflows:
+// first its source arc (T holds the source-arc flow in phase 2), then the flow from above
+// (D(z+1), moving the excess up to z+1), then the lateral inflows from (nbr, zi(z)) (moving it
+// to level zi(z) >= z).  E(v) = fs(v) + inflow - outflow <= fs(v) + inflow, so the
+// cancellation never runs out.  One launch per level processes every column; levels with
+// same-level arcs repeat until a pass sees no excess there (*left counts vertices with excess).
+__global__ void k_return_level(Geo g, Soa s, int z, unsigned *left) {
+    const int64_t ncol = (int64_t)g.X * g.Y;
+    unsigned myleft = 0;
+    for (int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; col < ncol;
+         col += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = col * g.Z + z;
+        int e = __ldcg(&s.E[v]);
+        if (e <= 0) continue;
+        myleft++;  // excess seen on this level in this pass (same-level passes repeat until none)
+        const int x = (int)(col / g.Y), y = (int)(col - (int64_t)x * g.Y);
+        int taken = 0;
+        auto cancel = [&](int32_t *res, int32_t *eto) {
+            const int r = min(e, *(volatile int32_t *)res);
+            if (r > 0) {
+                atomicSub(res, r);
+                if (eto) atomicAdd(eto, r);
+                e -= r;
+                taken += r;
+            }
+        };
+        cancel(&s.T[v], nullptr);  // back to s
+        if (e > 0 && z + 1 < g.Z) cancel(&s.D[v + 1], &s.E[v + 1]);
+#pragma unroll
+        for (int d = 0; d < 4 && e > 0; d++) {
+            const int64_t o = nbr_off(g, x, y, d);
+            const int zi = zi_of(z, delta_d(g, d), g.Z);
+            if (!o || zi < 0) continue;
+            const int64_t u = col * g.Z + o + zi;
+            if (!owned(g, u)) continue;
+            cancel(&s.L[d ^ 1][u], &s.E[u]);
+        }
+        if (taken) atomicSub(&s.E[v], taken);
+    }
+    myleft = warp_sum_i((int)myleft);
+    if (lane_id() == 0 && myleft) atomicAdd(left, myleft);
+}
+
+// Same-level flow circulations: where the lateral arcs of level z stay on level z (z = 0,
+// or Delta_d = 0), the two antiparallel arcs v -> u and u -> v may both carry flow; netting
+// them removes a 2-cycle without changing any excess (each pair is owned by the vertex on
+// its +x / +y side... i.e. by v for directions d = 0, 2).
+__global__ void k_net_level(Geo g, Soa s, int z) {
+    const int64_t ncol = (int64_t)g.X * g.Y;
+    for (int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; col < ncol;
+         col += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = col * g.Z + z;
+        const int x = (int)(col / g.Y), y = (int)(col - (int64_t)x * g.Y);
+#pragma unroll
+        for (int d = 0; d < 4; d += 2) {
+            if (zo_of(z, delta_d(g, d)) != z) continue;  // the arc leaves the level
+            const int64_t o = nbr_off(g, x, y, d);
+            if (!o || !owned(g, v + o)) continue;
+            const int a = s.L[d][v], b = s.L[d ^ 1][v + o];
+            const int m = min(a, b);
+            if (m > 0) {
+                s.L[d][v] = a - m;
+                s.L[d ^ 1][v + o] = b - m;
+            }
+        }
+    }
+}
+
+// vertices still holding excess -> *count
+__global__ void k_count_excess(Geo g, const Soa s, unsigned *count) {
+    unsigned c = 0;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < g.n; v += (int64_t)gridDim.x * blockDim.x)
+        c += s.E[v] != 0;
+    c = warp_sum_i((int)c);
+    if (lane_id() == 0 && c) atomicAdd(count, c);
+}
+
 // out planes (int32[7][n]): s->v, v->t, down v->v-1, lateral +x, -x, +y, -y.  Any vertex left
 // with excess sets *bad (the result would not be a flow).
 __global__ void k_flow_export(Geo g, const int32_t *__restrict__ in, int weight_mode, Soa s,

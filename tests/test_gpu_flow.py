@@ -171,3 +171,15 @@ def test_flow_errors(cg):
         assert cg.maxflow_export_flow(h, torch.zeros((4, 2, 3), dtype=torch.int32, device="cuda"))[0] == cg.CG_E_INVAL
     finally:
         cg.colgraph_free(h)
+
+
+def test_flow_generic_phase2(cg, monkeypatch):
+    """The generic phase 2 (push-relabel toward s; the fallback after capped same-level
+    cancellation) gives a valid maximum flow too."""
+    monkeypatch.setenv("CG_PHASE2_PR", "1")
+    for seed in range(1000, 1100):
+        c, delta = V.tiny_case(seed)
+        o = oracle.colgraph_solve(c, delta)
+        flow, F = export(cg, c, delta)
+        val, mask = check_flow(c, delta, F)
+        assert flow == val == o["flow"] and np.array_equal(mask, o["mask"]), seed
