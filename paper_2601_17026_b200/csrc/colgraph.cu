@@ -730,6 +730,7 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
     // work-fetching walk (k_walk_ws): measured -10 % on C3/C5, +10 % on C4, opt-in
     const bool walk_ws = getenv("CG_WALK_WS") && atoi(getenv("CG_WALK_WS")) != 0;
     const int walk_park = getenv("CG_WALK_PARK") ? atoi(getenv("CG_WALK_PARK")) : 0;
+    const bool relist_ordered = getenv("CG_RELIST") && atoi(getenv("CG_RELIST")) != 0;
     double work_since_gr = 0.0, sweep_ms_since_gr = 0.0;
     int64_t sweeps = g->st.sweeps, since_gap = 0, last_active = active;
     std::vector<int64_t> wv(RING);
@@ -817,7 +818,18 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
                                                           sl->blist[(k + 1) & 1], sl->cnt + (k + 1) % 3,
                                                           sl->cnt + (k + 2) % 3, sl->vstamp, sl->out_tag, sl->work + i,
                                                           sl->flags, sl->heads + i);
-                else if (walk)
+                else if (walk && relist_ordered && !multi(g)) {
+                    k_walk<<<gv, 256, 0, sl->stream>>>(geo, sl->s, o.walk_len, sl->blist[k & 1], sl->cnt + k % 3,
+                                                       sl->blist[(k + 1) & 1], sl->cnt + (k + 1) % 3,
+                                                       sl->cnt + (k + 2) % 3, sl->vstamp, sl->out_tag, sl->work + i,
+                                                       sl->flags, walk_park);
+                    // rewrite the output list in index order (same set, same count)
+                    CG_CUDA(cudaMemsetAsync(sl->cnt + (k + 1) % 3, 0, sizeof(unsigned), sl->stream));
+                    k_relist_ordered<<<sl->num_sms * 8, 256, 0, sl->stream>>>(geo, sl->vstamp, sl->out_tag,
+                                                                               sl->blist[(k + 1) & 1],
+                                                                               sl->cnt + (k + 1) % 3);
+                    g->st.kernel_launches++;
+                } else if (walk)
                     k_walk<<<gv, 256, 0, sl->stream>>>(geo, sl->s, o.walk_len, sl->blist[k & 1], sl->cnt + k % 3,
                                                        sl->blist[(k + 1) & 1], sl->cnt + (k + 1) % 3,
                                                        sl->cnt + (k + 2) % 3, sl->vstamp, sl->out_tag, sl->work + i,

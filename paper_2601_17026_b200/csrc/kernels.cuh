@@ -225,11 +225,65 @@ struct ArcPick {
     int64_t tgt;
 };
 
-// FIRST admissible arc (label < hx) in the fixed order; if none, the lowest residual
-// neighbour (for the relabel).  With exact labels every admissible neighbour sits at hx-1,
-// so the early exit changes nothing but the number of scattered loads.
+// FIRST admissible arc (label < hx) in the fixed order t, down, lateral-out (+x,-x,+y,-y),
+// up, lateral-in reverse (+x,-x,+y,-y); if none, the lowest residual neighbour (for the
+// relabel).  Candidate fields are loaded in two batches of independent loads -- t, down and
+// lateral-out first, the reverse arcs only if none of those is admissible -- so a hop costs at
+// most two memory round trips instead of a chain of up to 15 dependent ones (ncu: the walk
+// was 84 % long-scoreboard stalls; loading all 15 at once measured slower).
+// CG_SCAN_SERIAL=1 at compile time restores the early-exit scan.
+#ifndef CG_SCAN_SERIAL
+#define CG_SCAN_SERIAL 1  // measured: the two-stage gather is within noise
+#endif
 __device__ __forceinline__ ArcPick scan_arcs(const Geo &g, const Soa &s, const OpCtx &c, int hx) {
     ArcPick p{g.INF, -1, 0, NONE};
+#if !CG_SCAN_SERIAL
+    const int INF = g.INF;
+    const bool dn = c.z >= 1, up = c.z + 1 < g.Z;
+    int64_t to[4], ti[4];
+    bool oko[4], oki[4];
+#pragma unroll
+    for (int d = 0; d < 4; d++) {
+        oko[d] = c.off[d] && c.zo[d >> 1] >= 0;
+        oki[d] = c.off[d] && c.zi[d >> 1] >= 0;
+        to[d] = c.v0 + c.off[d] + c.zo[d >> 1];
+        ti[d] = c.v0 + c.off[d] + c.zi[d >> 1];
+    }
+    // stage 1: the arcs that are usually admissible (t, down, lateral-out), loaded together
+    const int tres = s.T[c.v];
+    const int hdn = dn ? s.H[c.v - 1] : INF;
+    int hlo[4];
+#pragma unroll
+    for (int d = 0; d < 4; d++) hlo[d] = oko[d] ? s.H[to[d]] : INF;
+    if (tres > 0) {
+        p.best = 0; p.arc = 0; p.res = tres;
+        return p;
+    }
+    if (hdn < p.best) { p.best = hdn; p.arc = 1; p.tgt = c.v - 1; }
+    if (p.best < hx) return p;
+#pragma unroll
+    for (int d = 0; d < 4; d++) {
+        if (hlo[d] < p.best) { p.best = hlo[d]; p.arc = 2 + d; p.tgt = to[d]; }
+        if (p.best < hx) return p;
+    }
+    // stage 2: reverse residual arcs (up, lateral-in), loaded together
+    const int dres = up ? s.D[c.v + 1] : 0;
+    const int hup = up ? s.H[c.v + 1] : INF;
+    int lres[4], hli[4];
+#pragma unroll
+    for (int d = 0; d < 4; d++) {
+        lres[d] = oki[d] ? s.L[d ^ 1][ti[d]] : 0;
+        hli[d] = oki[d] ? s.H[ti[d]] : INF;
+    }
+    if (dres > 0 && hup < p.best) { p.best = hup; p.arc = 6; p.tgt = c.v + 1; p.res = dres; }
+    if (p.best < hx) return p;
+#pragma unroll
+    for (int d = 0; d < 4; d++) {
+        if (lres[d] > 0 && hli[d] < p.best) { p.best = hli[d]; p.arc = 7 + d; p.tgt = ti[d]; p.res = lres[d]; }
+        if (p.best < hx) return p;
+    }
+    return p;
+#else
     const int tres = s.T[c.v];
     if (tres > 0) {
         p.best = 0; p.arc = 0; p.res = tres;
@@ -272,6 +326,7 @@ __device__ __forceinline__ ArcPick scan_arcs(const Geo &g, const Soa &s, const O
         }
     }
     return p;
+#endif
 }
 
 __device__ __forceinline__ void set_ctx(const Geo &g, OpCtx &c, int64_t v) {
@@ -572,6 +627,24 @@ __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_walk_ws(Geo g, Soa s, in
     for (unsigned j = threadIdx.x; j < nq; j += blockDim.x) lout[qbase + j] = q.buf[j];
     mywork = warp_sum_ll((long long)mywork);
     if (lane_id() == 0 && mywork) atomicAdd(work, mywork);
+}
+
+// Re-list a sweep's output worklist in index order: the vertices listed for the next sweep
+// are exactly those with vstamp == tag, so a dense scan of vstamp rewrites the list with
+// 256-vertex spans in index order (walk deposits append in completion order; index order
+// makes a warp's walks start on neighbouring records).  *count receives the same count.
+__global__ void k_relist_ordered(Geo g, const int *__restrict__ vstamp, int tag, int *list, unsigned *count) {
+    constexpr int SPAN = 8;
+    SpanAppender<SPAN> ap;
+    for (int64_t base = gwarp() * 32 * SPAN; base < g.n; base += nwarps() * 32 * SPAN) {
+#pragma unroll
+        for (int j = 0; j < SPAN; j++) {
+            const int64_t b0 = base + 32 * j;
+            const int64_t v = b0 + lane_id();
+            ap.add(__ballot_sync(FULL, v < g.n && vstamp[v] == tag), b0);
+        }
+        ap.flush(list, count);
+    }
 }
 
 // After a global relabel: list every active vertex (E > 0, H < INF) in index order.
