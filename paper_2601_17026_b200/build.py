@@ -51,6 +51,8 @@ def build(force: bool = False, verbose: bool = False, lib: str = LIB, defines=()
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv))
+    if "--debug-bounds" in sys.argv:
+        print(build(force=True, lib=os.path.join(PKG, "libcolgraph_dbg.so"), defines=("CG_DEBUG_BOUNDS=1",)))
     if "--serial-scan" in sys.argv:
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_serial.so"), defines=("CG_SCAN_SERIAL=1",)))
     if "--soa" in sys.argv:

@@ -150,6 +150,20 @@ struct DeviceGuard {
         if (s_ != CG_OK) return s_;  \
     } while (0)
 
+// CG_DEBUG_BOUNDS builds: CG_E_CUDA if any kernel indexed state out of range
+inline cg_status debug_check(cg_status s) {
+#ifdef CG_DEBUG_BOUNDS
+    unsigned long long oob = 0;
+    cudaDeviceSynchronize();
+    if (cudaMemcpyFromSymbol(&oob, g_oob, sizeof(oob)) != cudaSuccess) return CG_E_CUDA;
+    if (oob) {
+        fprintf(stderr, "colgraph: %llu out-of-range state accesses\n", oob);
+        return CG_E_CUDA;
+    }
+#endif
+    return s;
+}
+
 inline int grid_for(int64_t n, int block, int cap) {
     int64_t b = (n + block - 1) / block;
     if (b < 1) b = 1;
@@ -254,10 +268,10 @@ cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode) {
 #if CG_LAYOUT_AOS
     int32_t *rec = carve<int32_t>(p, 8 * plane) + 8 * geo.YZ;  // owned plane x = 0
     Field fl[8];
-    for (int i = 0; i < 8; i++) fl[i] = Field{rec + i};
+    for (int i = 0; i < 8; i++) fl[i] = Field{rec + i, -geo.YZ, geo.n + geo.YZ};
 #else
     Field fl[8];
-    for (int i = 0; i < 8; i++) fl[i] = Field{carve<int32_t>(p, plane) + geo.YZ};
+    for (int i = 0; i < 8; i++) fl[i] = Field{carve<int32_t>(p, plane) + geo.YZ, -geo.YZ, geo.n + geo.YZ};
 #endif
     sl->s.E = fl[0];
     sl->s.H = fl[1];
@@ -1022,7 +1036,7 @@ static cg_status build_common(const cg_dims *dims, const int32_t *cost_dev, int3
     return CG_OK;
 }
 
-cg_status colgraph_build(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight, const cg_dist *dist,
+static cg_status colgraph_build_impl(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight, const cg_dist *dist,
                          cg_graph **out) {
     cg_dist dd{0, 1, nullptr, 0, nullptr};
     if (dist) dd = *dist;
@@ -1030,13 +1044,23 @@ cg_status colgraph_build(const cg_dims *dims, const int32_t *cost_dev, int32_t i
     return build_common(dims, cost_dev, input_is_weight, &dd, dd.nranks, dd.rank, 1, false, out);
 }
 
-cg_status colgraph_build_slabs(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight, int32_t nslabs,
+cg_status colgraph_build(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight, const cg_dist *dist,
+                         cg_graph **out) {
+    return debug_check(colgraph_build_impl(dims, cost_dev, input_is_weight, dist, out));
+}
+
+static cg_status colgraph_build_slabs_impl(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight, int32_t nslabs,
                                const cg_dist *dist, cg_graph **out) {
     if (nslabs < 1) return CG_E_INVAL;
     return build_common(dims, cost_dev, input_is_weight, dist, nslabs, 0, nslabs, true, out);
 }
 
-cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_value, cg_solve_stats *stats) {
+cg_status colgraph_build_slabs(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight, int32_t nslabs,
+                               const cg_dist *dist, cg_graph **out) {
+    return debug_check(colgraph_build_slabs_impl(dims, cost_dev, input_is_weight, nslabs, dist, out));
+}
+
+static cg_status maxflow_solve_impl(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_value, cg_solve_stats *stats) {
     if (!g || !flow_value) return CG_E_INVAL;
     if (g->solved) return CG_E_STATE;
     DeviceGuard dg(g->dist.device);
@@ -1088,7 +1112,11 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
     return result;
 }
 
-cg_status mincut_extract_surface(cg_graph *g, int32_t *surface_dev, uint8_t *mask_dev) {
+cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_value, cg_solve_stats *stats) {
+    return debug_check(maxflow_solve_impl(g, opts, flow_value, stats));
+}
+
+static cg_status mincut_extract_surface_impl(cg_graph *g, int32_t *surface_dev, uint8_t *mask_dev) {
     if (!g || !surface_dev) return CG_E_INVAL;
     if (!g->solved || g->exported) return CG_E_STATE;
     DeviceGuard dg(g->dist.device);
@@ -1180,7 +1208,11 @@ cg_status mincut_extract_surface(cg_graph *g, int32_t *surface_dev, uint8_t *mas
     return e64 ? CG_E_EMPTY_COLUMN : CG_OK;
 }
 
-cg_status maxflow_export_flow(cg_graph *g, const int32_t *cost_dev, int32_t input_is_weight, const cg_solve_opts *opts,
+cg_status mincut_extract_surface(cg_graph *g, int32_t *surface_dev, uint8_t *mask_dev) {
+    return debug_check(mincut_extract_surface_impl(g, surface_dev, mask_dev));
+}
+
+static cg_status maxflow_export_flow_impl(cg_graph *g, const int32_t *cost_dev, int32_t input_is_weight, const cg_solve_opts *opts,
                               int32_t *flow_dev) {
     if (!g || !cost_dev || !flow_dev) return CG_E_INVAL;
     if (!g->solved || g->exported) return CG_E_STATE;
@@ -1258,6 +1290,11 @@ cg_status maxflow_export_flow(cg_graph *g, const int32_t *cost_dev, int32_t inpu
     CG_CUDA(cudaStreamSynchronize(sl->stream));
     g->exported = true;
     return r;
+}
+
+cg_status maxflow_export_flow(cg_graph *g, const int32_t *cost_dev, int32_t input_is_weight, const cg_solve_opts *opts,
+                              int32_t *flow_dev) {
+    return debug_check(maxflow_export_flow_impl(g, cost_dev, input_is_weight, opts, flow_dev));
 }
 
 cg_status colgraph_stats(const cg_graph *g, cg_solve_stats *stats) {

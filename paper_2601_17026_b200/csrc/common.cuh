@@ -40,10 +40,30 @@ struct Geo {
 #endif
 constexpr int FIELD_STRIDE = CG_LAYOUT_AOS ? 8 : 1;
 
+// CG_DEBUG_BOUNDS (debug build, `build --debug-bounds`): every state access checks its vertex
+// index against the slab's range including the ghost planes, [-YZ, n + YZ); a violation
+// increments g_oob and is clamped (no fault), and every API call then returns CG_E_CUDA.
+// compute-sanitizer is closed on this pool: this is the bad-access check.
+#ifdef CG_DEBUG_BOUNDS
+__device__ unsigned long long g_oob;
 struct Field {
     int32_t *p;
+    int64_t lo, hi;
+    __device__ __forceinline__ int32_t &operator[](int64_t i) const {
+        if (i < lo || i >= hi) {
+            atomicAdd(&g_oob, 1ull);
+            i = lo;
+        }
+        return p[i * FIELD_STRIDE];
+    }
+};
+#else
+struct Field {
+    int32_t *p;
+    int64_t lo, hi;  // valid vertex range (checked only in CG_DEBUG_BOUNDS builds)
     __device__ __forceinline__ int32_t &operator[](int64_t i) const { return p[i * FIELD_STRIDE]; }
 };
+#endif
 
 struct Soa {
     Field E, H, T, D;

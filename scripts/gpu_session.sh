@@ -1,4 +1,3 @@
 set -x
-timeout 60 python __graft_entry__.py smoke > gpurun_out/t_smoke.log 2>&1 || exit 1
-timeout 900 python scripts/ab.py C3,C4,C5 3 'base:' 'relist:CG_RELIST=1' > gpurun_out/t_ab.log 2>&1
-CG_RELIST=1 timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "tiny or c1 or c2 or full_size" > gpurun_out/t_tests.log 2>&1 || exit 3
+CG_LIB=paper_2601_17026_b200/libcolgraph_dbg.so timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/t_dbg_tests.log 2>&1
+echo rc=$? >> gpurun_out/t_dbg_tests.log
