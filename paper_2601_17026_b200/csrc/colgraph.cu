@@ -63,6 +63,7 @@ struct Slab {
     unsigned long long *work = nullptr;  // [RING] operations per sweep
     unsigned long long *visits = nullptr;  // [RING] tile visits per phase
     unsigned *heads = nullptr;             // [RING] work-fetch cursors of k_walk_ws
+    unsigned *visited = nullptr;           // [n/32 + 1] BFS visited bitmap (persistent BFS)
     unsigned long long *u64 = nullptr;   // [0]=N [1]=sumT0 [2]=sumT [3]=active [4]=gap lifted [5]=scratch
     int *flags = nullptr;                // [0]=overflow [1]=maxh [2]=gap [3]=empty
     int32_t *snap[2] = {nullptr, nullptr};   // ghost lateral residual at the last refresh
@@ -224,7 +225,7 @@ size_t workspace_bytes(const Geo &geo) {
          al(sizeof(int) * 16);
     b += 4 * al(sizeof(int32_t) * geo.YZ) + 4 * al(sizeof(int32_t) * 4 * std::max<int64_t>(geo.YZ, 2 * geo.Y));
     b += 5 * al(sizeof(int) * ncol) + al(sizeof(unsigned) * 4) + al(sizeof(unsigned long long) * RING) +
-         al(sizeof(unsigned long long) * 16) + al(sizeof(unsigned) * RING);
+         al(sizeof(unsigned long long) * 16) + al(sizeof(unsigned) * RING) + al(sizeof(unsigned) * (geo.n / 32 + 1));
     return b;
 }
 
@@ -299,6 +300,7 @@ cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode) {
     sl->tl.prof = carve<unsigned long long>(p, 16);
     sl->visits = carve<unsigned long long>(p, RING);
     sl->heads = carve<unsigned>(p, RING);
+    sl->visited = carve<unsigned>(p, n / 32 + 1);
     for (int side = 0; side < 2; side++) {
         sl->snap[side] = carve<int32_t>(p, geo.YZ);
         sl->hold[side] = carve<int32_t>(p, geo.YZ);
@@ -413,7 +415,7 @@ void k_fill_ghost_h(Slab *sl) {
 }
 
 // Strict level-synchronous BFS of one slab without neighbours (the single-GPU path).
-cg_status bfs_strict(cg_graph *g, Slab *sl) {
+cg_status bfs_strict(cg_graph *g, Slab *sl, bool allow_coop = true) {
     const Geo &geo = sl->geo;
     cudaStream_t st = sl->stream;
     CG_CUDA(cudaMemsetAsync(sl->bst, 0, sizeof(BfsState), st));
@@ -425,13 +427,15 @@ cg_status bfs_strict(cg_graph *g, Slab *sl) {
     CG_CUDA(cudaMemcpyAsync(&sl->bst->L, &sl->h_bst->L, sizeof(int), cudaMemcpyHostToDevice, st));
     CG_CUDA(cudaMemcpyAsync(&sl->bst->bu_alpha, &sl->h_bst->bu_alpha, 2 * sizeof(int) + sizeof(unsigned),
                             cudaMemcpyHostToDevice, st));
-    k_bfs_init<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, st>>>(geo, sl->s, sl->blist[0], &sl->bst->cnt[0]);
+    const bool coop = allow_coop && sl->bfs_coop_grid > 0;
+    k_bfs_init<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, st>>>(geo, sl->s, sl->blist[0], &sl->bst->cnt[0],
+                                                                        coop ? sl->visited : nullptr);
     k_bfs_seeded<<<1, 1, 0, st>>>(sl->bst);
     g->st.kernel_launches += 2;
     int L = 1;
-    if (sl->bfs_coop_grid > 0) {  // every level in one cooperative launch (k_bfs_run)
+    if (coop) {  // every level in one cooperative launch (k_bfs_run)
         void *args[] = {(void *)&sl->geo, (void *)&sl->s, (void *)&sl->blist[0], (void *)&sl->blist[1],
-                        (void *)&sl->bst};
+                        (void *)&sl->bst, (void *)&sl->visited};
         CG_CUDA(cudaLaunchCooperativeKernel((const void *)k_bfs_run, sl->bfs_coop_grid, 512, args, 0, st));
         g->st.kernel_launches++;
         CG_CUDA(cudaMemcpyAsync(sl->h_bst, sl->bst, sizeof(BfsState), cudaMemcpyDeviceToHost, st));

@@ -678,7 +678,10 @@ __global__ void k_rebuild_vertices(Geo g, const Soa s, int *lout, unsigned *cout
 //   u = (x,y,z-1)             up arc, residual D(v)
 //   u = (nbr, zi(z))          lateral arc of u into v, infinite
 //   u = (nbr_d, zo(z))        reverse of v's lateral arc in direction d, residual L_d(v)
-__global__ void k_bfs_init(Geo g, Soa s, int *lout, unsigned *cout) {
+// visited: nullable bitmap (1 bit per owned vertex, word = 32 consecutive vertices) written
+// whole here -- the persistent BFS claims through it (bfs_expand_multi) so that testing a
+// candidate hits an L2-resident word instead of the candidate's DRAM record.
+__global__ void k_bfs_init(Geo g, Soa s, int *lout, unsigned *cout, unsigned *visited = nullptr) {
     constexpr int SPAN = 8;
     SpanAppender<SPAN> ap;
     for (int64_t base = gwarp() * 32 * SPAN; base < g.n; base += nwarps() * 32 * SPAN) {
@@ -691,7 +694,9 @@ __global__ void k_bfs_init(Geo g, Soa s, int *lout, unsigned *cout) {
                 seed = s.T[v] > 0;
                 s.H[v] = seed ? 1 : g.INF;
             }
-            ap.add(__ballot_sync(FULL, seed), b0);
+            const unsigned m = __ballot_sync(FULL, seed);
+            if (visited && lane_id() == 0 && b0 < g.n) visited[b0 >> 5] = m;
+            ap.add(m, b0);
         }
         ap.flush(lout, cout);
     }
@@ -801,7 +806,7 @@ __device__ __forceinline__ void load_DL(const Soa &s, int v, int &D, int (&L)[4]
 
 template <int R>
 __device__ __forceinline__ void bfs_expand_multi(const Geo &g, const Soa &s, int nl, const int (&vv)[R], int *lout,
-                                                 unsigned *cout) {
+                                                 unsigned *cout, unsigned *visited) {
     const int INF = g.INF;
     int w[R][10], hw[R][10];
     unsigned cand[R], got[R];
@@ -830,18 +835,24 @@ __device__ __forceinline__ void bfs_expand_multi(const Geo &g, const Soa &s, int
             if (zo >= 0 && L[d] > 0 && owned(g, v0 + o + zo)) { w[r][6 + d] = v0 + o + zo; cand[r] |= 1u << (6 + d); }
         }
     }
+    // visited words (L2-resident bitmap): hw = 1 if the candidate is already labelled
 #pragma unroll
     for (int r = 0; r < R; r++)
 #pragma unroll
-        for (int j = 0; j < 10; j++) hw[r][j] = (cand[r] >> j & 1u) ? __ldcg(&s.H[w[r][j]]) : 0;
+        for (int j = 0; j < 10; j++)
+            hw[r][j] = (cand[r] >> j & 1u) ? (int)((__ldcg(&visited[w[r][j] >> 5]) >> (w[r][j] & 31)) & 1u) : 1;
     int k = 0;
 #pragma unroll
     for (int r = 0; r < R; r++)
 #pragma unroll
         for (int j = 0; j < 10; j++)
-            if ((cand[r] >> j & 1u) && hw[r][j] >= INF && atomicCAS(&s.H[w[r][j]], INF, nl) == INF) {
-                got[r] |= 1u << j;
-                k++;
+            if (!hw[r][j]) {
+                const unsigned bit = 1u << (w[r][j] & 31);
+                if (!(atomicOr(&visited[w[r][j] >> 5], bit) & bit)) {  // claimed: this lane owns w's label
+                    s.H[w[r][j]] = nl;
+                    got[r] |= 1u << j;
+                    k++;
+                }
             }
     const int incl = warp_incl_scan(k);
     const int total = __shfl_sync(FULL, incl, 31);
@@ -892,7 +903,8 @@ __global__ void k_bfs_seeded(BfsState *st) { st->claimed = st->cnt[0]; }
 // instead of ~15 scattered sectors per frontier vertex (Beamer's direction optimisation).
 // Race-free: u is written only by its own lane, and a vertex written L+1 during the level
 // is never read as L by another lane.
-__device__ __forceinline__ void bfs_bottom_up_level(const Geo &g, const Soa &s, int L, int *lout, unsigned *cout) {
+__device__ __forceinline__ void bfs_bottom_up_level(const Geo &g, const Soa &s, int L, int *lout, unsigned *cout,
+                                                    unsigned *visited = nullptr) {
     constexpr int SPAN = 4;
     SpanAppender<SPAN> ap;
     const int64_t nchunks = g.nchunks;
@@ -924,7 +936,10 @@ __device__ __forceinline__ void bfs_bottom_up_level(const Geo &g, const Soa &s, 
                             else if (zi >= 0 && s.L[d ^ 1][v0 + o + zi] > 0 && __ldcg(&s.H[v0 + o + zi]) == L) hit = true;
                         }
                     }
-                    if (hit) s.H[u] = L + 1;
+                    if (hit) {
+                        s.H[u] = L + 1;
+                        if (visited) atomicOr(&visited[u >> 5], 1u << (u & 31));
+                    }
                 }
             }
             ap.add(__ballot_sync(FULL, hit), b0);
@@ -1027,7 +1042,8 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks) {
 #ifndef CG_BFS_RUN_MINB
 #define CG_BFS_RUN_MINB 1
 #endif
-__global__ void __launch_bounds__(512, CG_BFS_RUN_MINB) k_bfs_run(Geo g, Soa s, int *list0, int *list1, BfsState *st) {
+__global__ void __launch_bounds__(512, CG_BFS_RUN_MINB) k_bfs_run(Geo g, Soa s, int *list0, int *list1, BfsState *st,
+                                                                  unsigned *visited) {
     unsigned *bar = st->bar;
     int L = *(volatile int *)&st->L;
     unsigned long long claimed = *(volatile unsigned long long *)&st->claimed;
@@ -1059,7 +1075,7 @@ __global__ void __launch_bounds__(512, CG_BFS_RUN_MINB) k_bfs_run(Geo g, Soa s, 
                             const unsigned jj = base + r * 32 + lane_id();
                             vv[r] = jj < c ? __ldcg(&lin[jj]) : -1;
                         }
-                        bfs_expand_multi<BFS_R>(g, s, L + 1, vv, lout, &st->cnt[(j + 1) % 3]);
+                        bfs_expand_multi<BFS_R>(g, s, L + 1, vv, lout, &st->cnt[(j + 1) % 3], visited);
                     }
                     __syncthreads();
                     ++L;
@@ -1091,14 +1107,14 @@ __global__ void __launch_bounds__(512, CG_BFS_RUN_MINB) k_bfs_run(Geo g, Soa s, 
                         (unsigned long long)count * (unsigned long long)st->bu_beta > (unsigned long long)g.n;
         if (bu) {
             if (blockIdx.x == 0 && threadIdx.x == 0) st->hist[7]++;
-            bfs_bottom_up_level(g, s, L, lout, &st->cnt[(i + 1) % 3]);
+            bfs_bottom_up_level(g, s, L, lout, &st->cnt[(i + 1) % 3], visited);
         } else {
             // few vertices per warp: spread them (R = 1); many: R per lane for load-level parallelism
             if ((int64_t)count < nwarps() * 32 * BFS_R) {
                 for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {
                     const int64_t j = base + lane_id();
                     int vv[1] = {j < count ? __ldcg(&lin[j]) : -1};
-                    bfs_expand_multi<1>(g, s, L + 1, vv, lout, &st->cnt[(i + 1) % 3]);
+                    bfs_expand_multi<1>(g, s, L + 1, vv, lout, &st->cnt[(i + 1) % 3], visited);
                 }
             } else {
                 for (int64_t base = gwarp() * 32 * BFS_R; base < count; base += nwarps() * 32 * BFS_R) {
@@ -1108,7 +1124,7 @@ __global__ void __launch_bounds__(512, CG_BFS_RUN_MINB) k_bfs_run(Geo g, Soa s, 
                         const int64_t j = base + r * 32 + lane_id();
                         vv[r] = j < count ? __ldcg(&lin[j]) : -1;
                     }
-                    bfs_expand_multi<BFS_R>(g, s, L + 1, vv, lout, &st->cnt[(i + 1) % 3]);
+                    bfs_expand_multi<BFS_R>(g, s, L + 1, vv, lout, &st->cnt[(i + 1) % 3], visited);
                 }
             }
         }

@@ -33,7 +33,8 @@ for name in sys.argv[1].split(","):
     s = r["stats"]
     print(json.dumps({"config": name, "flow": r["flow"], "med_ms": round(statistics.median(ts), 1), "all": [round(t) for t in ts],
                       "min_ms": round(min(ts), 1), "sweeps": s["sweeps"], "grs": s["global_relabels"],
-                      "ms_gr": round(s["ms_global_relabel"], 1), "ms_sw": round(s["ms_sweep_kernels"], 1)}), flush=True)
+                      "ms_gr": round(s["ms_global_relabel"], 1), "ms_sw": round(s["ms_sweep_kernels"], 1),
+                      "ns_per_op": round(1e6 * s["ms_sweep_kernels"] / max(1, s["work"]), 3)}), flush=True)
 '''.replace("ROOT", repr(ROOT))
 
 cfgs, reps = sys.argv[1], sys.argv[2]
@@ -48,7 +49,7 @@ for var in sys.argv[3:]:
     for line in out.stdout.splitlines():
         d = json.loads(line)
         print(f"{name:12s} {d['config']} flow={d['flow']} med={d['med_ms']} all={d['all']} sweeps={d['sweeps']} "
-              f"grs={d['grs']} gr_ms={d['ms_gr']} sw_ms={d['ms_sw']}", flush=True)
+              f"grs={d['grs']} gr_ms={d['ms_gr']} sw_ms={d['ms_sw']} ns/op={d['ns_per_op']}", flush=True)
     if out.returncode:
         print(name, "FAILED", out.stderr[-2000:])
     elif os.environ.get("AB_VERBOSE"):
