@@ -60,6 +60,10 @@ def _load():
         lib.oracle_colgraph_solve.restype = ctypes.c_int
         lib.oracle_colgraph_solve.argtypes = [i32p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                               ctypes.c_int, ctypes.c_int, ctypes.c_int, i64p, i32p, u8p, i32p, i64p]
+        lib.oracle_colgraph_solve_soft.restype = ctypes.c_int
+        lib.oracle_colgraph_solve_soft.argtypes = [i32p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                   ctypes.c_int, i32p, ctypes.c_int, ctypes.c_int, ctypes.c_int, i64p,
+                                                   i32p, u8p, i32p, i64p]
         lib.oracle_graph_maxflow.restype = ctypes.c_int
         lib.oracle_graph_maxflow.argtypes = [ctypes.c_int, ctypes.c_int, i32p, i32p, i64p, ctypes.c_int,
                                              ctypes.c_int, ctypes.c_int, i64p, u8p, i32p]
@@ -72,9 +76,10 @@ def _ptr(a, ct):
 
 
 def colgraph_solve(c: np.ndarray, delta, input_is_weight: bool = False, algo: str = "dinic",
-                   want_mask: bool = True) -> dict:
+                   want_mask: bool = True, penalty=None) -> dict:
     """Solve the column graph of cost (or weight) volume c[X][Y][Z].  delta: int (isotropic)
-    or (delta_x, delta_y).
+    or (delta_x, delta_y).  penalty: optional convex soft-smoothness penalty [f(1), .., f(K)],
+    K >= max(delta) (NEXT-1: finite arcs of capacity f(k+1) - 2 f(k) + f(k-1)).
 
     Returns dict(status, flow, surface[X,Y] int32, mask[X,Y,Z] uint8 or None,
     checks (bit set), n_arcs).
@@ -88,7 +93,10 @@ def colgraph_solve(c: np.ndarray, delta, input_is_weight: bool = False, algo: st
     checks = np.zeros(1, np.int32)
     n_arcs = np.zeros(1, np.int64)
     dx, dy = (int(delta[0]), int(delta[1])) if isinstance(delta, (tuple, list)) else (int(delta), -1)
-    st = lib.oracle_colgraph_solve(_ptr(c, ctypes.c_int32), X, Y, Z, dx, dy, int(bool(input_is_weight)),
+    pen = np.ascontiguousarray(penalty, dtype=np.int32) if penalty is not None else None
+    st = lib.oracle_colgraph_solve_soft(_ptr(c, ctypes.c_int32), X, Y, Z, dx, dy,
+                                   _ptr(pen, ctypes.c_int32) if pen is not None else None,
+                                   len(pen) if pen is not None else 0, int(bool(input_is_weight)),
                                    ALGOS[algo], _ptr(flow, ctypes.c_int64), _ptr(surface, ctypes.c_int32),
                                    _ptr(mask, ctypes.c_uint8) if want_mask else None,
                                    _ptr(checks, ctypes.c_int32), _ptr(n_arcs, ctypes.c_int64))

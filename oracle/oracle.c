@@ -117,6 +117,21 @@ static void column_weights(const int32_t *c, int64_t Z, int64_t col, int64_t *w)
 /* Inter-column arcs (x,y,z) -> (x',y',max(0,z-Delta_d)): the edge interval toward the
  * adjacent column in direction d, Delta_x for the x-neighbours and Delta_y for
  * the y-neighbours (Delta_x = Delta_y is the paper's isotropic case). */
+/* Soft smoothness (VCE-weight net surface): a convex
+ * penalty f(d) for |S(p) - S(q)| = d adds finite arcs (x,y,z) -> (x',y',z-k), k = 0..Delta_d-1,
+ * z-k >= 0, with capacity c_0 = f(1), c_k = f(k+1) - 2f(k) + f(k-1): the arc is cut for
+ * (d - k)_+ values of z, so the cut cost of the pair telescopes to f(d).
+ * penalty[i] = f(i+1), npenalty >= max(Delta_x, Delta_y); NULL = hard constraint only. */
+static const int32_t *g_penalty = NULL;
+static int g_npenalty = 0;
+
+static int64_t soft_cap(int k) {
+    const int64_t f1 = g_penalty[k];                         /* f(k+1) */
+    const int64_t f0 = k >= 1 ? g_penalty[k - 1] : 0;        /* f(k) */
+    const int64_t fm = k >= 2 ? g_penalty[k - 2] : 0;        /* f(k-1) */
+    return k == 0 ? f1 : f1 - 2 * f0 + fm;
+}
+
 static void colgraph_arcs(graph_t *g, int pass, const int32_t *in, int X, int Y, int Z, int delta, int delta_y,
                           int input_is_weight, int64_t *wbuf) {
     const int64_t n = (int64_t)X * Y * Z, s = n, t = n + 1;
@@ -140,6 +155,10 @@ static void colgraph_arcs(graph_t *g, int pass, const int32_t *in, int X, int Y,
                     const int64_t dl = d < 2 ? delta : delta_y;
                     const int64_t zt = z - dl > 0 ? z - dl : 0;
                     add_arc(g, pass, v, (x2 * Y + y2) * Z + zt, OR_INF);
+                    for (int64_t k = 0; g_penalty && k < dl && z - k >= 0; k++) {
+                        const int64_t cap = soft_cap((int)k);
+                        if (cap > 0) add_arc(g, pass, v, (x2 * Y + y2) * Z + z - k, cap);
+                    }
                 }
             }
         }
@@ -314,11 +333,28 @@ static int64_t run_maxflow(graph_t *g, int64_t s, int64_t t, int algo, int *err)
  *   n_arcs_out      number of explicit arcs built (nullable)
  * Returns 0, 1 (invalid dims), 3 (out of memory) or 6 (a column has no source-side vertex).
  */
+int oracle_colgraph_solve_soft(const int32_t *in, int X, int Y, int Z, int delta, int delta_y, const int32_t *penalty,
+                               int npenalty, int input_is_weight, int algo, int64_t *flow_out, int32_t *surface_out,
+                               uint8_t *mask_out, int32_t *checks_out, int64_t *n_arcs_out);
+
 int oracle_colgraph_solve(const int32_t *in, int X, int Y, int Z, int delta, int delta_y, int input_is_weight,
                           int algo, int64_t *flow_out, int32_t *surface_out, uint8_t *mask_out, int32_t *checks_out,
                           int64_t *n_arcs_out) {
+    return oracle_colgraph_solve_soft(in, X, Y, Z, delta, delta_y, NULL, 0, input_is_weight, algo, flow_out,
+                                      surface_out, mask_out, checks_out, n_arcs_out);
+}
+
+int oracle_colgraph_solve_soft(const int32_t *in, int X, int Y, int Z, int delta, int delta_y, const int32_t *penalty,
+                               int npenalty, int input_is_weight, int algo, int64_t *flow_out, int32_t *surface_out,
+                               uint8_t *mask_out, int32_t *checks_out, int64_t *n_arcs_out) {
     if (delta_y == -1) delta_y = delta; /* isotropic */
     if (!in || X < 1 || Y < 1 || Z < 1 || delta < 0 || delta_y < 0) return OR_E_INVAL;
+    if (penalty && npenalty < (delta > delta_y ? delta : delta_y)) return OR_E_INVAL;
+    g_penalty = penalty;
+    g_npenalty = npenalty;
+    if (penalty) /* convex, non-negative capacities */
+        for (int k = 0; k < npenalty; k++)
+            if (soft_cap(k) < 0) return OR_E_INVAL;
     if ((int64_t)X * Y * Z + 2 > INT32_MAX) return OR_E_INVAL;
     const int64_t n = (int64_t)X * Y * Z, s = n, t = n + 1;
     graph_t g;

@@ -13,6 +13,8 @@ reproduce:
     the weights w(0) = c(0) - (sum c + 1), w(z) = c(z) - c(z-1).
   * dp_line -- exact Viterbi DP for Y = 1 (or X = 1) volumes.
   * closed-form cases Delta >= Z-1 (independent columns) and Delta = 0 (flat).
+  * soft smoothness (NEXT-1, PAPER.md:42-43 VCE-weight net surface): brute force and line DP
+    with the cost sum c(x,y,S) + sum over 4-neighbour pairs of f(|S(p) - S(q)|).
   * brute_force_mincut -- all s-t cuts of a small general graph (PAPER.md
     Eq. 6 and Theorem 1), their minimum and the intersection of all minimum
     source sets (the minimal source set).
@@ -69,6 +71,58 @@ def brute_force_surfaces(c: np.ndarray, delta):
     best = cost.min()
     opt = S[cost == best]
     return int(best), opt.min(axis=0).reshape(X, Y).astype(np.int32), int(len(opt)), int(len(S))
+
+
+def soft_penalty_sum(S: np.ndarray, X: int, Y: int, penalty) -> np.ndarray:
+    """sum over 4-neighbour column pairs of f(|S(p) - S(q)|), f(0) = 0, f(d) = penalty[d-1];
+    S: (K, X*Y) top assignments."""
+    f = np.concatenate([[0], np.asarray(penalty, np.int64)])
+    T = S.reshape(-1, X, Y).astype(np.int64)
+    tot = np.zeros(S.shape[0], np.int64)
+    if X > 1:
+        tot += f[np.abs(T[:, 1:, :] - T[:, :-1, :])].sum(axis=(1, 2))
+    if Y > 1:
+        tot += f[np.abs(T[:, :, 1:] - T[:, :, :-1])].sum(axis=(1, 2))
+    return tot
+
+
+def brute_force_soft(c: np.ndarray, delta, penalty):
+    """(min of sum c(S) + sum f(|dS|) over Delta-feasible surfaces, lowest optimal surface)."""
+    X, Y, Z = c.shape
+    S = enumerate_surfaces(X, Y, Z, delta)
+    cols = c.reshape(X * Y, Z).astype(np.int64)
+    cost = cols[np.arange(X * Y)[None, :], S.astype(np.int64)].sum(axis=1) + soft_penalty_sum(S, X, Y, penalty)
+    best = cost.min()
+    opt = S[cost == best]
+    return int(best), opt.min(axis=0).reshape(X, Y).astype(np.int32)
+
+
+def dp_line_soft(cl: np.ndarray, delta: int, penalty):
+    """Viterbi on a line of columns with the soft penalty: (min cost, lowest optimal surface)."""
+    X, Z = cl.shape
+    cl = cl.astype(np.int64)
+    f = np.concatenate([[0], np.asarray(penalty, np.int64)])
+    big = np.iinfo(np.int64).max // 4
+
+    def step(prev):
+        out = np.full(Z, big, np.int64)
+        for d in range(-delta, delta + 1):
+            lo, hi = max(0, -d), min(Z, Z - d)
+            if lo < hi:
+                out[lo:hi] = np.minimum(out[lo:hi], prev[lo + d:hi + d] + f[abs(d)])
+        return out
+
+    F = np.zeros((X, Z), np.int64)
+    B = np.zeros((X, Z), np.int64)
+    F[0] = cl[0]
+    for x in range(1, X):
+        F[x] = cl[x] + step(F[x - 1])
+    B[X - 1] = cl[X - 1]
+    for x in range(X - 2, -1, -1):
+        B[x] = cl[x] + step(B[x + 1])
+    opt = int(F[X - 1].min())
+    through = F + B - cl
+    return opt, np.array([int(np.flatnonzero(through[x] == opt)[0]) for x in range(X)], np.int32)
 
 
 def brute_force_weight_closure(w: np.ndarray, delta):

@@ -247,3 +247,60 @@ def test_aniso_transpose_swaps_deltas():
     b = solve(np.ascontiguousarray(c.transpose(1, 0, 2)), (3, 1))
     assert a["flow"] == b["flow"] and np.array_equal(a["surface"], b["surface"].T)
     assert solve(c, (2, 2))["flow"] == solve(c, 2)["flow"]
+
+
+# ---------------------------------------------------------------- NEXT-1: soft smoothness (convex penalty)
+# VCE-weight net surface: cost sum c(x,y,S) + sum over 4-neighbour pairs of
+# f(|S(p) - S(q)|), f convex with f(0) = 0, |dS| <= Delta still hard.
+
+def _random_convex(rng, K):
+    inc = np.sort(rng.integers(0, 12, K))  # non-decreasing increments -> convex f
+    return np.cumsum(inc).astype(np.int32)
+
+
+def test_soft_random_tiny_bruteforce():
+    rng = np.random.default_rng(51)
+    for trial in range(150):
+        X, Y, Z = int(rng.integers(1, 4)), int(rng.integers(1, 4)), int(rng.integers(1, 8))
+        dx, dy = (int(v) for v in rng.integers(0, 4, 2))
+        pen = _random_convex(rng, max(dx, dy, 1))
+        c = rng.integers(0, (4, 10, 256)[trial % 3], size=(X, Y, Z)).astype(np.int32)
+        best, lowest = pins.brute_force_soft(c, (dx, dy), pen)
+        r = oracle.colgraph_solve(c, (dx, dy), algo="dinic" if trial % 2 else "ek", penalty=pen)
+        assert r["checks"] == oracle.ALL_CHECKS, trial
+        assert r["flow"] == best + pins.k0(c), (trial, r["flow"], best + pins.k0(c))
+        assert np.array_equal(r["surface"], lowest), trial
+
+
+@pytest.mark.parametrize("delta", [1, 3, 6])
+def test_soft_line_dp(delta):
+    rng = np.random.default_rng(52 + delta)
+    pen = _random_convex(rng, delta)
+    c = V.tiny(600 + delta, 40, 1, 14, 255)
+    opt, surf = pins.dp_line_soft(c.reshape(-1, 14), delta, pen)
+    r = solve(c, delta, penalty=pen)
+    assert r["flow"] == opt + pins.k0(c) and np.array_equal(r["surface"].ravel(), surf)
+
+
+def test_soft_zero_penalty_is_hard():
+    c = V.generate("C1")[:6, :5, :]
+    a, b = solve(c, 2), solve(c, 2, penalty=[0, 0])
+    assert a["flow"] == b["flow"] and np.array_equal(a["mask"], b["mask"])
+
+
+def test_soft_linear_penalty_limit():
+    """A penalty steeper than any cost difference forces a flat-in-pairs optimum: with
+    f(d) = M*d and M > 255*Z the optimal surface is flat (every |dS| >= 1 costs more than any
+    column can save)."""
+    c = V.tiny(77, 4, 3, 9, 255)
+    M = 255 * 9 + 1
+    r = solve(c, 3, penalty=[M, 2 * M, 3 * M])
+    tot = c.astype(np.int64).sum(axis=(0, 1))
+    assert (r["surface"] == int(tot.argmin())).all()
+    assert r["flow"] == int(tot.min()) + pins.k0(c)
+
+
+def test_soft_rejects_nonconvex():
+    c = np.zeros((2, 2, 4), np.int32)
+    assert oracle.colgraph_solve(c, 2, penalty=[5, 6])["status"] == 1   # f(2)-2f(1)+f(0) < 0
+    assert oracle.colgraph_solve(c, 3, penalty=[1, 2])["status"] == 1   # too short
