@@ -162,6 +162,21 @@ cg_status colgraph_build(const cg_dims *dims, const int32_t *cost_dev, int32_t i
 cg_status colgraph_build_slabs(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight,
                                int32_t nslabs, const cg_dist *dist, cg_graph **out);
 
+/* NEXT-1 -- soft smoothness: the VCE-weight net surface problem of PAPER.md:42-43 (edge
+ * costs convex over the edge interval), SURVEY.md §8(f).  As colgraph_build (single GPU,
+ * nranks = 1), plus a convex penalty f(d) on |S(p) - S(q)| = d for 4-neighbour columns
+ * (|dS| <= Delta_d stays hard):
+ *   penalty : HOST int32[npenalty], penalty[i] = f(i+1) (f(0) = 0); npenalty >= max(Delta_x,
+ *             Delta_y) <= 16; f convex: f(k+1) - 2 f(k) + f(k-1) >= 0, f(1) >= 0.  Copied.
+ * Each column pair gets finite arcs (x,y,z) -> (nbr, z-k), k < Delta_d, of capacity
+ * f(k+1) - 2 f(k) + f(k-1) (f(1) for k = 0): an arc is cut for (d - k)_+ values of z, so a
+ * pair costs f(d).  maxflow_solve / mincut_extract_surface then minimise
+ * sum c(x,y,S) + sum_pairs f(|dS|).  Tiles (CG_SWEEP_TILES), x-slabs and maxflow_export_flow
+ * are not available for soft graphs (CG_E_INVAL).
+ * Errors: as colgraph_build; CG_E_INVAL for a non-convex / too short / NULL penalty. */
+cg_status colgraph_build_soft(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight,
+                              const int32_t *penalty, int32_t npenalty, const cg_dist *dist, cg_graph **out);
+
 /* Fill id_out (128 bytes) with a fresh ncclUniqueId for colgraph_build's cg_dist.nccl_id
  * (rank 0 calls it and broadcasts the bytes, e.g. with torch.distributed).
  * Errors: CG_E_INVAL (NULL), CG_E_NCCL (libnccl.so.2 not loadable). */

@@ -72,6 +72,9 @@ def _load():
     P = ctypes.POINTER
     lib.colgraph_build.restype = ctypes.c_int
     lib.colgraph_build.argtypes = [P(cg_dims), ctypes.c_void_p, ctypes.c_int32, P(cg_dist), P(ctypes.c_void_p)]
+    lib.colgraph_build_soft.restype = ctypes.c_int
+    lib.colgraph_build_soft.argtypes = [P(cg_dims), ctypes.c_void_p, ctypes.c_int32, P(ctypes.c_int32), ctypes.c_int32,
+                                        P(cg_dist), P(ctypes.c_void_p)]
     lib.colgraph_build_slabs.restype = ctypes.c_int
     lib.colgraph_build_slabs.argtypes = [P(cg_dims), ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, P(cg_dist),
                                          P(ctypes.c_void_p)]
@@ -104,7 +107,7 @@ def _load():
 
 _lib = _load()
 
-EXPORTED = ["colgraph_build", "colgraph_build_slabs", "cg_nccl_unique_id", "maxflow_solve", "mincut_extract_surface",
+EXPORTED = ["colgraph_build", "colgraph_build_slabs", "colgraph_build_soft", "cg_nccl_unique_id", "maxflow_solve", "mincut_extract_surface",
             "maxflow_export_flow", "colgraph_solve_host",
             "colgraph_export_state", "colgraph_stats", "colgraph_free", "cg_status_str", "cg_slab_range", "cg_version"]
 
@@ -134,6 +137,25 @@ def _check_dev_int32(t, name):
     import torch
     if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.int32 and t.is_contiguous()):
         raise TypeError(f"{name} must be a contiguous CUDA int32 tensor")
+
+
+def colgraph_build_soft(cost, delta, penalty, input_is_weight: bool = False, stream=None):
+    """NEXT-1: soft smoothness, penalty = [f(1), ..., f(K)] convex (include/colgraph.h)."""
+    _check_dev_int32(cost, "cost")
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(cost.device)
+    X, Y, Z = cost.shape
+    dims = cg_dims(X, Y, Z, delta)
+    pen = (ctypes.c_int32 * len(penalty))(*[int(v) for v in penalty])
+    h = ctypes.c_void_p()
+    st = _lib.colgraph_build_soft(ctypes.byref(dims), ctypes.c_void_p(cost.data_ptr()), int(bool(input_is_weight)),
+                                  pen, len(penalty),
+                                  ctypes.byref(_dist(cost.device.index, ctypes.c_void_p(stream.cuda_stream), 0, 1,
+                                                     None)), ctypes.byref(h))
+    if st != CG_OK:
+        raise ColgraphError(st, "colgraph_build_soft")
+    return h
 
 
 def colgraph_build(cost, delta: int, input_is_weight: bool = False, stream=None, rank=0, nranks=1, nccl_id=None,
@@ -277,14 +299,18 @@ def cg_slab_range(X: int, Y: int, Z: int, delta: int, rank: int, nranks: int):
     return x0.value, x1.value
 
 
-def solve(cost, delta: int, input_is_weight: bool = False, want_mask: bool = True, opts=None, nslabs: int = 1):
+def solve(cost, delta: int, input_is_weight: bool = False, want_mask: bool = True, opts=None, nslabs: int = 1,
+          penalty=None):
     """Device-resident convenience: build -> solve -> extract on a CUDA int32 tensor
     (nslabs > 1: the in-process x-slab path).
     Returns dict(status, extract_status, flow, surface (tensor), mask (tensor), stats)."""
     import torch
     X, Y, Z = cost.shape
-    h = colgraph_build(cost, delta, input_is_weight) if nslabs == 1 else \
-        colgraph_build_slabs(cost, delta, nslabs, input_is_weight)
+    if penalty is not None:
+        h = colgraph_build_soft(cost, delta, penalty, input_is_weight)
+    else:
+        h = colgraph_build(cost, delta, input_is_weight) if nslabs == 1 else \
+            colgraph_build_slabs(cost, delta, nslabs, input_is_weight)
     try:
         st, flow, stats = maxflow_solve(h, opts)
         surface = torch.empty((X, Y), dtype=torch.int32, device=cost.device)

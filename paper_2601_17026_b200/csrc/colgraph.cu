@@ -218,6 +218,7 @@ size_t workspace_bytes(const Geo &geo) {
     const int64_t ncol = (int64_t)geo.X * geo.Y, plane = (int64_t)(geo.X + 2) * geo.YZ;
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
     size_t b = 8 * al(sizeof(int32_t) * plane);
+    if (geo.soft_k) b += al(sizeof(int32_t) * geo.n * 4 * geo.soft_k);
     b += 3 * al(sizeof(int) * geo.n);
     b += 3 * al(sizeof(int32_t) * (ncol + 2 * geo.Y)) + 2 * al(sizeof(int) * ncol);
     b += al(sizeof(unsigned) * GAP_BINS) + al(sizeof(BfsState));
@@ -274,6 +275,7 @@ cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode) {
     Field fl[8];
     for (int i = 0; i < 8; i++) fl[i] = Field{carve<int32_t>(p, plane) + geo.YZ, -geo.YZ, geo.n + geo.YZ};
 #endif
+    sl->s.SF = geo.soft_k ? carve<int32_t>(p, geo.n * 4 * geo.soft_k) : nullptr;
     sl->s.E = fl[0];
     sl->s.H = fl[1];
     sl->s.T = fl[2];
@@ -421,7 +423,7 @@ cg_status bfs_strict(cg_graph *g, Slab *sl, bool allow_coop = true) {
     CG_CUDA(cudaMemsetAsync(sl->bst, 0, sizeof(BfsState), st));
     sl->h_bst->L = 1;
     // direction optimisation measured slower than top-down on C3-C5: off unless asked
-    sl->h_bst->bu_alpha = getenv("CG_BU_ALPHA") ? atoi(getenv("CG_BU_ALPHA")) : 0;
+    sl->h_bst->bu_alpha = getenv("CG_BU_ALPHA") && !geo.soft_k ? atoi(getenv("CG_BU_ALPHA")) : 0;
     sl->h_bst->bu_beta = getenv("CG_BU_BETA") ? atoi(getenv("CG_BU_BETA")) : 64;
     sl->h_bst->small = getenv("CG_BFS_SMALL") ? (unsigned)atoi(getenv("CG_BFS_SMALL")) : BFS_RUN_SMALL;
     CG_CUDA(cudaMemcpyAsync(&sl->bst->L, &sl->h_bst->L, sizeof(int), cudaMemcpyHostToDevice, st));
@@ -607,6 +609,7 @@ int tile_max_threads_rt(int) { return 512; }
 // used then).  CG_TILE=TXxTY overrides the shape.
 bool tile_setup(Slab *sl, int steps, int relabel_every) {
     const Geo &geo = sl->geo;
+    if (geo.soft_k) return false;  // tiles hold hard arcs only
     const int need = (geo.Z + 31) / 32;
     static const int sizes[] = {1, 2, 3, 4, 6, 8};
     int S = 0;
@@ -696,6 +699,7 @@ cg_status normalize_opts(cg_graph *g, const cg_solve_opts *opts, cg_solve_opts &
     if (o.sweep_kind == CG_SWEEP_TILES && !use_tiles) return CG_E_INVAL;
     if (o.walk_len == 0) o.walk_len = getenv("CG_WALK") ? atoi(getenv("CG_WALK")) : 64;  // library default
     o.check_every = std::max(1, std::min(o.check_every, RING));
+    if (getenv("CG_OPS")) o.ops_per_sweep = atoi(getenv("CG_OPS"));  // experiments
     o.ops_per_sweep = std::max(1, o.ops_per_sweep);
     if (!(o.gr_factor > 0.f)) o.gr_factor = 1.0f;
     for (Slab *sl : g->slabs) sl->tiles = sl->tiles && use_tiles;
@@ -831,16 +835,17 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
                 const int gv = std::max(sl->num_sms, std::min(gridv, grid_for(2 * la, 256, gridv)));
                 const int k = sl->sweep_k++;
                 sl->out_tag = ++sl->tag;
+                const bool soft = geo.soft_k > 0;
                 if (walk && walk_ws)
-                    k_walk_ws<<<gv, 256, 0, sl->stream>>>(geo, sl->s, o.walk_len, sl->blist[k & 1], sl->cnt + k % 3,
+                    (soft ? k_walk_ws<true> : k_walk_ws<false>)<<<gv, 256, 0, sl->stream>>>(geo, sl->s, o.walk_len, sl->blist[k & 1], sl->cnt + k % 3,
                                                           sl->blist[(k + 1) & 1], sl->cnt + (k + 1) % 3,
                                                           sl->cnt + (k + 2) % 3, sl->vstamp, sl->out_tag, sl->work + i,
                                                           sl->flags, sl->heads + i);
                 else if (walk && relist_ordered && !multi(g)) {
-                    k_walk<<<gv, 256, 0, sl->stream>>>(geo, sl->s, o.walk_len, sl->blist[k & 1], sl->cnt + k % 3,
-                                                       sl->blist[(k + 1) & 1], sl->cnt + (k + 1) % 3,
-                                                       sl->cnt + (k + 2) % 3, sl->vstamp, sl->out_tag, sl->work + i,
-                                                       sl->flags, walk_park);
+                    (soft ? k_walk<true> : k_walk<false>)<<<gv, 256, 0, sl->stream>>>(
+                        geo, sl->s, o.walk_len, sl->blist[k & 1], sl->cnt + k % 3, sl->blist[(k + 1) & 1],
+                        sl->cnt + (k + 1) % 3, sl->cnt + (k + 2) % 3, sl->vstamp, sl->out_tag, sl->work + i,
+                        sl->flags, walk_park);
                     // rewrite the output list in index order (same set, same count)
                     CG_CUDA(cudaMemsetAsync(sl->cnt + (k + 1) % 3, 0, sizeof(unsigned), sl->stream));
                     k_relist_ordered<<<sl->num_sms * 8, 256, 0, sl->stream>>>(geo, sl->vstamp, sl->out_tag,
@@ -848,12 +853,12 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
                                                                                sl->cnt + (k + 1) % 3);
                     g->st.kernel_launches++;
                 } else if (walk)
-                    k_walk<<<gv, 256, 0, sl->stream>>>(geo, sl->s, o.walk_len, sl->blist[k & 1], sl->cnt + k % 3,
+                    (soft ? k_walk<true> : k_walk<false>)<<<gv, 256, 0, sl->stream>>>(geo, sl->s, o.walk_len, sl->blist[k & 1], sl->cnt + k % 3,
                                                        sl->blist[(k + 1) & 1], sl->cnt + (k + 1) % 3,
                                                        sl->cnt + (k + 2) % 3, sl->vstamp, sl->out_tag, sl->work + i,
                                                        sl->flags, walk_park);
                 else
-                    k_sweep_v<<<gv, 256, 0, sl->stream>>>(geo, sl->s, o.ops_per_sweep, sl->blist[k & 1],
+                    (soft ? k_sweep_v<true> : k_sweep_v<false>)<<<gv, 256, 0, sl->stream>>>(geo, sl->s, o.ops_per_sweep, sl->blist[k & 1],
                                                           sl->cnt + k % 3, sl->blist[(k + 1) & 1],
                                                           sl->cnt + (k + 1) % 3, sl->cnt + (k + 2) % 3, sl->vstamp,
                                                           sl->out_tag, sl->work + i, sl->flags);
@@ -972,8 +977,21 @@ void colgraph_free(cg_graph *g) {
 // Common constructor: `nslabs_local` slabs in this process starting at global slab `rank`.
 static cg_status build_common(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight,
                               const cg_dist *dist, int nranks, int rank, int nslabs_local, bool local,
-                              cg_graph **out) {
+                              cg_graph **out, const int32_t *penalty = nullptr, int32_t npenalty = 0) {
     CG_TRY(validate_dims(dims));
+    // soft smoothness (NEXT-1): capacities c_0 = f(1), c_k = f(k+1) - 2 f(k) + f(k-1) >= 0
+    int32_t soft_k = 0, soft_cap[SOFT_KMAX] = {0};
+    if (penalty) {
+        const int dy = dims->delta_y < 0 ? dims->delta : dims->delta_y;
+        soft_k = std::max(dims->delta, dy);
+        if (npenalty < soft_k || soft_k > SOFT_KMAX || nslabs_local != 1 || nranks != 1) return CG_E_INVAL;
+        for (int k = 0; k < soft_k; k++) {
+            const int64_t f1 = penalty[k], f0 = k >= 1 ? penalty[k - 1] : 0, fm = k >= 2 ? penalty[k - 2] : 0;
+            const int64_t c = k == 0 ? f1 : f1 - 2 * f0 + fm;
+            if (c < 0 || c > INT_MAX) return CG_E_INVAL;
+            soft_cap[k] = (int32_t)c;
+        }
+    }
     if (!cost_dev || !out) return CG_E_INVAL;
     *out = nullptr;
     if (nranks < 1 || nranks > dims->X) return CG_E_INVAL;
@@ -1022,6 +1040,8 @@ static cg_status build_common(const cg_dims *dims, const int32_t *cost_dev, int3
         sl->x0 = x0;
         sl->x1 = x1;
         sl->geo = make_geo(dims, x0, x1, nranks, r > 0, r + 1 < nranks, g->n_global);
+        sl->geo.soft_k = soft_k;
+        for (int k = 0; k < SOFT_KMAX; k++) sl->geo.soft_cap[k] = soft_cap[k];
         g->slabs.push_back(sl);
         // LOCAL: cost_dev is the whole volume; NCCL / single: this rank's slab
         const int32_t *src = local ? cost_dev + (int64_t)x0 * sl->geo.YZ : cost_dev;
@@ -1114,6 +1134,15 @@ static cg_status maxflow_solve_impl(cg_graph *g, const cg_solve_opts *opts, int6
     g->solved = true;
     if (stats) *stats = g->st;
     return result;
+}
+
+cg_status colgraph_build_soft(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight,
+                              const int32_t *penalty, int32_t npenalty, const cg_dist *dist, cg_graph **out) {
+    if (!penalty || npenalty < 1) return CG_E_INVAL;
+    cg_dist dd{0, 1, nullptr, 0, nullptr};
+    if (dist) dd = *dist;
+    if (dd.nranks != 1) return CG_E_INVAL;
+    return debug_check(build_common(dims, cost_dev, input_is_weight, &dd, 1, 0, 1, false, out, penalty, npenalty));
 }
 
 cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_value, cg_solve_stats *stats) {
@@ -1220,7 +1249,7 @@ static cg_status maxflow_export_flow_impl(cg_graph *g, const int32_t *cost_dev, 
                               int32_t *flow_dev) {
     if (!g || !cost_dev || !flow_dev) return CG_E_INVAL;
     if (!g->solved || g->exported) return CG_E_STATE;
-    if (multi(g) || g->slabs.size() != 1) return CG_E_INVAL;
+    if (multi(g) || g->slabs.size() != 1 || g->slabs[0]->geo.soft_k) return CG_E_INVAL;
     DeviceGuard dg(g->dist.device);
     cg_solve_opts o{};
     bool use_tiles = false;

@@ -24,7 +24,12 @@ struct Geo {
     int64_t YZ;              // vertices per x-plane
     int64_t nchunks;         // X*Y*CPC
     int32_t INF;             // n_global + 1: "cannot reach t"
+    // soft smoothness (NEXT-1): soft_k = K > 0 finite arcs per direction, (x,y,z) -> (nbr, z-k),
+    // k < Delta_d, capacity soft_cap[k] = f(k+1) - 2 f(k) + f(k-1); 0 = hard constraint only
+    int32_t soft_k;
+    int32_t soft_cap[16];
 };
+constexpr int SOFT_KMAX = 16;
 
 // Residual state: 8 int32 fields per vertex -- E excess, H height, T sink residual, D flow
 // on the down arc (= residual of the up arc into this vertex from below), L[d] flow on the
@@ -68,7 +73,13 @@ struct Field {
 struct Soa {
     Field E, H, T, D;
     Field L[4];
+    int32_t *SF;  // soft-arc flows, [v][d][k] (4 * soft_k ints per owned vertex); null if hard only
 };
+
+// flow on the soft arc (v, d, k): v -> (nbr_d, z - k)
+__device__ __forceinline__ int32_t *soft_flow(const Geo &g, const Soa &s, int64_t v, int d, int k) {
+    return s.SF + (v * 4 + d) * g.soft_k + k;
+}
 
 constexpr int64_t NONE = INT64_MIN;  // "no vertex" (ghost vertices of the x = -1 plane are negative)
 

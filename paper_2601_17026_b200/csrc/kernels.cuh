@@ -235,7 +235,48 @@ struct ArcPick {
 #ifndef CG_SCAN_SERIAL
 #define CG_SCAN_SERIAL 1  // measured: the two-stage gather is within noise
 #endif
+// Soft arcs (NEXT-1) are scanned after every hard arc: arc codes 11 + 16 d + k (forward, v ->
+// (nbr_d, z-k), residual cap_k - F) and 75 + 16 d + k (reverse of (nbr_d, z+k)'s arc in direction
+// d^1, residual its flow).  Only when no hard arc is admissible, so the hard path is unchanged.
+constexpr int ARC_SOFT_FWD = 11, ARC_SOFT_REV = 75;
+__device__ __noinline__ void scan_soft(const Geo &g, const Soa &s, const OpCtx &c, int hx, ArcPick &p) {
+    for (int d = 0; d < 4; d++) {
+        if (!c.off[d]) continue;
+        const int kmax = min(g.soft_k, delta_d(g, d));
+        for (int k = 0; k < kmax; k++) {
+            const int cap = g.soft_cap[k];
+            if (cap <= 0) continue;
+            if (c.z - k >= 0) {  // forward
+                const int r = cap - *soft_flow(g, s, c.v, d, k);
+                if (r > 0) {
+                    const int64_t t = c.v0 + c.off[d] + c.z - k;
+                    const int hh = s.H[t];
+                    if (hh < p.best) { p.best = hh; p.arc = ARC_SOFT_FWD + 16 * d + k; p.tgt = t; p.res = r; }
+                    if (p.best < hx) return;
+                }
+            }
+            if (c.z + k < g.Z) {  // reverse of the arc of u = (nbr_d, z+k) toward this column
+                const int64_t u = c.v0 + c.off[d] + c.z + k;
+                const int r = *soft_flow(g, s, u, d ^ 1, k);
+                if (r > 0) {
+                    const int hh = s.H[u];
+                    if (hh < p.best) { p.best = hh; p.arc = ARC_SOFT_REV + 16 * d + k; p.tgt = u; p.res = r; }
+                    if (p.best < hx) return;
+                }
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ ArcPick scan_arcs_hard(const Geo &g, const Soa &s, const OpCtx &c, int hx);
+template <bool SOFT>
 __device__ __forceinline__ ArcPick scan_arcs(const Geo &g, const Soa &s, const OpCtx &c, int hx) {
+    ArcPick p = scan_arcs_hard(g, s, c, hx);
+    if (SOFT && p.arc != 0 && p.best >= hx) scan_soft(g, s, c, hx, p);
+    return p;
+}
+
+__device__ __forceinline__ ArcPick scan_arcs_hard(const Geo &g, const Soa &s, const OpCtx &c, int hx) {
     ArcPick p{g.INF, -1, 0, NONE};
 #if !CG_SCAN_SERIAL
     const int INF = g.INF;
@@ -346,9 +387,10 @@ __device__ __forceinline__ void set_ctx(const Geo &g, OpCtx &c, int64_t v) {
 // Single push/relabel operation of the owner of c.v; returns the vertex that received
 // flow (NONE: none or t; ghost vertices have negative indices).  Decrements follow the
 // single-decrementer rule.
+template <bool SOFT>
 __device__ __forceinline__ int64_t pr_op(const Geo &g, const Soa &s, const OpCtx &c, int &e, int &h, int &sent,
                                          int *flags) {
-    const ArcPick p = scan_arcs(g, s, c, h);
+    const ArcPick p = scan_arcs<SOFT>(g, s, c, h);
     if (p.best >= g.INF) {  // no residual path known: dead until the next global relabel
         h = g.INF;
         s.H[c.v] = h;
@@ -377,10 +419,22 @@ __device__ __forceinline__ int64_t pr_op(const Geo &g, const Soa &s, const OpCtx
             df = min(e, p.res);
             atomicSub(&s.D[c.v + 1], df);
             break;
-        default:
+        case 7: case 8: case 9: case 10:
             df = min(e, p.res);
             atomicSub(&s.L[(p.arc - 7) ^ 1][p.tgt], df);
             break;
+        default: {  // soft arcs: this vertex is the only incrementer (forward) / decrementer (reverse)
+            df = min(e, p.res);
+            if (!SOFT) break;
+            if (p.arc < ARC_SOFT_REV) {
+                const int a = p.arc - ARC_SOFT_FWD;
+                atomicAdd(soft_flow(g, s, c.v, a >> 4, a & 15), df);
+            } else {
+                const int a = p.arc - ARC_SOFT_REV;
+                atomicSub(soft_flow(g, s, p.tgt, (a >> 4) ^ 1, a & 15), df);
+            }
+            break;
+        }
     }
     e -= df;
     sent += df;
@@ -399,6 +453,7 @@ __device__ __forceinline__ void mark_vertex(const Geo &g, int64_t id, int *vstam
     warp_append(add, (int)id, list, count);
 }
 
+template <bool SOFT>
 __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_sweep_v(Geo g, Soa s, int ops, const int *__restrict__ lin,
                                                  const unsigned *cin, int *lout, unsigned *cout, unsigned *czero,
                                                  int *vstamp, int tag, unsigned long long *work, int *flags) {
@@ -422,7 +477,7 @@ __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_sweep_v(Geo g, Soa s, in
             int64_t tgt = NONE;
             if (act) {
                 mywork++;
-                tgt = pr_op(g, s, c, e, h, sent, flags);
+                tgt = pr_op<SOFT>(g, s, c, e, h, sent, flags);
                 act = e > 0 && h < g.INF;
             }
             mark_vertex(g, tgt, vstamp, tag, lout, cout);
@@ -457,6 +512,27 @@ __device__ __forceinline__ int reserve(int32_t *p, int want) {
     return 0;
 }
 
+// raise *p by up to `want` without exceeding cap (several walkers may use the same soft arc)
+__device__ __forceinline__ int reserve_up(int32_t *p, int cap, int want) {
+    int cur = *(volatile int32_t *)p;
+    while (cur < cap) {
+        const int take = min(cap - cur, want);
+        const int old = atomicCAS(p, cur, cur + take);
+        if (old == cur) return take;
+        cur = old;
+    }
+    return 0;
+}
+
+__device__ __forceinline__ int walk_push_soft(const Geo &g, const Soa &s, const OpCtx &ctx, const ArcPick &p, int c) {
+    if (p.arc < ARC_SOFT_REV) {
+        const int a = p.arc - ARC_SOFT_FWD;
+        return reserve_up(soft_flow(g, s, ctx.v, a >> 4, a & 15), g.soft_cap[a & 15], c);
+    }
+    const int a = p.arc - ARC_SOFT_REV;
+    return reserve(soft_flow(g, s, p.tgt, (a >> 4) ^ 1, a & 15), c);
+}
+
 struct BlockQueue {  // block-local append buffer, flushed with one global atomic per block
     static constexpr int CAP = 2048;
     int buf[CAP];
@@ -474,6 +550,7 @@ __device__ __forceinline__ void deposit(const Geo &g, const Soa &s, int64_t x, i
     }
 }
 
+template <bool SOFT>
 __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_walk(Geo g, Soa s, int K, const int *__restrict__ lin, const unsigned *cin,
                                               int *lout, unsigned *cout, unsigned *czero, int *vstamp, int tag,
                                               unsigned long long *work, int *flags, int park) {
@@ -494,7 +571,7 @@ __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_walk(Geo g, Soa s, int K
         OpCtx ctx;
         set_ctx(g, ctx, v);
         for (int step = 0; c > 0; ++step) {
-            const ArcPick p = scan_arcs(g, s, ctx, hx);
+            const ArcPick p = scan_arcs<SOFT>(g, s, ctx, hx);
             mywork++;  // one push or relabel operation per hop
             if (p.best >= hx || step >= K) {  // stuck (or hop budget spent): deposit the carry here
                 if (p.best >= hx) {
@@ -514,7 +591,8 @@ __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_walk(Geo g, Soa s, int K
                 case 1: df = c; atomicAdd(&s.D[ctx.v], df); break;
                 case 2: case 3: case 4: case 5: df = c; atomicAdd(&s.L[p.arc - 2][ctx.v], df); break;
                 case 6: df = reserve(&s.D[ctx.v + 1], c); break;
-                default: df = reserve(&s.L[(p.arc - 7) ^ 1][p.tgt], c); break;
+                case 7: case 8: case 9: case 10: df = reserve(&s.L[(p.arc - 7) ^ 1][p.tgt], c); break;
+                default: df = SOFT ? walk_push_soft(g, s, ctx, p, c) : 0; break;
             }
             if (df == 0) continue;  // lost a reservation race: rescan this vertex
             if (p.arc == 0) {       // absorbed by t
@@ -544,6 +622,7 @@ __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_walk(Geo g, Soa s, int K
 // itself (warp-aggregated atomicAdd on *head), so every iteration of the loop advances 32
 // independent walks by one hop.  In k_walk a warp lasts as long as its longest walk (up to
 // K dependent hops) while the lanes whose walks ended idle.  Same hop semantics as k_walk.
+template <bool SOFT>
 __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_walk_ws(Geo g, Soa s, int K, const int *__restrict__ lin,
                                                      const unsigned *cin, int *lout, unsigned *cout, unsigned *czero,
                                                      int *vstamp, int tag, unsigned long long *work, int *flags,
@@ -587,7 +666,7 @@ __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_walk_ws(Geo g, Soa s, in
         if (!__any_sync(FULL, walking || !exhausted)) break;
         if (!walking) continue;
         // one hop of this lane's walk
-        const ArcPick p = scan_arcs(g, s, ctx, hx);
+        const ArcPick p = scan_arcs<SOFT>(g, s, ctx, hx);
         mywork++;
         if (p.best >= hx || step >= K) {  // stuck (or hop budget spent): deposit the carry here
             if (p.best >= hx) atomicMax(&s.H[ctx.v], p.best >= g.INF ? g.INF : p.best + 1);
@@ -602,7 +681,8 @@ __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_walk_ws(Geo g, Soa s, in
             case 1: df = c; atomicAdd(&s.D[ctx.v], df); break;
             case 2: case 3: case 4: case 5: df = c; atomicAdd(&s.L[p.arc - 2][ctx.v], df); break;
             case 6: df = reserve(&s.D[ctx.v + 1], c); break;
-            default: df = reserve(&s.L[(p.arc - 7) ^ 1][p.tgt], c); break;
+            case 7: case 8: case 9: case 10: df = reserve(&s.L[(p.arc - 7) ^ 1][p.tgt], c); break;
+            default: df = SOFT ? walk_push_soft(g, s, ctx, p, c) : 0; break;
         }
         if (df == 0) continue;  // lost a reservation race: rescan this vertex
         if (p.arc == 0) {       // absorbed by t
@@ -706,6 +786,46 @@ __global__ void k_bfs_init(Geo g, Soa s, int *lout, unsigned *cout, unsigned *vi
 // atomic per warp.  STRICT (single slab): claim unlabelled predecessors with
 // atomicCAS(H, INF, L+1) -- each vertex exactly once.  Otherwise label-correcting (x-slabs):
 // relax predecessors with atomicMin(H, H(v)+1) and list the improved ones once per wave.
+// Soft-arc predecessors of v (NEXT-1): w = (nbr_d, z+k) whose forward arc (d^1, k) into v has
+// residual, and w = (nbr_d, z-k) through the reverse of v's forward arc (d, k) when it carries
+// flow.  Each claim appends with its own atomic (no warp collectives: callable per lane).
+template <bool BITMAP>
+__device__ __noinline__ void bfs_soft_preds(const Geo &g, const Soa &s, int64_t v, int nl, int *lout, unsigned *cout,
+                                            unsigned *visited) {
+    const int64_t col = v / g.Z;
+    const int z = (int)(v - col * g.Z);
+    const int x = (int)(col / g.Y), y = (int)(col - (int64_t)x * g.Y);
+    const int64_t v0 = col * g.Z;
+    auto claim = [&](int64_t w) {
+        bool got;
+        if (BITMAP) {
+            const unsigned bit = 1u << (w & 31);
+            got = !(__ldcg(&visited[w >> 5]) & bit) && !(atomicOr(&visited[w >> 5], bit) & bit);
+            if (got) s.H[w] = nl;
+        } else {
+            got = __ldcg(&s.H[w]) >= g.INF && atomicCAS(&s.H[w], g.INF, nl) == g.INF;
+        }
+        if (got) lout[atomicAdd(cout, 1u)] = (int)w;
+    };
+    for (int d = 0; d < 4; d++) {
+        const int64_t o = nbr_off(g, x, y, d);
+        if (!o) continue;
+        const int kmax = min(g.soft_k, delta_d(g, d));
+        for (int k = 0; k < kmax; k++) {
+            const int cap = g.soft_cap[k];
+            if (cap <= 0) continue;
+            if (z + k < g.Z) {
+                const int64_t w = v0 + o + z + k;
+                if (owned(g, w) && cap - *soft_flow(g, s, w, d ^ 1, k) > 0) claim(w);
+            }
+            if (z - k >= 0) {
+                const int64_t w = v0 + o + z - k;
+                if (owned(g, w) && *soft_flow(g, s, v, d, k) > 0) claim(w);
+            }
+        }
+    }
+}
+
 template <bool STRICT>
 __device__ __forceinline__ void bfs_expand_warp(const Geo &g, const Soa &s, int nl, int64_t v, int *lout,
                                                 unsigned *cout, int *vstamp, int tag) {
@@ -775,6 +895,7 @@ __device__ __forceinline__ void bfs_expand_warp(const Geo &g, const Soa &s, int 
             }
         }
     }
+    if (STRICT && g.soft_k && v >= 0 && nl < INF) bfs_soft_preds<false>(g, s, v, nl, lout, cout, nullptr);
     const int k = __popc(got);
     const int incl = warp_incl_scan(k);
     const int total = __shfl_sync(FULL, incl, 31);
@@ -841,6 +962,9 @@ __device__ __forceinline__ void bfs_expand_multi(const Geo &g, const Soa &s, int
 #pragma unroll
         for (int j = 0; j < 10; j++)
             hw[r][j] = (cand[r] >> j & 1u) ? (int)((__ldcg(&visited[w[r][j] >> 5]) >> (w[r][j] & 31)) & 1u) : 1;
+    if (g.soft_k && nl < INF)
+        for (int r = 0; r < R; r++)
+            if (vv[r] >= 0) bfs_soft_preds<true>(g, s, vv[r], nl, lout, cout, visited);
     int k = 0;
 #pragma unroll
     for (int r = 0; r < R; r++)
@@ -1470,6 +1594,17 @@ __global__ void __launch_bounds__(256) k_ext_round(Geo g, Soa s, const int *__re
                 const int zi = z <= t ? zi_of(z, delta_d(g, d), g.Z) : -1;
                 if (zi >= 0 && nc[d] != INT64_MIN && s.L[d ^ 1][nc[d] * g.Z + zi] > 0) cd[d] = max(cd[d], zi);
             }
+            if (g.soft_k && z <= t)  // soft arcs with residual (NEXT-1)
+                for (int d = 0; d < 4; d++) {
+                    if (nc[d] == INT64_MIN) continue;
+                    const int kmax = min(g.soft_k, delta_d(g, d));
+                    for (int k = 0; k < kmax; k++) {
+                        const int cap = g.soft_cap[k];
+                        if (cap <= 0) continue;
+                        if (z - k >= 0 && cap - *soft_flow(g, s, v0 + z, d, k) > 0) cd[d] = max(cd[d], z - k);
+                        if (z + k < g.Z && *soft_flow(g, s, nc[d] * g.Z + z + k, d ^ 1, k) > 0) cd[d] = max(cd[d], z + k);
+                    }
+                }
         }
         int mark = -1;
 #pragma unroll
