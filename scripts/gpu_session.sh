@@ -1,3 +1,3 @@
 set -x
-timeout 600 python -m pytest tests/test_gpu_soft.py -x -q -k full_size > gpurun_out/t_soft_full.log 2>&1
-timeout 600 python scripts/soft_timing.py C2,C3,C4 > gpurun_out/t_soft_time.log 2>&1
+timeout 1500 python scripts/ab.py C4 6 'default:' 'ws:CG_WALK_WS=1' 'g2ws:CG_LIB=paper_2601_17026_b200/libcolgraph_gather2.so,CG_WALK_WS=1' > gpurun_out/t_ab.log 2>&1
+timeout 900 python scripts/ab.py C3,C5 3 'default:' 'ws:CG_WALK_WS=1' 'g2ws:CG_LIB=paper_2601_17026_b200/libcolgraph_gather2.so,CG_WALK_WS=1' >> gpurun_out/t_ab.log 2>&1
