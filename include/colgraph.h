@@ -21,6 +21,25 @@
  * Addressing is implicit (§3.2.3): vertex (x,y,z) has index
  * i = (x*Y + y)*Z + z (z fastest); no adjacency list is stored.
  *
+ * Environment (diagnostics and measured alternatives only; defaults are the measured
+ * best; results never depend on them -- the max-flow value and the minimal
+ * cut are unique):
+ *   CG_TRACE=1            per-batch / per-relabel trace on stderr
+ *   CG_DEBUG=1            print the failing CUDA / NCCL call on stderr
+ *   CG_WALK=K             hop budget of multi-hop walks (default 64)
+ *   CG_WALK_MIN=f         walks while >= f*n vertices are active (default 1e-3), single hops below
+ *   CG_WALK_WS=1          work-fetching walks (k_walk_ws)
+ *   CG_WALK_PARK=1        stuck walks wait for the next global relabel
+ *   CG_RELIST=1           re-list large sweep worklists in index order
+ *   CG_OPS=k              push/relabel operations per vertex per single-hop sweep
+ *   CG_GR_BETA=b          time trigger: relabel when sweep time since the last one >= b * its cost
+ *   CG_BFS_SMALL=k        persistent BFS: frontiers <= k run in block 0 alone (default 64)
+ *   CG_BU_ALPHA/BETA      direction-optimising (bottom-up) BFS levels (default off)
+ *   CG_BFS_LEVEL_LAUNCHES one kernel launch per BFS level instead of the persistent BFS
+ *   CG_PRECANCEL=1        exact per-column pre-cancellation before the first relabel
+ *   CG_SWEEP=1            tile sweeps (as sweep_kind = CG_SWEEP_TILES); CG_TILE=TXxTY,
+ *                         CG_TILE_STEPS, CG_TILE_RELABEL, CG_TILE_PROF=1 (clock counters)
+ *   CG_PHASE2_PR=1        maxflow_export_flow: generic push-relabel phase 2 only
  * Conventions for every entry point:
  *   - Errors are returned as cg_status, never thrown; no C++ exception crosses
  *     this ABI.
