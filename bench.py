@@ -220,14 +220,18 @@ def run_ours(args, spec):
     stats = []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         ev0.record(stream)
-        for _ in range(args.steps):
+        step_ev[0].record(stream)
+        for k in range(args.steps):
             flow, s, _ = step(cost)
             stats.append(s)
+            step_ev[k + 1].record(stream)
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier()
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    step_ms = sorted(step_ev[k].elapsed_time(step_ev[k + 1]) for k in range(args.steps))
     ms_step = ms_total / args.steps
     value = spec.n * args.steps / (ms_total / 1000.0) / 1e6  # whole volume per step, all ranks together
 
@@ -275,6 +279,7 @@ def run_ours(args, spec):
                 "share_of_step": sweep_ms * args.steps / (ms_total * len(stats)) if ms_total > 0 else None}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "time_to_min_cut_s": ms_step / 1000.0,
+            "ms_per_step_min_median_max": [step_ms[0], step_ms[len(step_ms) // 2], step_ms[-1]],
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
             "dtype": "int32", "data": "synthetic (seeded generator synth/volumes.py, sha256-pinned)",
             "config": workload_config(spec, {"parallelism": f"x-slab{world}" if world > 1 else "single-gpu"}),
