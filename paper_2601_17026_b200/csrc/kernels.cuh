@@ -788,40 +788,38 @@ __global__ void k_bfs_init(Geo g, Soa s, int *lout, unsigned *cout, unsigned *vi
 // relax predecessors with atomicMin(H, H(v)+1) and list the improved ones once per wave.
 // Soft-arc predecessors of v (NEXT-1): w = (nbr_d, z+k) whose forward arc (d^1, k) into v has
 // residual, and w = (nbr_d, z-k) through the reverse of v's forward arc (d, k) when it carries
-// flow.  Each claim appends with its own atomic (no warp collectives: callable per lane).
+// flow.  WARP-COLLECTIVE: every lane of the warp calls it (v < 0: no vertex); the loop over
+// (d, k) is warp-uniform and claims are appended with one atomic per warp (warp_append).
 template <bool BITMAP>
 __device__ __noinline__ void bfs_soft_preds(const Geo &g, const Soa &s, int64_t v, int nl, int *lout, unsigned *cout,
                                             unsigned *visited) {
-    const int64_t col = v / g.Z;
-    const int z = (int)(v - col * g.Z);
+    const bool has = v >= 0;
+    const int64_t col = has ? v / g.Z : 0;
+    const int z = has ? (int)(v - col * g.Z) : 0;
     const int x = (int)(col / g.Y), y = (int)(col - (int64_t)x * g.Y);
     const int64_t v0 = col * g.Z;
-    auto claim = [&](int64_t w) {
-        bool got;
+    auto claim = [&](int64_t w) -> bool {
         if (BITMAP) {
             const unsigned bit = 1u << (w & 31);
-            got = !(__ldcg(&visited[w >> 5]) & bit) && !(atomicOr(&visited[w >> 5], bit) & bit);
-            if (got) s.H[w] = nl;
-        } else {
-            got = __ldcg(&s.H[w]) >= g.INF && atomicCAS(&s.H[w], g.INF, nl) == g.INF;
+            if ((__ldcg(&visited[w >> 5]) & bit) || (atomicOr(&visited[w >> 5], bit) & bit)) return false;
+            s.H[w] = nl;
+            return true;
         }
-        if (got) lout[atomicAdd(cout, 1u)] = (int)w;
+        return __ldcg(&s.H[w]) >= g.INF && atomicCAS(&s.H[w], g.INF, nl) == g.INF;
     };
     for (int d = 0; d < 4; d++) {
-        const int64_t o = nbr_off(g, x, y, d);
-        if (!o) continue;
+        const int64_t o = has ? nbr_off(g, x, y, d) : 0;
         const int kmax = min(g.soft_k, delta_d(g, d));
         for (int k = 0; k < kmax; k++) {
             const int cap = g.soft_cap[k];
-            if (cap <= 0) continue;
-            if (z + k < g.Z) {
-                const int64_t w = v0 + o + z + k;
-                if (owned(g, w) && cap - *soft_flow(g, s, w, d ^ 1, k) > 0) claim(w);
+            bool up = false, dn = false;
+            const int64_t wu = v0 + o + z + k, wd = v0 + o + z - k;
+            if (o && cap > 0) {
+                up = z + k < g.Z && owned(g, wu) && cap - *soft_flow(g, s, wu, d ^ 1, k) > 0 && claim(wu);
+                dn = z - k >= 0 && owned(g, wd) && *soft_flow(g, s, v, d, k) > 0 && claim(wd);
             }
-            if (z - k >= 0) {
-                const int64_t w = v0 + o + z - k;
-                if (owned(g, w) && *soft_flow(g, s, v, d, k) > 0) claim(w);
-            }
+            warp_append(up, (int)wu, lout, cout);
+            warp_append(dn, (int)wd, lout, cout);
         }
     }
 }
@@ -895,7 +893,7 @@ __device__ __forceinline__ void bfs_expand_warp(const Geo &g, const Soa &s, int 
             }
         }
     }
-    if (STRICT && g.soft_k && v >= 0 && nl < INF) bfs_soft_preds<false>(g, s, v, nl, lout, cout, nullptr);
+    if (STRICT && g.soft_k && nl < INF) bfs_soft_preds<false>(g, s, v, nl, lout, cout, nullptr);  // warp-uniform
     const int k = __popc(got);
     const int incl = warp_incl_scan(k);
     const int total = __shfl_sync(FULL, incl, 31);
@@ -962,9 +960,8 @@ __device__ __forceinline__ void bfs_expand_multi(const Geo &g, const Soa &s, int
 #pragma unroll
         for (int j = 0; j < 10; j++)
             hw[r][j] = (cand[r] >> j & 1u) ? (int)((__ldcg(&visited[w[r][j] >> 5]) >> (w[r][j] & 31)) & 1u) : 1;
-    if (g.soft_k && nl < INF)
-        for (int r = 0; r < R; r++)
-            if (vv[r] >= 0) bfs_soft_preds<true>(g, s, vv[r], nl, lout, cout, visited);
+    if (g.soft_k && nl < INF)  // warp-uniform: every lane calls it
+        for (int r = 0; r < R; r++) bfs_soft_preds<true>(g, s, vv[r], nl, lout, cout, visited);
     int k = 0;
 #pragma unroll
     for (int r = 0; r < R; r++)
