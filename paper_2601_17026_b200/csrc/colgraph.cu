@@ -180,6 +180,57 @@ inline bool tracing() { return getenv("CG_TRACE") != nullptr; }
 // Grid for worklist kernels: enough warps to fill every SM (8 x 256 threads per SM).
 inline int list_grid(const Slab *sl, int64_t items) { return grid_for(items * 32, 256, sl->num_sms * 8); }
 
+// NCCL communicators, cached by (unique id, rank, nranks, device): ncclCommInitRank costs tens
+// to hundreds of milliseconds, and a job that builds one handle per solve with the same id
+// (bench.py --gpus N) would otherwise pay it inside every solve.  A communicator is in use by
+// at most one handle at a time; colgraph_free returns it to the cache.
+struct CommEntry {
+    unsigned char id[sizeof(ncclUniqueId)];
+    int rank, nranks, device;
+    ncclComm_t comm;
+    bool in_use;
+};
+std::mutex g_comm_mu;
+std::vector<CommEntry> g_comms;
+
+cg_status comm_acquire(const void *id, int rank, int nranks, int device, ncclComm_t *out) {
+    {
+        std::lock_guard<std::mutex> lk(g_comm_mu);
+        for (CommEntry &e : g_comms)
+            if (!e.in_use && e.rank == rank && e.nranks == nranks && e.device == device &&
+                memcmp(e.id, id, sizeof(e.id)) == 0) {
+                e.in_use = true;
+                *out = e.comm;
+                return CG_OK;
+            }
+    }
+    ncclUniqueId uid;
+    memcpy(&uid, id, sizeof(uid));
+    ncclComm_t comm = nullptr;
+    if (nccl().commInitRank(&comm, nranks, uid, rank) != ncclSuccess) return CG_E_NCCL;
+    std::lock_guard<std::mutex> lk(g_comm_mu);
+    CommEntry e{};
+    memcpy(e.id, id, sizeof(e.id));
+    e.rank = rank;
+    e.nranks = nranks;
+    e.device = device;
+    e.comm = comm;
+    e.in_use = true;
+    g_comms.push_back(e);
+    *out = comm;
+    return CG_OK;
+}
+
+void comm_release(ncclComm_t comm) {
+    std::lock_guard<std::mutex> lk(g_comm_mu);
+    for (CommEntry &e : g_comms)
+        if (e.comm == comm) {
+            e.in_use = false;
+            return;
+        }
+    nccl().commDestroy(comm);  // not from the cache
+}
+
 // Pinned host scratch blocks, recycled across handles: cudaHostAlloc / cudaFreeHost pin pages
 // and synchronise the device, which made repeated build/free cycles occasionally cost
 // tens of milliseconds.
@@ -965,7 +1016,7 @@ void colgraph_free(cg_graph *g) {
     {
         DeviceGuard dg(g->dist.device);
         for (Slab *sl : g->slabs) slab_free(sl);
-        if (g->comm) nccl().commDestroy(g->comm);
+        if (g->comm) comm_release(g->comm);
         if (g->d_red) cudaFree(g->d_red);
         if (g->h_red) cudaFreeHost(g->h_red);
         if (g->ev0) cudaEventDestroy(g->ev0);
@@ -1015,9 +1066,7 @@ static cg_status build_common(const cg_dims *dims, const int32_t *cost_dev, int3
     if (cudaEventCreate(&g->ev0) != cudaSuccess || cudaEventCreate(&g->ev1) != cudaSuccess) return fail(CG_E_CUDA);
     if (!local && nranks > 1) {
         if (!dd.nccl_id || !nccl().ok) return fail(CG_E_NCCL);
-        ncclUniqueId id;
-        memcpy(&id, dd.nccl_id, sizeof(id));
-        if (nccl().commInitRank(&g->comm, nranks, id, rank) != ncclSuccess) return fail(CG_E_NCCL);
+        if (comm_acquire(dd.nccl_id, rank, nranks, dd.device, &g->comm) != CG_OK) return fail(CG_E_NCCL);
         if (cudaMalloc(&g->d_red, 64 * sizeof(int64_t)) != cudaSuccess ||
             cudaHostAlloc(&g->h_red, 64 * sizeof(int64_t), cudaHostAllocDefault) != cudaSuccess)
             return fail(CG_E_NOMEM);
