@@ -190,11 +190,17 @@ cg_status colgraph_build_slabs(const cg_dims *dims, const int32_t *cost_dev, int
  * Each column pair gets finite arcs (x,y,z) -> (nbr, z-k), k < Delta_d, of capacity
  * f(k+1) - 2 f(k) + f(k-1) (f(1) for k = 0): an arc is cut for (d - k)_+ values of z, so a
  * pair costs f(d).  maxflow_solve / mincut_extract_surface then minimise
- * sum c(x,y,S) + sum_pairs f(|dS|).  Tiles (CG_SWEEP_TILES), x-slabs and maxflow_export_flow
- * are not available for soft graphs (CG_E_INVAL).
+ * sum c(x,y,S) + sum_pairs f(|dS|).  With cg_dist.nranks > 1 it is the NCCL x-slab path of
+ * colgraph_build (the halo message grows by 2 K planes of soft-arc flows).  Tiles
+ * (CG_SWEEP_TILES) and maxflow_export_flow are not available for soft graphs (CG_E_INVAL).
  * Errors: as colgraph_build; CG_E_INVAL for a non-convex / too short / NULL penalty. */
 cg_status colgraph_build_soft(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight,
                               const int32_t *penalty, int32_t npenalty, const cg_dist *dist, cg_graph **out);
+
+/* colgraph_build_slabs with the soft penalty of colgraph_build_soft (in-process x-slabs). */
+cg_status colgraph_build_slabs_soft(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight,
+                                    const int32_t *penalty, int32_t npenalty, int32_t nslabs, const cg_dist *dist,
+                                    cg_graph **out);
 
 /* Fill id_out (128 bytes) with a fresh ncclUniqueId for colgraph_build's cg_dist.nccl_id
  * (rank 0 calls it and broadcasts the bytes, e.g. with torch.distributed).

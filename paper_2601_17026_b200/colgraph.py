@@ -75,6 +75,9 @@ def _load():
     lib.colgraph_build_soft.restype = ctypes.c_int
     lib.colgraph_build_soft.argtypes = [P(cg_dims), ctypes.c_void_p, ctypes.c_int32, P(ctypes.c_int32), ctypes.c_int32,
                                         P(cg_dist), P(ctypes.c_void_p)]
+    lib.colgraph_build_slabs_soft.restype = ctypes.c_int
+    lib.colgraph_build_slabs_soft.argtypes = [P(cg_dims), ctypes.c_void_p, ctypes.c_int32, P(ctypes.c_int32),
+                                              ctypes.c_int32, ctypes.c_int32, P(cg_dist), P(ctypes.c_void_p)]
     lib.colgraph_build_slabs.restype = ctypes.c_int
     lib.colgraph_build_slabs.argtypes = [P(cg_dims), ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, P(cg_dist),
                                          P(ctypes.c_void_p)]
@@ -107,7 +110,7 @@ def _load():
 
 _lib = _load()
 
-EXPORTED = ["colgraph_build", "colgraph_build_slabs", "colgraph_build_soft", "cg_nccl_unique_id", "maxflow_solve", "mincut_extract_surface",
+EXPORTED = ["colgraph_build", "colgraph_build_slabs", "colgraph_build_soft", "colgraph_build_slabs_soft", "cg_nccl_unique_id", "maxflow_solve", "mincut_extract_surface",
             "maxflow_export_flow", "colgraph_solve_host",
             "colgraph_export_state", "colgraph_stats", "colgraph_free", "cg_status_str", "cg_slab_range", "cg_version"]
 
@@ -155,6 +158,25 @@ def colgraph_build_soft(cost, delta, penalty, input_is_weight: bool = False, str
                                                      None)), ctypes.byref(h))
     if st != CG_OK:
         raise ColgraphError(st, "colgraph_build_soft")
+    return h
+
+
+def colgraph_build_slabs_soft(cost, delta, penalty, nslabs: int, input_is_weight: bool = False, stream=None):
+    """In-process x-slabs of a soft-smoothness graph (include/colgraph.h)."""
+    _check_dev_int32(cost, "cost")
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(cost.device)
+    X, Y, Z = cost.shape
+    dims = cg_dims(X, Y, Z, delta)
+    pen = (ctypes.c_int32 * len(penalty))(*[int(v) for v in penalty])
+    h = ctypes.c_void_p()
+    st = _lib.colgraph_build_slabs_soft(ctypes.byref(dims), ctypes.c_void_p(cost.data_ptr()),
+                                        int(bool(input_is_weight)), pen, len(penalty), int(nslabs),
+                                        ctypes.byref(_dist(cost.device.index, ctypes.c_void_p(stream.cuda_stream))),
+                                        ctypes.byref(h))
+    if st != CG_OK:
+        raise ColgraphError(st, "colgraph_build_slabs_soft")
     return h
 
 
@@ -307,7 +329,8 @@ def solve(cost, delta: int, input_is_weight: bool = False, want_mask: bool = Tru
     import torch
     X, Y, Z = cost.shape
     if penalty is not None:
-        h = colgraph_build_soft(cost, delta, penalty, input_is_weight)
+        h = colgraph_build_soft(cost, delta, penalty, input_is_weight) if nslabs == 1 else \
+            colgraph_build_slabs_soft(cost, delta, penalty, nslabs, input_is_weight)
     else:
         h = colgraph_build(cost, delta, input_is_weight) if nslabs == 1 else \
             colgraph_build_slabs(cost, delta, nslabs, input_is_weight)

@@ -67,6 +67,7 @@ struct Slab {
     unsigned long long *u64 = nullptr;   // [0]=N [1]=sumT0 [2]=sumT [3]=active [4]=gap lifted [5]=scratch
     int *flags = nullptr;                // [0]=overflow [1]=maxh [2]=gap [3]=empty
     int32_t *snap[2] = {nullptr, nullptr};   // ghost lateral residual at the last refresh
+    int32_t *ssnap[2] = {nullptr, nullptr};  // ghost soft-arc flows at the last refresh (soft graphs)
     int32_t *hold[2] = {nullptr, nullptr};   // ghost heights before the last relabel exchange
     int32_t *hsend[2] = {nullptr, nullptr};  // halo messages (4 planes)
     int32_t *hrecv[2] = {nullptr, nullptr};
@@ -265,17 +266,23 @@ T *carve(char *&p, int64_t count) {
     return r;
 }
 
+// halo message per side: 4 planes (dE, dL, H, L) + for soft graphs 2 K planes (dF, F)
+int64_t halo_msg_ints(const Geo &geo) {
+    return std::max<int64_t>((4 + 2 * (int64_t)geo.soft_k) * geo.YZ, 8 * (int64_t)geo.Y);
+}
+
 size_t workspace_bytes(const Geo &geo) {
     const int64_t ncol = (int64_t)geo.X * geo.Y, plane = (int64_t)(geo.X + 2) * geo.YZ;
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
     size_t b = 8 * al(sizeof(int32_t) * plane);
-    if (geo.soft_k) b += al(sizeof(int32_t) * geo.n * 4 * geo.soft_k);
+    // soft flows over the owned and the two ghost planes; per side a snapshot of the ghost copy
+    if (geo.soft_k) b += al(sizeof(int32_t) * plane * 4 * geo.soft_k) + 2 * al(sizeof(int32_t) * geo.YZ * geo.soft_k);
     b += 3 * al(sizeof(int) * geo.n);
     b += 3 * al(sizeof(int32_t) * (ncol + 2 * geo.Y)) + 2 * al(sizeof(int) * ncol);
     b += al(sizeof(unsigned) * GAP_BINS) + al(sizeof(BfsState));
     b += al(sizeof(unsigned) * 16) + al(sizeof(unsigned long long) * RING) + al(sizeof(unsigned long long) * 16) +
          al(sizeof(int) * 16);
-    b += 4 * al(sizeof(int32_t) * geo.YZ) + 4 * al(sizeof(int32_t) * 4 * std::max<int64_t>(geo.YZ, 2 * geo.Y));
+    b += 4 * al(sizeof(int32_t) * geo.YZ) + 4 * al(sizeof(int32_t) * halo_msg_ints(geo));
     b += 5 * al(sizeof(int) * ncol) + al(sizeof(unsigned) * 4) + al(sizeof(unsigned long long) * RING) +
          al(sizeof(unsigned long long) * 16) + al(sizeof(unsigned) * RING) + al(sizeof(unsigned) * (geo.n / 32 + 1));
     return b;
@@ -326,7 +333,9 @@ cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode) {
     Field fl[8];
     for (int i = 0; i < 8; i++) fl[i] = Field{carve<int32_t>(p, plane) + geo.YZ, -geo.YZ, geo.n + geo.YZ};
 #endif
-    sl->s.SF = geo.soft_k ? carve<int32_t>(p, geo.n * 4 * geo.soft_k) : nullptr;
+    // soft flows: vertex index v in [-YZ, n + YZ) (ghost planes included), 4 K ints each
+    sl->s.SF = geo.soft_k ? carve<int32_t>(p, plane * 4 * geo.soft_k) + geo.YZ * 4 * geo.soft_k : nullptr;
+    for (int side = 0; side < 2; side++) sl->ssnap[side] = geo.soft_k ? carve<int32_t>(p, geo.YZ * geo.soft_k) : nullptr;
     sl->s.E = fl[0];
     sl->s.H = fl[1];
     sl->s.T = fl[2];
@@ -346,7 +355,7 @@ cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode) {
     sl->work = carve<unsigned long long>(p, RING);
     sl->u64 = carve<unsigned long long>(p, 16);
     sl->flags = carve<int>(p, 16);
-    const int64_t msg = 4 * std::max<int64_t>(geo.YZ, 2 * geo.Y);
+    const int64_t msg = halo_msg_ints(geo);
     for (int k = 0; k < 4; k++) sl->tl.list[k] = carve<int>(p, ncol);
     sl->tl.stamp = carve<int>(p, ncol);
     sl->tl.cnt = carve<unsigned>(p, 4);
@@ -437,10 +446,10 @@ cg_status halo_sweep(cg_graph *g) {
     for (Slab *sl : g->slabs) {
         const Geo &geo = sl->geo;
         const int grid = grid_for(geo.YZ, 256, sl->num_sms * 4);
-        if (geo.gl) k_halo_pack<<<grid, 256, 0, sl->stream>>>(geo, sl->s, 0, sl->snap[0], sl->hsend[0]);
-        if (geo.gh) k_halo_pack<<<grid, 256, 0, sl->stream>>>(geo, sl->s, 1, sl->snap[1], sl->hsend[1]);
+        if (geo.gl) k_halo_pack<<<grid, 256, 0, sl->stream>>>(geo, sl->s, 0, sl->snap[0], sl->ssnap[0], sl->hsend[0]);
+        if (geo.gh) k_halo_pack<<<grid, 256, 0, sl->stream>>>(geo, sl->s, 1, sl->snap[1], sl->ssnap[1], sl->hsend[1]);
     }
-    CG_TRY(transfer(g, 4 * g->slabs[0]->geo.YZ));
+    CG_TRY(transfer(g, (4 + 2 * (int64_t)g->slabs[0]->geo.soft_k) * g->slabs[0]->geo.YZ));
     for (Slab *sl : g->slabs) {
         const Geo &geo = sl->geo;
         const int grid = grid_for(geo.YZ, 256, sl->num_sms * 4);
@@ -449,7 +458,7 @@ cg_status halo_sweep(cg_graph *g) {
         for (int side = 0; side < 2; side++)
             if (side ? geo.gh : geo.gl)
                 k_halo_unpack<<<grid, 256, 0, sl->stream>>>(geo, sl->s, side, sl->hrecv[side], sl->hsend[side],
-                                                            sl->snap[side], sl->blist[k & 1], sl->cnt + k % 3,
+                                                            sl->snap[side], sl->ssnap[side], sl->blist[k & 1], sl->cnt + k % 3,
                                                             sl->vstamp, tag, sl->flags);
         g->st.kernel_launches += geo.gl + geo.gh;
     }
@@ -1035,7 +1044,7 @@ static cg_status build_common(const cg_dims *dims, const int32_t *cost_dev, int3
     if (penalty) {
         const int dy = dims->delta_y < 0 ? dims->delta : dims->delta_y;
         soft_k = std::max(dims->delta, dy);
-        if (npenalty < soft_k || soft_k > SOFT_KMAX || nslabs_local != 1 || nranks != 1) return CG_E_INVAL;
+        if (npenalty < soft_k || soft_k > SOFT_KMAX) return CG_E_INVAL;
         for (int k = 0; k < soft_k; k++) {
             const int64_t f1 = penalty[k], f0 = k >= 1 ? penalty[k - 1] : 0, fm = k >= 2 ? penalty[k - 2] : 0;
             const int64_t c = k == 0 ? f1 : f1 - 2 * f0 + fm;
@@ -1190,8 +1199,17 @@ cg_status colgraph_build_soft(const cg_dims *dims, const int32_t *cost_dev, int3
     if (!penalty || npenalty < 1) return CG_E_INVAL;
     cg_dist dd{0, 1, nullptr, 0, nullptr};
     if (dist) dd = *dist;
-    if (dd.nranks != 1) return CG_E_INVAL;
-    return debug_check(build_common(dims, cost_dev, input_is_weight, &dd, 1, 0, 1, false, out, penalty, npenalty));
+    if (dd.nranks < 1 || dd.rank < 0 || dd.rank >= dd.nranks) return CG_E_INVAL;
+    return debug_check(build_common(dims, cost_dev, input_is_weight, &dd, dd.nranks, dd.rank, 1, false, out, penalty,
+                                    npenalty));
+}
+
+cg_status colgraph_build_slabs_soft(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight,
+                                    const int32_t *penalty, int32_t npenalty, int32_t nslabs, const cg_dist *dist,
+                                    cg_graph **out) {
+    if (!penalty || npenalty < 1 || nslabs < 1) return CG_E_INVAL;
+    return debug_check(build_common(dims, cost_dev, input_is_weight, dist, nslabs, 0, nslabs, true, out, penalty,
+                                    npenalty));
 }
 
 cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_value, cg_solve_stats *stats) {

@@ -790,22 +790,26 @@ __global__ void k_bfs_init(Geo g, Soa s, int *lout, unsigned *cout, unsigned *vi
 // residual, and w = (nbr_d, z-k) through the reverse of v's forward arc (d, k) when it carries
 // flow.  WARP-COLLECTIVE: every lane of the warp calls it (v < 0: no vertex); the loop over
 // (d, k) is warp-uniform and claims are appended with one atomic per warp (warp_append).
-template <bool BITMAP>
+// MODE 0: claim through the visited bitmap (k_bfs_run); 1: CAS on INF labels (k_bfs_step);
+// 2: label-correcting relaxation with atomicMin, listed once per wave through vstamp == tag
+// (x-slab relabel, nl per lane).
+template <int MODE>
 __device__ __noinline__ void bfs_soft_preds(const Geo &g, const Soa &s, int64_t v, int nl, int *lout, unsigned *cout,
-                                            unsigned *visited) {
-    const bool has = v >= 0;
+                                            unsigned *visited, int *vstamp = nullptr, int tag = 0) {
+    const bool has = v >= 0 && nl < g.INF;  // lists hold owned vertices only; -1 = no vertex
     const int64_t col = has ? v / g.Z : 0;
     const int z = has ? (int)(v - col * g.Z) : 0;
     const int x = (int)(col / g.Y), y = (int)(col - (int64_t)x * g.Y);
     const int64_t v0 = col * g.Z;
     auto claim = [&](int64_t w) -> bool {
-        if (BITMAP) {
+        if (MODE == 0) {
             const unsigned bit = 1u << (w & 31);
             if ((__ldcg(&visited[w >> 5]) & bit) || (atomicOr(&visited[w >> 5], bit) & bit)) return false;
             s.H[w] = nl;
             return true;
         }
-        return __ldcg(&s.H[w]) >= g.INF && atomicCAS(&s.H[w], g.INF, nl) == g.INF;
+        if (MODE == 1) return __ldcg(&s.H[w]) >= g.INF && atomicCAS(&s.H[w], g.INF, nl) == g.INF;
+        return s.H[w] > nl && atomicMin(&s.H[w], nl) > nl && vstamp[w] != tag && atomicExch(&vstamp[w], tag) != tag;
     };
     for (int d = 0; d < 4; d++) {
         const int64_t o = has ? nbr_off(g, x, y, d) : 0;
@@ -893,7 +897,8 @@ __device__ __forceinline__ void bfs_expand_warp(const Geo &g, const Soa &s, int 
             }
         }
     }
-    if (STRICT && g.soft_k && nl < INF) bfs_soft_preds<false>(g, s, v, nl, lout, cout, nullptr);  // warp-uniform
+    if (g.soft_k)  // warp-uniform: every lane calls it
+        bfs_soft_preds < STRICT ? 1 : 2 > (g, s, v, v >= 0 ? nl : INF, lout, cout, nullptr, vstamp, tag);
     const int k = __popc(got);
     const int incl = warp_incl_scan(k);
     const int total = __shfl_sync(FULL, incl, 31);
@@ -961,7 +966,7 @@ __device__ __forceinline__ void bfs_expand_multi(const Geo &g, const Soa &s, int
         for (int j = 0; j < 10; j++)
             hw[r][j] = (cand[r] >> j & 1u) ? (int)((__ldcg(&visited[w[r][j] >> 5]) >> (w[r][j] & 31)) & 1u) : 1;
     if (g.soft_k && nl < INF)  // warp-uniform: every lane calls it
-        for (int r = 0; r < R; r++) bfs_soft_preds<true>(g, s, vv[r], nl, lout, cout, visited);
+        for (int r = 0; r < R; r++) bfs_soft_preds<0>(g, s, vv[r], nl, lout, cout, visited);
     int k = 0;
 #pragma unroll
     for (int r = 0; r < R; r++)
@@ -1303,6 +1308,37 @@ __global__ void k_lc_ghost(Geo g, Soa s, int side, const int32_t *__restrict__ o
         }
         warp_append(u0 >= 0, u0, lout, cout);
         warp_append(u1 >= 0, u1, lout, cout);
+        if (g.soft_k) {  // soft arcs between the boundary plane and the ghost plane (warp-uniform loop)
+            const int bdir = side ? 0 : 1;  // this slab's arcs toward the ghost plane
+            const int kmax = min(g.soft_k, g.delta);
+            bool live = false;
+            int nl = 0, z = 0;
+            int64_t gv = 0, col0 = 0;
+            if (i < g.YZ) {
+                gv = gbase + i;
+                const int l = s.H[gv];
+                live = l < g.INF && l < old[i];
+                nl = l + 1;
+                z = (int)(i % g.Z);
+                col0 = bbase + (i - z);
+            }
+            for (int k = 0; k < kmax; k++) {
+                const int cap = g.soft_cap[k];
+                int a = -1, b = -1;
+                auto relax = [&](int64_t w) -> int {
+                    if (s.H[w] > nl && atomicMin(&s.H[w], nl) > nl && vstamp[w] != tag &&
+                        atomicExch(&vstamp[w], tag) != tag)
+                        return (int)w;
+                    return -1;
+                };
+                if (live && cap > 0) {
+                    if (z + k < g.Z && cap - *soft_flow(g, s, col0 + z + k, bdir, k) > 0) a = relax(col0 + z + k);
+                    if (z - k >= 0 && *soft_flow(g, s, gv, ldir, k) > 0) b = relax(col0 + z - k);
+                }
+                warp_append(a >= 0, a, lout, cout);
+                warp_append(b >= 0, b, lout, cout);
+            }
+        }
     }
 }
 
@@ -1315,20 +1351,30 @@ __global__ void k_lc_ghost(Geo g, Soa s, int side, const int32_t *__restrict__ o
 //   [3] L  : the boundary plane's lateral flow toward the neighbour (its ghost residual)
 // The receiver adds dE, subtracts dL (it is the single decrementer's delta), lists the
 // vertices that received excess, and refreshes its ghost plane with H and L - (its own dL).
-__global__ void k_halo_pack(Geo g, Soa s, int side, const int32_t *__restrict__ snap, int32_t *send) {
+// Soft graphs add 2 K planes: [4 YZ + i K + k] the consumed part of the ghost copy of the
+// neighbour's soft flows toward us (its reverse arcs were used here), [4 YZ + YZ K + i K + k]
+// this slab's boundary soft flows toward the neighbour (refreshes its ghost copy).  Same rule
+// as L: a flow lives at its tail, the other side only decrements a lower-bound copy.
+__global__ void k_halo_pack(Geo g, Soa s, int side, const int32_t *__restrict__ snap, const int32_t *__restrict__ ssnap,
+                            int32_t *send) {
     const int64_t gbase = side ? g.n : -g.YZ, bbase = side ? g.n - g.YZ : 0;
     const int gdir = side ? 1 : 0, bdir = side ? 0 : 1;
+    const int K = g.soft_k;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.YZ; i += (int64_t)gridDim.x * blockDim.x) {
         send[i] = s.E[gbase + i];
         send[g.YZ + i] = snap[i] - s.L[gdir][gbase + i];
         send[2 * g.YZ + i] = s.H[bbase + i];
         send[3 * g.YZ + i] = s.L[bdir][bbase + i];
+        for (int k = 0; k < K; k++) {
+            send[4 * g.YZ + i * K + k] = ssnap[i * K + k] - *soft_flow(g, s, gbase + i, gdir, k);
+            send[4 * g.YZ + g.YZ * K + i * K + k] = *soft_flow(g, s, bbase + i, bdir, k);
+        }
     }
 }
 
 __global__ void k_halo_unpack(Geo g, Soa s, int side, const int32_t *__restrict__ recv,
-                              const int32_t *__restrict__ sent, int32_t *snap, int *lout, unsigned *cout, int *vstamp,
-                              int tag, int *flags) {
+                              const int32_t *__restrict__ sent, int32_t *snap, int32_t *ssnap, int *lout,
+                              unsigned *cout, int *vstamp, int tag, int *flags) {
     const int64_t gbase = side ? g.n : -g.YZ, bbase = side ? g.n - g.YZ : 0;
     const int gdir = side ? 1 : 0, bdir = side ? 0 : 1;
     for (int64_t b0 = gwarp() * 32; b0 < g.YZ; b0 += nwarps() * 32) {
@@ -1350,6 +1396,13 @@ __global__ void k_halo_unpack(Geo g, Soa s, int side, const int32_t *__restrict_
             s.L[gdir][gv] = lg;
             snap[i] = lg;
             s.E[gv] = 0;
+            const int K = g.soft_k;
+            for (int k = 0; k < K; k++) {
+                *soft_flow(g, s, bv, bdir, k) -= recv[4 * g.YZ + i * K + k];
+                const int fg = recv[4 * g.YZ + g.YZ * K + i * K + k] - sent[4 * g.YZ + i * K + k];
+                *soft_flow(g, s, gv, gdir, k) = fg;
+                ssnap[i * K + k] = fg;
+            }
         }
         warp_append(add, (int)(bbase + i), lout, cout);
     }

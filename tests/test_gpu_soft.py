@@ -115,3 +115,26 @@ def test_soft_full_size_c3(cg):
     f = np.array([0] + pen, np.int64)
     assert r["flow"] == pins.surface_cost(c, s) + int(f[dsx].sum() + f[dsy].sum()) + pins.k0(c)
     assert np.array_equal(r["mask"].sum(axis=2) - 1, s)
+
+
+def test_soft_slabs_random(cg):
+    """x-slabs (in-process transport: the NCCL path's messages, device copies) with soft arcs."""
+    for i, (c, dxy, pen) in enumerate(cases(250, 65)):
+        if c.shape[0] < 2:
+            continue
+        ns = 2 + i % min(3, c.shape[0] - 1)
+        t = torch.from_numpy(c).cuda()
+        r = cg.solve(t, dxy, penalty=pen, nslabs=ns)
+        o = oracle.colgraph_solve(c, dxy, penalty=pen)
+        assert r["status"] == 0, (i, r["status"])
+        assert r["flow"] == o["flow"], (i, ns, c.shape, dxy, pen)
+        assert np.array_equal(r["mask"].cpu().numpy(), o["mask"]), (i, ns)
+
+
+@pytest.mark.parametrize("name,ns,pen", [("C1", 3, [3, 8]), ("C2", 4, [5, 12, 25])])
+def test_soft_slabs_configs(cg, name, ns, pen):
+    c = V.generate(name)
+    delta = V.CONFIGS[name].delta
+    o = oracle.colgraph_solve(c, delta, penalty=pen)
+    r = cg.solve(torch.from_numpy(c).cuda(), delta, penalty=pen, nslabs=ns)
+    assert r["flow"] == o["flow"] and np.array_equal(r["mask"].cpu().numpy(), o["mask"])
