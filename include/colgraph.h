@@ -192,7 +192,7 @@ cg_status colgraph_build_slabs(const cg_dims *dims, const int32_t *cost_dev, int
  * pair costs f(d).  maxflow_solve / mincut_extract_surface then minimise
  * sum c(x,y,S) + sum_pairs f(|dS|).  With cg_dist.nranks > 1 it is the NCCL x-slab path of
  * colgraph_build (the halo message grows by 2 K planes of soft-arc flows).  Tiles
- * (CG_SWEEP_TILES) and maxflow_export_flow are not available for soft graphs (CG_E_INVAL).
+ * (CG_SWEEP_TILES) are not available for soft graphs (CG_E_INVAL).
  * Errors: as colgraph_build; CG_E_INVAL for a non-convex / too short / NULL penalty. */
 cg_status colgraph_build_soft(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight,
                               const int32_t *penalty, int32_t npenalty, const cg_dist *dist, cg_graph **out);
@@ -232,10 +232,12 @@ cg_status mincut_extract_surface(cg_graph *g, int32_t *surface_dev, uint8_t *mas
  *   cost_dev : the SAME device input and mode passed to colgraph_build (the source / sink
  *              capacities are recomputed from it; the handle does not keep them).
  *   opts     : solver options for phase 2 (nullable; sweep_kind is forced to the vertex kind).
- *   flow_dev : device int32[7 * n], planes of n = X*Y*Z in index order (x*Y + y)*Z + z:
+ *   flow_dev : device int32[(7 + 4 K) * n] (K = 0, or max(Delta_x, Delta_y) for soft graphs),
+ *              planes of n = X*Y*Z in index order (x*Y + y)*Z + z:
  *              [0] s->v   [1] v->t   [2] down arc v -> (x,y,z-1)
  *              [3..6] lateral arc of v in direction +x, -x, +y, -y, i.e. v -> (nbr, zo(z))
- *              with zo(0) = 0, zo(z) = z - Delta for z > Delta (reading R2).
+ *              with zo(0) = 0, zo(z) = z - Delta for z > Delta (reading R2)
+ *              [7 + d K + k] soft graphs: the soft arc v -> (nbr_d, z - k).
  * Single-slab handles only.  Call mincut_extract_surface BEFORE this (afterwards it returns
  * CG_E_STATE: the handle then holds a flow, not a preflow).
  * Errors: CG_E_INVAL (NULL, multi-slab handle), CG_E_STATE (not solved / already exported),

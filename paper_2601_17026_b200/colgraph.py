@@ -259,14 +259,15 @@ def colgraph_stats(handle) -> dict:
     return stats.as_dict()
 
 
-def maxflow_export_flow(handle, cost, input_is_weight: bool = False, flow=None, opts: cg_solve_opts | None = None):
+def maxflow_export_flow(handle, cost, input_is_weight: bool = False, flow=None, opts: cg_solve_opts | None = None,
+                        soft_k: int = 0):
     """Phase 2 + flow export (include/colgraph.h).  cost: the CUDA int32 input given to
-    colgraph_build.  Returns (status, flow) with flow a CUDA int32 tensor [7, X, Y, Z]:
-    s->v, v->t, down, lateral +x, -x, +y, -y."""
+    colgraph_build.  Returns (status, flow) with flow a CUDA int32 tensor [7 + 4 K, X, Y, Z]:
+    s->v, v->t, down, lateral +x, -x, +y, -y, then the soft arcs (soft_k = K for soft graphs)."""
     import torch
     _check_dev_int32(cost, "cost")
     if flow is None:
-        flow = torch.empty((7,) + tuple(cost.shape), dtype=torch.int32, device=cost.device)
+        flow = torch.empty((7 + 4 * soft_k,) + tuple(cost.shape), dtype=torch.int32, device=cost.device)
     _check_dev_int32(flow, "flow")
     st = _lib.maxflow_export_flow(handle, ctypes.c_void_p(cost.data_ptr()), int(bool(input_is_weight)),
                                   ctypes.byref(opts) if opts is not None else None, ctypes.c_void_p(flow.data_ptr()))

@@ -1316,7 +1316,7 @@ static cg_status maxflow_export_flow_impl(cg_graph *g, const int32_t *cost_dev, 
                               int32_t *flow_dev) {
     if (!g || !cost_dev || !flow_dev) return CG_E_INVAL;
     if (!g->solved || g->exported) return CG_E_STATE;
-    if (multi(g) || g->slabs.size() != 1 || g->slabs[0]->geo.soft_k) return CG_E_INVAL;
+    if (multi(g) || g->slabs.size() != 1) return CG_E_INVAL;
     DeviceGuard dg(g->dist.device);
     cg_solve_opts o{};
     bool use_tiles = false;
@@ -1344,7 +1344,8 @@ static cg_status maxflow_export_flow_impl(cg_graph *g, const int32_t *cost_dev, 
         // lateral arcs stay on the level (z = 0, Delta_d = 0) first net antiparallel flows,
         // then repeat until a pass sees no excess there (at most SAME_LEVEL_PASSES)
         constexpr int SAME_LEVEL_PASSES = 64;
-        const bool flat = geo.delta == 0 || geo.delta_y == 0;
+        // soft graphs: k = 0 soft arcs stay on every level
+        const bool flat = geo.delta == 0 || geo.delta_y == 0 || (geo.soft_k > 0 && geo.soft_cap[0] > 0);
         const int grid = grid_for(ncol, 256, sl->num_sms * 8);
         for (int z = 0; z < geo.Z; z++) {
             const bool same_level = z == 0 || flat;

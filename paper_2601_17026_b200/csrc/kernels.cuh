@@ -130,6 +130,17 @@ __global__ void k_return_level(Geo g, Soa s, int z, unsigned *left) {
             if (!owned(g, u)) continue;
             cancel(&s.L[d ^ 1][u], &s.E[u]);
         }
+        for (int d = 0; d < 4 && e > 0 && g.soft_k; d++) {  // soft inflows from (nbr, z + k), level >= z
+            const int64_t o = nbr_off(g, x, y, d);
+            if (!o) continue;
+            const int kmax = min(g.soft_k, delta_d(g, d));
+            for (int k = 0; k < kmax && e > 0; k++) {
+                if (z + k >= g.Z) break;
+                const int64_t u = col * g.Z + o + z + k;
+                if (!owned(g, u)) continue;
+                cancel(soft_flow(g, s, u, d ^ 1, k), &s.E[u]);
+            }
+        }
         if (taken) atomicSub(&s.E[v], taken);
     }
     myleft = warp_sum_i((int)myleft);
@@ -156,6 +167,18 @@ __global__ void k_net_level(Geo g, Soa s, int z) {
             if (m > 0) {
                 s.L[d][v] = a - m;
                 s.L[d ^ 1][v + o] = b - m;
+            }
+        }
+#pragma unroll
+        for (int d = 0; d < 4; d += 2) {  // soft arcs with k = 0 stay on the level
+            if (!g.soft_k || g.soft_cap[0] <= 0 || delta_d(g, d) < 1) continue;
+            const int64_t o = nbr_off(g, x, y, d);
+            if (!o || !owned(g, v + o)) continue;
+            int32_t *fa = soft_flow(g, s, v, d, 0), *fb = soft_flow(g, s, v + o, d ^ 1, 0);
+            const int m = min(*fa, *fb);
+            if (m > 0) {
+                *fa -= m;
+                *fb -= m;
             }
         }
     }
@@ -188,6 +211,8 @@ __global__ void k_flow_export(Geo g, const int32_t *__restrict__ in, int weight_
             out[2 * n + v] = s.D[v];
 #pragma unroll
             for (int d = 0; d < 4; d++) out[(3 + d) * n + v] = s.L[d][v];
+            for (int d = 0; d < 4 && g.soft_k; d++)  // soft graphs: planes 7 + d K + k
+                for (int k = 0; k < g.soft_k; k++) out[(7 + d * g.soft_k + k) * n + v] = *soft_flow(g, s, v, d, k);
             b |= s.E[v] != 0;
         }
     }

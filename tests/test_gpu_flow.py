@@ -39,10 +39,18 @@ def sl(dx, X):  # (source slice, target slice) along one axis for a shift dx
     return slice(max(0, -dx), X - max(0, dx)), slice(max(0, dx), X - max(0, -dx))
 
 
-def check_flow(c, delta, F, weight=False):
+def soft_caps(penalty):
+    f = [0] + [int(v) for v in penalty]
+    return [f[1]] + [f[k + 1] - 2 * f[k] + f[k - 1] for k in range(1, len(penalty))]
+
+
+def check_flow(c, delta, F, weight=False, penalty=None):
     X, Y, Z = c.shape
     n = X * Y * Z
     fs, ft, fd, *L = [F[i].astype(np.int64) for i in range(7)]
+    dxy0 = tuple(delta) if isinstance(delta, (tuple, list)) else (delta, delta)
+    K = max(dxy0) if penalty is not None else 0  # the library's soft arcs per direction
+    caps = soft_caps(penalty)[:K] if K else []
     w = weights(c, weight)
     E0, T0 = np.maximum(-w, 0), np.maximum(w, 0)
     zs = np.arange(Z)
@@ -59,6 +67,20 @@ def check_flow(c, delta, F, weight=False):
         if dx == -1: assert (L[d][0] == 0).all()
         if dy == 1: assert (L[d][:, Y - 1] == 0).all()
         if dy == -1: assert (L[d][:, 0] == 0).all()
+    dxy_ = tuple(delta) if isinstance(delta, (tuple, list)) else (delta, delta)
+    SF = {}
+    for d in range(4 if K else 0):
+        for k in range(K):
+            f = F[7 + d * K + k].astype(np.int64)
+            SF[d, k] = f
+            dx, dy = DIRS[d]
+            exists = np.zeros((X, Y, Z), bool)
+            if k < dxy_[d >> 1] and caps[k] > 0:
+                xs, _ = sl(dx, X)
+                ys, _ = sl(dy, Y)
+                exists[xs, ys, k:] = True
+            assert (f >= 0).all() and (f <= (caps[k] if caps else 0)).all(), (d, k)
+            assert (f[~exists] == 0).all(), (d, k)
     # Eq. 4: conservation at every vertex
     net = fs - ft - fd
     net[:, :, :-1] += fd[:, :, 1:]
@@ -72,6 +94,13 @@ def check_flow(c, delta, F, weight=False):
         tgt = net[xt, yt]
         for k, z in enumerate(zs[valid]):
             tgt[:, :, zo[z]] += src[:, :, k]
+    for (d, k), f in SF.items():
+        dx, dy = DIRS[d]
+        xs, xt = sl(dx, X)
+        ys, yt = sl(dy, Y)
+        net -= f
+        if Z - k > 0:
+            net[xt, yt, :Z - k] += f[xs, ys, k:]
     assert not net.any(), "conservation violated"
     assert ft.sum() == fs.sum()
     # residual graph of the flow; BFS from s
@@ -95,6 +124,19 @@ def check_flow(c, delta, F, weight=False):
         rows.append(tail.ravel()); cols.append(head.ravel())
         m = L[d][xs, ys][:, :, vz] > 0
         rows.append(head[m]); cols.append(tail[m])
+    for (d, k), f in SF.items():
+        if Z - k <= 0:
+            continue
+        dx, dy = DIRS[d]
+        xs, xt = sl(dx, X)
+        ys, yt = sl(dy, Y)
+        tail = idx[xs, ys][:, :, k:]
+        head = idx[xt, yt][:, :, :Z - k]
+        fk = f[xs, ys][:, :, k:]
+        m = fk < caps[k]
+        rows.append(tail[m]); cols.append(head[m])
+        m = fk > 0
+        rows.append(head[m]); cols.append(tail[m])
     r = np.concatenate(rows); cl = np.concatenate(cols)
     g = sp.csr_matrix((np.ones(len(r), np.int8), (r, cl)), shape=(n + 2, n + 2))
     reach = breadth_first_order(g, s_node, directed=True, return_predecessors=False)
@@ -104,16 +146,17 @@ def check_flow(c, delta, F, weight=False):
     return int(ft.sum()), mask.reshape(X, Y, Z)
 
 
-def export(cg, c, delta, weight=False, opts=None, extract_first=True):
+def export(cg, c, delta, weight=False, opts=None, extract_first=True, penalty=None):
     t = torch.from_numpy(np.ascontiguousarray(c, np.int32)).cuda()
-    h = cg.colgraph_build(t, delta, weight)
+    h = cg.colgraph_build_soft(t, delta, penalty, weight) if penalty is not None else cg.colgraph_build(t, delta, weight)
     try:
         st, flow, _ = cg.maxflow_solve(h, None)
         assert st == 0
         if extract_first:
             surf = torch.empty(c.shape[:2], dtype=torch.int32, device="cuda")
             assert cg.mincut_extract_surface(h, surf) in (0, 6)
-        st, F = cg.maxflow_export_flow(h, t, weight, opts=opts)
+        dxy0 = tuple(delta) if isinstance(delta, (tuple, list)) else (delta, delta)
+        st, F = cg.maxflow_export_flow(h, t, weight, opts=opts, soft_k=max(dxy0) if penalty is not None else 0)
         assert st == 0, cg.STATUS.get(st)
         if extract_first:
             surf2 = torch.empty(c.shape[:2], dtype=torch.int32, device="cuda")

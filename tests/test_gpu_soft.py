@@ -94,7 +94,6 @@ def test_soft_errors(cg):
     try:
         assert cg.maxflow_solve(h, cg.make_opts(sweep_kind=cg.SWEEP_TILES))[0] == cg.CG_E_INVAL
         assert cg.maxflow_solve(h, None)[0] == 0
-        assert cg.maxflow_export_flow(h, t)[0] == cg.CG_E_INVAL
     finally:
         cg.colgraph_free(h)
 
@@ -138,3 +137,22 @@ def test_soft_slabs_configs(cg, name, ns, pen):
     o = oracle.colgraph_solve(c, delta, penalty=pen)
     r = cg.solve(torch.from_numpy(c).cuda(), delta, penalty=pen, nslabs=ns)
     assert r["flow"] == o["flow"] and np.array_equal(r["mask"].cpu().numpy(), o["mask"])
+
+
+def test_soft_flow_export(cg, monkeypatch):
+    """NEXT-1 x NEXT-2: the maximum flow of a soft graph, checked against the definitions
+    (capacities incl. soft arcs, conservation, value = oracle, residual cut = oracle mask)."""
+    from tests.test_gpu_flow import check_flow, export
+    for i, (c, dxy, pen) in enumerate(cases(150, 66)):
+        K = max(dxy[0], dxy[1], 1)
+        pen = list(pen[:K]) + [int(pen[-1])] * (K - len(pen))
+        o = oracle.colgraph_solve(c, dxy, penalty=pen)
+        flow, F = export(cg, c, dxy, penalty=pen)
+        val, mask = check_flow(c, dxy, F, penalty=pen)
+        assert flow == val == o["flow"] and np.array_equal(mask, o["mask"]), i
+    monkeypatch.setenv("CG_PHASE2_PR", "1")  # the generic phase 2 on soft graphs
+    for i, (c, dxy, pen) in enumerate(cases(60, 67)):
+        o = oracle.colgraph_solve(c, dxy, penalty=pen)
+        flow, F = export(cg, c, dxy, penalty=list(pen))
+        val, mask = check_flow(c, dxy, F, penalty=list(pen))
+        assert flow == val == o["flow"] and np.array_equal(mask, o["mask"]), i
