@@ -1,2 +1,2 @@
 set -x
-timeout 900 python -m pytest tests/test_gpu_soft.py tests/test_gpu_flow.py -x -q > gpurun_out/t_soft.log 2>&1
+timeout 900 python scripts/soft_timing.py C2,C3,C4 > gpurun_out/softtime.log 2>&1
