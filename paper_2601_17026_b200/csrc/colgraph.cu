@@ -389,6 +389,7 @@ cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode) {
 // this process's sum on entry).
 cg_status gsum(cg_graph *g, int64_t *v, int count) {
     if (g->local || g->nranks == 1) return CG_OK;
+    if (count > RING + 8) return CG_E_INVAL;
     Slab *sl = g->slabs[0];
     memcpy(g->h_red, v, sizeof(int64_t) * count);
     CG_CUDA(cudaMemcpyAsync(g->d_red, g->h_red, sizeof(int64_t) * count, cudaMemcpyHostToDevice, sl->stream));
@@ -1076,8 +1077,9 @@ static cg_status build_common(const cg_dims *dims, const int32_t *cost_dev, int3
     if (!local && nranks > 1) {
         if (!dd.nccl_id || !nccl().ok) return fail(CG_E_NCCL);
         if (comm_acquire(dd.nccl_id, rank, nranks, dd.device, &g->comm) != CG_OK) return fail(CG_E_NCCL);
-        if (cudaMalloc(&g->d_red, 64 * sizeof(int64_t)) != cudaSuccess ||
-            cudaHostAlloc(&g->h_red, 64 * sizeof(int64_t), cudaHostAllocDefault) != cudaSuccess)
+        // allreduce buffers: one counter per sweep of a batch (<= RING) + the overflow flag
+        if (cudaMalloc(&g->d_red, (RING + 8) * sizeof(int64_t)) != cudaSuccess ||
+            cudaHostAlloc(&g->h_red, (RING + 8) * sizeof(int64_t), cudaHostAllocDefault) != cudaSuccess)
             return fail(CG_E_NOMEM);
     }
     for (int i = 0; i < nslabs_local; i++) {
