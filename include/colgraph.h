@@ -238,9 +238,11 @@ cg_status mincut_extract_surface(cg_graph *g, int32_t *surface_dev, uint8_t *mas
  *              [3..6] lateral arc of v in direction +x, -x, +y, -y, i.e. v -> (nbr, zo(z))
  *              with zo(0) = 0, zo(z) = z - Delta for z > Delta (reading R2)
  *              [7 + d K + k] soft graphs: the soft arc v -> (nbr_d, z - k).
- * Single-slab handles only.  Call mincut_extract_surface BEFORE this (afterwards it returns
- * CG_E_STATE: the handle then holds a flow, not a preflow).
- * Errors: CG_E_INVAL (NULL, multi-slab handle), CG_E_STATE (not solved / already exported),
+ * x-slabs: with colgraph_build_slabs* the input and flow_dev are whole-volume arrays (planes of
+ * n = X*Y*Z); with NCCL ranks each rank passes its own slab (planes of n = X_r*Y*Z).  Collective.
+ * Call mincut_extract_surface BEFORE this (afterwards it returns CG_E_STATE: the handle then
+ * holds a flow, not a preflow).
+ * Errors: CG_E_INVAL (NULL), CG_E_STATE (not solved / already exported),
  *         CG_E_NOT_CONVERGED (max_sweeps hit, or excess left), CG_E_CUDA. */
 cg_status maxflow_export_flow(cg_graph *g, const int32_t *cost_dev, int32_t input_is_weight, const cg_solve_opts *opts,
                               int32_t *flow_dev);

@@ -1318,52 +1318,69 @@ static cg_status maxflow_export_flow_impl(cg_graph *g, const int32_t *cost_dev, 
                               int32_t *flow_dev) {
     if (!g || !cost_dev || !flow_dev) return CG_E_INVAL;
     if (!g->solved || g->exported) return CG_E_STATE;
-    if (multi(g) || g->slabs.size() != 1) return CG_E_INVAL;
     DeviceGuard dg(g->dist.device);
     cg_solve_opts o{};
     bool use_tiles = false;
     cg_solve_opts oo = opts ? *opts : cg_solve_opts{};
     oo.sweep_kind = CG_SWEEP_VERTEX;  // phase 2 runs on the vertex worklists
     CG_TRY(normalize_opts(g, &oo, o, use_tiles));
-    Slab *sl = g->slabs[0];
-    const Geo &geo = sl->geo;
-    const int64_t ncol = (int64_t)geo.X * geo.Y;
-    int32_t *tmp = nullptr;
-    CG_CUDA(cudaMallocAsync(&tmp, sizeof(int32_t) * geo.n, sl->stream));
-    // phase 2 (NEXT-2): the terminal of the push-relabel becomes s -- T(v) := flow on s->v,
-    // the phase-1 sink residuals are parked in tmp -- and the same solver returns every unit of
-    // stranded excess to s.  Vertices with excess cannot reach t (maximum preflow), so no
-    // flow into t changes.
-    k_phase2_setup<<<grid_for(ncol * 32, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(geo, cost_dev,
-                                                                                       input_is_weight ? 1 : 0,
-                                                                                       sl->s, tmp);
-    g->st.kernel_launches++;
+    const int ns = (int)g->slabs.size();
+    // LOCAL slabs: cost_dev / flow_dev are whole-volume arrays; NCCL / single: this slab's
+    const int64_t plane_stride = g->local ? g->n_global : g->slabs[0]->geo.n;
+    std::vector<int32_t *> tmp(ns, nullptr);
+    for (int i = 0; i < ns; i++) {
+        Slab *sl = g->slabs[i];
+        const Geo &geo = sl->geo;
+        const int64_t ncol = (int64_t)geo.X * geo.Y;
+        const int32_t *src = g->local ? cost_dev + (int64_t)sl->x0 * geo.YZ : cost_dev;
+        CG_CUDA(cudaMallocAsync(&tmp[i], sizeof(int32_t) * std::max<int64_t>(1, geo.n), sl->stream));
+        // phase 2 (NEXT-2): the terminal becomes s -- T(v) := flow on s->v, the phase-1 sink
+        // residuals are parked in tmp.  Vertices with excess cannot reach t (maximum preflow),
+        // so no flow into t changes.
+        k_phase2_setup<<<grid_for(ncol * 32, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(geo, src,
+                                                                                           input_is_weight ? 1 : 0,
+                                                                                           sl->s, tmp[i]);
+        g->st.kernel_launches++;
+    }
     CG_CUDA(cudaGetLastError());
     cg_status r = CG_OK;
     const bool pr_only = getenv("CG_PHASE2_PR") != nullptr;  // the generic alternative (slow tail)
+    const Geo &g0 = g->slabs[0]->geo;
     if (!pr_only) {
-        // level-ordered cancellation (k_return_level): one launch per level; levels whose
-        // lateral arcs stay on the level (z = 0, Delta_d = 0) first net antiparallel flows,
-        // then repeat until a pass sees no excess there (at most SAME_LEVEL_PASSES)
+        // level-ordered cancellation (k_return_level): one pass per level; levels whose lateral
+        // arcs stay on the level (z = 0, Delta_d = 0, k = 0 soft arcs) first net antiparallel
+        // flows, then repeat until a pass sees no excess there (at most SAME_LEVEL_PASSES).
+        // x-slabs: a halo exchange after every pass delivers the excess cancelled into ghost
+        // vertices (and the consumed ghost residuals) before the owner reaches that level.
         constexpr int SAME_LEVEL_PASSES = 64;
-        // soft graphs: k = 0 soft arcs stay on every level
-        const bool flat = geo.delta == 0 || geo.delta_y == 0 || (geo.soft_k > 0 && geo.soft_cap[0] > 0);
-        const int grid = grid_for(ncol, 256, sl->num_sms * 8);
-        for (int z = 0; z < geo.Z; z++) {
+        const bool flat = g0.delta == 0 || g0.delta_y == 0 || (g0.soft_k > 0 && g0.soft_cap[0] > 0);
+        for (int z = 0; z < g0.Z && r == CG_OK; z++) {
             const bool same_level = z == 0 || flat;
-            if (same_level) {
-                k_net_level<<<grid, 256, 0, sl->stream>>>(geo, sl->s, z);
-                g->st.kernel_launches++;
-            }
+            for (Slab *sl : g->slabs)
+                if (same_level) {
+                    k_net_level<<<grid_for((int64_t)sl->geo.X * sl->geo.Y, 256, sl->num_sms * 8), 256, 0,
+                                  sl->stream>>>(sl->geo, sl->s, z);
+                    g->st.kernel_launches++;
+                }
             for (int it = 0; it < (same_level ? SAME_LEVEL_PASSES : 1); it++) {
-                if (same_level) CG_CUDA(cudaMemsetAsync(sl->cnt + 13, 0, sizeof(unsigned), sl->stream));
-                k_return_level<<<grid, 256, 0, sl->stream>>>(geo, sl->s, z, sl->cnt + 13);
-                g->st.kernel_launches++;
+                for (Slab *sl : g->slabs) {
+                    if (same_level) CG_CUDA(cudaMemsetAsync(sl->cnt + 13, 0, sizeof(unsigned), sl->stream));
+                    k_return_level<<<grid_for((int64_t)sl->geo.X * sl->geo.Y, 256, sl->num_sms * 8), 256, 0,
+                                     sl->stream>>>(sl->geo, sl->s, z, sl->cnt + 13);
+                    g->st.kernel_launches++;
+                }
+                if (multi(g)) CG_TRY(halo_sweep(g));
                 if (!same_level) break;
-                CG_CUDA(cudaMemcpyAsync(sl->h_cnt + 13, sl->cnt + 13, sizeof(unsigned), cudaMemcpyDeviceToHost,
-                                        sl->stream));
-                CG_CUDA(cudaStreamSynchronize(sl->stream));
-                if (sl->h_cnt[13] == 0) break;
+                int64_t seen = 0;
+                for (Slab *sl : g->slabs)
+                    CG_CUDA(cudaMemcpyAsync(sl->h_cnt + 13, sl->cnt + 13, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                            sl->stream));
+                for (Slab *sl : g->slabs) {
+                    CG_CUDA(cudaStreamSynchronize(sl->stream));
+                    seen += sl->h_cnt[13];
+                }
+                CG_TRY(gsum(g, &seen, 1));
+                if (seen == 0) break;
             }
         }
         CG_CUDA(cudaGetLastError());
@@ -1371,26 +1388,47 @@ static cg_status maxflow_export_flow_impl(cg_graph *g, const int32_t *cost_dev, 
     {
         // whatever a capped same-level level left (cycles longer than 2) goes back to s by the
         // generic phase-2 push-relabel (exact; rarely needed)
-        CG_CUDA(cudaMemsetAsync(sl->cnt + 14, 0, sizeof(unsigned), sl->stream));
-        k_count_excess<<<grid_for(geo.n, 256, sl->num_sms * 8), 256, 0, sl->stream>>>(geo, sl->s, sl->cnt + 14);
-        CG_CUDA(cudaMemcpyAsync(sl->h_cnt + 14, sl->cnt + 14, sizeof(unsigned), cudaMemcpyDeviceToHost, sl->stream));
-        CG_CUDA(cudaStreamSynchronize(sl->stream));
-        if (pr_only || sl->h_cnt[14]) {
+        int64_t left = 0;
+        for (Slab *sl : g->slabs) {
+            CG_CUDA(cudaMemsetAsync(sl->cnt + 14, 0, sizeof(unsigned), sl->stream));
+            k_count_excess<<<grid_for(sl->geo.n, 256, sl->num_sms * 8), 256, 0, sl->stream>>>(sl->geo, sl->s,
+                                                                                               sl->cnt + 14);
+            CG_CUDA(cudaMemcpyAsync(sl->h_cnt + 14, sl->cnt + 14, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                    sl->stream));
+        }
+        for (Slab *sl : g->slabs) {
+            CG_CUDA(cudaStreamSynchronize(sl->stream));
+            left += sl->h_cnt[14];
+        }
+        CG_TRY(gsum(g, &left, 1));
+        if (pr_only || left) {
             double ms_gr = 0.0;
             r = pr_loop(g, o, false, ms_gr);
         }
     }
     if (r == CG_OK) {
-        CG_CUDA(cudaMemsetAsync(sl->flags + 3, 0, sizeof(int), sl->stream));
-        k_flow_export<<<grid_for(ncol * 32, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(
-            geo, cost_dev, input_is_weight ? 1 : 0, sl->s, tmp, flow_dev, sl->flags + 3);
-        g->st.kernel_launches++;
-        CG_CUDA(cudaMemcpyAsync(sl->h_flags + 3, sl->flags + 3, sizeof(int), cudaMemcpyDeviceToHost, sl->stream));
-        CG_CUDA(cudaStreamSynchronize(sl->stream));
-        if (sl->h_flags[3]) r = CG_E_NOT_CONVERGED;  // some vertex kept excess: not a flow
+        int64_t bad = 0;
+        for (int i = 0; i < ns; i++) {
+            Slab *sl = g->slabs[i];
+            const Geo &geo = sl->geo;
+            const int64_t ncol = (int64_t)geo.X * geo.Y;
+            const int32_t *src = g->local ? cost_dev + (int64_t)sl->x0 * geo.YZ : cost_dev;
+            int32_t *dst = g->local ? flow_dev + (int64_t)sl->x0 * geo.YZ : flow_dev;
+            CG_CUDA(cudaMemsetAsync(sl->flags + 3, 0, sizeof(int), sl->stream));
+            k_flow_export<<<grid_for(ncol * 32, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(
+                geo, src, input_is_weight ? 1 : 0, sl->s, tmp[i], dst, plane_stride, sl->flags + 3);
+            g->st.kernel_launches++;
+            CG_CUDA(cudaMemcpyAsync(sl->h_flags + 3, sl->flags + 3, sizeof(int), cudaMemcpyDeviceToHost, sl->stream));
+        }
+        for (Slab *sl : g->slabs) {
+            CG_CUDA(cudaStreamSynchronize(sl->stream));
+            bad |= sl->h_flags[3];
+        }
+        CG_TRY(gmax(g, &bad));
+        if (bad) r = CG_E_NOT_CONVERGED;  // some vertex kept excess: not a flow
     }
-    cudaFreeAsync(tmp, sl->stream);
-    CG_CUDA(cudaStreamSynchronize(sl->stream));
+    for (int i = 0; i < ns; i++) cudaFreeAsync(tmp[i], g->slabs[i]->stream);
+    for (Slab *sl : g->slabs) CG_CUDA(cudaStreamSynchronize(sl->stream));
     g->exported = true;
     return r;
 }

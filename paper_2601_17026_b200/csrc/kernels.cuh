@@ -126,8 +126,7 @@ __global__ void k_return_level(Geo g, Soa s, int z, unsigned *left) {
             const int64_t o = nbr_off(g, x, y, d);
             const int zi = zi_of(z, delta_d(g, d), g.Z);
             if (!o || zi < 0) continue;
-            const int64_t u = col * g.Z + o + zi;
-            if (!owned(g, u)) continue;
+            const int64_t u = col * g.Z + o + zi;  // may be a ghost vertex: the halo delivers E(u)
             cancel(&s.L[d ^ 1][u], &s.E[u]);
         }
         for (int d = 0; d < 4 && e > 0 && g.soft_k; d++) {  // soft inflows from (nbr, z + k), level >= z
@@ -137,7 +136,6 @@ __global__ void k_return_level(Geo g, Soa s, int z, unsigned *left) {
             for (int k = 0; k < kmax && e > 0; k++) {
                 if (z + k >= g.Z) break;
                 const int64_t u = col * g.Z + o + z + k;
-                if (!owned(g, u)) continue;
                 cancel(soft_flow(g, s, u, d ^ 1, k), &s.E[u]);
             }
         }
@@ -196,8 +194,8 @@ __global__ void k_count_excess(Geo g, const Soa s, unsigned *count) {
 // out planes (int32[7][n]): s->v, v->t, down v->v-1, lateral +x, -x, +y, -y.  Any vertex left
 // with excess sets *bad (the result would not be a flow).
 __global__ void k_flow_export(Geo g, const int32_t *__restrict__ in, int weight_mode, Soa s,
-                              const int32_t *__restrict__ tmp, int32_t *out, int *bad) {
-    const int64_t ncol = (int64_t)g.X * g.Y, n = g.n;
+                              const int32_t *__restrict__ tmp, int32_t *out, int64_t n, int *bad) {
+    const int64_t ncol = (int64_t)g.X * g.Y;  // n: plane stride of out (whole volume for in-process slabs)
     bool b = false;
     for (int64_t col = gwarp(); col < ncol; col += nwarps()) {
         const int32_t *cc = in + col * g.Z;
