@@ -15,8 +15,8 @@ rf = bench['roofline']
 mm = bench.get('ms_per_step_min_median_max', [bench['ms_per_step']] * 3)
 table = f"""## Measured results (round 1, one B200, commit {H})
 
-Library time (build + solve + extract from the library's own timers; second run of
-`scripts/diag_solve.py`).  Parity: |f|, minimal source set and surface bit-identical to the
+Library time (build + solve + extract from the library's own timers; the median of 3 runs
+after a warm-up, `scripts/diag_solve.py`).  Parity: |f|, minimal source set and surface bit-identical to the
 CPU oracle -- C1, C2 and the tiny sweeps live, C3/C4 against stored oracle results, C5
 through |f| = cost(surface) + K0 with a Delta-feasible surface (its stored oracle result is
 still being computed on the CPU).
