@@ -277,13 +277,24 @@ def run_ours(args, spec):
                 "alg_bytes_def": "44 B per push/relabel operation: 32 B vertex state read + 12 B push writes "
                                  "(DESIGN.md 'Algorithmic bytes')",
                 "share_of_step": sweep_ms * args.steps / (ms_total * len(stats)) if ms_total > 0 else None}
+    # the sweep is a scattered traversal: its access-pattern roofline is the B200's random 32-byte
+    # record gather throughput (bench_tools/random_gather.cu, profiles/r01_random_gather.json)
+    rg_path = os.path.join(ROOT, "profiles", "r01_random_gather.json")
+    roofline_ra = None
+    if os.path.exists(rg_path):
+        rg = json.load(open(rg_path))
+        rg_peak = max(v for k, v in rg.items() if k.startswith("gather_") and k.endswith("_gbs"))
+        roofline_ra = {"kernel": roofline["kernel"], "bound": "hbm-random-32B", "achieved": achieved, "peak": rg_peak,
+                       "unit": "GB/s", "frac": achieved / rg_peak,
+                       "peak_source": "measured random 32-B record gather over 2 GiB (bench_tools/random_gather.cu, "
+                                      "profiles/r01_random_gather.json)"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "time_to_min_cut_s": ms_step / 1000.0,
             "ms_per_step_min_median_max": [step_ms[0], step_ms[len(step_ms) // 2], step_ms[-1]],
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
             "dtype": "int32", "data": "synthetic (seeded generator synth/volumes.py, sha256-pinned)",
             "config": workload_config(spec, {"parallelism": f"x-slab{world}" if world > 1 else "single-gpu"}),
-            "flow": flow, "roofline": roofline,
+            "flow": flow, "roofline": roofline, "roofline_random_access": roofline_ra,
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms, "h2d_bytes_per_step": 4 * spec.n,
                     "d2h_bytes_per_step": 4 * X * Y + 8},
             "gpu_launches": int(sum(s["kernel_launches"] for s in stats)),
