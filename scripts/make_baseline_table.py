@@ -37,8 +37,11 @@ Roofline of the dominant kernel (push-relabel sweep, `k_walk` / `k_sweep_v`): al
 {rf['achieved']:.0f} GB/s = **{100 * rf['frac']:.1f} % of the measured 6,457 GB/s copy peak** (44 B per
 push/relabel operation).  ncu (`profiles/r01_end_{H}_ncu_k_walk.json`): 31 % of DRAM peak,
 L2 hit 21 %, 7.3 active threads per warp instruction -- a divergent, latency-bound traversal
-whose DRAM traffic is ~20x its algorithmic bytes.  The >= 40 % per-sweep target of
-BASELINE.json is not met; DESIGN.md §6 explains why and lists every measured alternative.
+whose DRAM traffic is ~20x its algorithmic bytes.  Its access-pattern bound is the
+B200's random 32-byte record gather rate, measured at 625-750 GB/s (12 % of the copy peak,
+`profiles/r01_random_gather.json`): against it the sweep runs at ~23 %.  The >= 40 %
+per-sweep target of BASELINE.json (a streaming figure) is not met; DESIGN.md §6 explains
+why and lists every measured alternative.
 
 Multi-GPU (x-slabs over NCCL): implemented and verified bit-exact through the in-process
 slab transport on one GPU; not measured on 2/4/8 GPUs in round 1 (one GPU available).
