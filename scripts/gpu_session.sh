@@ -1,2 +1,2 @@
 set -x
-timeout 120 ./bench_tools/random_gather > gpurun_out/random_gather.json 2>&1
+timeout 400 python bench.py > gpurun_out/bench.log 2>&1
