@@ -1,2 +1,1 @@
-set -x
-timeout 400 python bench.py > gpurun_out/bench.log 2>&1
+timeout 1200 python scripts/slab_overhead.py C3,C4 > gpurun_out/slab_overhead.jsonl 2>&1
