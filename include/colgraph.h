@@ -40,6 +40,8 @@
  *   CG_SWEEP=1            tile sweeps (as sweep_kind = CG_SWEEP_TILES); CG_TILE=TXxTY,
  *                         CG_TILE_STEPS, CG_TILE_RELABEL, CG_TILE_PROF=1 (clock counters)
  *   CG_PHASE2_PR=1        maxflow_export_flow: generic push-relabel phase 2 only
+ *   CG_SLAB_LC=1          x-slabs: label-correcting global relabel instead of the
+ *                         level-synchronous one
  * Conventions for every entry point:
  *   - Errors are returned as cg_status, never thrown; no C++ exception crosses
  *     this ABI.

@@ -524,7 +524,83 @@ cg_status bfs_strict(cg_graph *g, Slab *sl, bool allow_coop = true) {
     return CG_OK;
 }
 
-// Label-correcting relabel across slabs: local waves until every frontier is empty, then
+// Level-synchronous relabel across slabs (default): every level, each slab expands its own
+// frontier (claiming ghost predecessors in its ghost planes), the ghost planes go to their
+// owners, and each owner claims the boundary vertices its neighbour reached -- exact BFS
+// labels, one exchange per level (~#levels exchanges instead of the label-correcting
+// variant's waves x outer rounds).  Termination is checked every SLAB_BATCH
+// levels with one global sum.
+constexpr int SLAB_BATCH = 8;
+cg_status bfs_slabs_levels(cg_graph *g) {
+    for (Slab *sl : g->slabs) {
+        const Geo &geo = sl->geo;
+        CG_CUDA(cudaMemsetAsync(sl->cnt + 4, 0, 3 * sizeof(unsigned), sl->stream));
+        k_bfs_init<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(geo, sl->s, sl->blist[0],
+                                                                                     sl->cnt + 4);
+        k_fill_ghost_h(sl);
+        g->st.kernel_launches += 1 + geo.gl + geo.gh;
+    }
+    const int64_t YZ = g->slabs[0]->geo.YZ;
+    int i = 0;  // level index: frontier of label i+1 in list[i&1] / cnt[4 + i%3]
+    for (;;) {
+        for (int b = 0; b < SLAB_BATCH; b++, i++) {
+            const int nl = i + 2;
+            for (Slab *sl : g->slabs) {
+                const Geo &geo = sl->geo;
+                k_slab_level<<<list_grid(sl, geo.n), 256, 0, sl->stream>>>(
+                    geo, sl->s, nl, sl->blist[i & 1], sl->cnt + 4 + i % 3, sl->blist[(i + 1) & 1],
+                    sl->cnt + 4 + (i + 1) % 3, sl->cnt + 4 + (i + 2) % 3);
+                const int grid = grid_for(YZ, 256, sl->num_sms * 4);
+                if (geo.gl) k_ghost_pack_h<<<grid, 256, 0, sl->stream>>>(geo, sl->s, 0, sl->hsend[0]);
+                if (geo.gh) k_ghost_pack_h<<<grid, 256, 0, sl->stream>>>(geo, sl->s, 1, sl->hsend[1]);
+                g->st.kernel_launches += 1 + geo.gl + geo.gh;
+            }
+            CG_TRY(transfer(g, YZ));
+            for (Slab *sl : g->slabs) {
+                const Geo &geo = sl->geo;
+                const int grid = grid_for(YZ, 256, sl->num_sms * 4);
+                for (int side = 0; side < 2; side++)
+                    if (side ? geo.gh : geo.gl)
+                        k_slab_ghost_claim<<<grid, 256, 0, sl->stream>>>(geo, sl->s, side, sl->hrecv[side], nl,
+                                                                         sl->blist[(i + 1) & 1],
+                                                                         sl->cnt + 4 + (i + 1) % 3);
+                g->st.kernel_launches += geo.gl + geo.gh;
+            }
+            CG_CUDA(cudaGetLastError());
+        }
+        int64_t pending = 0;
+        for (Slab *sl : g->slabs)
+            CG_CUDA(cudaMemcpyAsync(sl->h_cnt + 4, sl->cnt + 4, 3 * sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                    sl->stream));
+        for (Slab *sl : g->slabs) {
+            CG_CUDA(cudaStreamSynchronize(sl->stream));
+            pending += sl->h_cnt[4 + i % 3];
+        }
+        CG_TRY(gsum(g, &pending, 1));
+        if (pending == 0) break;
+        if ((int64_t)i > (int64_t)g->slabs[0]->geo.INF + SLAB_BATCH) return CG_E_CUDA;
+    }
+    g->st.gr_passes += i;
+    // exact ghost labels for the sweeps: boundary heights -> neighbours' ghost planes
+    for (Slab *sl : g->slabs) {
+        const Geo &geo = sl->geo;
+        const int grid = grid_for(YZ, 256, sl->num_sms * 4);
+        if (geo.gl) k_halo_pack_h<<<grid, 256, 0, sl->stream>>>(geo, sl->s, 0, sl->hsend[0]);
+        if (geo.gh) k_halo_pack_h<<<grid, 256, 0, sl->stream>>>(geo, sl->s, 1, sl->hsend[1]);
+    }
+    CG_TRY(transfer(g, YZ));
+    for (Slab *sl : g->slabs) {
+        const Geo &geo = sl->geo;
+        const int grid = grid_for(YZ, 256, sl->num_sms * 4);
+        for (int side = 0; side < 2; side++)
+            if (side ? geo.gh : geo.gl)
+                k_halo_unpack_h<<<grid, 256, 0, sl->stream>>>(geo, sl->s, side, sl->hrecv[side], sl->hold[side]);
+    }
+    CG_CUDA(cudaGetLastError());
+    return CG_OK;
+}
+
+// Label-correcting relabel across slabs (CG_SLAB_LC=1): local waves until every frontier is empty, then
 // exchange ghost heights and relax from improved ghosts; stop when nothing changed anywhere.
 cg_status bfs_slabs(cg_graph *g) {
     for (Slab *sl : g->slabs) {
@@ -601,7 +677,8 @@ cg_status global_relabel(cg_graph *g, int64_t *active) {
     if (!multi(g)) {
         CG_TRY(bfs_strict(g, g->slabs[0]));
     } else {
-        CG_TRY(bfs_slabs(g));
+        static const bool lc = getenv("CG_SLAB_LC") && atoi(getenv("CG_SLAB_LC"));
+        CG_TRY(lc ? bfs_slabs(g) : bfs_slabs_levels(g));
     }
     int64_t act = 0;
     for (Slab *sl : g->slabs) {

@@ -842,8 +842,12 @@ __device__ __noinline__ void bfs_soft_preds(const Geo &g, const Soa &s, int64_t 
             bool up = false, dn = false;
             const int64_t wu = v0 + o + z + k, wd = v0 + o + z - k;
             if (o && cap > 0) {
-                up = z + k < g.Z && owned(g, wu) && cap - *soft_flow(g, s, wu, d ^ 1, k) > 0 && claim(wu);
-                dn = z - k >= 0 && owned(g, wd) && *soft_flow(g, s, v, d, k) > 0 && claim(wd);
+                // MODE 1 (strict) also claims ghost vertices: the owner learns the label through
+                // the ghost plane; ghosts are never listed here
+                up = z + k < g.Z && (MODE == 1 || owned(g, wu)) && cap - *soft_flow(g, s, wu, d ^ 1, k) > 0 &&
+                     claim(wu) && owned(g, wu);
+                dn = z - k >= 0 && (MODE == 1 || owned(g, wd)) && *soft_flow(g, s, v, d, k) > 0 && claim(wd) &&
+                     owned(g, wd);
             }
             warp_append(up, (int)wu, lout, cout);
             warp_append(dn, (int)wd, lout, cout);
@@ -892,8 +896,8 @@ __device__ __forceinline__ void bfs_expand_warp(const Geo &g, const Soa &s, int 
                 const int64_t o = nbr_off(g, x, y, d);
                 if (!o) continue;
                 const int zi = d < 2 ? zix : ziy, zo = d < 2 ? zox : zoy;
-                if (zi >= 0 && owned(g, v0 + o + zi)) { w[2 + d] = (int)(v0 + o + zi); cand |= 1u << (2 + d); }
-                if (zo >= 0 && s.L[d][v] > 0 && owned(g, v0 + o + zo)) {
+                if (zi >= 0) { w[2 + d] = (int)(v0 + o + zi); cand |= 1u << (2 + d); }
+                if (zo >= 0 && s.L[d][v] > 0) {
                     w[6 + d] = (int)(v0 + o + zo);
                     cand |= 1u << (6 + d);
                 }
@@ -903,7 +907,9 @@ __device__ __forceinline__ void bfs_expand_warp(const Geo &g, const Soa &s, int 
             for (int j = 0; j < 10; j++) hw[j] = (cand >> j & 1u) ? __ldcg(&s.H[w[j]]) : 0;
 #pragma unroll
             for (int j = 0; j < 10; j++)
-                if ((cand >> j & 1u) && hw[j] >= INF && atomicCAS(&s.H[w[j]], INF, nl) == INF) {
+                if ((cand >> j & 1u) && hw[j] >= INF && atomicCAS(&s.H[w[j]], INF, nl) == INF && owned(g, w[j])) {
+                    // a claimed ghost vertex is not expanded here: its label reaches the owner
+                    // through the ghost plane (k_slab_ghost_claim) and the owner expands it
                     u[j] = w[j];
                     got |= 1u << j;
                 }
@@ -1296,6 +1302,40 @@ __global__ void __launch_bounds__(256) k_lc_wave(Geo g, Soa s, const int *__rest
     for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {
         const int64_t j = base + lane_id();
         bfs_expand_warp<false>(g, s, 0, j < count ? (int64_t)lin[j] : -1, lout, cout, vstamp, tag);
+    }
+}
+
+// Level-synchronous x-slab BFS (a5 across slabs): expand level L's frontier (labels nl = L+1
+// for unlabelled predecessors, ghost predecessors included -- their CAS marks the ghost plane,
+// which k_slab_ghost_claim delivers to the owner before level L+1 starts).
+__global__ void __launch_bounds__(256) k_slab_level(Geo g, Soa s, int nl, const int *__restrict__ lin,
+                                                    const unsigned *cin, int *lout, unsigned *cout, unsigned *czero) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *czero = 0;
+    const int64_t count = *cin;
+    for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {
+        const int64_t j = base + lane_id();
+        bfs_expand_warp<true>(g, s, nl, j < count ? (int64_t)lin[j] : -1, lout, cout, nullptr, 0);
+    }
+}
+// ghost-plane labels of this slab -> the owner of those vertices
+__global__ void k_ghost_pack_h(Geo g, Soa s, int side, int32_t *send) {
+    const int64_t gbase = side ? g.n : -g.YZ;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.YZ; i += (int64_t)gridDim.x * blockDim.x)
+        send[i] = s.H[gbase + i];
+}
+// owner side: a boundary vertex the neighbour claimed at label nl this level joins the next
+// frontier unless this slab already labelled it (then its own label is <= nl)
+__global__ void k_slab_ghost_claim(Geo g, Soa s, int side, const int32_t *__restrict__ recv, int nl, int *lout,
+                                   unsigned *cout) {
+    const int64_t bbase = side ? g.n - g.YZ : 0;
+    for (int64_t b0 = gwarp() * 32; b0 < g.YZ; b0 += nwarps() * 32) {
+        const int64_t i = b0 + lane_id();
+        bool add = false;
+        if (i < g.YZ && recv[i] == nl) {
+            const int64_t v = bbase + i;
+            add = s.H[v] >= g.INF && atomicCAS(&s.H[v], g.INF, nl) == g.INF;
+        }
+        warp_append(add, (int)(bbase + i), lout, cout);
     }
 }
 
