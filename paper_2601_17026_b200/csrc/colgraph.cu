@@ -550,21 +550,16 @@ cg_status bfs_slabs_levels(cg_graph *g) {
                 k_slab_level<<<list_grid(sl, geo.n), 256, 0, sl->stream>>>(
                     geo, sl->s, nl, sl->blist[i & 1], sl->cnt + 4 + i % 3, sl->blist[(i + 1) & 1],
                     sl->cnt + 4 + (i + 1) % 3, sl->cnt + 4 + (i + 2) % 3);
-                const int grid = grid_for(YZ, 256, sl->num_sms * 4);
-                if (geo.gl) k_ghost_pack_h<<<grid, 256, 0, sl->stream>>>(geo, sl->s, 0, sl->hsend[0]);
-                if (geo.gh) k_ghost_pack_h<<<grid, 256, 0, sl->stream>>>(geo, sl->s, 1, sl->hsend[1]);
-                g->st.kernel_launches += 1 + geo.gl + geo.gh;
+                k_ghost_pack_h<<<grid_for(2 * YZ, 256, sl->num_sms * 4), 256, 0, sl->stream>>>(
+                    geo, sl->s, sl->hsend[0], sl->hsend[1]);
+                g->st.kernel_launches += 2;
             }
             CG_TRY(transfer(g, YZ));
             for (Slab *sl : g->slabs) {
                 const Geo &geo = sl->geo;
-                const int grid = grid_for(YZ, 256, sl->num_sms * 4);
-                for (int side = 0; side < 2; side++)
-                    if (side ? geo.gh : geo.gl)
-                        k_slab_ghost_claim<<<grid, 256, 0, sl->stream>>>(geo, sl->s, side, sl->hrecv[side], nl,
-                                                                         sl->blist[(i + 1) & 1],
-                                                                         sl->cnt + 4 + (i + 1) % 3);
-                g->st.kernel_launches += geo.gl + geo.gh;
+                k_slab_ghost_claim<<<grid_for(2 * YZ * 32, 256, sl->num_sms * 4), 256, 0, sl->stream>>>(
+                    geo, sl->s, sl->hrecv[0], sl->hrecv[1], nl, sl->blist[(i + 1) & 1], sl->cnt + 4 + (i + 1) % 3);
+                g->st.kernel_launches++;
             }
             CG_CUDA(cudaGetLastError());
         }

@@ -1317,25 +1317,29 @@ __global__ void __launch_bounds__(256) k_slab_level(Geo g, Soa s, int nl, const 
         bfs_expand_warp<true>(g, s, nl, j < count ? (int64_t)lin[j] : -1, lout, cout, nullptr, 0);
     }
 }
-// ghost-plane labels of this slab -> the owner of those vertices
-__global__ void k_ghost_pack_h(Geo g, Soa s, int side, int32_t *send) {
-    const int64_t gbase = side ? g.n : -g.YZ;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.YZ; i += (int64_t)gridDim.x * blockDim.x)
-        send[i] = s.H[gbase + i];
+// ghost-plane labels of this slab (both sides, one launch) -> the owners of those vertices
+__global__ void k_ghost_pack_h(Geo g, Soa s, int32_t *send0, int32_t *send1) {
+    const int64_t m = (int64_t)(g.gl + g.gh) * g.YZ;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x) {
+        const bool hi = !g.gl || t >= g.YZ;
+        const int64_t i = t - (g.gl && hi ? g.YZ : 0);
+        (hi ? send1 : send0)[i] = s.H[(hi ? g.n : -g.YZ) + i];
+    }
 }
-// owner side: a boundary vertex the neighbour claimed at label nl this level joins the next
+// owner side: a boundary vertex a neighbour claimed at label nl this level joins the next
 // frontier unless this slab already labelled it (then its own label is <= nl)
-__global__ void k_slab_ghost_claim(Geo g, Soa s, int side, const int32_t *__restrict__ recv, int nl, int *lout,
-                                   unsigned *cout) {
-    const int64_t bbase = side ? g.n - g.YZ : 0;
-    for (int64_t b0 = gwarp() * 32; b0 < g.YZ; b0 += nwarps() * 32) {
-        const int64_t i = b0 + lane_id();
+__global__ void k_slab_ghost_claim(Geo g, Soa s, const int32_t *__restrict__ recv0, const int32_t *__restrict__ recv1,
+                                   int nl, int *lout, unsigned *cout) {
+    const int64_t m = (int64_t)(g.gl + g.gh) * g.YZ;
+    for (int64_t b0 = gwarp() * 32; b0 < m; b0 += nwarps() * 32) {
+        const int64_t t = b0 + lane_id();
+        const bool hi = !g.gl || t >= g.YZ;
+        const int64_t i = t - (g.gl && hi ? g.YZ : 0);
+        const int64_t v = (hi ? g.n - g.YZ : 0) + i;
         bool add = false;
-        if (i < g.YZ && recv[i] == nl) {
-            const int64_t v = bbase + i;
+        if (t < m && (hi ? recv1 : recv0)[i] == nl)
             add = s.H[v] >= g.INF && atomicCAS(&s.H[v], g.INF, nl) == g.INF;
-        }
-        warp_append(add, (int)(bbase + i), lout, cout);
+        warp_append(add, (int)v, lout, cout);
     }
 }
 
