@@ -55,5 +55,7 @@ if __name__ == "__main__":
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_dbg.so"), defines=("CG_DEBUG_BOUNDS=1",)))
     if "--serial-scan" in sys.argv:
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_serial.so"), defines=("CG_SCAN_SERIAL=1",)))
+    if "--hplane" in sys.argv:
+        print(build(force=True, lib=os.path.join(PKG, "libcolgraph_hplane.so"), defines=("CG_H_PLANE=1",)))
     if "--soa" in sys.argv:
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_soa.so"), defines=("CG_LAYOUT_AOS=0",)))

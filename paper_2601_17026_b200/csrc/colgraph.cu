@@ -274,7 +274,7 @@ int64_t halo_msg_ints(const Geo &geo) {
 size_t workspace_bytes(const Geo &geo) {
     const int64_t ncol = (int64_t)geo.X * geo.Y, plane = (int64_t)(geo.X + 2) * geo.YZ;
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-    size_t b = 8 * al(sizeof(int32_t) * plane);
+    size_t b = (8 + (CG_LAYOUT_AOS && CG_H_PLANE)) * al(sizeof(int32_t) * plane);
     // soft flows over the owned and the two ghost planes; per side a snapshot of the ghost copy
     if (geo.soft_k) b += al(sizeof(int32_t) * plane * 4 * geo.soft_k) + 2 * al(sizeof(int32_t) * geo.YZ * geo.soft_k);
     b += 3 * al(sizeof(int) * geo.n);
@@ -337,7 +337,11 @@ cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode) {
     sl->s.SF = geo.soft_k ? carve<int32_t>(p, plane * 4 * geo.soft_k) + geo.YZ * 4 * geo.soft_k : nullptr;
     for (int side = 0; side < 2; side++) sl->ssnap[side] = geo.soft_k ? carve<int32_t>(p, geo.YZ * geo.soft_k) : nullptr;
     sl->s.E = fl[0];
-    sl->s.H = fl[1];
+#if CG_LAYOUT_AOS && CG_H_PLANE
+    sl->s.H = FieldH{carve<int32_t>(p, plane) + geo.YZ, -geo.YZ, geo.n + geo.YZ};
+#else
+    sl->s.H = FieldH{fl[1].p, fl[1].lo, fl[1].hi};
+#endif
     sl->s.T = fl[2];
     sl->s.D = fl[3];
     for (int d = 0; d < 4; d++) sl->s.L[d] = fl[4 + d];
@@ -1522,10 +1526,14 @@ cg_status colgraph_export_state(cg_graph *g, int32_t *out_dev) {
     const int64_t ntot = g->local ? g->n_global : g->slabs[0]->geo.n;
     for (Slab *sl : g->slabs) {
         const int64_t off = g->local ? (int64_t)sl->x0 * sl->geo.YZ : 0;
-        const Field planes[8] = {sl->s.E, sl->s.H, sl->s.T, sl->s.D, sl->s.L[0], sl->s.L[1], sl->s.L[2], sl->s.L[3]};
-        for (int f = 0; f < 8; f++)
-            k_export<<<grid_for(sl->geo.n, 256, sl->num_sms * 8), 256, 0, sl->stream>>>(planes[f], sl->geo.n,
-                                                                                          out_dev + f * ntot + off);
+        const Field planes[8] = {sl->s.E, sl->s.E, sl->s.T, sl->s.D, sl->s.L[0], sl->s.L[1], sl->s.L[2], sl->s.L[3]};
+        const int grid = grid_for(sl->geo.n, 256, sl->num_sms * 8);
+        for (int f = 0; f < 8; f++) {
+            if (f == 1)
+                k_export<<<grid, 256, 0, sl->stream>>>(sl->s.H, sl->geo.n, out_dev + f * ntot + off);
+            else
+                k_export<<<grid, 256, 0, sl->stream>>>(planes[f], sl->geo.n, out_dev + f * ntot + off);
+        }
         CG_CUDA(cudaGetLastError());
     }
     for (Slab *sl : g->slabs) CG_CUDA(cudaStreamSynchronize(sl->stream));

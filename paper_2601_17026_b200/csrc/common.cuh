@@ -51,7 +51,8 @@ constexpr int FIELD_STRIDE = CG_LAYOUT_AOS ? 8 : 1;
 // compute-sanitizer is closed on this pool: this is the bad-access check.
 #ifdef CG_DEBUG_BOUNDS
 __device__ unsigned long long g_oob;
-struct Field {
+template <int S>
+struct FieldT {
     int32_t *p;
     int64_t lo, hi;
     __device__ __forceinline__ int32_t &operator[](int64_t i) const {
@@ -59,19 +60,30 @@ struct Field {
             atomicAdd(&g_oob, 1ull);
             i = lo;
         }
-        return p[i * FIELD_STRIDE];
+        return p[i * S];
     }
 };
 #else
-struct Field {
+template <int S>
+struct FieldT {
     int32_t *p;
     int64_t lo, hi;  // valid vertex range (checked only in CG_DEBUG_BOUNDS builds)
-    __device__ __forceinline__ int32_t &operator[](int64_t i) const { return p[i * FIELD_STRIDE]; }
+    __device__ __forceinline__ int32_t &operator[](int64_t i) const { return p[i * S]; }
 };
 #endif
+// CG_H_PLANE = 1 (AoS variant, `build --hplane`): the heights live in their own int32 plane
+// (the record's H slot is unused), so the neighbour-height reads of the arc scans and the
+// relabel hit 8 heights per sector instead of one record per height.
+#ifndef CG_H_PLANE
+#define CG_H_PLANE 0
+#endif
+using Field = FieldT<FIELD_STRIDE>;
+using FieldH = FieldT<(CG_LAYOUT_AOS && CG_H_PLANE) ? 1 : FIELD_STRIDE>;
 
 struct Soa {
-    Field E, H, T, D;
+    Field E;
+    FieldH H;
+    Field T, D;
     Field L[4];
     int32_t *SF;  // soft-arc flows, [v][d][k] (4 * soft_k ints per owned vertex); null if hard only
 };

@@ -218,13 +218,15 @@ __global__ void k_flow_export(Geo g, const int32_t *__restrict__ in, int weight_
 }
 
 // f[lo .. lo+n) = v
-__global__ void k_fill(Field f, int64_t lo, int64_t n, int32_t v) {
+template <class F>
+__global__ void k_fill(F f, int64_t lo, int64_t n, int32_t v) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         f[lo + i] = v;
 }
 
 // out[0 .. n) = f[0 .. n)  (state export to plain planes)
-__global__ void k_export(Field f, int64_t n, int32_t *out) {
+template <class F>
+__global__ void k_export(F f, int64_t n, int32_t *out) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         out[i] = f[i];
 }
@@ -1494,7 +1496,7 @@ __global__ void k_halo_unpack_h(Geo g, Soa s, int side, const int32_t *__restric
 // Cherkassky-Goldberg gap: if no vertex has label g (0 < g < max
 // finite label), every vertex labelled above g cannot reach t: lift it to INF.
 constexpr int GAP_BINS = 1 << 20;
-__global__ void k_gap_hist(Geo g, const Field H, unsigned *hist, int *maxh) {
+__global__ void k_gap_hist(Geo g, const FieldH H, unsigned *hist, int *maxh) {
     int mymax = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += (int64_t)gridDim.x * blockDim.x) {
         const int h = H[i];
@@ -1522,7 +1524,7 @@ __global__ void k_gap_find(const unsigned *hist, const int *maxh, int *gap) {
         *gap = b;
     }
 }
-__global__ void k_gap_lift(Geo g, Field H, const int *gap, unsigned long long *lifted) {
+__global__ void k_gap_lift(Geo g, FieldH H, const int *gap, unsigned long long *lifted) {
     const int gp = *gap;
     int c = 0;
     if (gp != INT_MAX) {

@@ -14,4 +14,7 @@ spec = V.CONFIGS[name]
 c = torch.from_numpy(V.generate(name)).cuda()
 r = cg.solve(c, spec.delta, want_mask=False)
 torch.cuda.synchronize()
-print(name, r["status"], r["flow"], {k: r["stats"][k] for k in ("sweeps", "global_relabels", "gr_passes", "kernel_launches")})
+import json  # noqa: E402
+print(json.dumps({"config": name, "status": r["status"], "flow": r["flow"],
+                  **{k: r["stats"][k] for k in ("sweeps", "global_relabels", "gr_passes", "kernel_launches",
+                                                 "sweep_bytes_alg", "ms_sweep_kernels") if k in r["stats"]}}))
