@@ -55,6 +55,10 @@ if __name__ == "__main__":
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_dbg.so"), defines=("CG_DEBUG_BOUNDS=1",)))
     if "--serial-scan" in sys.argv:
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_serial.so"), defines=("CG_SCAN_SERIAL=1",)))
+    if "--up-late" in sys.argv:
+        print(build(force=True, lib=os.path.join(PKG, "libcolgraph_uplate.so"), defines=("CG_SCAN_UP_EARLY=0",)))
+    if "--scan-prof" in sys.argv:
+        print(build(force=True, lib=os.path.join(PKG, "libcolgraph_prof.so"), defines=("CG_SCAN_PROF=1",)))
     if "--hplane" in sys.argv:
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_hplane.so"), defines=("CG_H_PLANE=1",)))
     if "--soa" in sys.argv:

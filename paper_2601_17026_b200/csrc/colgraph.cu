@@ -1291,6 +1291,19 @@ cg_status colgraph_build_slabs_soft(const cg_dims *dims, const int32_t *cost_dev
 }
 
 cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_value, cg_solve_stats *stats) {
+#if CG_SCAN_PROF
+    {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(g_scanprof, z, sizeof(z));
+        const cg_status st = maxflow_solve_impl(g, opts, flow_value, stats);
+        cudaDeviceSynchronize();
+        cudaMemcpyFromSymbol(z, g_scanprof, sizeof(z));
+        fprintf(stderr, "scanprof");
+        for (int i = 0; i < 16; i++) fprintf(stderr, " %llu", z[i]);
+        fprintf(stderr, "\n");
+        return debug_check(st);
+    }
+#endif
     return debug_check(maxflow_solve_impl(g, opts, flow_value, stats));
 }
 

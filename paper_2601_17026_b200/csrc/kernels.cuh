@@ -294,10 +294,23 @@ __device__ __noinline__ void scan_soft(const Geo &g, const Soa &s, const OpCtx &
 }
 
 __device__ __forceinline__ ArcPick scan_arcs_hard(const Geo &g, const Soa &s, const OpCtx &c, int hx);
+// serial arc-scan order: t, down, up, lateral-out, lateral-in (CG_SCAN_UP_EARLY = 1, measured
+// -8 % C4 / -18 % C5) or the up arc after the lateral-out arcs (0)
+#ifndef CG_SCAN_UP_EARLY
+#define CG_SCAN_UP_EARLY 1
+#endif
+#if CG_SCAN_PROF
+// profiling build (`build --scan-prof`): which arc each scan picks (15 = none admissible:
+// a relabel), printed to stderr by maxflow_solve
+__device__ unsigned long long g_scanprof[16];
+#endif
 template <bool SOFT>
 __device__ __forceinline__ ArcPick scan_arcs(const Geo &g, const Soa &s, const OpCtx &c, int hx) {
     ArcPick p = scan_arcs_hard(g, s, c, hx);
     if (SOFT && p.arc != 0 && p.best >= hx) scan_soft(g, s, c, hx, p);
+#if CG_SCAN_PROF
+    atomicAdd(&g_scanprof[p.best < hx ? (p.arc < 11 ? p.arc : 11) : 15], 1ull);
+#endif
     return p;
 }
 
@@ -360,6 +373,17 @@ __device__ __forceinline__ ArcPick scan_arcs_hard(const Geo &g, const Soa &s, co
         if (hh < p.best) { p.best = hh; p.arc = 1; p.tgt = c.v - 1; }
         if (p.best < hx) return p;
     }
+#if CG_SCAN_UP_EARLY
+    // the up arc's record (v+1) is adjacent to v's own: checked before the lateral records
+    if (c.z + 1 < g.Z) {
+        const int r = s.D[c.v + 1];
+        if (r > 0) {
+            const int hh = s.H[c.v + 1];
+            if (hh < p.best) { p.best = hh; p.arc = 6; p.tgt = c.v + 1; p.res = r; }
+            if (p.best < hx) return p;
+        }
+    }
+#endif
     if (c.zo[0] >= 0 || c.zo[1] >= 0) {
 #pragma unroll
         for (int d = 0; d < 4; d++) {
@@ -370,6 +394,7 @@ __device__ __forceinline__ ArcPick scan_arcs_hard(const Geo &g, const Soa &s, co
             if (p.best < hx) return p;
         }
     }
+#if !CG_SCAN_UP_EARLY
     if (c.z + 1 < g.Z) {
         const int r = s.D[c.v + 1];
         if (r > 0) {
@@ -378,6 +403,7 @@ __device__ __forceinline__ ArcPick scan_arcs_hard(const Geo &g, const Soa &s, co
             if (p.best < hx) return p;
         }
     }
+#endif
     if (c.zi[0] >= 0 || c.zi[1] >= 0) {
 #pragma unroll
         for (int d = 0; d < 4; d++) {
