@@ -30,6 +30,7 @@
  *   CG_WALK_MIN=f         walks while >= f*n vertices are active (default 1e-3), single hops below
  *   CG_WALK_WS=1          work-fetching walks (k_walk_ws)
  *   CG_WALK_PARK=1        stuck walks wait for the next global relabel
+ *   CG_WALK_RCONT=k       a stuck walk may relabel and go on up to k times (default 0)
  *   CG_RELIST=1           re-list large sweep worklists in index order
  *   CG_OPS=k              push/relabel operations per vertex per single-hop sweep
  *   CG_GR_BETA=b          time trigger: relabel when sweep time since the last one >= b * its cost

@@ -888,7 +888,9 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
     const double gr_beta = getenv("CG_GR_BETA") ? atof(getenv("CG_GR_BETA")) : 1.0;
     // work-fetching walk (k_walk_ws): measured -10 % on C3/C5, +10 % on C4, opt-in
     const bool walk_ws = getenv("CG_WALK_WS") && atoi(getenv("CG_WALK_WS")) != 0;
-    const int walk_park = getenv("CG_WALK_PARK") ? atoi(getenv("CG_WALK_PARK")) : 0;
+    // k_walk's last argument: bit 0 = park stuck walks, bits 8.. = relabel-and-continue budget
+    const int walk_park = (getenv("CG_WALK_PARK") ? atoi(getenv("CG_WALK_PARK")) & 1 : 0) |
+                          (getenv("CG_WALK_RCONT") ? atoi(getenv("CG_WALK_RCONT")) << 8 : 0);
     const bool relist_ordered = getenv("CG_RELIST") && atoi(getenv("CG_RELIST")) != 0;
     double work_since_gr = 0.0, sweep_ms_since_gr = 0.0;
     int64_t sweeps = g->st.sweeps, since_gap = 0, last_active = active;

@@ -621,13 +621,24 @@ __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_walk(Geo g, Soa s, int K
         atomicSub(&s.E[v], c);  // the owner takes its whole excess
         OpCtx ctx;
         set_ctx(g, ctx, v);
+        int rcont = park >> 8;  // relabels after which this walk may go on (CG_WALK_RCONT)
         for (int step = 0; c > 0; ++step) {
             const ArcPick p = scan_arcs<SOFT>(g, s, ctx, hx);
             mywork++;  // one push or relabel operation per hop
-            if (p.best >= hx || step >= K) {  // stuck (or hop budget spent): deposit the carry here
+            bool go_on = false;
+            if (p.best >= hx && rcont > 0 && step < K && p.best < g.INF) {
+                // relabel to min + 1 and push through the minimum arc the scan just found,
+                // unless a concurrent relabel of this vertex went higher
+                const int nh = p.best + 1;
+                if (atomicMax(&s.H[ctx.v], nh) <= nh) {
+                    rcont--;
+                    go_on = true;
+                }
+            }
+            if (!go_on && (p.best >= hx || step >= K)) {  // stuck (or hop budget spent): deposit the carry here
                 if (p.best >= hx) {
                     atomicMax(&s.H[ctx.v], p.best >= g.INF ? g.INF : p.best + 1);
-                    if (park) {  // parked until the next global relabel (not re-listed)
+                    if (park & 1) {  // parked until the next global relabel (not re-listed)
                         const int old = atomicAdd(&s.E[ctx.v], c);
                         if (old > INT_MAX - c) atomicOr(flags, FLAG_OVERFLOW);
                         break;

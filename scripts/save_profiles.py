@@ -42,7 +42,7 @@ def ncu_summary(rep, name):
 
 
 for src, dst in [("bench.log", "bench_c4.json"), ("bench_ref.log", "bench_reference_c4.json"),
-                 ("diag.log", "diag_all_configs.jsonl")]:
+                 ("diag.log", "diag_all_configs.jsonl"), ("gpu_tests.log", "gpu_tests.txt")]:
     p = os.path.join(OUT, src)
     if os.path.exists(p):
         shutil.copy(p, os.path.join(PROF, f"{tag}_{dst}"))
@@ -56,8 +56,30 @@ for rep, name in [("prof_walk.ncu-rep", "k_walk"), ("prof_bfs.ncu-rep", "k_bfs_r
     p = os.path.join(OUT, rep)
     if os.path.exists(p):
         avg = ncu_summary(p, name)
-        if name == "k_walk":
-            json.dump({"kernel": "k_walk", "sweep_dram_bytes_per_launch": avg,
-                       "launches": "C4 solve, k_walk launches 5-7 (ncu --set full -s 4 -c 3)",
-                       "source": f"profiles/{tag}_ncu_k_walk.json"}, open(os.path.join(PROF, "traffic.json"), "w"), indent=1)
+# the bench's `traffic`: DRAM bytes of EVERY sweep launch of one C4 solve, with that solve's
+# own algorithmic bytes (profile_one.py's line in sweep_traffic.log)
+st_csv, st_log = os.path.join(OUT, "sweep_traffic.csv"), os.path.join(OUT, "sweep_traffic.log")
+if os.path.exists(st_csv) and os.path.exists(st_log):
+    import io
+    lines = open(st_csv).read().splitlines()
+    i0 = next(k for k, l in enumerate(lines) if l.startswith('"ID"'))
+    per = {}
+    for r in csv.DictReader(io.StringIO("\n".join(lines[i0:]))):
+        if r["Metric Name"].startswith("dram__bytes"):
+            per[r["ID"]] = per.get(r["ID"], 0.0) + float(r["Metric Value"].replace(",", "")) * SCALE[r["Metric Unit"]]
+    alg = next(json.loads(l) for l in open(st_log) if l.startswith("{"))
+    tot, n = sum(per.values()), len(per)
+    json.dump({"kernel": "k_walk / k_sweep_v (all sweep launches of one C4 solve)",
+               "sweep_dram_bytes_per_launch": tot / n,
+               "sweep_alg_bytes_per_launch_same_run": alg["sweep_bytes_alg"] / n,
+               "traffic_over_alg": tot / alg["sweep_bytes_alg"], "launches": n, "dram_bytes_total": tot,
+               "alg_bytes_total": alg["sweep_bytes_alg"],
+               "note": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over EVERY k_walk/k_sweep_v launch of "
+                       "one C4 solve (scripts/gpu_session.sh); the algorithmic bytes are that same solve's "
+                       "(profile_one.py). Under ncu the relabel time trigger sees replay-slowed kernels, so that "
+                       "solve runs fewer, larger sweeps than the bench: compare traffic_over_alg.",
+               "source": f"profiles/{tag}_sweep_traffic_c4.csv.gz"}, open(os.path.join(PROF, "traffic.json"), "w"),
+              indent=1)
+    with open(st_csv, "rb") as f, gzip.open(os.path.join(PROF, f"{tag}_sweep_traffic_c4.csv.gz"), "wb") as g:
+        g.write(f.read())
 print("saved", tag)
