@@ -272,8 +272,8 @@ def run_ours(args, spec):
     roofline = {"kernel": "push-relabel sweep (k_walk / k_sweep_v)", "bound": "hbm", "achieved": achieved,
                 "peak": peak, "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
                 "traffic": tr.get("sweep_dram_bytes_per_launch") if tr else None,
-                # the ncu'd solve runs fewer, larger sweeps (replay-slowed relabel trigger): its
-                # own algorithmic bytes per launch and the ratio are the comparable numbers
+                # the ncu'd solve replays an unprofiled solve's relabel schedule (CG_GR_SCHEDULE);
+                # its own algorithmic bytes per launch and the ratio are given beside the traffic
                 "traffic_alg_bytes_per_launch": tr.get("sweep_alg_bytes_per_launch_same_run") if tr else None,
                 "traffic_over_alg": tr.get("traffic_over_alg") if tr else None,
                 "traffic_source": tr.get("source") if tr else None,

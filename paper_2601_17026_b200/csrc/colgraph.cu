@@ -895,6 +895,20 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
     double work_since_gr = 0.0, sweep_ms_since_gr = 0.0;
     int64_t sweeps = g->st.sweeps, since_gap = 0, last_active = active;
     std::vector<int64_t> wv(RING);
+    // Profiling aid (vertex loop): CG_GR_LOG=file appends the sweep counts at which this solve's
+    // triggers fired; CG_GR_SCHEDULE="s1,s2,..." replays such a schedule instead of the work /
+    // time triggers, so a run under ncu (whose replay-slowed kernels distort the time trigger)
+    // follows the relabel schedule of an unprofiled run.
+    std::vector<int64_t> sched, fired;
+    if (const char *e = getenv("CG_GR_SCHEDULE"))
+        for (const char *q = e; *q;) {
+            char *end = nullptr;
+            const long long v = strtoll(q, &end, 10);
+            if (end == q) break;
+            sched.push_back(v);
+            q = *end ? end + 1 : end;
+        }
+    size_t sched_i = 0;
     cg_status result = CG_OK;
     while (use_tiles && active > 0) {
         // a3 on tiles: batches of checkerboard phases, no host sync inside a batch
@@ -1044,8 +1058,11 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
         g->st.sweeps = sweeps;
         // the time-based trigger is a local measurement: agree on it across ranks
         int64_t trigger = quiescent || work_since_gr >= gr_budget || sweep_ms_since_gr >= gr_beta * std::max(last_gr_ms, 0.05);
+        if (!sched.empty()) trigger = quiescent || (sched_i < sched.size() && sweeps >= sched[sched_i]);
         CG_TRY(gmax(g, &trigger));
         if (trigger) {
+            fired.push_back(sweeps);
+            while (sched_i < sched.size() && sched[sched_i] <= sweeps) sched_i++;
             // a4: termination is decided only after an exact global relabel
             CG_TRY(timed_gr());
             last_active = active;
@@ -1055,6 +1072,13 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
         } else if (o.gap_every > 0 && since_gap >= o.gap_every && !multi(g)) {
             CG_TRY(run_gap(g, s0));
             since_gap = 0;
+        }
+    }
+    if (const char *path = getenv("CG_GR_LOG")) {
+        if (FILE *f = fopen(path, "a")) {
+            for (size_t i = 0; i < fired.size(); i++) fprintf(f, i ? ",%lld" : "%lld", (long long)fired[i]);
+            fprintf(f, "\n");
+            fclose(f);
         }
     }
     return result;

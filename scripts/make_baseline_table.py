@@ -1,10 +1,14 @@
-"""Regenerate BASELINE.md's "Measured results" section from profiles/r01_end_<commit>_*.
-usage: python scripts/make_baseline_table.py <commit>"""
+"""Regenerate BASELINE.md's "Measured results" section from profiles/<tag>_*.
+usage: python scripts/make_baseline_table.py <tag>   (e.g. r01_late_7b92e68)"""
 import json, sys
-H = sys.argv[1]
-diag = [json.loads(l) for l in open(f'profiles/r01_end_{H}_diag_all_configs.jsonl')]
-bench = json.loads(open(f'profiles/r01_end_{H}_bench_c4.json').read().strip().splitlines()[-1])
-ref = json.loads(open(f'profiles/r01_end_{H}_bench_reference_c4.json').read().strip().splitlines()[-1])
+T = sys.argv[1]
+H = T.rsplit('_', 1)[-1]
+diag = [json.loads(l) for l in open(f'profiles/{T}_diag_all_configs.jsonl')]
+bench = json.loads(open(f'profiles/{T}_bench_c4.json').read().strip().splitlines()[-1])
+ref = json.loads(open(f'profiles/{T}_bench_reference_c4.json').read().strip().splitlines()[-1])
+tr = json.load(open('profiles/traffic.json'))
+wk = json.load(open(f'profiles/{T}_ncu_k_walk.json'))['captures']
+ra = bench['roofline_random_access']
 n = {'C1': 8192, 'C2': 2097152, 'C3': 16777216, 'C4': 67108864, 'C5': 100663296}
 rows = []
 for d in diag:
@@ -35,11 +39,14 @@ host API with the 256 MiB H2D copy and the surface D2H inside the timed region:
 
 Roofline of the dominant kernel (push-relabel sweep, `k_walk` / `k_sweep_v`): algorithmic
 {rf['achieved']:.0f} GB/s = **{100 * rf['frac']:.1f} % of the measured 6,457 GB/s copy peak** (44 B per
-push/relabel operation).  ncu (`profiles/r01_end_{H}_ncu_k_walk.json`): 31 % of DRAM peak,
-L2 hit 21 %, 7.3 active threads per warp instruction -- a divergent, latency-bound traversal
-whose DRAM traffic is ~20x its algorithmic bytes.  Its access-pattern bound is the
-B200's random 32-byte record gather rate, measured at 625-750 GB/s (12 % of the copy peak,
-`profiles/r01_random_gather.json`): against it the sweep runs at ~23 %.  The >= 40 %
+push/relabel operation).  ncu (`profiles/{T}_ncu_k_walk.json`, early launches):
+{float(wk[0]['gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed [%]']):.0f} % of DRAM peak, L2 hit
+{float(wk[0]['lts__t_sector_hit_rate.pct [%]']):.0f} %, {float(wk[0]['smsp__thread_inst_executed_per_inst_executed.ratio']):.1f} active threads per warp
+instruction -- a divergent, scattered traversal whose DRAM traffic over every sweep launch of
+a solve is {tr['traffic_over_alg']:.1f}x its algorithmic bytes (`profiles/traffic.json`).  Its access-pattern
+bound is the B200's random 32-byte record gather rate, measured at 625-750 GB/s (12 % of the
+copy peak, `profiles/r01_random_gather.json`): against it the sweep runs at
+{100 * ra['frac']:.0f} %.  The >= 40 %
 per-sweep target of BASELINE.json (a streaming figure) is not met; DESIGN.md §6 explains
 why and lists every measured alternative.
 

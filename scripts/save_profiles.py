@@ -76,8 +76,8 @@ if os.path.exists(st_csv) and os.path.exists(st_log):
                "alg_bytes_total": alg["sweep_bytes_alg"],
                "note": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over EVERY k_walk/k_sweep_v launch of "
                        "one C4 solve (scripts/gpu_session.sh); the algorithmic bytes are that same solve's "
-                       "(profile_one.py). Under ncu the relabel time trigger sees replay-slowed kernels, so that "
-                       "solve runs fewer, larger sweeps than the bench: compare traffic_over_alg.",
+                       "(profile_one.py), run with the relabel schedule of an unprofiled solve replayed "
+                       "(CG_GR_SCHEDULE) so its sweeps match the bench's.",
                "source": f"profiles/{tag}_sweep_traffic_c4.csv.gz"}, open(os.path.join(PROF, "traffic.json"), "w"),
               indent=1)
     with open(st_csv, "rb") as f, gzip.open(os.path.join(PROF, f"{tag}_sweep_traffic_c4.csv.gz"), "wb") as g:
