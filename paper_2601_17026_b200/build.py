@@ -55,6 +55,14 @@ if __name__ == "__main__":
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_dbg.so"), defines=("CG_DEBUG_BOUNDS=1",)))
     if "--serial-scan" in sys.argv:
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_serial.so"), defines=("CG_SCAN_SERIAL=1",)))
+    if "--lat-serial" in sys.argv:
+        print(build(force=True, lib=os.path.join(PKG, "libcolgraph_lats.so"), defines=("CG_SCAN_LAT_GATHER=0",)))
+    if "--lat-one" in sys.argv:
+        print(build(force=True, lib=os.path.join(PKG, "libcolgraph_lat1.so"), defines=("CG_SCAN_LAT_ONE=1",)))
+    if "--minb4" in sys.argv:
+        print(build(force=True, lib=os.path.join(PKG, "libcolgraph_minb4.so"), defines=("CG_SWEEP_MINB=4",)))
+    if "--col-serial" in sys.argv:
+        print(build(force=True, lib=os.path.join(PKG, "libcolgraph_cols.so"), defines=("CG_SCAN_COL_GATHER=0",)))
     if "--up-late" in sys.argv:
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_uplate.so"), defines=("CG_SCAN_UP_EARLY=0",)))
     if "--scan-prof" in sys.argv:

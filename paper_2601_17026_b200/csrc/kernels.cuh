@@ -18,7 +18,7 @@ namespace cg {
 
 // Occupancy targets of the latency-bound worklist kernels (blocks per SM).
 #ifndef CG_SWEEP_MINB
-#define CG_SWEEP_MINB 4
+#define CG_SWEEP_MINB 3
 #endif
 #ifndef CG_BFS_MINB
 #define CG_BFS_MINB 2
@@ -299,6 +299,17 @@ __device__ __forceinline__ ArcPick scan_arcs_hard(const Geo &g, const Soa &s, co
 #ifndef CG_SCAN_UP_EARLY
 #define CG_SCAN_UP_EARLY 1
 #endif
+// lateral records gathered per group (CG_SCAN_LAT_GATHER, measured -1..-8 %);
+// own-column checks gathered in one round (CG_SCAN_COL_GATHER)
+#ifndef CG_SCAN_LAT_GATHER
+#define CG_SCAN_LAT_GATHER 1
+#endif
+#ifndef CG_SCAN_COL_GATHER
+#define CG_SCAN_COL_GATHER 1
+#endif
+#ifndef CG_SCAN_LAT_ONE
+#define CG_SCAN_LAT_ONE 0
+#endif
 #if CG_SCAN_PROF
 // profiling build (`build --scan-prof`): which arc each scan picks (15 = none admissible:
 // a relabel), printed to stderr by maxflow_solve
@@ -363,6 +374,23 @@ __device__ __forceinline__ ArcPick scan_arcs_hard(const Geo &g, const Soa &s, co
     }
     return p;
 #else
+#if CG_SCAN_COL_GATHER && CG_SCAN_UP_EARLY
+    {  // own column in one round: t residual, H(v-1), D(v+1) and H(v+1) (adjacent records)
+        const int tres = s.T[c.v];
+        const int hdn = c.z >= 1 ? s.H[c.v - 1] : g.INF;
+        const bool up = c.z + 1 < g.Z;
+        const int rup = up ? s.D[c.v + 1] : 0;
+        const int hup = up ? s.H[c.v + 1] : g.INF;
+        if (tres > 0) {
+            p.best = 0; p.arc = 0; p.res = tres;
+            return p;
+        }
+        if (hdn < p.best) { p.best = hdn; p.arc = 1; p.tgt = c.v - 1; }
+        if (p.best < hx) return p;
+        if (rup > 0 && hup < p.best) { p.best = hup; p.arc = 6; p.tgt = c.v + 1; p.res = rup; }
+        if (p.best < hx) return p;
+    }
+#else
     const int tres = s.T[c.v];
     if (tres > 0) {
         p.best = 0; p.arc = 0; p.res = tres;
@@ -373,7 +401,8 @@ __device__ __forceinline__ ArcPick scan_arcs_hard(const Geo &g, const Soa &s, co
         if (hh < p.best) { p.best = hh; p.arc = 1; p.tgt = c.v - 1; }
         if (p.best < hx) return p;
     }
-#if CG_SCAN_UP_EARLY
+#endif
+#if CG_SCAN_UP_EARLY && !CG_SCAN_COL_GATHER
     // the up arc's record (v+1) is adjacent to v's own: checked before the lateral records
     if (c.z + 1 < g.Z) {
         const int r = s.D[c.v + 1];
@@ -382,6 +411,51 @@ __device__ __forceinline__ ArcPick scan_arcs_hard(const Geo &g, const Soa &s, co
             if (hh < p.best) { p.best = hh; p.arc = 6; p.tgt = c.v + 1; p.res = r; }
             if (p.best < hx) return p;
         }
+    }
+#endif
+#if CG_SCAN_LAT_GATHER && CG_SCAN_UP_EARLY
+    // lateral records: the four lateral-out heights in one round of independent loads, then
+    // the four lateral-in (residual, height) pairs in another -- two latency steps instead of
+    // up to eight dependent ones for the scans that reach them (relabels: a third of all ops)
+    {
+        int64_t t4[4];
+        int h4[4];
+#pragma unroll
+        for (int d = 0; d < 4; d++) {
+            const bool ok = c.off[d] && c.zo[d >> 1] >= 0;
+            t4[d] = c.v0 + c.off[d] + c.zo[d >> 1];
+            h4[d] = ok ? s.H[t4[d]] : g.INF;
+        }
+#if CG_SCAN_LAT_ONE  // all eight lateral records in one round
+        int64_t ti4[4];
+        int r4[4], hi4[4];
+#pragma unroll
+        for (int d = 0; d < 4; d++) {
+            const bool ok = c.off[d] && c.zi[d >> 1] >= 0;
+            ti4[d] = c.v0 + c.off[d] + c.zi[d >> 1];
+            r4[d] = ok ? s.L[d ^ 1][ti4[d]] : 0;
+            hi4[d] = ok ? s.H[ti4[d]] : g.INF;
+        }
+#endif
+#pragma unroll
+        for (int d = 0; d < 4; d++)
+            if (h4[d] < p.best) { p.best = h4[d]; p.arc = 2 + d; p.tgt = t4[d]; }
+        if (p.best < hx) return p;
+#if !CG_SCAN_LAT_ONE
+        int64_t ti4[4];
+        int r4[4], hi4[4];
+#pragma unroll
+        for (int d = 0; d < 4; d++) {
+            const bool ok = c.off[d] && c.zi[d >> 1] >= 0;
+            ti4[d] = c.v0 + c.off[d] + c.zi[d >> 1];
+            r4[d] = ok ? s.L[d ^ 1][ti4[d]] : 0;
+            hi4[d] = ok ? s.H[ti4[d]] : g.INF;
+        }
+#endif
+#pragma unroll
+        for (int d = 0; d < 4; d++)
+            if (r4[d] > 0 && hi4[d] < p.best) { p.best = hi4[d]; p.arc = 7 + d; p.tgt = ti4[d]; p.res = r4[d]; }
+        return p;
     }
 #endif
     if (c.zo[0] >= 0 || c.zo[1] >= 0) {
