@@ -32,7 +32,8 @@
  *   CG_WALK_PARK=1        stuck walks wait for the next global relabel
  *   CG_WALK_RCONT=k       a stuck walk may relabel and go on up to k times (default 0)
  *   CG_GR_LOG=file        append the sweep counts at which the relabel triggers fired
- *   CG_GR_SCHEDULE=s1,..  replay such a schedule (profiling under ncu)
+ *   CG_GR_SCHEDULE=s1,..  replay such a schedule (profiling under ncu); afterwards the
+ *                         usual triggers
  *   CG_RELIST=1           re-list large sweep worklists in index order
  *   CG_OPS=k              push/relabel operations per vertex per single-hop sweep
  *   CG_GR_BETA=b          time trigger: relabel when sweep time since the last one >= b * its cost

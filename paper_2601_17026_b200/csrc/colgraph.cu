@@ -676,7 +676,7 @@ cg_status global_relabel(cg_graph *g, int64_t *active) {
     if (!multi(g)) {
         CG_TRY(bfs_strict(g, g->slabs[0]));
     } else {
-        static const bool lc = getenv("CG_SLAB_LC") && atoi(getenv("CG_SLAB_LC"));
+        const bool lc = getenv("CG_SLAB_LC") && atoi(getenv("CG_SLAB_LC"));
         CG_TRY(lc ? bfs_slabs(g) : bfs_slabs_levels(g));
     }
     int64_t act = 0;
@@ -898,7 +898,8 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
     // Profiling aid (vertex loop): CG_GR_LOG=file appends the sweep counts at which this solve's
     // triggers fired; CG_GR_SCHEDULE="s1,s2,..." replays such a schedule instead of the work /
     // time triggers, so a run under ncu (whose replay-slowed kernels distort the time trigger)
-    // follows the relabel schedule of an unprofiled run.
+    // follows the relabel schedule of an unprofiled run; once the schedule is used up the
+    // work / time triggers apply again.
     std::vector<int64_t> sched, fired;
     if (const char *e = getenv("CG_GR_SCHEDULE"))
         for (const char *q = e; *q;) {
@@ -1058,7 +1059,7 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
         g->st.sweeps = sweeps;
         // the time-based trigger is a local measurement: agree on it across ranks
         int64_t trigger = quiescent || work_since_gr >= gr_budget || sweep_ms_since_gr >= gr_beta * std::max(last_gr_ms, 0.05);
-        if (!sched.empty()) trigger = quiescent || (sched_i < sched.size() && sweeps >= sched[sched_i]);
+        if (sched_i < sched.size()) trigger = quiescent || sweeps >= sched[sched_i];  // then the usual triggers
         CG_TRY(gmax(g, &trigger));
         if (trigger) {
             fired.push_back(sweeps);

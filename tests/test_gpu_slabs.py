@@ -111,3 +111,19 @@ def test_slab_state_export_is_a_max_preflow(cg):
     finally:
         cg.colgraph_free(h)
     _certificate(c, 3, state)
+
+
+def test_label_correcting_slab_relabel(cg, monkeypatch):
+    """The label-correcting x-slab relabel (CG_SLAB_LC=1), kept for comparison with the
+    default level-synchronous one, must give the same unique results."""
+    monkeypatch.setenv("CG_SLAB_LC", "1")
+    for seed in range(3000, 3060):
+        c, delta = V.tiny_case(seed)
+        ns = 2 + seed % 4
+        if c.shape[0] < ns:
+            continue
+        same(run(cg, c, delta, ns), oracle.colgraph_solve(c, delta), f"seed {seed} slabs {ns}")
+    c = V.generate("C1")
+    o = oracle.colgraph_solve(c, V.CONFIGS["C1"].delta)
+    for ns in (2, 3):
+        same(run(cg, c, V.CONFIGS["C1"].delta, ns), o, f"C1 x{ns}")

@@ -2,7 +2,10 @@
   - CG_SWEEP_TILES: checkerboard tile discharge in shared memory (tile.cuh), incl. ragged
     tiles (X, Y not multiples of the tile shape) and every instantiated lane segment S;
   - k_walk_ws (CG_WALK_WS=1): work-fetching multi-hop walks;
-  - level-per-launch BFS (CG_BFS_LEVEL_LAUNCHES=1) vs the persistent cooperative BFS.
+  - level-per-launch BFS (CG_BFS_LEVEL_LAUNCHES=1) vs the persistent cooperative BFS;
+  - the sweep/relabel knobs of include/colgraph.h: relabel-and-continue (CG_WALK_RCONT),
+    a replayed relabel schedule (CG_GR_SCHEDULE), parking, ordered re-listing, work-only
+    trigger.
 The options change the schedule only; the max-flow value, the minimal source set and the
 surface are unique, so results must be identical."""
 import os
@@ -84,7 +87,11 @@ def test_tiles_rejects_tall_columns(cg):
 
 @pytest.mark.parametrize("var", [{"CG_WALK_WS": "1"}, {"CG_BFS_LEVEL_LAUNCHES": "1"},
                                  {"CG_WALK_WS": "1", "CG_WALK_MIN": "0"}, {"CG_BFS_SMALL": "2048"},
-                                 {"CG_BFS_SMALL": "0"}, {"CG_BU_ALPHA": "2"}])
+                                 {"CG_BFS_SMALL": "0"}, {"CG_BU_ALPHA": "2"},
+                                 {"CG_WALK_RCONT": "1"}, {"CG_WALK_RCONT": "16"},
+                                 {"CG_GR_SCHEDULE": "1,2,3,5,8,13,21,34"},
+                                 {"CG_WALK_PARK": "1"}, {"CG_RELIST": "1"}, {"CG_RELIST": "1", "CG_WALK_PARK": "1"},
+                                 {"CG_GR_BETA": "1000"}, {"CG_OPS": "4"}])
 def test_schedule_variants(cg, env, var):
     for k, v in var.items():
         env.setenv(k, v)
