@@ -57,6 +57,8 @@ if __name__ == "__main__":
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_serial.so"), defines=("CG_SCAN_SERIAL=1",)))
     if "--lat-serial" in sys.argv:
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_lats.so"), defines=("CG_SCAN_LAT_GATHER=0",)))
+    if "--soft-serial" in sys.argv:
+        print(build(force=True, lib=os.path.join(PKG, "libcolgraph_softs.so"), defines=("CG_SOFT_GATHER=0",)))
     if "--lat-one" in sys.argv:
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_lat1.so"), defines=("CG_SCAN_LAT_ONE=1",)))
     if "--minb4" in sys.argv:

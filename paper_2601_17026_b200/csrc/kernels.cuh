@@ -264,10 +264,45 @@ struct ArcPick {
 // (nbr_d, z-k), residual cap_k - F) and 75 + 16 d + k (reverse of (nbr_d, z+k)'s arc in direction
 // d^1, residual its flow).  Only when no hard arc is admissible, so the hard path is unchanged.
 constexpr int ARC_SOFT_FWD = 11, ARC_SOFT_REV = 75;
+#ifndef CG_SOFT_GATHER
+#define CG_SOFT_GATHER 1
+#endif
 __device__ __noinline__ void scan_soft(const Geo &g, const Soa &s, const OpCtx &c, int hx, ArcPick &p) {
     for (int d = 0; d < 4; d++) {
         if (!c.off[d]) continue;
         const int kmax = min(g.soft_k, delta_d(g, d));
+#if CG_SOFT_GATHER
+        // four offsets k at a time: their soft-flow values in one round of loads, then the
+        // heights of the targets with residual in another (instead of one dependent chain per arc)
+        for (int k0 = 0; k0 < kmax; k0 += 4) {
+            int rf[4], rr[4], hf[4], hr[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const int k = k0 + j;
+                const int cap = k < kmax ? g.soft_cap[k] : 0;
+                rf[j] = (cap > 0 && c.z - k >= 0) ? cap - *soft_flow(g, s, c.v, d, k) : 0;
+                rr[j] = (cap > 0 && c.z + k < g.Z) ? *soft_flow(g, s, c.v0 + c.off[d] + c.z + k, d ^ 1, k) : 0;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const int k = k0 + j;
+                hf[j] = rf[j] > 0 ? s.H[c.v0 + c.off[d] + c.z - k] : g.INF;
+                hr[j] = rr[j] > 0 ? s.H[c.v0 + c.off[d] + c.z + k] : g.INF;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const int k = k0 + j;
+                if (hf[j] < p.best) {
+                    p.best = hf[j]; p.arc = ARC_SOFT_FWD + 16 * d + k; p.tgt = c.v0 + c.off[d] + c.z - k; p.res = rf[j];
+                }
+                if (p.best < hx) return;
+                if (hr[j] < p.best) {
+                    p.best = hr[j]; p.arc = ARC_SOFT_REV + 16 * d + k; p.tgt = c.v0 + c.off[d] + c.z + k; p.res = rr[j];
+                }
+                if (p.best < hx) return;
+            }
+        }
+#else
         for (int k = 0; k < kmax; k++) {
             const int cap = g.soft_cap[k];
             if (cap <= 0) continue;
@@ -290,6 +325,7 @@ __device__ __noinline__ void scan_soft(const Geo &g, const Soa &s, const OpCtx &
                 }
             }
         }
+#endif
     }
 }
 
