@@ -1104,7 +1104,11 @@ const char *cg_status_str(cg_status s) {
 
 const char *cg_version(void) {
     return "colgraph 0.4 sm_100a (lock-free push-relabel: multi-hop walks + single-hop sweeps over vertex worklists, "
-           "device-driven frontier BFS relabel, worklist extraction, x-slab halos over NCCL)";
+           "device-driven frontier BFS relabel, worklist extraction, x-slab halos over NCCL)"
+#ifdef CG_DEBUG_BOUNDS
+           " [debug-bounds build]"
+#endif
+        ;
 }
 
 cg_status cg_slab_range(const cg_dims *dims, int32_t rank, int32_t nranks, int32_t *x0, int32_t *x1) {
