@@ -269,7 +269,7 @@ def run_ours(args, spec):
     peak, peak_src = measured_peak()
     achieved = sweep_bytes / (sweep_ms / 1000.0) / 1e9 if sweep_ms > 0 else 0.0
     tr = ncu_traffic()
-    roofline = {"kernel": "push-relabel sweep (k_walk / k_sweep_v)", "bound": "hbm", "achieved": achieved,
+    roofline = {"kernel": "push-relabel sweep (k_walk_ws / k_sweep_v)", "bound": "hbm", "achieved": achieved,
                 "peak": peak, "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
                 "traffic": tr.get("sweep_dram_bytes_per_launch") if tr else None,
                 # the ncu'd solve replays an unprofiled solve's relabel schedule (CG_GR_SCHEDULE);

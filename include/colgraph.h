@@ -28,7 +28,8 @@
  *   CG_DEBUG=1            print the failing CUDA / NCCL call on stderr
  *   CG_WALK=K             hop budget of multi-hop walks (default 64)
  *   CG_WALK_MIN=f         walks while >= f*n vertices are active (default 1e-3), single hops below
- *   CG_WALK_WS=1          work-fetching walks (k_walk_ws)
+ *   CG_WALK_WS=0          k_walk instead of the work-fetching walk k_walk_ws (default);
+ *                         CG_WALK_PARK / CG_WALK_RCONT / CG_RELIST apply to k_walk only
  *   CG_WALK_PARK=1        stuck walks wait for the next global relabel
  *   CG_WALK_RCONT=k       a stuck walk may relabel and go on up to k times (default 0)
  *   CG_GR_LOG=file        append the sweep counts at which the relabel triggers fired

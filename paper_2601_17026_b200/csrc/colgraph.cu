@@ -886,8 +886,9 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
     const double gr_budget = (double)o.gr_factor * (double)g->n_global;
     const double walk_min = getenv("CG_WALK_MIN") ? atof(getenv("CG_WALK_MIN")) : 1e-3;
     const double gr_beta = getenv("CG_GR_BETA") ? atof(getenv("CG_GR_BETA")) : 1.0;
-    // work-fetching walk (k_walk_ws): measured -10 % on C3/C5, +10 % on C4, opt-in
-    const bool walk_ws = getenv("CG_WALK_WS") && atoi(getenv("CG_WALK_WS")) != 0;
+    // work-fetching walk (k_walk_ws): default since the gathered scan (C4 -11 %);
+    // CG_WALK_WS=0 runs k_walk (which also takes the park / relabel-and-continue / relist knobs)
+    const bool walk_ws = !getenv("CG_WALK_WS") || atoi(getenv("CG_WALK_WS")) != 0;
     // k_walk's last argument: bit 0 = park stuck walks, bits 8.. = relabel-and-continue budget
     const int walk_park = (getenv("CG_WALK_PARK") ? atoi(getenv("CG_WALK_PARK")) & 1 : 0) |
                           (getenv("CG_WALK_RCONT") ? atoi(getenv("CG_WALK_RCONT")) << 8 : 0);
