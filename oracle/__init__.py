@@ -67,6 +67,9 @@ def _load():
         lib.oracle_graph_maxflow.restype = ctypes.c_int
         lib.oracle_graph_maxflow.argtypes = [ctypes.c_int, ctypes.c_int, i32p, i32p, i64p, ctypes.c_int,
                                              ctypes.c_int, ctypes.c_int, i64p, u8p, i32p]
+        lib.oracle_graph_check.restype = ctypes.c_int
+        lib.oracle_graph_check.argtypes = [ctypes.c_int, ctypes.c_int, i32p, i32p, i64p, i64p, i64p, ctypes.c_int,
+                                           ctypes.c_int, u8p, ctypes.c_int64, i32p]
         _lib = lib
     return _lib
 
@@ -118,3 +121,24 @@ def graph_maxflow(nn: int, arcs, s: int, t: int, algo: str = "dinic") -> dict:
                                   _ptr(caps, ctypes.c_int64), s, t, ALGOS[algo], _ptr(flow, ctypes.c_int64),
                                   _ptr(side, ctypes.c_uint8), _ptr(checks, ctypes.c_int32))
     return {"status": int(st), "flow": int(flow[0]), "source_side": side.astype(bool), "checks": int(checks[0])}
+
+
+def graph_check(nn: int, arcs, res_fwd, res_rev, s: int, t: int, source_side, flow: int) -> int:
+    """check_invariants on a GIVEN residual state: arcs [(u, v, cap)], res_fwd[i] / res_rev[i] the
+    residuals of arc i and of its reverse slot, source_side the claimed S, flow the claimed |f|.
+    Returns the CHECK_BITS that hold (test entry point that pins the checker itself)."""
+    lib = _load()
+    arcs = list(arcs)
+    tails = np.array([a[0] for a in arcs], np.int32)
+    heads = np.array([a[1] for a in arcs], np.int32)
+    caps = np.array([a[2] for a in arcs], np.int64)
+    rf = np.ascontiguousarray(res_fwd, np.int64)
+    rr = np.ascontiguousarray(res_rev, np.int64)
+    side = np.ascontiguousarray(source_side, np.uint8)
+    checks = np.zeros(1, np.int32)
+    st = lib.oracle_graph_check(nn, len(arcs), _ptr(tails, ctypes.c_int32), _ptr(heads, ctypes.c_int32),
+                                _ptr(caps, ctypes.c_int64), _ptr(rf, ctypes.c_int64), _ptr(rr, ctypes.c_int64), s, t,
+                                _ptr(side, ctypes.c_uint8), int(flow), _ptr(checks, ctypes.c_int32))
+    if st != 0:
+        raise ValueError(f"oracle_graph_check: status {st}")
+    return int(checks[0])

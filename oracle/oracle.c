@@ -415,3 +415,37 @@ int oracle_graph_maxflow(int nn, int m, const int32_t *tails, const int32_t *hea
     g_free(&g); free(mark);
     return OR_OK;
 }
+
+/*
+ * Invariant checker on a GIVEN residual state (test entry point; pins check_invariants itself).
+ * The explicit graph is built from the arc list exactly as oracle_graph_maxflow builds it, then
+ * the residuals are overwritten with the caller's: res_fwd[i] on arc i (tail -> head, original
+ * capacity caps[i]) and res_rev[i] on its paired reverse slot (capacity 0).  The claimed flow value
+ * and source-side marks are checked as they are, so a corrupted state must clear the bit of the
+ * invariant it breaks: capacity (Eq. 2), antisymmetry (Eq. 3), conservation
+ * (Eq. 4), value (Eq. 5), t not in S, cut == flow (Theorem 1; Eq. 6).
+ */
+int oracle_graph_check(int nn, int m, const int32_t *tails, const int32_t *heads, const int64_t *caps,
+                       const int64_t *res_fwd, const int64_t *res_rev, int s, int t, const uint8_t *source_side,
+                       int64_t flow, int32_t *checks_out) {
+    if (nn < 2 || m < 0 || s < 0 || t < 0 || s >= nn || t >= nn || s == t || !checks_out) return OR_E_INVAL;
+    graph_t g;
+    if (g_alloc(&g, nn)) return OR_E_NOMEM;
+    for (int i = 0; i < m; i++) {
+        if (tails[i] < 0 || tails[i] >= nn || heads[i] < 0 || heads[i] >= nn || caps[i] < 0) {
+            g_free(&g);
+            return OR_E_INVAL;
+        }
+        add_arc(&g, 0, tails[i], heads[i], caps[i]);
+    }
+    if (g_finish_count(&g)) { g_free(&g); return OR_E_NOMEM; }
+    for (int i = 0; i < m; i++) {
+        const int64_t a = g.fill[tails[i]]; /* the slot add_arc is about to use for arc i */
+        add_arc(&g, 1, tails[i], heads[i], caps[i]);
+        g.res[a] = res_fwd[i];
+        g.res[g.rev[a]] = res_rev[i];
+    }
+    *checks_out = check_invariants(&g, s, t, source_side, flow);
+    g_free(&g);
+    return OR_OK;
+}

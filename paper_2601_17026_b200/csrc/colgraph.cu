@@ -895,7 +895,7 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
     const bool relist_ordered = getenv("CG_RELIST") && atoi(getenv("CG_RELIST")) != 0;
     double work_since_gr = 0.0, sweep_ms_since_gr = 0.0;
     int64_t sweeps = g->st.sweeps, since_gap = 0, last_active = active;
-    std::vector<int64_t> wv(RING);
+    std::vector<int64_t> wv(RING + 1);  // batch <= RING counters + the overflow flag
     // Profiling aid (vertex loop): CG_GR_LOG=file appends the sweep counts at which this solve's
     // triggers fired; CG_GR_SCHEDULE="s1,s2,..." replays such a schedule instead of the work /
     // time triggers, so a run under ncu (whose replay-slowed kernels distort the time trigger)
