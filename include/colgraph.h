@@ -214,6 +214,16 @@ cg_status colgraph_build_slabs_soft(const cg_dims *dims, const int32_t *cost_dev
  * Errors: CG_E_INVAL (NULL), CG_E_NCCL (libnccl.so.2 not loadable). */
 cg_status cg_nccl_unique_id(void *id_out);
 
+/* TEST HOOK -- enable != 0 replaces NCCL with an in-process loopback transport
+ * (csrc/nccl_loopback.h) for every later NCCL call of this process: all ranks of a job live in
+ * this process on one device, one host thread per rank, each passing its own stream and a
+ * cg_nccl_unique_id() obtained AFTER enabling.  The x-slab driver then runs its NCCL code path
+ * (communicator cache, grouped send/recv halos, allreduce counters) unchanged, which lets a
+ * one-GPU test suite execute it (§3.2.1-3.2.2: segment boundary exchange and
+ * per-level synchronisation).  enable = 0 restores libnccl.  Not for production use.
+ * Errors: none (CG_OK). */
+cg_status cg_nccl_loopback(int32_t enable);
+
 /* a2-a6 -- lock-free push-relabel to a maximum preflow (§2.1,
  * Alg. 2) with exact global relabels from the sink (Alg. 3,
  * §3.2.2), optional gap relabeling (L170-184) and termination decided after an

@@ -83,6 +83,8 @@ def _load():
                                          P(ctypes.c_void_p)]
     lib.cg_nccl_unique_id.restype = ctypes.c_int
     lib.cg_nccl_unique_id.argtypes = [ctypes.c_void_p]
+    lib.cg_nccl_loopback.restype = ctypes.c_int
+    lib.cg_nccl_loopback.argtypes = [ctypes.c_int32]
     lib.maxflow_solve.restype = ctypes.c_int
     lib.maxflow_solve.argtypes = [ctypes.c_void_p, P(cg_solve_opts), P(ctypes.c_int64), P(cg_solve_stats)]
     lib.mincut_extract_surface.restype = ctypes.c_int
@@ -110,7 +112,7 @@ def _load():
 
 _lib = _load()
 
-EXPORTED = ["colgraph_build", "colgraph_build_slabs", "colgraph_build_soft", "colgraph_build_slabs_soft", "cg_nccl_unique_id", "maxflow_solve", "mincut_extract_surface",
+EXPORTED = ["colgraph_build", "colgraph_build_slabs", "colgraph_build_soft", "colgraph_build_slabs_soft", "cg_nccl_unique_id", "cg_nccl_loopback", "maxflow_solve", "mincut_extract_surface",
             "maxflow_export_flow", "colgraph_solve_host",
             "colgraph_export_state", "colgraph_stats", "colgraph_free", "cg_status_str", "cg_slab_range", "cg_version"]
 
@@ -142,20 +144,25 @@ def _check_dev_int32(t, name):
         raise TypeError(f"{name} must be a contiguous CUDA int32 tensor")
 
 
-def colgraph_build_soft(cost, delta, penalty, input_is_weight: bool = False, stream=None):
-    """NEXT-1: soft smoothness, penalty = [f(1), ..., f(K)] convex (include/colgraph.h)."""
+def colgraph_build_soft(cost, delta, penalty, input_is_weight: bool = False, stream=None, rank=0, nranks=1,
+                        nccl_id=None, dims=None):
+    """NEXT-1: soft smoothness, penalty = [f(1), ..., f(K)] convex (include/colgraph.h).  With
+    nranks > 1: this rank's slab of the full volume dims (as colgraph_build)."""
     _check_dev_int32(cost, "cost")
     import torch
     if stream is None:
         stream = torch.cuda.current_stream(cost.device)
-    X, Y, Z = cost.shape
-    dims = cg_dims(X, Y, Z, delta)
+    if dims is None:
+        X, Y, Z = cost.shape
+        dims = cg_dims(X, Y, Z, delta)
     pen = (ctypes.c_int32 * len(penalty))(*[int(v) for v in penalty])
     h = ctypes.c_void_p()
+    idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
     st = _lib.colgraph_build_soft(ctypes.byref(dims), ctypes.c_void_p(cost.data_ptr()), int(bool(input_is_weight)),
                                   pen, len(penalty),
-                                  ctypes.byref(_dist(cost.device.index, ctypes.c_void_p(stream.cuda_stream), 0, 1,
-                                                     None)), ctypes.byref(h))
+                                  ctypes.byref(_dist(cost.device.index, ctypes.c_void_p(stream.cuda_stream), rank,
+                                                     nranks, ctypes.cast(idbuf, ctypes.c_void_p)
+                                                     if idbuf is not None else None)), ctypes.byref(h))
     if st != CG_OK:
         raise ColgraphError(st, "colgraph_build_soft")
     return h
@@ -229,6 +236,14 @@ def nccl_unique_id() -> bytes:
     if st != CG_OK:
         raise ColgraphError(st, "cg_nccl_unique_id")
     return buf.raw
+
+
+def nccl_loopback(enable: bool) -> None:
+    """TEST HOOK: route every later NCCL call of this process through the in-process loopback
+    transport (all ranks as host threads on one device; include/colgraph.h cg_nccl_loopback)."""
+    st = _lib.cg_nccl_loopback(int(bool(enable)))
+    if st != CG_OK:
+        raise ColgraphError(st, "cg_nccl_loopback")
 
 
 def maxflow_solve(handle, opts: cg_solve_opts | None = None):

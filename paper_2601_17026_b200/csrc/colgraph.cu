@@ -26,6 +26,7 @@
 #include "colgraph.h"
 #include "kernels.cuh"
 #include "nccl_shim.h"
+#include "nccl_loopback.h"
 #include "tile.cuh"
 
 #include <algorithm>
@@ -895,7 +896,7 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
     const bool relist_ordered = getenv("CG_RELIST") && atoi(getenv("CG_RELIST")) != 0;
     double work_since_gr = 0.0, sweep_ms_since_gr = 0.0;
     int64_t sweeps = g->st.sweeps, since_gap = 0, last_active = active;
-    std::vector<int64_t> wv(RING + 1);  // batch <= RING counters + the overflow flag
+    std::vector<int64_t> wv(RING + 2);  // batch <= RING counters + the overflow flag + the time trigger
     // Profiling aid (vertex loop): CG_GR_LOG=file appends the sweep counts at which this solve's
     // triggers fired; CG_GR_SCHEDULE="s1,s2,..." replays such a schedule instead of the work /
     // time triggers, so a run under ncu (whose replay-slowed kernels distort the time trigger)
@@ -1040,7 +1041,10 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
         g->st.ms_sweep_kernels += ms;
         sweep_ms_since_gr += ms;
         wv[batch] = overflow;
-        CG_TRY(gsum(g, wv.data(), batch + 1));
+        // the time-based relabel trigger is a local measurement: ranks agree on it through the
+        // same allreduce as the sweep counters (one collective per batch)
+        wv[batch + 1] = sweep_ms_since_gr >= gr_beta * std::max(last_gr_ms, 0.05);
+        CG_TRY(gsum(g, wv.data(), batch + 2));
         if (wv[batch]) { result = CG_E_OVERFLOW; break; }
         if (trace) {
             fprintf(stderr, "[cg] sweeps %lld..%lld ops:", (long long)sweeps, (long long)(sweeps + batch - 1));
@@ -1058,10 +1062,8 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
         sweeps += batch;
         since_gap += batch;
         g->st.sweeps = sweeps;
-        // the time-based trigger is a local measurement: agree on it across ranks
-        int64_t trigger = quiescent || work_since_gr >= gr_budget || sweep_ms_since_gr >= gr_beta * std::max(last_gr_ms, 0.05);
+        bool trigger = quiescent || work_since_gr >= gr_budget || wv[batch + 1] > 0;
         if (sched_i < sched.size()) trigger = quiescent || sweeps >= sched[sched_i];  // then the usual triggers
-        CG_TRY(gmax(g, &trigger));
         if (trigger) {
             fired.push_back(sweeps);
             while (sched_i < sched.size() && sched[sched_i] <= sweeps) sched_i++;
@@ -1117,6 +1119,12 @@ cg_status cg_slab_range(const cg_dims *dims, int32_t rank, int32_t nranks, int32
     const int32_t q = dims->X / nranks, r = dims->X % nranks;
     *x0 = rank * q + std::min(rank, r);
     *x1 = *x0 + q + (rank < r ? 1 : 0);
+    return CG_OK;
+}
+
+cg_status cg_nccl_loopback(int32_t enable) {
+    static const NcclApi lb = loopback::api();
+    nccl_active() = enable ? &lb : nullptr;
     return CG_OK;
 }
 

@@ -23,7 +23,7 @@ struct NcclApi {
     ncclResult_t (*groupEnd)() = nullptr;
 };
 
-inline const NcclApi &nccl() {
+inline const NcclApi &nccl_real() {
     static NcclApi api = [] {
         NcclApi a;
         void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
@@ -43,6 +43,17 @@ inline const NcclApi &nccl() {
         return a;
     }();
     return api;
+}
+
+// The active table: the real libnccl, or a test transport installed with nccl_set_active()
+// (nccl_loopback.h via cg_nccl_loopback).
+inline const NcclApi *&nccl_active() {
+    static const NcclApi *p = nullptr;
+    return p;
+}
+inline const NcclApi &nccl() {
+    const NcclApi *p = nccl_active();
+    return p ? *p : nccl_real();
 }
 
 }  // namespace cg
