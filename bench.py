@@ -224,13 +224,26 @@ def run_ours(args, spec):
         ev0.record(stream)
         step_ev[0].record(stream)
         for k in range(args.steps):
-            flow, s, _ = step(cost)
+            flow, s, surf_last = step(cost)
+            s = dict(s, flow=flow)
             stats.append(s)
             step_ev[k + 1].record(stream)
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier()
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    # every timed step's |f| and the last step's surface against the oracle's stored result
+    # (tests/golden, written by scripts/make_oracle_golden.py from oracle/ only)
+    golden_ok = None
+    gpath = os.path.join(ROOT, "tests", "golden", f"oracle_{spec.name}.json")
+    if os.path.exists(gpath):
+        import hashlib
+        gold = json.load(open(gpath))
+        flows = {st["flow"] for st in stats}
+        assert flows == {gold["flow"]}, (flows, gold["flow"])
+        surf_all = cgd.gather_slabs(surf_last.cpu().numpy()) if world > 1 else surf_last.cpu().numpy()
+        assert hashlib.sha256(surf_all.astype("<i4").tobytes()).hexdigest() == gold["surface_sha256"]
+        golden_ok = True
     step_ms = sorted(step_ev[k].elapsed_time(step_ev[k + 1]) for k in range(args.steps))
     ms_step = ms_total / args.steps
     value = spec.n * args.steps / (ms_total / 1000.0) / 1e6  # whole volume per step, all ranks together
@@ -279,27 +292,27 @@ def run_ours(args, spec):
                 "traffic_source": tr.get("source") if tr else None,
                 "alg_bytes_per_launch": sweep_bytes / max(sweeps, 1),
                 "avg_launch_us": 1000.0 * sweep_ms / max(sweeps, 1),
-                "alg_bytes_def": "44 B per push/relabel operation: 32 B vertex state read + 12 B push writes "
-                                 "(DESIGN.md 'Algorithmic bytes')",
+                "alg_bytes_def": "SURVEY.md §8(d): 32 B per vertex visit (state read) + 12 B per push + "
+                                 "4 B per relabel",
+                "relabel_share_of_ops": sum(s["relabel_ops"] for s in stats) / max(1, sum(s["work"] for s in stats)),
                 "share_of_step": sweep_ms * args.steps / (ms_total * len(stats)) if ms_total > 0 else None}
-    # the sweep is a scattered traversal: its access-pattern roofline is the B200's random 32-byte
-    # record gather throughput (bench_tools/random_gather.cu, profiles/r01_random_gather.json)
-    rg_path = os.path.join(ROOT, "profiles", "r01_random_gather.json")
-    roofline_ra = None
-    if os.path.exists(rg_path):
-        rg = json.load(open(rg_path))
-        rg_peak = max(v for k, v in rg.items() if k.startswith("gather_") and k.endswith("_gbs"))
-        roofline_ra = {"kernel": roofline["kernel"], "bound": "hbm-random-32B", "achieved": achieved, "peak": rg_peak,
-                       "unit": "GB/s", "frac": achieved / rg_peak,
-                       "peak_source": "measured random 32-B record gather over 2 GiB (bench_tools/random_gather.cu, "
-                                      "profiles/r01_random_gather.json)"}
+    # global relabel (a2/a5): SURVEY.md §8(d) prices a full pass at 28 B per vertex (read T, D, L;
+    # write H); achieved = that x n per relabel / the relabel's average wall time in the solve
+    n_gr = sum(s["global_relabels"] for s in stats)
+    gr_ms = sum(s["ms_global_relabel"] for s in stats)
+    gr_alg = 28.0 * spec.n
+    roofline_gr = {"kernel": "global relabel (exact reverse BFS / column fixpoint)", "bound": "hbm",
+                   "achieved": gr_alg * n_gr / (gr_ms / 1000.0) / 1e9 if gr_ms > 0 else 0.0, "peak": peak,
+                   "unit": "GB/s", "alg_bytes_per_relabel": gr_alg, "avg_relabel_ms": gr_ms / max(n_gr, 1),
+                   "alg_bytes_def": "28 B per vertex per relabel (SURVEY.md §8(d))"}
+    roofline_gr["frac"] = roofline_gr["achieved"] / peak
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "time_to_min_cut_s": ms_step / 1000.0,
             "ms_per_step_min_median_max": [step_ms[0], step_ms[len(step_ms) // 2], step_ms[-1]],
-            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "int32", "data": "synthetic (seeded generator synth/volumes.py, sha256-pinned)",
             "config": workload_config(spec, {"parallelism": f"x-slab{world}" if world > 1 else "single-gpu"}),
-            "flow": flow, "roofline": roofline, "roofline_random_access": roofline_ra,
+            "flow": flow, "flow_matches_oracle_golden": golden_ok, "roofline": roofline, "roofline_relabel": roofline_gr,
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms, "h2d_bytes_per_step": 4 * spec.n,
                     "d2h_bytes_per_step": 4 * X * Y + 8},
             "gpu_launches": int(sum(s["kernel_launches"] for s in stats)),

@@ -28,25 +28,19 @@
  *   CG_DEBUG=1            print the failing CUDA / NCCL call on stderr
  *   CG_WALK=K             hop budget of multi-hop walks (default 64)
  *   CG_WALK_MIN=f         walks while >= f*n vertices are active (default 1e-3), single hops below
- *   CG_WALK_WS=0          k_walk instead of the work-fetching walk k_walk_ws (default);
- *                         CG_WALK_PARK / CG_WALK_RCONT / CG_RELIST apply to k_walk only
- *   CG_WALK_PARK=1        stuck walks wait for the next global relabel
- *   CG_WALK_RCONT=k       a stuck walk may relabel and go on up to k times (default 0)
  *   CG_GR_LOG=file        append the sweep counts at which the relabel triggers fired
  *   CG_GR_SCHEDULE=s1,..  replay such a schedule (profiling under ncu); afterwards the
  *                         usual triggers
- *   CG_RELIST=1           re-list large sweep worklists in index order
  *   CG_OPS=k              push/relabel operations per vertex per single-hop sweep
  *   CG_GR_BETA=b          time trigger: relabel when sweep time since the last one >= b * its cost
  *   CG_BFS_SMALL=k        persistent BFS: frontiers <= k run in block 0 alone (default 64)
- *   CG_BU_ALPHA/BETA      direction-optimising (bottom-up) BFS levels (default off)
  *   CG_BFS_LEVEL_LAUNCHES one kernel launch per BFS level instead of the persistent BFS
- *   CG_PRECANCEL=1        exact per-column pre-cancellation before the first relabel
  *   CG_SWEEP=1            tile sweeps (as sweep_kind = CG_SWEEP_TILES); CG_TILE=TXxTY,
  *                         CG_TILE_STEPS, CG_TILE_RELABEL, CG_TILE_PROF=1 (clock counters)
  *   CG_PHASE2_PR=1        maxflow_export_flow: generic push-relabel phase 2 only
- *   CG_SLAB_LC=1          x-slabs: label-correcting global relabel instead of the
- *                         level-synchronous one
+ *   CG_RELABEL=bfs        global relabel by the vertex-frontier BFS instead of the column
+ *                         fixpoint (the BFS also serves soft graphs, Z > 256 and tiles)
+ *   CG_COLGR_SMALL=k      column fixpoint: worklists <= k columns run in block 0 alone
  * Conventions for every entry point:
  *   - Errors are returned as cg_status, never thrown; no C++ exception crosses
  *     this ABI.
@@ -155,10 +149,11 @@ typedef struct {
     int64_t source_capacity;   /* N = sum of source-arc capacities (int64) */
     int64_t kernel_launches;   /* library kernel launches during solve + extract */
     double ms_sweep_kernels;   /* CUDA-event time of all sweep launches (on the library stream) */
-    double sweep_bytes_alg;    /* algorithmic bytes moved by all sweeps: vertex worklists 44 B per
-                                  push/relabel operation; tiles (64 B per tile vertex + 8 B per halo
-                                  vertex) per tile visit */
+    double sweep_bytes_alg;    /* algorithmic bytes moved by all sweeps: vertex
+                                  worklists 32 B per vertex visit + 12 B per push + 4 B per relabel;
+                                  tiles (64 B per tile vertex + 8 B per halo vertex) per tile visit */
     int64_t tile_visits;       /* tile visits summed over all phases (tile sweeps only) */
+    int64_t relabel_ops;       /* sweep operations that were relabels (vertex worklists) */
 } cg_solve_stats;
 
 /* a1 -- build the int32 structure-of-arrays residual graph.

@@ -25,6 +25,7 @@
 //           with device-to-device copies -- used to test the multi-slab algorithm on one GPU.
 #include "colgraph.h"
 #include "kernels.cuh"
+#include "relabel.cuh"
 #include "nccl_shim.h"
 #include "nccl_loopback.h"
 #include "tile.cuh"
@@ -61,10 +62,14 @@ struct Slab {
     unsigned *hist = nullptr;
     BfsState *bst = nullptr;
     unsigned *cnt = nullptr;             // [0..2] sweep lists, [4..6] lc waves, [8..10] extraction, [12] changes
-    unsigned long long *work = nullptr;  // [RING] operations per sweep
+    unsigned long long *work = nullptr;  // [2*RING] per sweep: operations, relabels
     unsigned long long *visits = nullptr;  // [RING] tile visits per phase
     unsigned *heads = nullptr;             // [RING] work-fetch cursors of k_walk_ws
     unsigned *visited = nullptr;           // [n/32 + 1] BFS visited bitmap (persistent BFS)
+    int32_t *lab = nullptr;                // column-fixpoint relabel: labels, planes [-YZ, n + YZ)
+    uint8_t *gflags = nullptr;             // column-fixpoint relabel: residual-arc flags, same range
+    ColGrState *cst = nullptr, *h_cst = nullptr;
+    int colgr_grid = 0;                    // > 0: cooperative grid of k_colgr_run
     unsigned long long *u64 = nullptr;   // [0]=N [1]=sumT0 [2]=sumT [3]=active [4]=gap lifted [5]=scratch
     int *flags = nullptr;                // [0]=overflow [1]=maxh [2]=gap [3]=empty
     int32_t *snap[2] = {nullptr, nullptr};   // ghost lateral residual at the last refresh
@@ -281,11 +286,12 @@ size_t workspace_bytes(const Geo &geo) {
     b += 3 * al(sizeof(int) * geo.n);
     b += 3 * al(sizeof(int32_t) * (ncol + 2 * geo.Y)) + 2 * al(sizeof(int) * ncol);
     b += al(sizeof(unsigned) * GAP_BINS) + al(sizeof(BfsState));
-    b += al(sizeof(unsigned) * 16) + al(sizeof(unsigned long long) * RING) + al(sizeof(unsigned long long) * 16) +
+    b += al(sizeof(unsigned) * 16) + al(sizeof(unsigned long long) * 2 * RING) + al(sizeof(unsigned long long) * 16) +
          al(sizeof(int) * 16);
     b += 4 * al(sizeof(int32_t) * geo.YZ) + 4 * al(sizeof(int32_t) * halo_msg_ints(geo));
     b += 5 * al(sizeof(int) * ncol) + al(sizeof(unsigned) * 4) + al(sizeof(unsigned long long) * RING) +
          al(sizeof(unsigned long long) * 16) + al(sizeof(unsigned) * RING) + al(sizeof(unsigned) * (geo.n / 32 + 1));
+    b += al(sizeof(int32_t) * plane) + al(plane) + al(sizeof(ColGrState));
     return b;
 }
 
@@ -318,11 +324,12 @@ cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode) {
     {
         char *hp = sl->h_block;
         sl->h_cnt = carve<unsigned>(hp, 16);
-        sl->h_work = carve<unsigned long long>(hp, RING);
+        sl->h_work = carve<unsigned long long>(hp, 2 * RING);
         sl->h_u64 = carve<unsigned long long>(hp, 16);
         sl->h_flags = carve<int>(hp, 16);
         sl->h_bst = carve<BfsState>(hp, 1);
         sl->h_visits = carve<unsigned long long>(hp, RING);
+        sl->h_cst = carve<ColGrState>(hp, 1);
         if (hp > sl->h_block + PINNED_BLOCK) return CG_E_NOMEM;
     }
     char *p = sl->ws;
@@ -357,7 +364,7 @@ cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode) {
     sl->hist = carve<unsigned>(p, GAP_BINS);
     sl->bst = carve<BfsState>(p, 1);
     sl->cnt = carve<unsigned>(p, 16);
-    sl->work = carve<unsigned long long>(p, RING);
+    sl->work = carve<unsigned long long>(p, 2 * RING);
     sl->u64 = carve<unsigned long long>(p, 16);
     sl->flags = carve<int>(p, 16);
     const int64_t msg = halo_msg_ints(geo);
@@ -368,6 +375,9 @@ cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode) {
     sl->visits = carve<unsigned long long>(p, RING);
     sl->heads = carve<unsigned>(p, RING);
     sl->visited = carve<unsigned>(p, n / 32 + 1);
+    sl->lab = carve<int32_t>(p, plane) + geo.YZ;
+    sl->gflags = carve<uint8_t>(p, plane) + geo.YZ;
+    sl->cst = carve<ColGrState>(p, 1);
     for (int side = 0; side < 2; side++) {
         sl->snap[side] = carve<int32_t>(p, geo.YZ);
         sl->hold[side] = carve<int32_t>(p, geo.YZ);
@@ -482,29 +492,41 @@ void k_fill_ghost_h(Slab *sl) {
     if (geo.gh) k_fill<<<grid, 256, 0, sl->stream>>>(sl->s.H, geo.n, geo.YZ, geo.INF);
 }
 
-// Strict level-synchronous BFS of one slab without neighbours (the single-GPU path).
-cg_status bfs_strict(cg_graph *g, Slab *sl, bool allow_coop = true) {
+// Strict level-synchronous BFS of one slab without neighbours (the single-GPU path).  flag_plane:
+// the flag-plane BFS (k_bfs2_init + k_bfs_run<true>, labels in sl->lab; the default for hard
+// graphs), else the record BFS (k_bfs_init + k_bfs_run<false> / k_bfs_step, labels in the records).
+cg_status bfs_strict(cg_graph *g, Slab *sl, bool allow_coop = true, bool flag_plane = false) {
     const Geo &geo = sl->geo;
     cudaStream_t st = sl->stream;
     CG_CUDA(cudaMemsetAsync(sl->bst, 0, sizeof(BfsState), st));
     sl->h_bst->L = 1;
-    // direction optimisation measured slower than top-down on C3-C5: off unless asked
-    sl->h_bst->bu_alpha = getenv("CG_BU_ALPHA") && !geo.soft_k ? atoi(getenv("CG_BU_ALPHA")) : 0;
-    sl->h_bst->bu_beta = getenv("CG_BU_BETA") ? atoi(getenv("CG_BU_BETA")) : 64;
     sl->h_bst->small = getenv("CG_BFS_SMALL") ? (unsigned)atoi(getenv("CG_BFS_SMALL")) : BFS_RUN_SMALL;
     CG_CUDA(cudaMemcpyAsync(&sl->bst->L, &sl->h_bst->L, sizeof(int), cudaMemcpyHostToDevice, st));
-    CG_CUDA(cudaMemcpyAsync(&sl->bst->bu_alpha, &sl->h_bst->bu_alpha, 2 * sizeof(int) + sizeof(unsigned),
-                            cudaMemcpyHostToDevice, st));
+    CG_CUDA(cudaMemcpyAsync(&sl->bst->small, &sl->h_bst->small, sizeof(unsigned), cudaMemcpyHostToDevice, st));
     const bool coop = allow_coop && sl->bfs_coop_grid > 0;
-    k_bfs_init<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, st>>>(geo, sl->s, sl->blist[0], &sl->bst->cnt[0],
-                                                                        coop ? sl->visited : nullptr);
-    k_bfs_seeded<<<1, 1, 0, st>>>(sl->bst);
+    if (flag_plane && !coop) return CG_E_INVAL;
+    if (flag_plane) {
+        // early stop once every vertex with excess is labelled (CG_BFS_FULL=1: run every level)
+        const int early = getenv("CG_BFS_FULL") && atoi(getenv("CG_BFS_FULL")) ? 0 : 1;
+        CG_CUDA(cudaMemcpyAsync(&sl->bst->early, &early, sizeof(int), cudaMemcpyHostToDevice, st));
+        k_bfs2_init<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, st>>>(
+            geo, sl->s, sl->gflags, sl->lab, sl->visited, sl->blist[0], &sl->bst->cnt[0], &sl->bst->act_total);
+        k_bfs2_seeded<<<sl->num_sms, 256, 0, st>>>(sl->bst, sl->gflags, sl->blist[0]);
+        CG_CUDA(cudaStreamSynchronize(st));  // `early` is a host stack value
+    } else {
+        k_bfs_init<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, st>>>(geo, sl->s, sl->blist[0], &sl->bst->cnt[0],
+                                                                            coop ? sl->visited : nullptr);
+        k_bfs_seeded<<<1, 1, 0, st>>>(sl->bst);
+    }
     g->st.kernel_launches += 2;
     int L = 1;
     if (coop) {  // every level in one cooperative launch (k_bfs_run)
+        const uint8_t *fl = flag_plane ? sl->gflags : nullptr;
+        int32_t *lb = flag_plane ? sl->lab : nullptr;
         void *args[] = {(void *)&sl->geo, (void *)&sl->s, (void *)&sl->blist[0], (void *)&sl->blist[1],
-                        (void *)&sl->bst, (void *)&sl->visited};
-        CG_CUDA(cudaLaunchCooperativeKernel((const void *)k_bfs_run, sl->bfs_coop_grid, 512, args, 0, st));
+                        (void *)&sl->bst, (void *)&sl->visited, (void *)&fl, (void *)&lb};
+        CG_CUDA(cudaLaunchCooperativeKernel(flag_plane ? (const void *)k_bfs_run<true> : (const void *)k_bfs_run<false>,
+                                            sl->bfs_coop_grid, 512, args, 0, st));
         g->st.kernel_launches++;
         CG_CUDA(cudaMemcpyAsync(sl->h_bst, sl->bst, sizeof(BfsState), cudaMemcpyDeviceToHost, st));
         CG_CUDA(cudaStreamSynchronize(st));
@@ -526,6 +548,126 @@ cg_status bfs_strict(cg_graph *g, Slab *sl, bool allow_coop = true) {
         if ((int64_t)L > (int64_t)geo.INF + 2) return CG_E_CUDA;  // every level claims >= 1 vertex
     }
     g->st.gr_passes += L - 1;
+    return CG_OK;
+}
+
+// ---- column-scan fixpoint relabel (relabel.cuh; default for hard graphs with Z <= 256)
+const void *colgr_kernel(int Z) {
+    if (Z <= 32) return (const void *)k_colgr_run<1>;
+    if (Z <= 64) return (const void *)k_colgr_run<2>;
+    if (Z <= 96) return (const void *)k_colgr_run<3>;
+    if (Z <= 128) return (const void *)k_colgr_run<4>;
+    if (Z <= 32 * COLGR_MAX_CPC) return (const void *)k_colgr_run<COLGR_MAX_CPC>;
+    return nullptr;
+}
+
+// the column fixpoint serves hard graphs with Z <= 256 on a device with cooperative launch;
+// CG_RELABEL=bfs selects the vertex-frontier BFS (measured alternative)
+// Relabel flavour: FLAGS = the flag-plane vertex BFS (default for hard graphs on
+// one slab), COLGR = the column fixpoint (default on x-slabs: its exchanges count slab-boundary
+// crossings, not BFS levels), RECORD = the record BFS (soft graphs, tiles, Z > 256 for the
+// fixpoint, no cooperative launch).  CG_RELABEL = flags | colgr | bfs overrides where applicable.
+enum RelabelKind { RELABEL_RECORD, RELABEL_FLAGS, RELABEL_COLGR };
+RelabelKind relabel_kind(const cg_graph *g) {
+    const Slab *sl = g->slabs[0];
+    if (sl->geo.soft_k || sl->tiles) return RELABEL_RECORD;
+    const char *e = getenv("CG_RELABEL");
+    if (e && !strcmp(e, "bfs")) return RELABEL_RECORD;
+    const bool colgr_ok = sl->colgr_grid > 0;
+    const bool flags_ok = sl->bfs_coop_grid > 0 && !multi(g);
+    if (e && !strcmp(e, "colgr") && colgr_ok) return RELABEL_COLGR;
+    if (e && !strcmp(e, "flags") && flags_ok) return RELABEL_FLAGS;
+    if (multi(g)) return colgr_ok ? RELABEL_COLGR : RELABEL_RECORD;
+    return flags_ok ? RELABEL_FLAGS : RELABEL_RECORD;
+}
+
+cg_status colgr_launch(Slab *sl, int dense) {
+    void *args[] = {(void *)&sl->geo, (void *)&sl->gflags, (void *)&sl->lab, (void *)&sl->collist[0],
+                    (void *)&sl->collist[1], (void *)&sl->cst, (void *)&sl->colstamp, (void *)&dense};
+    CG_CUDA(cudaLaunchCooperativeKernel(colgr_kernel(sl->geo.Z), sl->colgr_grid, 512, args, 0, sl->stream));
+    return CG_OK;
+}
+
+// flags of the residual arcs + labels reset to INF over owned and ghost planes, fixpoint state
+cg_status colgr_begin(cg_graph *g, Slab *sl) {
+    const Geo &geo = sl->geo;
+    CG_CUDA(cudaMemsetAsync(sl->cst, 0, sizeof(ColGrState), sl->stream));
+    sl->h_cst->small = getenv("CG_COLGR_SMALL") ? (unsigned)atoi(getenv("CG_COLGR_SMALL")) : 16;
+    sl->h_cst->tag0 = sl->tag + 1;
+    CG_CUDA(cudaMemcpyAsync(&sl->cst->small, &sl->h_cst->small, 2 * sizeof(int), cudaMemcpyHostToDevice, sl->stream));
+    const int64_t lo = geo.gl ? -geo.YZ : 0, hi = geo.n + (geo.gh ? geo.YZ : 0);
+    k_colgr_flags<<<grid_for(hi - lo, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(geo, sl->s, sl->gflags, sl->lab, lo,
+                                                                                     hi);
+    g->st.kernel_launches++;
+    CG_CUDA(cudaGetLastError());
+    return CG_OK;
+}
+
+// after the fixpoint: round count, tags consumed
+cg_status colgr_end(cg_graph *g, Slab *sl) {
+    CG_CUDA(cudaMemcpyAsync(sl->h_cst, sl->cst, sizeof(ColGrState), cudaMemcpyDeviceToHost, sl->stream));
+    CG_CUDA(cudaStreamSynchronize(sl->stream));
+    sl->tag = sl->h_cst->tag0 + sl->h_cst->round + 1;
+    g->st.gr_passes += sl->h_cst->round;
+    return CG_OK;
+}
+
+// one slab without neighbours: flags, one cooperative launch for every round
+cg_status colgr_strict(cg_graph *g, Slab *sl) {
+    CG_TRY(colgr_begin(g, sl));
+    CG_TRY(colgr_launch(sl, 1));
+    g->st.kernel_launches++;
+    return colgr_end(g, sl);
+}
+
+// x-slabs: every slab runs its fixpoint to local convergence, then the boundary planes' labels go
+// to the neighbours' ghost planes; a boundary column facing a ghost column whose labels dropped
+// restarts the fixpoint.  Stop when no slab listed anything (one global sum per exchange): the
+// number of exchanges is the number of slab-boundary crossings of the shortest paths (+1), not the
+// BFS depth (§3.2.2 L274-289 synchronises every level).
+cg_status colgr_slabs(cg_graph *g) {
+    for (Slab *sl : g->slabs) {
+        CG_TRY(colgr_begin(g, sl));
+        CG_TRY(colgr_launch(sl, 1));
+        g->st.kernel_launches++;
+    }
+    const int64_t YZ = g->slabs[0]->geo.YZ;
+    for (int iter = 0;; iter++) {
+        for (Slab *sl : g->slabs) {
+            k_colgr_pack<<<grid_for(2 * YZ, 256, sl->num_sms * 4), 256, 0, sl->stream>>>(sl->geo, sl->lab, sl->hsend[0],
+                                                                                        sl->hsend[1]);
+            g->st.kernel_launches++;
+        }
+        CG_TRY(transfer(g, YZ));
+        int64_t listed = 0;
+        for (Slab *sl : g->slabs) {
+            const Geo &geo = sl->geo;
+            k_colgr_unpack<<<grid_for((int64_t)(geo.gl + geo.gh) * geo.Y * 32, 256, sl->num_sms * 4), 256, 0,
+                             sl->stream>>>(geo, sl->lab, sl->hrecv[0], sl->hrecv[1], sl->colstamp, sl->collist[0],
+                                           sl->collist[1], sl->cst);
+            g->st.kernel_launches++;
+            CG_CUDA(cudaGetLastError());
+            CG_CUDA(cudaMemcpyAsync(sl->h_cst, sl->cst, sizeof(ColGrState), cudaMemcpyDeviceToHost, sl->stream));
+        }
+        for (Slab *sl : g->slabs) {
+            CG_CUDA(cudaStreamSynchronize(sl->stream));
+            listed += sl->h_cst->cnt[sl->h_cst->round % 3];
+        }
+        CG_TRY(gsum(g, &listed, 1));
+        if (listed == 0) break;
+        if (iter > 4 * (int64_t)g->dims.X + 64) return CG_E_CUDA;  // every exchange lowers some label
+        for (Slab *sl : g->slabs)
+            if (sl->h_cst->cnt[sl->h_cst->round % 3]) {
+                CG_TRY(colgr_launch(sl, 0));
+                g->st.kernel_launches++;
+            }
+    }
+    for (Slab *sl : g->slabs) {
+        const Geo &geo = sl->geo;
+        k_colgr_ghost_h<<<grid_for(2 * YZ, 256, sl->num_sms * 4), 256, 0, sl->stream>>>(geo, sl->s, sl->lab);
+        g->st.kernel_launches++;
+        CG_TRY(colgr_end(g, sl));
+    }
     return CG_OK;
 }
 
@@ -600,85 +742,18 @@ cg_status bfs_slabs_levels(cg_graph *g) {
     return CG_OK;
 }
 
-// Label-correcting relabel across slabs (CG_SLAB_LC=1): local waves until every frontier is empty, then
-// exchange ghost heights and relax from improved ghosts; stop when nothing changed anywhere.
-cg_status bfs_slabs(cg_graph *g) {
-    for (Slab *sl : g->slabs) {
-        const Geo &geo = sl->geo;
-        CG_CUDA(cudaMemsetAsync(sl->cnt + 4, 0, 3 * sizeof(unsigned), sl->stream));
-        k_bfs_init<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(geo, sl->s, sl->blist[0],
-                                                                                     sl->cnt + 4);
-        // ghost heights start unknown (INF)
-        k_fill_ghost_h(sl);
-        sl->wave_k = 0;
-        g->st.kernel_launches += 1;
-    }
-    for (int outer = 0;; outer++) {
-        // local waves
-        for (;;) {
-            int64_t pending = 0;
-            for (Slab *sl : g->slabs) {
-                const Geo &geo = sl->geo;
-                const int grid = list_grid(sl, geo.n);
-                for (int b = 0; b < LC_BATCH; b++) {
-                    const int w = sl->wave_k++;
-                    k_lc_wave<<<grid, 256, 0, sl->stream>>>(geo, sl->s, sl->blist[w & 1], sl->cnt + 4 + w % 3,
-                                                             sl->blist[(w + 1) & 1], sl->cnt + 4 + (w + 1) % 3,
-                                                             sl->cnt + 4 + (w + 2) % 3, sl->vstamp, ++sl->tag);
-                }
-                g->st.kernel_launches += LC_BATCH;
-                g->st.gr_passes += LC_BATCH;
-                CG_CUDA(cudaGetLastError());
-                CG_CUDA(cudaMemcpyAsync(sl->h_cnt + 4, sl->cnt + 4, 3 * sizeof(unsigned), cudaMemcpyDeviceToHost,
-                                        sl->stream));
-            }
-            for (Slab *sl : g->slabs) {
-                CG_CUDA(cudaStreamSynchronize(sl->stream));
-                pending += sl->h_cnt[4 + sl->wave_k % 3];
-            }
-            if (pending == 0) break;
-        }
-        // ghost heights
-        for (Slab *sl : g->slabs) {
-            const Geo &geo = sl->geo;
-            const int grid = grid_for(geo.YZ, 256, sl->num_sms * 4);
-            if (geo.gl) k_halo_pack_h<<<grid, 256, 0, sl->stream>>>(geo, sl->s, 0, sl->hsend[0]);
-            if (geo.gh) k_halo_pack_h<<<grid, 256, 0, sl->stream>>>(geo, sl->s, 1, sl->hsend[1]);
-        }
-        CG_TRY(transfer(g, g->slabs[0]->geo.YZ));
-        int64_t relaxed = 0;
-        for (Slab *sl : g->slabs) {
-            const Geo &geo = sl->geo;
-            const int grid = grid_for(geo.YZ, 256, sl->num_sms * 4);
-            const int w = sl->wave_k;  // the next wave reads list[w&1] / cnt[4 + w%3] (now empty)
-            const int tag = ++sl->tag;
-            for (int side = 0; side < 2; side++) {
-                if (!(side ? geo.gh : geo.gl)) continue;
-                k_halo_unpack_h<<<grid, 256, 0, sl->stream>>>(geo, sl->s, side, sl->hrecv[side], sl->hold[side]);
-                k_lc_ghost<<<grid, 256, 0, sl->stream>>>(geo, sl->s, side, sl->hold[side], sl->blist[w & 1],
-                                                         sl->cnt + 4 + w % 3, sl->vstamp, tag);
-            }
-            CG_CUDA(cudaGetLastError());
-            CG_CUDA(cudaMemcpyAsync(sl->h_cnt + 4, sl->cnt + 4, 3 * sizeof(unsigned), cudaMemcpyDeviceToHost,
-                                    sl->stream));
-        }
-        for (Slab *sl : g->slabs) {
-            CG_CUDA(cudaStreamSynchronize(sl->stream));
-            relaxed += sl->h_cnt[4 + sl->wave_k % 3];
-        }
-        CG_TRY(gsum(g, &relaxed, 1));
-        if (relaxed == 0) break;
-    }
-    return CG_OK;
-}
-
 // a2/a5: global relabel + rebuild of every slab's active list; returns the global active count.
 cg_status global_relabel(cg_graph *g, int64_t *active) {
-    if (!multi(g)) {
+    const RelabelKind kind = relabel_kind(g);
+    const bool colgr = kind != RELABEL_RECORD;  // labels are in sl->lab: the rebuild writes the records' H
+    if (kind == RELABEL_COLGR) {
+        CG_TRY(multi(g) ? colgr_slabs(g) : colgr_strict(g, g->slabs[0]));
+    } else if (kind == RELABEL_FLAGS) {
+        CG_TRY(bfs_strict(g, g->slabs[0], true, true));
+    } else if (!multi(g)) {
         CG_TRY(bfs_strict(g, g->slabs[0]));
     } else {
-        const bool lc = getenv("CG_SLAB_LC") && atoi(getenv("CG_SLAB_LC"));
-        CG_TRY(lc ? bfs_slabs(g) : bfs_slabs_levels(g));
+        CG_TRY(bfs_slabs_levels(g));
     }
     int64_t act = 0;
     for (Slab *sl : g->slabs) {
@@ -691,8 +766,13 @@ cg_status global_relabel(cg_graph *g, int64_t *active) {
                                                                     sl->u64 + 3);
         } else {
             CG_CUDA(cudaMemsetAsync(sl->cnt, 0, 3 * sizeof(unsigned), sl->stream));
-            k_rebuild_vertices<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(
-                geo, sl->s, sl->blist[0], sl->cnt, sl->vstamp, ++sl->tag, sl->u64 + 3);
+            if (colgr)  // records' H = the relabel's labels, fused with the active list
+                k_colgr_rebuild<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(
+                    geo, sl->s, sl->lab, sl->blist[0], sl->cnt, sl->vstamp, ++sl->tag, sl->u64 + 3,
+                    kind == RELABEL_FLAGS ? sl->bst : nullptr);
+            else
+                k_rebuild_vertices<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(
+                    geo, sl->s, sl->blist[0], sl->cnt, sl->vstamp, ++sl->tag, sl->u64 + 3);
         }
         g->st.kernel_launches++;
         sl->sweep_k = 0;
@@ -710,16 +790,46 @@ cg_status global_relabel(cg_graph *g, int64_t *active) {
     return CG_OK;
 }
 
-cg_status run_gap(cg_graph *g, Slab *sl) {
-    const Geo &geo = sl->geo;
-    cudaStream_t st = sl->stream;
-    CG_CUDA(cudaMemsetAsync(sl->hist, 0, sizeof(unsigned) * GAP_BINS, st));
-    CG_CUDA(cudaMemsetAsync(sl->flags + 1, 0, sizeof(int), st));
-    k_gap_hist<<<sl->num_sms * 8, 256, 0, st>>>(geo, sl->s.H, sl->hist, sl->flags + 1);
-    k_gap_find<<<1, 1024, 0, st>>>(sl->hist, sl->flags + 1, sl->flags + 2);
-    k_gap_lift<<<sl->num_sms * 8, 256, 0, st>>>(geo, sl->s.H, sl->flags + 2, sl->u64 + 4);
+// a5 gap heuristic (§2.1) over every slab of the job: the label histogram is
+// summed over all slabs (LOCAL: added into slab 0's on the shared stream; NCCL: an int32
+// allreduce of the histogram up to the global maximum label), so every slab finds the same
+// smallest empty label g and lifts its own vertices above g to INF.  Ghost copies of lifted
+// vertices are refreshed by the next halo exchange; a push into a stale ghost copy only moves
+// excess onto a vertex that then waits at INF for the next exact relabel (a4 stays the safety net).
+cg_status run_gap(cg_graph *g) {
+    for (Slab *sl : g->slabs) {
+        CG_CUDA(cudaMemsetAsync(sl->hist, 0, sizeof(unsigned) * GAP_BINS, sl->stream));
+        CG_CUDA(cudaMemsetAsync(sl->flags + 1, 0, sizeof(int), sl->stream));
+        k_gap_hist<<<sl->num_sms * 8, 256, 0, sl->stream>>>(sl->geo, sl->s.H, sl->hist, sl->flags + 1);
+        g->st.kernel_launches++;
+    }
+    Slab *s0 = g->slabs[0];
+    if (g->local) {  // in-process slabs share one stream: fold every histogram and maximum into slab 0's
+        for (size_t i = 1; i < g->slabs.size(); i++) {
+            Slab *sl = g->slabs[i];
+            k_hist_fold<<<s0->num_sms * 4, 256, 0, s0->stream>>>(sl->hist, sl->flags + 1, s0->hist, s0->flags + 1);
+            g->st.kernel_launches++;
+        }
+    } else if (multi(g)) {  // NCCL ranks: global maximum label, then the histogram up to it
+        CG_CUDA(cudaMemcpyAsync(s0->h_flags + 1, s0->flags + 1, sizeof(int), cudaMemcpyDeviceToHost, s0->stream));
+        CG_CUDA(cudaStreamSynchronize(s0->stream));
+        int64_t mh = s0->h_flags[1];
+        CG_TRY(gmax(g, &mh));
+        const int32_t m32 = (int32_t)mh;
+        CG_CUDA(cudaMemcpyAsync(s0->flags + 1, &m32, sizeof(int), cudaMemcpyHostToDevice, s0->stream));
+        const size_t bins = (size_t)std::min<int64_t>(mh + 1, GAP_BINS);
+        CG_NCCL(nccl().allReduce(s0->hist, s0->hist, bins, ncclInt32, ncclSum, g->comm, s0->stream));
+        CG_CUDA(cudaStreamSynchronize(s0->stream));  // m32 is a host stack value
+    }
+    k_gap_find<<<1, 1024, 0, s0->stream>>>(s0->hist, s0->flags + 1, s0->flags + 2);
+    g->st.kernel_launches++;
+    for (Slab *sl : g->slabs) {
+        if (sl != s0) CG_CUDA(cudaMemcpyAsync(sl->flags + 2, s0->flags + 2, sizeof(int), cudaMemcpyDeviceToDevice,
+                                              s0->stream));
+        k_gap_lift<<<sl->num_sms * 8, 256, 0, sl->stream>>>(sl->geo, sl->s.H, sl->flags + 2, sl->u64 + 4);
+        g->st.kernel_launches++;
+    }
     CG_CUDA(cudaGetLastError());
-    g->st.kernel_launches += 3;
     g->st.gap_runs++;
     return CG_OK;
 }
@@ -872,6 +982,8 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
             fprintf(stderr, "[cg] GR#%lld levels=%lld active=%lld ms=%.3f (sweeps %lld) flow=%lld\n",
                     (long long)g->st.global_relabels, (long long)(g->st.gr_passes - p0), (long long)active, last_gr_ms,
                     (long long)g->st.sweeps, (long long)-sumT);
+            fprintf(stderr, "[cg]   early stop %d (vertices with excess labelled %llu of %llu)\n", s0->h_bst->early,
+                    (unsigned long long)s0->h_bst->act_claimed, (unsigned long long)s0->h_bst->act_total);
             const unsigned *h = s0->h_bst->hist;
             fprintf(stderr, "[cg]   levels by frontier: <=32 %u <=256 %u <=2K %u <=16K %u <=128K %u <=1M %u more %u "
                     "(bottom-up %u)\n", h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
@@ -887,16 +999,9 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
     const double gr_budget = (double)o.gr_factor * (double)g->n_global;
     const double walk_min = getenv("CG_WALK_MIN") ? atof(getenv("CG_WALK_MIN")) : 1e-3;
     const double gr_beta = getenv("CG_GR_BETA") ? atof(getenv("CG_GR_BETA")) : 1.0;
-    // work-fetching walk (k_walk_ws): default since the gathered scan (C4 -11 %);
-    // CG_WALK_WS=0 runs k_walk (which also takes the park / relabel-and-continue / relist knobs)
-    const bool walk_ws = !getenv("CG_WALK_WS") || atoi(getenv("CG_WALK_WS")) != 0;
-    // k_walk's last argument: bit 0 = park stuck walks, bits 8.. = relabel-and-continue budget
-    const int walk_park = (getenv("CG_WALK_PARK") ? atoi(getenv("CG_WALK_PARK")) & 1 : 0) |
-                          (getenv("CG_WALK_RCONT") ? atoi(getenv("CG_WALK_RCONT")) << 8 : 0);
-    const bool relist_ordered = getenv("CG_RELIST") && atoi(getenv("CG_RELIST")) != 0;
     double work_since_gr = 0.0, sweep_ms_since_gr = 0.0;
     int64_t sweeps = g->st.sweeps, since_gap = 0, last_active = active;
-    std::vector<int64_t> wv(RING + 2);  // batch <= RING counters + the overflow flag + the time trigger
+    std::vector<int64_t> wv(RING + 3);  // batch <= RING op counters, the overflow flag, the time trigger, relabels
     // Profiling aid (vertex loop): CG_GR_LOG=file appends the sweep counts at which this solve's
     // triggers fired; CG_GR_SCHEDULE="s1,s2,..." replays such a schedule instead of the work /
     // time triggers, so a run under ncu (whose replay-slowed kernels distort the time trigger)
@@ -919,16 +1024,16 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
         const int batch = (int)std::min<int64_t>(o.check_every, o.max_sweeps - sweeps);
         Slab *sl = s0;
         const TileKernel tk = tile_kernel(sl->tS);
-        CG_CUDA(cudaMemsetAsync(sl->work, 0, sizeof(unsigned long long) * batch, st0));
+        CG_CUDA(cudaMemsetAsync(sl->work, 0, sizeof(unsigned long long) * 2 * batch, st0));
         CG_CUDA(cudaEventRecord(g->ev0, st0));
         for (int i = 0; i < batch; i++) {
             tk<<<sl->tgrid, sl->tg.NC * 32, sl->tsmem, st0>>>(sl->geo, sl->tg, sl->s, sl->tl, sl->tphase++,
-                                                               sl->work + i, sl->visits + i, sl->flags);
+                                                               sl->work + 2 * i, sl->visits + i, sl->flags);
             g->st.kernel_launches++;
         }
         CG_CUDA(cudaEventRecord(g->ev1, st0));
         CG_CUDA(cudaGetLastError());
-        CG_CUDA(cudaMemcpyAsync(sl->h_work, sl->work, sizeof(unsigned long long) * batch, cudaMemcpyDeviceToHost, st0));
+        CG_CUDA(cudaMemcpyAsync(sl->h_work, sl->work, sizeof(unsigned long long) * 2 * batch, cudaMemcpyDeviceToHost, st0));
         CG_CUDA(cudaMemcpyAsync(sl->h_visits, sl->visits, sizeof(unsigned long long) * batch, cudaMemcpyDeviceToHost,
                                 st0));
         CG_CUDA(cudaMemcpyAsync(sl->h_cnt, sl->tl.cnt, 4 * sizeof(unsigned), cudaMemcpyDeviceToHost, st0));
@@ -944,7 +1049,7 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
         const double visit_bytes = (64.0 * sl->tg.NC + 8.0 * sl->tg.NH) * (double)sl->geo.Z;
         int64_t wsum = 0;
         for (int i = 0; i < batch; i++) {
-            wsum += (int64_t)sl->h_work[i];
+            wsum += (int64_t)sl->h_work[2 * i];
             g->st.sweep_bytes_alg += visit_bytes * (double)sl->h_visits[i];
             g->st.tile_visits += (int64_t)sl->h_visits[i];
         }
@@ -979,8 +1084,8 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
         // multi-hop walks while many vertices are active; single hops in the sparse tail
         const bool walk = o.walk_len > 0 && (double)last_active >= walk_min * (double)g->n_global;
         for (Slab *sl : g->slabs) {
-            CG_CUDA(cudaMemsetAsync(sl->work, 0, sizeof(unsigned long long) * batch, sl->stream));
-            if (walk && walk_ws) CG_CUDA(cudaMemsetAsync(sl->heads, 0, sizeof(unsigned) * batch, sl->stream));
+            CG_CUDA(cudaMemsetAsync(sl->work, 0, sizeof(unsigned long long) * 2 * batch, sl->stream));
+            if (walk) CG_CUDA(cudaMemsetAsync(sl->heads, 0, sizeof(unsigned) * batch, sl->stream));
         }
         CG_CUDA(cudaEventRecord(g->ev0, st0));
         for (int i = 0; i < batch; i++) {
@@ -992,32 +1097,16 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
                 const int k = sl->sweep_k++;
                 sl->out_tag = ++sl->tag;
                 const bool soft = geo.soft_k > 0;
-                if (walk && walk_ws)
-                    (soft ? k_walk_ws<true> : k_walk_ws<false>)<<<gv, 256, 0, sl->stream>>>(geo, sl->s, o.walk_len, sl->blist[k & 1], sl->cnt + k % 3,
-                                                          sl->blist[(k + 1) & 1], sl->cnt + (k + 1) % 3,
-                                                          sl->cnt + (k + 2) % 3, sl->vstamp, sl->out_tag, sl->work + i,
-                                                          sl->flags, sl->heads + i);
-                else if (walk && relist_ordered && !multi(g)) {
-                    (soft ? k_walk<true> : k_walk<false>)<<<gv, 256, 0, sl->stream>>>(
+                if (walk)  // multi-hop work-fetching walks
+                    (soft ? k_walk_ws<true> : k_walk_ws<false>)<<<gv, 256, 0, sl->stream>>>(
                         geo, sl->s, o.walk_len, sl->blist[k & 1], sl->cnt + k % 3, sl->blist[(k + 1) & 1],
-                        sl->cnt + (k + 1) % 3, sl->cnt + (k + 2) % 3, sl->vstamp, sl->out_tag, sl->work + i,
-                        sl->flags, walk_park);
-                    // rewrite the output list in index order (same set, same count)
-                    CG_CUDA(cudaMemsetAsync(sl->cnt + (k + 1) % 3, 0, sizeof(unsigned), sl->stream));
-                    k_relist_ordered<<<sl->num_sms * 8, 256, 0, sl->stream>>>(geo, sl->vstamp, sl->out_tag,
-                                                                               sl->blist[(k + 1) & 1],
-                                                                               sl->cnt + (k + 1) % 3);
-                    g->st.kernel_launches++;
-                } else if (walk)
-                    (soft ? k_walk<true> : k_walk<false>)<<<gv, 256, 0, sl->stream>>>(geo, sl->s, o.walk_len, sl->blist[k & 1], sl->cnt + k % 3,
-                                                       sl->blist[(k + 1) & 1], sl->cnt + (k + 1) % 3,
-                                                       sl->cnt + (k + 2) % 3, sl->vstamp, sl->out_tag, sl->work + i,
-                                                       sl->flags, walk_park);
+                        sl->cnt + (k + 1) % 3, sl->cnt + (k + 2) % 3, sl->vstamp, sl->out_tag, sl->work + 2 * i,
+                        sl->flags, sl->heads + i);
                 else
                     (soft ? k_sweep_v<true> : k_sweep_v<false>)<<<gv, 256, 0, sl->stream>>>(geo, sl->s, o.ops_per_sweep, sl->blist[k & 1],
                                                           sl->cnt + k % 3, sl->blist[(k + 1) & 1],
                                                           sl->cnt + (k + 1) % 3, sl->cnt + (k + 2) % 3, sl->vstamp,
-                                                          sl->out_tag, sl->work + i, sl->flags);
+                                                          sl->out_tag, sl->work + 2 * i, sl->flags);
                 g->st.kernel_launches++;
             }
             if (multi(g)) CG_TRY(halo_sweep(g));
@@ -1025,16 +1114,19 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
         CG_CUDA(cudaEventRecord(g->ev1, st0));
         CG_CUDA(cudaGetLastError());
         for (Slab *sl : g->slabs) {
-            CG_CUDA(cudaMemcpyAsync(sl->h_work, sl->work, sizeof(unsigned long long) * batch, cudaMemcpyDeviceToHost,
+            CG_CUDA(cudaMemcpyAsync(sl->h_work, sl->work, sizeof(unsigned long long) * 2 * batch, cudaMemcpyDeviceToHost,
                                     sl->stream));
             CG_CUDA(cudaMemcpyAsync(sl->h_flags, sl->flags, sizeof(int), cudaMemcpyDeviceToHost, sl->stream));
         }
         int64_t overflow = 0;
-        std::fill(wv.begin(), wv.begin() + batch, 0);
+        std::fill(wv.begin(), wv.begin() + batch + 3, 0);
         for (Slab *sl : g->slabs) {
             CG_CUDA(cudaStreamSynchronize(sl->stream));
             overflow |= sl->h_flags[0] & FLAG_OVERFLOW;
-            for (int i = 0; i < batch; i++) wv[i] += (int64_t)sl->h_work[i];
+            for (int i = 0; i < batch; i++) {
+                wv[i] += (int64_t)sl->h_work[2 * i];
+                wv[batch + 2] += (int64_t)sl->h_work[2 * i + 1];
+            }
         }
         float ms = 0.f;
         cudaEventElapsedTime(&ms, g->ev0, g->ev1);
@@ -1044,7 +1136,7 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
         // the time-based relabel trigger is a local measurement: ranks agree on it through the
         // same allreduce as the sweep counters (one collective per batch)
         wv[batch + 1] = sweep_ms_since_gr >= gr_beta * std::max(last_gr_ms, 0.05);
-        CG_TRY(gsum(g, wv.data(), batch + 2));
+        CG_TRY(gsum(g, wv.data(), batch + 3));
         if (wv[batch]) { result = CG_E_OVERFLOW; break; }
         if (trace) {
             fprintf(stderr, "[cg] sweeps %lld..%lld ops:", (long long)sweeps, (long long)(sweeps + batch - 1));
@@ -1053,12 +1145,18 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
         }
         bool quiescent = false;
         last_active = wv[batch - 1];
+        // algorithmic bytes: 32 B per vertex visit (its state read once), +12 B per
+        // push (own E, target E, residual), +4 B per relabel (H)
+        const int64_t rel = wv[batch + 2];
+        int64_t ops = 0;
         for (int i = 0; i < batch; i++) {
-            g->st.sweep_bytes_alg += 44.0 * (double)wv[i];  // 32 B state read + 12 B push writes
             if (wv[i] == 0) { quiescent = true; break; }
+            ops += wv[i];
             work_since_gr += (double)wv[i];
             g->st.work += wv[i];
         }
+        g->st.relabel_ops += rel;
+        g->st.sweep_bytes_alg += 32.0 * (double)ops + 12.0 * (double)(ops - rel) + 4.0 * (double)rel;
         sweeps += batch;
         since_gap += batch;
         g->st.sweeps = sweeps;
@@ -1073,8 +1171,8 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
             work_since_gr = 0.0;
             sweep_ms_since_gr = 0.0;
             since_gap = 0;
-        } else if (o.gap_every > 0 && since_gap >= o.gap_every && !multi(g)) {
-            CG_TRY(run_gap(g, s0));
+        } else if (o.gap_every > 0 && since_gap >= o.gap_every) {
+            CG_TRY(run_gap(g));
             since_gap = 0;
         }
     }
@@ -1210,8 +1308,13 @@ static cg_status build_common(const cg_dims *dims, const int32_t *cost_dev, int3
             int per_sm = 0, coop = 0;
             cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dd.device);
             if (coop && !getenv("CG_BFS_LEVEL_LAUNCHES") &&
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bfs_run, 512, 0) == cudaSuccess && per_sm > 0)
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bfs_run<true>, 512, 0) == cudaSuccess && per_sm > 0)
                 sl->bfs_coop_grid = num_sms * std::min(per_sm, CG_BFS_RUN_MINB);
+            const void *kc = colgr_kernel(dims->Z);
+            per_sm = 0;
+            if (coop && kc && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kc, 512, 0) == cudaSuccess &&
+                per_sm > 0)
+                sl->colgr_grid = num_sms * std::min(per_sm, 2);
         }
         sl->x0 = x0;
         sl->x1 = x1;
@@ -1270,18 +1373,6 @@ static cg_status maxflow_solve_impl(cg_graph *g, const cg_solve_opts *opts, int6
     const bool trace = tracing();
     const double t0 = now_ms();
     Slab *s0 = g->slabs[0];
-    // a1': optional exact per-column pre-cancellation (valid initial preflow)
-    const size_t pc_smem = (size_t)8 * (g->dims.Z + 1) * sizeof(long long);
-    if (getenv("CG_PRECANCEL") && pc_smem <= 200 * 1024) {  // opt-in: measured slower on C4/C5
-        if (pc_smem > 48 * 1024)
-            CG_CUDA(cudaFuncSetAttribute(k_precancel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pc_smem));
-        for (Slab *sl : g->slabs) {
-            k_precancel<<<grid_for((int64_t)sl->geo.X * sl->geo.Y * 32, 256, sl->num_sms * 16), 256, pc_smem,
-                          sl->stream>>>(sl->geo, sl->s, sl->flags);
-            g->st.kernel_launches++;
-        }
-        CG_CUDA(cudaGetLastError());
-    }
     double ms_gr = 0.0;
     const cg_status result = pr_loop(g, o, use_tiles, ms_gr);
     if (result != CG_OK && result != CG_E_NOT_CONVERGED) return result;

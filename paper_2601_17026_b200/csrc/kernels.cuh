@@ -1,10 +1,10 @@
 // kernels.cuh -- the sm_100a kernels of the column-graph max-flow hot path.
 //
 //   a1  build             k_build                      PAPER.md §1.2; §2.1 L134 (init)
-//   a1' pre-cancellation  k_precancel (opt-in)         not in the paper
-//   a2/a5 global relabel  k_bfs_init + k_bfs_step      PAPER.md §2.1; Alg. 3; §3.2.2
-//                         k_lc_wave/k_lc_ghost (slabs) label-correcting variant across x-slabs
-//   a3  sweep             k_walk (multi-hop), k_sweep_v PAPER.md §2.1; Alg. 2
+//   a2/a5 global relabel  column fixpoint: relabel.cuh; vertex-frontier BFS (soft graphs, Z > 256,
+//                         CG_RELABEL=bfs): k_bfs_init + k_bfs_run / k_bfs_step, x-slab levels
+//                         k_slab_level   PAPER.md §2.1; Alg. 3; §3.2.2
+//   a3  sweep             k_walk_ws (multi-hop), k_sweep_v PAPER.md §2.1; Alg. 2
 //   a4  termination       k_rebuild_vertices + host    PAPER.md §3.2.4; Alg. 1
 //   a5  gap               k_gap_*                      PAPER.md §2.1
 //   a6  flow value        k_sum_T                      PAPER.md Eq. 5
@@ -550,14 +550,16 @@ __device__ __forceinline__ void set_ctx(const Geo &g, OpCtx &c, int64_t v) {
 // single-decrementer rule.
 template <bool SOFT>
 __device__ __forceinline__ int64_t pr_op(const Geo &g, const Soa &s, const OpCtx &c, int &e, int &h, int &sent,
-                                         int *flags) {
+                                         int *flags, unsigned long long &nrel) {
     const ArcPick p = scan_arcs<SOFT>(g, s, c, h);
     if (p.best >= g.INF) {  // no residual path known: dead until the next global relabel
         h = g.INF;
         s.H[c.v] = h;
+        nrel++;
         return NONE;
     }
     if (h <= p.best) {  // relabel
+        nrel++;
         h = p.best + 1;
         s.H[c.v] = h;
         if (h >= g.INF) return NONE;
@@ -614,13 +616,23 @@ __device__ __forceinline__ void mark_vertex(const Geo &g, int64_t id, int *vstam
     warp_append(add, (int)id, list, count);
 }
 
+// per-sweep counters: work[0] += push/relabel operations (vertex visits), work[1] += relabels
+__device__ __forceinline__ void flush_work(unsigned long long *work, unsigned long long ops, unsigned long long rel) {
+    ops = warp_sum_ll((long long)ops);
+    rel = warp_sum_ll((long long)rel);
+    if (lane_id() == 0) {
+        if (ops) atomicAdd(work, ops);
+        if (rel) atomicAdd(work + 1, rel);
+    }
+}
+
 template <bool SOFT>
 __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_sweep_v(Geo g, Soa s, int ops, const int *__restrict__ lin,
                                                  const unsigned *cin, int *lout, unsigned *cout, unsigned *czero,
                                                  int *vstamp, int tag, unsigned long long *work, int *flags) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *czero = 0;
     const int64_t count = *cin;
-    unsigned long long mywork = 0;
+    unsigned long long mywork = 0, myrel = 0;
     for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {
         const int64_t i = base + lane_id();
         OpCtx c;
@@ -638,7 +650,7 @@ __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_sweep_v(Geo g, Soa s, in
             int64_t tgt = NONE;
             if (act) {
                 mywork++;
-                tgt = pr_op<SOFT>(g, s, c, e, h, sent, flags);
+                tgt = pr_op<SOFT>(g, s, c, e, h, sent, flags, myrel);
                 act = e > 0 && h < g.INF;
             }
             mark_vertex(g, tgt, vstamp, tag, lout, cout);
@@ -647,8 +659,7 @@ __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_sweep_v(Geo g, Soa s, in
         if (sent) atomicSub(&s.E[c.v], sent);
         mark_vertex(g, act ? c.v : NONE, vstamp, tag, lout, cout);
     }
-    mywork = warp_sum_ll((long long)mywork);
-    if (lane_id() == 0 && mywork) atomicAdd(work, mywork);
+    flush_work(work, mywork, myrel);
 }
 
 // ------------------------------------------------------------------ a3': multi-hop sweep ("walk")
@@ -711,89 +722,10 @@ __device__ __forceinline__ void deposit(const Geo &g, const Soa &s, int64_t x, i
     }
 }
 
-template <bool SOFT>
-__global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_walk(Geo g, Soa s, int K, const int *__restrict__ lin, const unsigned *cin,
-                                              int *lout, unsigned *cout, unsigned *czero, int *vstamp, int tag,
-                                              unsigned long long *work, int *flags, int park) {
-    __shared__ BlockQueue q;
-    __shared__ unsigned qbase;
-    if (threadIdx.x == 0) q.n = 0;
-    if (blockIdx.x == 0 && threadIdx.x == 0) *czero = 0;
-    __syncthreads();
-    const int64_t count = *cin;
-    unsigned long long mywork = 0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t v = lin[i];
-        int c = s.E[v];
-        int hx = s.H[v];
-        if (!(c > 0 && hx < g.INF)) continue;
-        atomicSub(&s.E[v], c);  // the owner takes its whole excess
-        OpCtx ctx;
-        set_ctx(g, ctx, v);
-        int rcont = park >> 8;  // relabels after which this walk may go on (CG_WALK_RCONT)
-        for (int step = 0; c > 0; ++step) {
-            const ArcPick p = scan_arcs<SOFT>(g, s, ctx, hx);
-            mywork++;  // one push or relabel operation per hop
-            bool go_on = false;
-            if (p.best >= hx && rcont > 0 && step < K && p.best < g.INF) {
-                // relabel to min + 1 and push through the minimum arc the scan just found,
-                // unless a concurrent relabel of this vertex went higher
-                const int nh = p.best + 1;
-                if (atomicMax(&s.H[ctx.v], nh) <= nh) {
-                    rcont--;
-                    go_on = true;
-                }
-            }
-            if (!go_on && (p.best >= hx || step >= K)) {  // stuck (or hop budget spent): deposit the carry here
-                if (p.best >= hx) {
-                    atomicMax(&s.H[ctx.v], p.best >= g.INF ? g.INF : p.best + 1);
-                    if (park & 1) {  // parked until the next global relabel (not re-listed)
-                        const int old = atomicAdd(&s.E[ctx.v], c);
-                        if (old > INT_MAX - c) atomicOr(flags, FLAG_OVERFLOW);
-                        break;
-                    }
-                }
-                deposit(g, s, ctx.v, c, vstamp, tag, q, lout, cout, flags);
-                break;
-            }
-            int df;
-            switch (p.arc) {
-                case 0: df = reserve(&s.T[ctx.v], c); break;
-                case 1: df = c; atomicAdd(&s.D[ctx.v], df); break;
-                case 2: case 3: case 4: case 5: df = c; atomicAdd(&s.L[p.arc - 2][ctx.v], df); break;
-                case 6: df = reserve(&s.D[ctx.v + 1], c); break;
-                case 7: case 8: case 9: case 10: df = reserve(&s.L[(p.arc - 7) ^ 1][p.tgt], c); break;
-                default: df = SOFT ? walk_push_soft(g, s, ctx, p, c) : 0; break;
-            }
-            if (df == 0) continue;  // lost a reservation race: rescan this vertex
-            if (p.arc == 0) {       // absorbed by t
-                c -= df;
-                continue;
-            }
-            if (df < c) deposit(g, s, ctx.v, c - df, vstamp, tag, q, lout, cout, flags);
-            c = df;
-            if (!owned(g, p.tgt)) {  // crossed into a neighbour slab: hand the carry over
-                deposit(g, s, p.tgt, c, vstamp, tag, q, lout, cout, flags);
-                break;
-            }
-            hx = p.best;
-            set_ctx(g, ctx, p.tgt);
-        }
-    }
-    __syncthreads();
-    const unsigned nq = min(q.n, (unsigned)BlockQueue::CAP);
-    if (threadIdx.x == 0 && nq) qbase = atomicAdd(cout, nq);
-    __syncthreads();
-    for (unsigned j = threadIdx.x; j < nq; j += blockDim.x) lout[qbase + j] = q.buf[j];
-    mywork = warp_sum_ll((long long)mywork);
-    if (lane_id() == 0 && mywork) atomicAdd(work, mywork);
-}
-
-// Work-fetching variant of k_walk: a lane whose walk has ended takes the next worklist item
-// itself (warp-aggregated atomicAdd on *head), so every iteration of the loop advances 32
-// independent walks by one hop.  In k_walk a warp lasts as long as its longest walk (up to
-// K dependent hops) while the lanes whose walks ended idle.  Same hop semantics as k_walk.
+// Work-fetching walk: a lane whose walk has ended takes the next worklist item itself
+// (warp-aggregated atomicAdd on *head), so every iteration of the loop advances 32 independent
+// walks by one hop (a warp-per-item walk lasts as long as its longest walk while the lanes whose
+// walks ended idle: measured -25 % sweep time per batch).
 template <bool SOFT>
 __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_walk_ws(Geo g, Soa s, int K, const int *__restrict__ lin,
                                                      const unsigned *cin, int *lout, unsigned *cout, unsigned *czero,
@@ -805,7 +737,7 @@ __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_walk_ws(Geo g, Soa s, in
     if (blockIdx.x == 0 && threadIdx.x == 0) *czero = 0;
     __syncthreads();
     const unsigned count = *cin;
-    unsigned long long mywork = 0;
+    unsigned long long mywork = 0, myrel = 0;
     bool exhausted = false, walking = false;
     int c = 0, hx = 0, step = 0;
     OpCtx ctx;
@@ -841,7 +773,10 @@ __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_walk_ws(Geo g, Soa s, in
         const ArcPick p = scan_arcs<SOFT>(g, s, ctx, hx);
         mywork++;
         if (p.best >= hx || step >= K) {  // stuck (or hop budget spent): deposit the carry here
-            if (p.best >= hx) atomicMax(&s.H[ctx.v], p.best >= g.INF ? g.INF : p.best + 1);
+            if (p.best >= hx) {
+                myrel++;
+                atomicMax(&s.H[ctx.v], p.best >= g.INF ? g.INF : p.best + 1);
+            }
             deposit(g, s, ctx.v, c, vstamp, tag, q, lout, cout, flags);
             walking = false;
             continue;
@@ -877,26 +812,7 @@ __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_walk_ws(Geo g, Soa s, in
     if (threadIdx.x == 0 && nq) qbase = atomicAdd(cout, nq);
     __syncthreads();
     for (unsigned j = threadIdx.x; j < nq; j += blockDim.x) lout[qbase + j] = q.buf[j];
-    mywork = warp_sum_ll((long long)mywork);
-    if (lane_id() == 0 && mywork) atomicAdd(work, mywork);
-}
-
-// Re-list a sweep's output worklist in index order: the vertices listed for the next sweep
-// are exactly those with vstamp == tag, so a dense scan of vstamp rewrites the list with
-// 256-vertex spans in index order (walk deposits append in completion order; index order
-// makes a warp's walks start on neighbouring records).  *count receives the same count.
-__global__ void k_relist_ordered(Geo g, const int *__restrict__ vstamp, int tag, int *list, unsigned *count) {
-    constexpr int SPAN = 8;
-    SpanAppender<SPAN> ap;
-    for (int64_t base = gwarp() * 32 * SPAN; base < g.n; base += nwarps() * 32 * SPAN) {
-#pragma unroll
-        for (int j = 0; j < SPAN; j++) {
-            const int64_t b0 = base + 32 * j;
-            const int64_t v = b0 + lane_id();
-            ap.add(__ballot_sync(FULL, v < g.n && vstamp[v] == tag), b0);
-        }
-        ap.flush(list, count);
-    }
+    flush_work(work, mywork, myrel);
 }
 
 // After a global relabel: list every active vertex (E > 0, H < INF) in index order.
@@ -955,19 +871,17 @@ __global__ void k_bfs_init(Geo g, Soa s, int *lout, unsigned *cout, unsigned *vi
 }
 
 // Expand one frontier vertex per lane (v < 0: none) and append the new frontier with one
-// atomic per warp.  STRICT (single slab): claim unlabelled predecessors with
-// atomicCAS(H, INF, L+1) -- each vertex exactly once.  Otherwise label-correcting (x-slabs):
-// relax predecessors with atomicMin(H, H(v)+1) and list the improved ones once per wave.
+// atomic per warp: claim unlabelled predecessors with atomicCAS(H, INF, L+1) -- each vertex
+// exactly once.
 // Soft-arc predecessors of v (NEXT-1): w = (nbr_d, z+k) whose forward arc (d^1, k) into v has
 // residual, and w = (nbr_d, z-k) through the reverse of v's forward arc (d, k) when it carries
 // flow.  WARP-COLLECTIVE: every lane of the warp calls it (v < 0: no vertex); the loop over
 // (d, k) is warp-uniform and claims are appended with one atomic per warp (warp_append).
-// MODE 0: claim through the visited bitmap (k_bfs_run); 1: CAS on INF labels (k_bfs_step);
-// 2: label-correcting relaxation with atomicMin, listed once per wave through vstamp == tag
-// (x-slab relabel, nl per lane).
+// MODE 0: claim through the visited bitmap (k_bfs_run); 1: CAS on INF labels (k_bfs_step,
+// x-slab levels).
 template <int MODE>
 __device__ __noinline__ void bfs_soft_preds(const Geo &g, const Soa &s, int64_t v, int nl, int *lout, unsigned *cout,
-                                            unsigned *visited, int *vstamp = nullptr, int tag = 0) {
+                                            unsigned *visited) {
     const bool has = v >= 0 && nl < g.INF;  // lists hold owned vertices only; -1 = no vertex
     const int64_t col = has ? v / g.Z : 0;
     const int z = has ? (int)(v - col * g.Z) : 0;
@@ -980,8 +894,7 @@ __device__ __noinline__ void bfs_soft_preds(const Geo &g, const Soa &s, int64_t 
             s.H[w] = nl;
             return true;
         }
-        if (MODE == 1) return __ldcg(&s.H[w]) >= g.INF && atomicCAS(&s.H[w], g.INF, nl) == g.INF;
-        return s.H[w] > nl && atomicMin(&s.H[w], nl) > nl && vstamp[w] != tag && atomicExch(&vstamp[w], tag) != tag;
+        return __ldcg(&s.H[w]) >= g.INF && atomicCAS(&s.H[w], g.INF, nl) == g.INF;
     };
     for (int d = 0; d < 4; d++) {
         const int64_t o = has ? nbr_off(g, x, y, d) : 0;
@@ -1004,79 +917,49 @@ __device__ __noinline__ void bfs_soft_preds(const Geo &g, const Soa &s, int64_t 
     }
 }
 
-template <bool STRICT>
 __device__ __forceinline__ void bfs_expand_warp(const Geo &g, const Soa &s, int nl, int64_t v, int *lout,
-                                                unsigned *cout, int *vstamp, int tag) {
+                                                unsigned *cout) {
     const int INF = g.INF;
     int u[10];
     unsigned got = 0;
-    if (v >= 0) {
-        if (!STRICT) nl = s.H[v] + 1;
+    if (v >= 0 && nl < INF) {
         const int64_t col = v / g.Z;
         const int z = (int)(v - col * g.Z);
         const int x = (int)(col / g.Y), y = (int)(col - (int64_t)x * g.Y);
         const int64_t v0 = col * g.Z;
         const int zox = zo_of(z, g.delta), zix = zi_of(z, g.delta, g.Z);
         const int zoy = zo_of(z, g.delta_y), ziy = zi_of(z, g.delta_y, g.Z);
-        auto claim = [&](int slot, int64_t w) {
-            if (!owned(g, w)) return;  // ghost labels come from their owner
-            if (STRICT) {
-                if (__ldcg(&s.H[w]) >= INF && atomicCAS(&s.H[w], INF, nl) == INF) {
-                    u[slot] = (int)w;
-                    got |= 1u << slot;
-                }
-            } else {
-                if (s.H[w] > nl && atomicMin(&s.H[w], nl) > nl && vstamp[w] != tag &&
-                    atomicExch(&vstamp[w], tag) != tag) {
-                    u[slot] = (int)w;
-                    got |= 1u << slot;
-                }
-            }
-        };
-        if (STRICT && nl < INF) {
-            // all candidate predecessors and their labels first (independent loads in flight
-            // together), then CAS only the unlabelled ones: one latency chain per vertex
-            int w[10];  // vertex indices fit int32 (validate_dims: n + ghosts < 2^31)
-            unsigned cand = 0;
-            if (z + 1 < g.Z) { w[0] = (int)(v + 1); cand |= 1u; }
-            if (z >= 1 && s.D[v] > 0) { w[1] = (int)(v - 1); cand |= 2u; }
+        // all candidate predecessors and their labels first (independent loads in flight
+        // together), then CAS only the unlabelled ones: one latency chain per vertex
+        int w[10];  // vertex indices fit int32 (validate_dims: n + ghosts < 2^31)
+        unsigned cand = 0;
+        if (z + 1 < g.Z) { w[0] = (int)(v + 1); cand |= 1u; }
+        if (z >= 1 && s.D[v] > 0) { w[1] = (int)(v - 1); cand |= 2u; }
 #pragma unroll
-            for (int d = 0; d < 4; d++) {
-                const int64_t o = nbr_off(g, x, y, d);
-                if (!o) continue;
-                const int zi = d < 2 ? zix : ziy, zo = d < 2 ? zox : zoy;
-                if (zi >= 0) { w[2 + d] = (int)(v0 + o + zi); cand |= 1u << (2 + d); }
-                if (zo >= 0 && s.L[d][v] > 0) {
-                    w[6 + d] = (int)(v0 + o + zo);
-                    cand |= 1u << (6 + d);
-                }
-            }
-            int hw[10];
-#pragma unroll
-            for (int j = 0; j < 10; j++) hw[j] = (cand >> j & 1u) ? __ldcg(&s.H[w[j]]) : 0;
-#pragma unroll
-            for (int j = 0; j < 10; j++)
-                if ((cand >> j & 1u) && hw[j] >= INF && atomicCAS(&s.H[w[j]], INF, nl) == INF && owned(g, w[j])) {
-                    // a claimed ghost vertex is not expanded here: its label reaches the owner
-                    // through the ghost plane (k_slab_ghost_claim) and the owner expands it
-                    u[j] = w[j];
-                    got |= 1u << j;
-                }
-        } else if (nl < INF) {
-            if (z + 1 < g.Z) claim(0, v + 1);
-            if (z >= 1 && s.D[v] > 0) claim(1, v - 1);
-#pragma unroll
-            for (int d = 0; d < 4; d++) {
-                const int64_t o = nbr_off(g, x, y, d);
-                if (!o) continue;
-                const int zi = d < 2 ? zix : ziy, zo = d < 2 ? zox : zoy;
-                if (zi >= 0) claim(2 + d, v0 + o + zi);
-                if (zo >= 0 && s.L[d][v] > 0) claim(6 + d, v0 + o + zo);
+        for (int d = 0; d < 4; d++) {
+            const int64_t o = nbr_off(g, x, y, d);
+            if (!o) continue;
+            const int zi = d < 2 ? zix : ziy, zo = d < 2 ? zox : zoy;
+            if (zi >= 0) { w[2 + d] = (int)(v0 + o + zi); cand |= 1u << (2 + d); }
+            if (zo >= 0 && s.L[d][v] > 0) {
+                w[6 + d] = (int)(v0 + o + zo);
+                cand |= 1u << (6 + d);
             }
         }
+        int hw[10];
+#pragma unroll
+        for (int j = 0; j < 10; j++) hw[j] = (cand >> j & 1u) ? __ldcg(&s.H[w[j]]) : 0;
+#pragma unroll
+        for (int j = 0; j < 10; j++)
+            if ((cand >> j & 1u) && hw[j] >= INF && atomicCAS(&s.H[w[j]], INF, nl) == INF && owned(g, w[j])) {
+                // a claimed ghost vertex is not expanded here: its label reaches the owner
+                // through the ghost plane (k_slab_ghost_claim) and the owner expands it
+                u[j] = w[j];
+                got |= 1u << j;
+            }
     }
     if (g.soft_k)  // warp-uniform: every lane calls it
-        bfs_soft_preds < STRICT ? 1 : 2 > (g, s, v, v >= 0 ? nl : INF, lout, cout, nullptr, vstamp, tag);
+        bfs_soft_preds<1>(g, s, v, v >= 0 ? nl : INF, lout, cout, nullptr);
     const int k = __popc(got);
     const int incl = warp_incl_scan(k);
     const int total = __shfl_sync(FULL, incl, 31);
@@ -1106,9 +989,15 @@ __device__ __forceinline__ void load_DL(const Soa &s, int v, int &D, int (&L)[4]
 #endif
 }
 
-template <int R>
+// FL (flag-plane BFS, hard graphs): a frontier vertex's in-arc residuals come from its flag byte
+// (bit 1: D(v) > 0, bits 2+d: L_d(v) > 0; relabel.cuh k_bfs2_init) instead of its 32-B record, and
+// claimed labels go to the label plane `lab` (the records' H is written once by the rebuild): the
+// flag plane (1 B / vertex) and the visited bitmap stay L2-resident, so a level touches DRAM only
+// for the label stores and the frontier lists.
+template <int R, bool FL = false>
 __device__ __forceinline__ void bfs_expand_multi(const Geo &g, const Soa &s, int nl, const int (&vv)[R], int *lout,
-                                                 unsigned *cout, unsigned *visited) {
+                                                 unsigned *cout, unsigned *visited, const uint8_t *flags = nullptr,
+                                                 int32_t *lab = nullptr, unsigned long long *act_claimed = nullptr) {
     const int INF = g.INF;
     int w[R][10], hw[R][10];
     unsigned cand[R], got[R];
@@ -1125,7 +1014,14 @@ __device__ __forceinline__ void bfs_expand_multi(const Geo &g, const Soa &s, int
         const int zox = zo_of(z, g.delta), zix = zi_of(z, g.delta, g.Z);
         const int zoy = zo_of(z, g.delta_y), ziy = zi_of(z, g.delta_y, g.Z);
         int D, L[4];
-        load_DL(s, v, D, L);
+        if (FL) {
+            const unsigned f = __ldg(&flags[v]);
+            D = f & 2;
+#pragma unroll
+            for (int d = 0; d < 4; d++) L[d] = f & (4u << d);
+        } else {
+            load_DL(s, v, D, L);
+        }
         if (z + 1 < g.Z) { w[r][0] = v + 1; cand[r] |= 1u; }
         if (z >= 1 && D > 0) { w[r][1] = v - 1; cand[r] |= 2u; }
 #pragma unroll
@@ -1143,7 +1039,7 @@ __device__ __forceinline__ void bfs_expand_multi(const Geo &g, const Soa &s, int
 #pragma unroll
         for (int j = 0; j < 10; j++)
             hw[r][j] = (cand[r] >> j & 1u) ? (int)((__ldcg(&visited[w[r][j] >> 5]) >> (w[r][j] & 31)) & 1u) : 1;
-    if (g.soft_k && nl < INF)  // warp-uniform: every lane calls it
+    if (!FL && g.soft_k && nl < INF)  // warp-uniform: every lane calls it
         for (int r = 0; r < R; r++) bfs_soft_preds<0>(g, s, vv[r], nl, lout, cout, visited);
     int k = 0;
 #pragma unroll
@@ -1153,11 +1049,22 @@ __device__ __forceinline__ void bfs_expand_multi(const Geo &g, const Soa &s, int
             if (!hw[r][j]) {
                 const unsigned bit = 1u << (w[r][j] & 31);
                 if (!(atomicOr(&visited[w[r][j] >> 5], bit) & bit)) {  // claimed: this lane owns w's label
-                    s.H[w[r][j]] = nl;
+                    if (FL) lab[w[r][j]] = nl;
+                    else s.H[w[r][j]] = nl;
                     got[r] |= 1u << j;
                     k++;
                 }
             }
+    if (FL) {  // claimed vertices holding excess (flag bit 6)
+        int na = 0;
+#pragma unroll
+        for (int r = 0; r < R; r++)
+#pragma unroll
+            for (int j = 0; j < 10; j++)
+                if (got[r] >> j & 1u) na += (__ldg(&flags[w[r][j]]) >> 6) & 1;
+        na = warp_sum_i(na);
+        if (lane_id() == 0 && na) atomicAdd(act_claimed, (unsigned long long)na);
+    }
     const int incl = warp_incl_scan(k);
     const int total = __shfl_sync(FULL, incl, 31);
     if (total == 0) return;
@@ -1189,68 +1096,18 @@ struct BfsState {
     unsigned bar[2];       // grid barrier of k_bfs_run (arrivals, generation)
     unsigned hist[8];      // levels by frontier size: <=32, <=256, <=2048, <=16K, <=128K, <=1M, more; [7] bottom-up
     unsigned long long cyc[8];  // block-0 clock cycles spent in levels of each bucket ([7]: bottom-up levels)
-    int bu_alpha, bu_beta;      // bottom-up when count*alpha > unvisited and count*beta > n
     unsigned small;             // k_bfs_run: frontiers <= small are run by block 0 alone
     unsigned long long svert;   // vertices expanded in block-0 (small) levels
+    // flag-plane BFS early stop: once every vertex with excess is labelled (act_claimed == act_total
+    // > 0) the levels stop; the unlabelled vertices take L + 1 (relabel.cuh k_colgr_rebuild)
+    unsigned long long act_total, act_claimed;
+    int early;                  // 1: early stop enabled; set to 2 by the kernel when it stopped early
 };
 __device__ __forceinline__ int bfs_bucket(unsigned c) {
     return c <= 32 ? 0 : c <= 256 ? 1 : c <= 2048 ? 2 : c <= 16384 ? 3 : c <= 131072 ? 4 : c <= 1048576 ? 5 : 6;
 }
 
 __global__ void k_bfs_seeded(BfsState *st) { st->claimed = st->cnt[0]; }
-
-// Bottom-up (pull) level for large frontiers: every unlabelled vertex u of a 32-z chunk
-// looks for a residual out-arc into level L -- t-arc (L = 0 only), down (u-1), up (u+1 if
-// D(u+1) > 0), lateral-out (nbr, zo), lateral-in reverse (nbr, zi) if L_{d^1}(nbr, zi) > 0 --
-// and takes label L+1.  All loads of a warp are coalesced lines of the chunk or its
-// shifted neighbour chunks, so a level costs ~4 B/vertex plus the unlabelled vertices,
-// instead of ~15 scattered sectors per frontier vertex (Beamer's direction optimisation).
-// Race-free: u is written only by its own lane, and a vertex written L+1 during the level
-// is never read as L by another lane.
-__device__ __forceinline__ void bfs_bottom_up_level(const Geo &g, const Soa &s, int L, int *lout, unsigned *cout,
-                                                    unsigned *visited = nullptr) {
-    constexpr int SPAN = 4;
-    SpanAppender<SPAN> ap;
-    const int64_t nchunks = g.nchunks;
-    for (int64_t cb = gwarp() * SPAN; cb < nchunks; cb += nwarps() * SPAN) {
-#pragma unroll
-        for (int j = 0; j < SPAN; j++) {
-            const int64_t ch = cb + j;
-            bool hit = false;
-            int64_t b0 = 0;
-            if (ch < nchunks) {
-                const int64_t col = ch / g.CPC;
-                const int z = (int)(ch - col * g.CPC) * 32 + lane_id();
-                const int64_t v0 = col * g.Z;
-                b0 = v0 + (z - lane_id());
-                const bool valid = z < g.Z;
-                const int64_t u = v0 + z;
-                const bool need = valid && __ldcg(&s.H[u]) >= g.INF;
-                if (__any_sync(FULL, need) && need) {
-                    if (z >= 1 && __ldcg(&s.H[u - 1]) == L) hit = true;
-                    if (!hit && z + 1 < g.Z && s.D[u + 1] > 0 && __ldcg(&s.H[u + 1]) == L) hit = true;
-                    if (!hit) {
-                        const int x = (int)(col / g.Y), y = (int)(col - (int64_t)x * g.Y);
-#pragma unroll
-                        for (int d = 0; d < 4 && !hit; d++) {
-                            const int64_t o = nbr_off(g, x, y, d);
-                            if (!o) continue;
-                            const int zo = zo_of(z, delta_d(g, d)), zi = zi_of(z, delta_d(g, d), g.Z);
-                            if (zo >= 0 && __ldcg(&s.H[v0 + o + zo]) == L) hit = true;
-                            else if (zi >= 0 && s.L[d ^ 1][v0 + o + zi] > 0 && __ldcg(&s.H[v0 + o + zi]) == L) hit = true;
-                        }
-                    }
-                    if (hit) {
-                        s.H[u] = L + 1;
-                        if (visited) atomicOr(&visited[u >> 5], 1u << (u & 31));
-                    }
-                }
-            }
-            ap.add(__ballot_sync(FULL, hit), b0);
-        }
-        ap.flush(lout, cout);
-    }
-}
 
 __global__ void __launch_bounds__(512, CG_BFS_MINB) k_bfs_step(Geo g, Soa s, int *list0, int *list1, BfsState *st) {
     __shared__ int sL;
@@ -1268,8 +1125,7 @@ __global__ void __launch_bounds__(512, CG_BFS_MINB) k_bfs_step(Geo g, Soa s, int
             if (threadIdx.x == 0) st->cnt[(i + 2) % 3] = 0;
             for (unsigned base = (threadIdx.x >> 5) * 32; base < count; base += (blockDim.x >> 5) * 32) {
                 const unsigned j = base + lane_id();
-                bfs_expand_warp<true>(g, s, L + 1, j < count ? (int64_t)lin[j] : -1, lout, &st->cnt[(i + 1) % 3],
-                                      nullptr, 0);
+                bfs_expand_warp(g, s, L + 1, j < count ? (int64_t)lin[j] : -1, lout, &st->cnt[(i + 1) % 3]);
             }
             __syncthreads();
             ++L;
@@ -1285,19 +1141,9 @@ __global__ void __launch_bounds__(512, CG_BFS_MINB) k_bfs_step(Geo g, Soa s, int
     const int *lin = (i & 1) ? list1 : list0;
     int *lout = (i & 1) ? list0 : list1;
     if (blockIdx.x == 0 && threadIdx.x == 0) st->cnt[(i + 2) % 3] = 0;
-    // direction optimisation: a top-down expansion touches ~15 scattered sectors per frontier
-    // vertex; a bottom-up level ~4 B per vertex plus ~10 coalesced loads per unlabelled vertex
-    const unsigned long long unvisited = (unsigned long long)g.n - *(volatile unsigned long long *)&st->claimed;
-    // (unreachable vertices stay unvisited and are re-checked every bottom-up level, so only
-    // switch when the frontier is a large share of what is left)
-    if ((unsigned long long)count * 2ull > unvisited && (unsigned long long)count * 64ull > (unsigned long long)g.n) {
-        bfs_bottom_up_level(g, s, L, lout, &st->cnt[(i + 1) % 3]);
-    } else {
-        for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {
-            const int64_t j = base + lane_id();
-            bfs_expand_warp<true>(g, s, L + 1, j < count ? (int64_t)lin[j] : -1, lout, &st->cnt[(i + 1) % 3],
-                                  nullptr, 0);
-        }
+    for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {
+        const int64_t j = base + lane_id();
+        bfs_expand_warp(g, s, L + 1, j < count ? (int64_t)lin[j] : -1, lout, &st->cnt[(i + 1) % 3]);
     }
     __threadfence();
     __syncthreads();
@@ -1346,14 +1192,27 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks) {
 #ifndef CG_BFS_RUN_MINB
 #define CG_BFS_RUN_MINB 1
 #endif
+template <bool FL>
 __global__ void __launch_bounds__(512, CG_BFS_RUN_MINB) k_bfs_run(Geo g, Soa s, int *list0, int *list1, BfsState *st,
-                                                                  unsigned *visited) {
+                                                                  unsigned *visited, const uint8_t *flags,
+                                                                  int32_t *lab) {
     unsigned *bar = st->bar;
     int L = *(volatile int *)&st->L;
     unsigned long long claimed = *(volatile unsigned long long *)&st->claimed;
+    // early stop (flag-plane BFS): every vertex with excess is labelled, so every label <= L is
+    // exact and the rest may take L + 1 (a valid labelling: d > L for all of them)
+    auto all_active = [&]() {
+        if (!FL || st->early != 1) return false;
+        const unsigned long long tot = *(volatile unsigned long long *)&st->act_total;
+        return tot > 0 && *(volatile unsigned long long *)&st->act_claimed >= tot;
+    };
     for (int guard = 0; guard <= g.INF + 2; guard++) {
         const unsigned count = *(volatile unsigned *)&st->cnt[(L - 1) % 3];
         if (count == 0) break;
+        if (all_active()) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) st->early = 2;
+            break;
+        }
         const int i = L - 1;
         if (count <= st->small) {
             // everyone has read this level's counter before block 0 starts recycling counters
@@ -1379,14 +1238,15 @@ __global__ void __launch_bounds__(512, CG_BFS_RUN_MINB) k_bfs_run(Geo g, Soa s, 
                             const unsigned jj = base + r * 32 + lane_id();
                             vv[r] = jj < c ? __ldcg(&lin[jj]) : -1;
                         }
-                        bfs_expand_multi<BFS_R>(g, s, L + 1, vv, lout, &st->cnt[(j + 1) % 3], visited);
+                        bfs_expand_multi<BFS_R, FL>(g, s, L + 1, vv, lout, &st->cnt[(j + 1) % 3], visited, flags, lab,
+                                                    &st->act_claimed);
                     }
                     __syncthreads();
                     ++L;
                     c = *(volatile unsigned *)&st->cnt[(L - 1) % 3];
                     if (threadIdx.x == 0) st->claimed += c;
                     __syncthreads();
-                    if (c == 0 || c > st->small) break;
+                    if (c == 0 || c > st->small || all_active()) break;
                 }
                 if (threadIdx.x == 0) {
                     st->L = L;
@@ -1406,19 +1266,14 @@ __global__ void __launch_bounds__(512, CG_BFS_RUN_MINB) k_bfs_run(Geo g, Soa s, 
             st->hist[bfs_bucket(count)]++;
         }
         const long long t0 = clock64();
-        const unsigned long long unvisited = (unsigned long long)g.n - claimed;
-        const bool bu = (unsigned long long)count * (unsigned long long)st->bu_alpha > unvisited &&
-                        (unsigned long long)count * (unsigned long long)st->bu_beta > (unsigned long long)g.n;
-        if (bu) {
-            if (blockIdx.x == 0 && threadIdx.x == 0) st->hist[7]++;
-            bfs_bottom_up_level(g, s, L, lout, &st->cnt[(i + 1) % 3], visited);
-        } else {
+        {
             // few vertices per warp: spread them (R = 1); many: R per lane for load-level parallelism
             if ((int64_t)count < nwarps() * 32 * BFS_R) {
                 for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {
                     const int64_t j = base + lane_id();
                     int vv[1] = {j < count ? __ldcg(&lin[j]) : -1};
-                    bfs_expand_multi<1>(g, s, L + 1, vv, lout, &st->cnt[(i + 1) % 3], visited);
+                    bfs_expand_multi<1, FL>(g, s, L + 1, vv, lout, &st->cnt[(i + 1) % 3], visited, flags, lab,
+                                            &st->act_claimed);
                 }
             } else {
                 for (int64_t base = gwarp() * 32 * BFS_R; base < count; base += nwarps() * 32 * BFS_R) {
@@ -1428,29 +1283,19 @@ __global__ void __launch_bounds__(512, CG_BFS_RUN_MINB) k_bfs_run(Geo g, Soa s, 
                         const int64_t j = base + r * 32 + lane_id();
                         vv[r] = j < count ? __ldcg(&lin[j]) : -1;
                     }
-                    bfs_expand_multi<BFS_R>(g, s, L + 1, vv, lout, &st->cnt[(i + 1) % 3], visited);
+                    bfs_expand_multi<BFS_R, FL>(g, s, L + 1, vv, lout, &st->cnt[(i + 1) % 3], visited, flags, lab,
+                                                &st->act_claimed);
                 }
             }
         }
         grid_barrier(bar, gridDim.x);
-        if (blockIdx.x == 0 && threadIdx.x == 0) st->cyc[bu ? 7 : bfs_bucket(count)] += clock64() - t0;
+        if (blockIdx.x == 0 && threadIdx.x == 0) st->cyc[bfs_bucket(count)] += clock64() - t0;
         ++L;
         claimed += *(volatile unsigned *)&st->cnt[(L - 1) % 3];  // every block: same value
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         st->L = L;
         st->claimed = claimed;
-    }
-}
-
-// Label-correcting wave (x-slab mode): relax the predecessors of every listed vertex.
-__global__ void __launch_bounds__(256) k_lc_wave(Geo g, Soa s, const int *__restrict__ lin, const unsigned *cin,
-                                                 int *lout, unsigned *cout, unsigned *czero, int *vstamp, int tag) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) *czero = 0;
-    const int64_t count = *cin;
-    for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {
-        const int64_t j = base + lane_id();
-        bfs_expand_warp<false>(g, s, 0, j < count ? (int64_t)lin[j] : -1, lout, cout, vstamp, tag);
     }
 }
 
@@ -1463,7 +1308,7 @@ __global__ void __launch_bounds__(256) k_slab_level(Geo g, Soa s, int nl, const 
     const int64_t count = *cin;
     for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {
         const int64_t j = base + lane_id();
-        bfs_expand_warp<true>(g, s, nl, j < count ? (int64_t)lin[j] : -1, lout, cout, nullptr, 0);
+        bfs_expand_warp(g, s, nl, j < count ? (int64_t)lin[j] : -1, lout, cout);
     }
 }
 // ghost-plane labels of this slab (both sides, one launch) -> the owners of those vertices
@@ -1489,72 +1334,6 @@ __global__ void k_slab_ghost_claim(Geo g, Soa s, const int32_t *__restrict__ rec
         if (t < m && (hi ? recv1 : recv0)[i] == nl)
             add = s.H[v] >= g.INF && atomicCAS(&s.H[v], g.INF, nl) == g.INF;
         warp_append(add, (int)v, lout, cout);
-    }
-}
-
-// Ghost seeds: a ghost vertex gv whose label decreased (vs. old[]) relaxes its residual
-// predecessors in this slab's boundary plane:
-//   u = (boundary, zi(z))  lateral arc of u into gv (infinite)
-//   u = (boundary, zo(z))  reverse of gv's lateral arc toward this slab, residual L_dir(gv)
-__global__ void k_lc_ghost(Geo g, Soa s, int side, const int32_t *__restrict__ old, int *lout, unsigned *cout,
-                           int *vstamp, int tag) {
-    const int64_t gbase = side ? g.n : -g.YZ;
-    const int64_t bbase = side ? g.n - g.YZ : 0;
-    const int ldir = side ? 1 : 0;  // direction of the ghost's arcs toward this slab
-    for (int64_t b0 = gwarp() * 32; b0 < g.YZ; b0 += nwarps() * 32) {
-        const int64_t i = b0 + lane_id();
-        int u0 = -1, u1 = -1;
-        if (i < g.YZ) {
-            const int64_t gv = gbase + i;
-            const int l = s.H[gv];
-            if (l < g.INF && l < old[i]) {
-                const int nl = l + 1;
-                const int z = (int)(i % g.Z);
-                const int64_t col0 = bbase + (i - z);
-                const int zi = zi_of(z, g.delta, g.Z), zo = zo_of(z, g.delta);
-                auto relax = [&](int64_t w) -> int {
-                    if (s.H[w] > nl && atomicMin(&s.H[w], nl) > nl && vstamp[w] != tag &&
-                        atomicExch(&vstamp[w], tag) != tag)
-                        return (int)w;
-                    return -1;
-                };
-                if (zi >= 0) u0 = relax(col0 + zi);
-                if (zo >= 0 && s.L[ldir][gv] > 0) u1 = relax(col0 + zo);
-            }
-        }
-        warp_append(u0 >= 0, u0, lout, cout);
-        warp_append(u1 >= 0, u1, lout, cout);
-        if (g.soft_k) {  // soft arcs between the boundary plane and the ghost plane (warp-uniform loop)
-            const int bdir = side ? 0 : 1;  // this slab's arcs toward the ghost plane
-            const int kmax = min(g.soft_k, g.delta);
-            bool live = false;
-            int nl = 0, z = 0;
-            int64_t gv = 0, col0 = 0;
-            if (i < g.YZ) {
-                gv = gbase + i;
-                const int l = s.H[gv];
-                live = l < g.INF && l < old[i];
-                nl = l + 1;
-                z = (int)(i % g.Z);
-                col0 = bbase + (i - z);
-            }
-            for (int k = 0; k < kmax; k++) {
-                const int cap = g.soft_cap[k];
-                int a = -1, b = -1;
-                auto relax = [&](int64_t w) -> int {
-                    if (s.H[w] > nl && atomicMin(&s.H[w], nl) > nl && vstamp[w] != tag &&
-                        atomicExch(&vstamp[w], tag) != tag)
-                        return (int)w;
-                    return -1;
-                };
-                if (live && cap > 0) {
-                    if (z + k < g.Z && cap - *soft_flow(g, s, col0 + z + k, bdir, k) > 0) a = relax(col0 + z + k);
-                    if (z - k >= 0 && *soft_flow(g, s, gv, ldir, k) > 0) b = relax(col0 + z - k);
-                }
-                warp_append(a >= 0, a, lout, cout);
-                warp_append(b >= 0, b, lout, cout);
-            }
-        }
     }
 }
 
@@ -1655,6 +1434,13 @@ __global__ void k_gap_hist(Geo g, const FieldH H, unsigned *hist, int *maxh) {
     mymax = warp_max_i(mymax);
     if (lane_id() == 0) atomicMax(maxh, mymax);
 }
+// in-process slabs: dst histogram += src histogram, dst max = max(dst, src)
+__global__ void k_hist_fold(const unsigned *src, const int *src_max, unsigned *dst, int *dst_max) {
+    const int lim = min(*src_max + 1, GAP_BINS);
+    for (int h = blockIdx.x * blockDim.x + threadIdx.x; h < lim; h += gridDim.x * blockDim.x)
+        if (src[h]) dst[h] += src[h];
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicMax(dst_max, *src_max);
+}
 __global__ void k_gap_find(const unsigned *hist, const int *maxh, int *gap) {
     const int lim = min(*maxh, GAP_BINS - 1);
     int best = INT_MAX;
@@ -1692,94 +1478,6 @@ __global__ void k_sum_T(Geo g, const Field T, unsigned long long *out) {
         acc += T[i];
     acc = warp_sum_ll(acc);
     if (lane_id() == 0 && acc) atomicAdd(out, (unsigned long long)acc);
-}
-
-// ------------------------------------------------------------------ a1': column pre-cancellation
-// Exact max-flow of every column in isolation (ignoring lateral arcs), applied as the
-// initial preflow: source excess may only move DOWN a column (infinite down arcs) into
-// sink arcs below it, and the top-down greedy is optimal because the set of sinks a
-// source can feed is nested.  With a(z) = E(z) - T(z) and S(z) = sum_{j>=z} a(j):
-//   carry leaving z downward    c(z) = S(z) - min_{m in [z, Z]} S(m)       (S(Z) = 0)
-//   absorbed at a sink          ab(z) = min(T(z), c(z+1))
-//   flow on the down arc z->z-1 f(z) = min(c(z), sum_{z'<z} ab(z'))  (only what is absorbed below)
-//   new state  T -= ab,  D = f,  E = f(z+1) + E(z) - ab(z) - f(z) >= 0.
-// Not in the paper: an accelerator whose result is a valid preflow, so the maximum flow
-// and the minimal cut are unchanged.  One warp per column, z in chunks of 32.
-__device__ __forceinline__ long long warp_suffix_sum_ll(long long v) {
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const long long t = __shfl_down_sync(FULL, v, o);
-        if (lane_id() + o < 32) v += t;
-    }
-    return v;
-}
-__device__ __forceinline__ long long warp_suffix_min_ll(long long v) {
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const long long t = __shfl_down_sync(FULL, v, o);
-        if (lane_id() + o < 32) v = min(v, t);
-    }
-    return v;
-}
-__device__ __forceinline__ long long warp_excl_prefix_sum_ll(long long v) {
-    long long x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const long long t = __shfl_up_sync(FULL, x, o);
-        if (lane_id() >= o) x += t;
-    }
-    return x - v;
-}
-
-__global__ void __launch_bounds__(256) k_precancel(Geo g, Soa s, int *flags) {
-    extern __shared__ long long sh_c[];  // per warp: Z+1 carries c(z)
-    long long *cz = sh_c + (int64_t)(threadIdx.x >> 5) * (g.Z + 1);
-    const int64_t ncol = (int64_t)g.X * g.Y;
-    const int last_c0 = ((g.Z - 1) >> 5) << 5;
-    bool bad = false;
-    for (int64_t col = gwarp(); col < ncol; col += nwarps()) {
-        const int64_t v0 = col * g.Z;
-        long long sum_above = 0, min_above = 0;  // S over chunks above; min over m above incl. S(Z) = 0
-        if (lane_id() == 0) cz[g.Z] = 0;
-        for (int c0 = last_c0; c0 >= 0; c0 -= 32) {
-            const int z = c0 + lane_id();
-            long long a = 0;
-            if (z < g.Z) a = (long long)s.E[v0 + z] - (long long)s.T[v0 + z];
-            const long long S = warp_suffix_sum_ll(a) + sum_above;
-            const long long m = min(warp_suffix_min_ll(z < g.Z ? S : LLONG_MAX), min_above);
-            if (z < g.Z) cz[z] = S - m;
-            sum_above = __shfl_sync(FULL, S, 0);
-            min_above = __shfl_sync(FULL, m, 0);
-        }
-        __syncwarp();
-        long long ab_below = 0;
-        for (int c0 = 0; c0 < g.Z; c0 += 32) {
-            const int z = c0 + lane_id();
-            const bool ok = z < g.Z;
-            int e = 0, t = 0;
-            long long ab = 0, f = 0;
-            if (ok) {
-                e = s.E[v0 + z];
-                t = s.T[v0 + z];
-                ab = t > 0 ? min((long long)t, cz[z + 1]) : 0;
-            }
-            const long long AB = warp_excl_prefix_sum_ll(ab) + ab_below;
-            if (ok && z >= 1) f = min(cz[z], AB);
-            long long f_up = __shfl_down_sync(FULL, f, 1);
-            const long long ab_total = __shfl_sync(FULL, AB + ab, 31);
-            if (lane_id() == 31) f_up = (z + 1 < g.Z) ? min(cz[z + 1], ab_total) : 0;
-            if (ok) {
-                const long long ne = f_up + (long long)e - ab - f;
-                if (ne < 0 || ne > INT_MAX || f > INT_MAX) bad = true;
-                s.E[v0 + z] = (int32_t)ne;
-                s.T[v0 + z] = t - (int32_t)ab;
-                s.D[v0 + z] = (int32_t)f;
-            }
-            ab_below = ab_total;
-        }
-        __syncwarp();
-    }
-    if (bad) atomicOr(flags, FLAG_OVERFLOW);
 }
 
 // ------------------------------------------------------------------ a7: extraction

@@ -67,7 +67,7 @@ def solve_ranks(cg, c, delta, R, penalty=None, weight=False, opts=None, want_mas
                     planes = 7 + (4 * kk if penalty is not None else 0)
                     with torch.cuda.stream(s):
                         fl = torch.empty(planes * xr * Y * Z, dtype=torch.int32, device="cuda")
-                    fst = cg.maxflow_export_flow(h, slabs[r], weight, fl, opts)
+                    fst, fl = cg.maxflow_export_flow(h, slabs[r], weight, fl, opts)
                     fl = (fst, fl)
                 stats = cg.colgraph_stats(h)
             finally:

@@ -83,7 +83,7 @@ def test_weight_mode_slabs(cg):
         assert r["extract_status"] == (6 if o["status"] == 6 else 0), trial
 
 
-@pytest.mark.parametrize("name,ns", [("C3", 2), ("C3", 5), ("C4", 8)])
+@pytest.mark.parametrize("name,ns", [("C3", 2), ("C3", 5), ("C4", 8), ("C5", 4)])
 def test_full_size_slabs(cg, name, ns):
     spec = V.CONFIGS[name]
     gfile = os.path.join(GOLDEN_DIR, f"oracle_{name}.json")
@@ -113,10 +113,10 @@ def test_slab_state_export_is_a_max_preflow(cg):
     _certificate(c, 3, state)
 
 
-def test_label_correcting_slab_relabel(cg, monkeypatch):
-    """The label-correcting x-slab relabel (CG_SLAB_LC=1), kept for comparison with the
-    default level-synchronous one, must give the same unique results."""
-    monkeypatch.setenv("CG_SLAB_LC", "1")
+def test_bfs_slab_relabel(cg, monkeypatch):
+    """The level-synchronous vertex-BFS x-slab relabel (CG_RELABEL=bfs), the alternative to the
+    default column fixpoint with boundary exchanges, must give the same unique results."""
+    monkeypatch.setenv("CG_RELABEL", "bfs")
     for seed in range(3000, 3060):
         c, delta = V.tiny_case(seed)
         ns = 2 + seed % 4

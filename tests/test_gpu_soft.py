@@ -56,7 +56,7 @@ def test_soft_schedules(cg, opts):
         assert_same(gpu_soft(cg, c, dxy, pen, opts=cg.make_opts(**opts)), o, f"{opts} case {i}")
 
 
-@pytest.mark.parametrize("var", [{"CG_BFS_LEVEL_LAUNCHES": "1"}, {"CG_WALK_WS": "0"}])
+@pytest.mark.parametrize("var", [{"CG_BFS_LEVEL_LAUNCHES": "1"}, {"CG_WALK_MIN": "0"}])
 def test_soft_variants(cg, monkeypatch, var):
     for k, v in var.items():
         monkeypatch.setenv(k, v)

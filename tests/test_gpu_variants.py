@@ -1,11 +1,10 @@
 """GPU parity of the alternative a3/a2 implementations against the CPU oracle (bit-exact):
   - CG_SWEEP_TILES: checkerboard tile discharge in shared memory (tile.cuh), incl. ragged
     tiles (X, Y not multiples of the tile shape) and every instantiated lane segment S;
-  - k_walk (CG_WALK_WS=0) instead of the default work-fetching walk k_walk_ws;
-  - level-per-launch BFS (CG_BFS_LEVEL_LAUNCHES=1) vs the persistent cooperative BFS;
-  - the sweep/relabel knobs of include/colgraph.h: relabel-and-continue (CG_WALK_RCONT),
-    a replayed relabel schedule (CG_GR_SCHEDULE), parking, ordered re-listing, work-only
-    trigger.
+  - the vertex-frontier BFS relabel (CG_RELABEL=bfs) vs the default column fixpoint, and
+    within it the level-per-launch BFS (CG_BFS_LEVEL_LAUNCHES=1) vs the persistent one;
+  - the sweep/relabel knobs of include/colgraph.h: a replayed relabel schedule
+    (CG_GR_SCHEDULE), work-only trigger, single hops only, small-worklist thresholds.
 The options change the schedule only; the max-flow value, the minimal source set and the
 surface are unique, so results must be identical."""
 import os
@@ -85,13 +84,10 @@ def test_tiles_rejects_tall_columns(cg):
         cg.colgraph_free(h)
 
 
-@pytest.mark.parametrize("var", [{"CG_WALK_WS": "0"}, {"CG_BFS_LEVEL_LAUNCHES": "1"},
-                                 {"CG_WALK_MIN": "0"}, {"CG_BFS_SMALL": "2048"},
-                                 {"CG_BFS_SMALL": "0"}, {"CG_BU_ALPHA": "2"},
-                                 {"CG_WALK_WS": "0", "CG_WALK_RCONT": "1"}, {"CG_WALK_WS": "0", "CG_WALK_RCONT": "16"},
-                                 {"CG_GR_SCHEDULE": "1,2,3,5,8,13,21,34"},
-                                 {"CG_WALK_WS": "0", "CG_WALK_PARK": "1"}, {"CG_WALK_WS": "0", "CG_RELIST": "1"},
-                                 {"CG_WALK_WS": "0", "CG_RELIST": "1", "CG_WALK_PARK": "1"},
+@pytest.mark.parametrize("var", [{"CG_RELABEL": "bfs"}, {"CG_RELABEL": "bfs", "CG_BFS_LEVEL_LAUNCHES": "1"},
+                                 {"CG_WALK_MIN": "0"}, {"CG_RELABEL": "bfs", "CG_BFS_SMALL": "2048"},
+                                 {"CG_RELABEL": "bfs", "CG_BFS_SMALL": "0"}, {"CG_COLGR_SMALL": "0"},
+                                 {"CG_COLGR_SMALL": "100000"}, {"CG_GR_SCHEDULE": "1,2,3,5,8,13,21,34"},
                                  {"CG_GR_BETA": "1000"}, {"CG_OPS": "4"}])
 def test_schedule_variants(cg, env, var):
     for k, v in var.items():
