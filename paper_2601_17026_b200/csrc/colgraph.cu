@@ -65,6 +65,7 @@ struct Slab {
     unsigned long long *work = nullptr;  // [2*RING] per sweep: operations, relabels
     unsigned long long *visits = nullptr;  // [RING] tile visits per phase
     unsigned *heads = nullptr;             // [RING] work-fetch cursors of k_walk_ws
+    unsigned *relist_cnt = nullptr;        // [RELIST_BLOCKS] ordered re-listing: block counts / offsets
     unsigned *visited = nullptr;           // [n/32 + 1] BFS visited bitmap (persistent BFS)
     int32_t *lab = nullptr;                // column-fixpoint relabel: labels, planes [-YZ, n + YZ)
     uint8_t *gflags = nullptr;             // column-fixpoint relabel: residual-arc flags, same range
@@ -291,7 +292,7 @@ size_t workspace_bytes(const Geo &geo) {
     b += 4 * al(sizeof(int32_t) * geo.YZ) + 4 * al(sizeof(int32_t) * halo_msg_ints(geo));
     b += 5 * al(sizeof(int) * ncol) + al(sizeof(unsigned) * 4) + al(sizeof(unsigned long long) * RING) +
          al(sizeof(unsigned long long) * 16) + al(sizeof(unsigned) * RING) + al(sizeof(unsigned) * (geo.n / 32 + 1));
-    b += al(sizeof(int32_t) * plane) + al(plane) + al(sizeof(ColGrState));
+    b += al(sizeof(int32_t) * plane) + al(plane) + al(sizeof(ColGrState)) + al(sizeof(unsigned) * RELIST_BLOCKS);
     return b;
 }
 
@@ -374,6 +375,7 @@ cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode) {
     sl->tl.prof = carve<unsigned long long>(p, 16);
     sl->visits = carve<unsigned long long>(p, RING);
     sl->heads = carve<unsigned>(p, RING);
+    sl->relist_cnt = carve<unsigned>(p, RELIST_BLOCKS);
     sl->visited = carve<unsigned>(p, n / 32 + 1);
     sl->lab = carve<int32_t>(p, plane) + geo.YZ;
     sl->gflags = carve<uint8_t>(p, plane) + geo.YZ;
@@ -505,19 +507,13 @@ cg_status bfs_strict(cg_graph *g, Slab *sl, bool allow_coop = true, bool flag_pl
     CG_CUDA(cudaMemcpyAsync(&sl->bst->small, &sl->h_bst->small, sizeof(unsigned), cudaMemcpyHostToDevice, st));
     const bool coop = allow_coop && sl->bfs_coop_grid > 0;
     if (flag_plane && !coop) return CG_E_INVAL;
-    if (flag_plane) {
-        // early stop once every vertex with excess is labelled (CG_BFS_FULL=1: run every level)
-        const int early = getenv("CG_BFS_FULL") && atoi(getenv("CG_BFS_FULL")) ? 0 : 1;
-        CG_CUDA(cudaMemcpyAsync(&sl->bst->early, &early, sizeof(int), cudaMemcpyHostToDevice, st));
-        k_bfs2_init<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, st>>>(
-            geo, sl->s, sl->gflags, sl->lab, sl->visited, sl->blist[0], &sl->bst->cnt[0], &sl->bst->act_total);
-        k_bfs2_seeded<<<sl->num_sms, 256, 0, st>>>(sl->bst, sl->gflags, sl->blist[0]);
-        CG_CUDA(cudaStreamSynchronize(st));  // `early` is a host stack value
-    } else {
+    if (flag_plane)
+        k_bfs2_init<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, st>>>(geo, sl->s, sl->gflags, sl->lab,
+                                                                             sl->visited, sl->blist[0], &sl->bst->cnt[0]);
+    else
         k_bfs_init<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, st>>>(geo, sl->s, sl->blist[0], &sl->bst->cnt[0],
                                                                             coop ? sl->visited : nullptr);
-        k_bfs_seeded<<<1, 1, 0, st>>>(sl->bst);
-    }
+    k_bfs_seeded<<<1, 1, 0, st>>>(sl->bst);
     g->st.kernel_launches += 2;
     int L = 1;
     if (coop) {  // every level in one cooperative launch (k_bfs_run)
@@ -768,8 +764,7 @@ cg_status global_relabel(cg_graph *g, int64_t *active) {
             CG_CUDA(cudaMemsetAsync(sl->cnt, 0, 3 * sizeof(unsigned), sl->stream));
             if (colgr)  // records' H = the relabel's labels, fused with the active list
                 k_colgr_rebuild<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(
-                    geo, sl->s, sl->lab, sl->blist[0], sl->cnt, sl->vstamp, ++sl->tag, sl->u64 + 3,
-                    kind == RELABEL_FLAGS ? sl->bst : nullptr);
+                    geo, sl->s, sl->lab, sl->blist[0], sl->cnt, sl->vstamp, ++sl->tag, sl->u64 + 3);
             else
                 k_rebuild_vertices<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(
                     geo, sl->s, sl->blist[0], sl->cnt, sl->vstamp, ++sl->tag, sl->u64 + 3);
@@ -800,7 +795,7 @@ cg_status run_gap(cg_graph *g) {
     for (Slab *sl : g->slabs) {
         CG_CUDA(cudaMemsetAsync(sl->hist, 0, sizeof(unsigned) * GAP_BINS, sl->stream));
         CG_CUDA(cudaMemsetAsync(sl->flags + 1, 0, sizeof(int), sl->stream));
-        k_gap_hist<<<sl->num_sms * 8, 256, 0, sl->stream>>>(sl->geo, sl->s.H, sl->hist, sl->flags + 1);
+        k_gap_hist<<<sl->num_sms * 2, 512, 0, sl->stream>>>(sl->geo, sl->s.H, sl->hist, sl->flags + 1);
         g->st.kernel_launches++;
     }
     Slab *s0 = g->slabs[0];
@@ -982,8 +977,6 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
             fprintf(stderr, "[cg] GR#%lld levels=%lld active=%lld ms=%.3f (sweeps %lld) flow=%lld\n",
                     (long long)g->st.global_relabels, (long long)(g->st.gr_passes - p0), (long long)active, last_gr_ms,
                     (long long)g->st.sweeps, (long long)-sumT);
-            fprintf(stderr, "[cg]   early stop %d (vertices with excess labelled %llu of %llu)\n", s0->h_bst->early,
-                    (unsigned long long)s0->h_bst->act_claimed, (unsigned long long)s0->h_bst->act_total);
             const unsigned *h = s0->h_bst->hist;
             fprintf(stderr, "[cg]   levels by frontier: <=32 %u <=256 %u <=2K %u <=16K %u <=128K %u <=1M %u more %u "
                     "(bottom-up %u)\n", h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
@@ -999,6 +992,10 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
     const double gr_budget = (double)o.gr_factor * (double)g->n_global;
     const double walk_min = getenv("CG_WALK_MIN") ? atof(getenv("CG_WALK_MIN")) : 1e-3;
     const double gr_beta = getenv("CG_GR_BETA") ? atof(getenv("CG_GR_BETA")) : 1.0;
+    // CG_RELIST=1: index-ordered worklists for the walks (lists >= n / CG_RELIST_DIV entries, default 64)
+    const bool relist = getenv("CG_RELIST") && atoi(getenv("CG_RELIST")) != 0;
+    const unsigned relist_min =
+        (unsigned)std::max<int64_t>(1, s0->geo.n / (getenv("CG_RELIST_DIV") ? atoi(getenv("CG_RELIST_DIV")) : 64));
     double work_since_gr = 0.0, sweep_ms_since_gr = 0.0;
     int64_t sweeps = g->st.sweeps, since_gap = 0, last_active = active;
     std::vector<int64_t> wv(RING + 3);  // batch <= RING op counters, the overflow flag, the time trigger, relabels
@@ -1097,11 +1094,22 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
                 const int k = sl->sweep_k++;
                 sl->out_tag = ++sl->tag;
                 const bool soft = geo.soft_k > 0;
-                if (walk)  // multi-hop work-fetching walks
+                if (walk) {  // multi-hop work-fetching walks
                     (soft ? k_walk_ws<true> : k_walk_ws<false>)<<<gv, 256, 0, sl->stream>>>(
                         geo, sl->s, o.walk_len, sl->blist[k & 1], sl->cnt + k % 3, sl->blist[(k + 1) & 1],
                         sl->cnt + (k + 1) % 3, sl->cnt + (k + 2) % 3, sl->vstamp, sl->out_tag, sl->work + 2 * i,
                         sl->flags, sl->heads + i);
+                    if (relist && !multi(g)) {  // index-ordered next worklist (lists >= relist_min only)
+                        k_relist_count<<<RELIST_BLOCKS, 256, 0, sl->stream>>>(geo, sl->vstamp, sl->out_tag,
+                                                                              sl->cnt + (k + 1) % 3, relist_min,
+                                                                              sl->relist_cnt);
+                        k_relist_scan<<<1, 1024, 0, sl->stream>>>(sl->cnt + (k + 1) % 3, relist_min, sl->relist_cnt);
+                        k_relist_write<<<RELIST_BLOCKS, 256, 0, sl->stream>>>(geo, sl->vstamp, sl->out_tag,
+                                                                              sl->cnt + (k + 1) % 3, relist_min,
+                                                                              sl->relist_cnt, sl->blist[(k + 1) & 1]);
+                        g->st.kernel_launches += 3;
+                    }
+                }
                 else
                     (soft ? k_sweep_v<true> : k_sweep_v<false>)<<<gv, 256, 0, sl->stream>>>(geo, sl->s, o.ops_per_sweep, sl->blist[k & 1],
                                                           sl->cnt + k % 3, sl->blist[(k + 1) & 1],

@@ -815,6 +815,82 @@ __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_walk_ws(Geo g, Soa s, in
     flush_work(work, mywork, myrel);
 }
 
+// Ordered re-listing of a large sweep worklist (CG_RELIST=1, measured alternative): the vertices
+// listed for the next sweep are exactly those with vstamp == tag, so a two-pass compaction over
+// vstamp rewrites the list in vertex-index order (block b owns a contiguous index range: pass 1
+// counts, the host-free scan in pass 2 turns counts into offsets, pass 3 writes in order).  With
+// index order, the walks a work-fetching sweep runs at the same time start in a contiguous window
+// of the volume, so their neighbour records are shared through L2.  Lists shorter than `min_count`
+// are left as they are (the kernels return at once).
+constexpr int RELIST_BLOCKS = 1184;
+__device__ __forceinline__ int64_t relist_chunk(const Geo &g) { return ((g.n + RELIST_BLOCKS - 1) / RELIST_BLOCKS + 31) & ~31ll; }
+__global__ void __launch_bounds__(256) k_relist_count(Geo g, const int *__restrict__ vstamp, int tag, const unsigned *count,
+                                                      unsigned min_count, unsigned *bcnt) {
+    if (*count < min_count) return;
+    const int64_t ch = relist_chunk(g), lo = blockIdx.x * ch, hi = min(g.n, lo + ch);
+    unsigned c = 0;
+    for (int64_t v = lo + threadIdx.x; v < hi; v += blockDim.x) c += __ldcg(&vstamp[v]) == tag;
+    c = warp_sum_i((int)c);
+    __shared__ unsigned ws[8];
+    if (lane_id() == 0) ws[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned t = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); i++) t += ws[i];
+        bcnt[blockIdx.x] = t;
+    }
+}
+__global__ void __launch_bounds__(1024) k_relist_scan(const unsigned *count, unsigned min_count, unsigned *bcnt) {
+    if (*count < min_count) return;
+    __shared__ unsigned part[32];
+    constexpr int PER = (RELIST_BLOCKS + 1023) / 1024;
+    unsigned loc[PER], sum = 0;
+#pragma unroll
+    for (int k = 0; k < PER; k++) {
+        const int i = threadIdx.x * PER + k;
+        loc[k] = i < RELIST_BLOCKS ? bcnt[i] : 0;
+        sum += loc[k];
+    }
+    const unsigned incl = (unsigned)warp_incl_scan((int)sum);
+    if (lane_id() == 31) part[threadIdx.x >> 5] = incl;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const unsigned p = part[threadIdx.x];
+        const unsigned pi = (unsigned)warp_incl_scan((int)p);
+        part[threadIdx.x] = pi - p;
+    }
+    __syncthreads();
+    unsigned off = part[threadIdx.x >> 5] + incl - sum;
+#pragma unroll
+    for (int k = 0; k < PER; k++) {
+        const int i = threadIdx.x * PER + k;
+        if (i < RELIST_BLOCKS) bcnt[i] = off;
+        off += loc[k];
+    }
+}
+__global__ void __launch_bounds__(256) k_relist_write(Geo g, const int *__restrict__ vstamp, int tag, const unsigned *count,
+                                                      unsigned min_count, const unsigned *boff, int *list) {
+    if (*count < min_count) return;
+    const int64_t ch = relist_chunk(g), lo = blockIdx.x * ch, hi = min(g.n, lo + ch);
+    __shared__ unsigned wc[8];
+    unsigned run = boff[blockIdx.x];
+    for (int64_t t0 = lo; t0 < hi; t0 += blockDim.x) {
+        const int64_t v = t0 + threadIdx.x;
+        const bool on = v < hi && __ldcg(&vstamp[v]) == tag;
+        const unsigned m = __ballot_sync(FULL, on);
+        if (lane_id() == 0) wc[threadIdx.x >> 5] = __popc(m);
+        __syncthreads();
+        unsigned before = 0, tot = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); i++) {
+            if (i < (int)(threadIdx.x >> 5)) before += wc[i];
+            tot += wc[i];
+        }
+        if (on) list[run + before + __popc(m & lanemask_lt())] = (int)v;
+        run += tot;
+        __syncthreads();
+    }
+}
+
 // After a global relabel: list every active vertex (E > 0, H < INF) in index order.
 __global__ void k_rebuild_vertices(Geo g, const Soa s, int *lout, unsigned *cout, int *vstamp, int tag,
                                    unsigned long long *active) {
@@ -997,7 +1073,7 @@ __device__ __forceinline__ void load_DL(const Soa &s, int v, int &D, int (&L)[4]
 template <int R, bool FL = false>
 __device__ __forceinline__ void bfs_expand_multi(const Geo &g, const Soa &s, int nl, const int (&vv)[R], int *lout,
                                                  unsigned *cout, unsigned *visited, const uint8_t *flags = nullptr,
-                                                 int32_t *lab = nullptr, unsigned long long *act_claimed = nullptr) {
+                                                 int32_t *lab = nullptr) {
     const int INF = g.INF;
     int w[R][10], hw[R][10];
     unsigned cand[R], got[R];
@@ -1055,16 +1131,6 @@ __device__ __forceinline__ void bfs_expand_multi(const Geo &g, const Soa &s, int
                     k++;
                 }
             }
-    if (FL) {  // claimed vertices holding excess (flag bit 6)
-        int na = 0;
-#pragma unroll
-        for (int r = 0; r < R; r++)
-#pragma unroll
-            for (int j = 0; j < 10; j++)
-                if (got[r] >> j & 1u) na += (__ldg(&flags[w[r][j]]) >> 6) & 1;
-        na = warp_sum_i(na);
-        if (lane_id() == 0 && na) atomicAdd(act_claimed, (unsigned long long)na);
-    }
     const int incl = warp_incl_scan(k);
     const int total = __shfl_sync(FULL, incl, 31);
     if (total == 0) return;
@@ -1098,10 +1164,6 @@ struct BfsState {
     unsigned long long cyc[8];  // block-0 clock cycles spent in levels of each bucket ([7]: bottom-up levels)
     unsigned small;             // k_bfs_run: frontiers <= small are run by block 0 alone
     unsigned long long svert;   // vertices expanded in block-0 (small) levels
-    // flag-plane BFS early stop: once every vertex with excess is labelled (act_claimed == act_total
-    // > 0) the levels stop; the unlabelled vertices take L + 1 (relabel.cuh k_colgr_rebuild)
-    unsigned long long act_total, act_claimed;
-    int early;                  // 1: early stop enabled; set to 2 by the kernel when it stopped early
 };
 __device__ __forceinline__ int bfs_bucket(unsigned c) {
     return c <= 32 ? 0 : c <= 256 ? 1 : c <= 2048 ? 2 : c <= 16384 ? 3 : c <= 131072 ? 4 : c <= 1048576 ? 5 : 6;
@@ -1199,20 +1261,9 @@ __global__ void __launch_bounds__(512, CG_BFS_RUN_MINB) k_bfs_run(Geo g, Soa s, 
     unsigned *bar = st->bar;
     int L = *(volatile int *)&st->L;
     unsigned long long claimed = *(volatile unsigned long long *)&st->claimed;
-    // early stop (flag-plane BFS): every vertex with excess is labelled, so every label <= L is
-    // exact and the rest may take L + 1 (a valid labelling: d > L for all of them)
-    auto all_active = [&]() {
-        if (!FL || st->early != 1) return false;
-        const unsigned long long tot = *(volatile unsigned long long *)&st->act_total;
-        return tot > 0 && *(volatile unsigned long long *)&st->act_claimed >= tot;
-    };
     for (int guard = 0; guard <= g.INF + 2; guard++) {
         const unsigned count = *(volatile unsigned *)&st->cnt[(L - 1) % 3];
         if (count == 0) break;
-        if (all_active()) {
-            if (blockIdx.x == 0 && threadIdx.x == 0) st->early = 2;
-            break;
-        }
         const int i = L - 1;
         if (count <= st->small) {
             // everyone has read this level's counter before block 0 starts recycling counters
@@ -1238,15 +1289,14 @@ __global__ void __launch_bounds__(512, CG_BFS_RUN_MINB) k_bfs_run(Geo g, Soa s, 
                             const unsigned jj = base + r * 32 + lane_id();
                             vv[r] = jj < c ? __ldcg(&lin[jj]) : -1;
                         }
-                        bfs_expand_multi<BFS_R, FL>(g, s, L + 1, vv, lout, &st->cnt[(j + 1) % 3], visited, flags, lab,
-                                                    &st->act_claimed);
+                        bfs_expand_multi<BFS_R, FL>(g, s, L + 1, vv, lout, &st->cnt[(j + 1) % 3], visited, flags, lab);
                     }
                     __syncthreads();
                     ++L;
                     c = *(volatile unsigned *)&st->cnt[(L - 1) % 3];
                     if (threadIdx.x == 0) st->claimed += c;
                     __syncthreads();
-                    if (c == 0 || c > st->small || all_active()) break;
+                    if (c == 0 || c > st->small) break;
                 }
                 if (threadIdx.x == 0) {
                     st->L = L;
@@ -1272,8 +1322,7 @@ __global__ void __launch_bounds__(512, CG_BFS_RUN_MINB) k_bfs_run(Geo g, Soa s, 
                 for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {
                     const int64_t j = base + lane_id();
                     int vv[1] = {j < count ? __ldcg(&lin[j]) : -1};
-                    bfs_expand_multi<1, FL>(g, s, L + 1, vv, lout, &st->cnt[(i + 1) % 3], visited, flags, lab,
-                                            &st->act_claimed);
+                    bfs_expand_multi<1, FL>(g, s, L + 1, vv, lout, &st->cnt[(i + 1) % 3], visited, flags, lab);
                 }
             } else {
                 for (int64_t base = gwarp() * 32 * BFS_R; base < count; base += nwarps() * 32 * BFS_R) {
@@ -1283,8 +1332,7 @@ __global__ void __launch_bounds__(512, CG_BFS_RUN_MINB) k_bfs_run(Geo g, Soa s, 
                         const int64_t j = base + r * 32 + lane_id();
                         vv[r] = j < count ? __ldcg(&lin[j]) : -1;
                     }
-                    bfs_expand_multi<BFS_R, FL>(g, s, L + 1, vv, lout, &st->cnt[(i + 1) % 3], visited, flags, lab,
-                                                &st->act_claimed);
+                    bfs_expand_multi<BFS_R, FL>(g, s, L + 1, vv, lout, &st->cnt[(i + 1) % 3], visited, flags, lab);
                 }
             }
         }
@@ -1422,17 +1470,28 @@ __global__ void k_halo_unpack_h(Geo g, Soa s, int side, const int32_t *__restric
 // Cherkassky-Goldberg gap: if no vertex has label g (0 < g < max
 // finite label), every vertex labelled above g cannot reach t: lift it to INF.
 constexpr int GAP_BINS = 1 << 20;
-__global__ void k_gap_hist(Geo g, const FieldH H, unsigned *hist, int *maxh) {
+// Label histogram: a block-private shared-memory histogram of the labels < GAP_SMEM (one global
+// atomic per non-empty bin per block afterwards); larger labels go straight to global memory.  A
+// global atomic per vertex serialised on the few hundred busy bins (measured: ~10 ms per C4 pass).
+constexpr int GAP_SMEM = 8192;
+__global__ void __launch_bounds__(512) k_gap_hist(Geo g, const FieldH H, unsigned *hist, int *maxh) {
+    __shared__ unsigned sh[GAP_SMEM];
+    for (int i = threadIdx.x; i < GAP_SMEM; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
     int mymax = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += (int64_t)gridDim.x * blockDim.x) {
         const int h = H[i];
         if (h < g.INF) {
             mymax = max(mymax, h);
-            if (h < GAP_BINS) atomicAdd(&hist[h], 1u);
+            if (h < GAP_SMEM) atomicAdd(&sh[h], 1u);
+            else if (h < GAP_BINS) atomicAdd(&hist[h], 1u);
         }
     }
     mymax = warp_max_i(mymax);
     if (lane_id() == 0) atomicMax(maxh, mymax);
+    __syncthreads();
+    for (int i = threadIdx.x; i < GAP_SMEM; i += blockDim.x)
+        if (sh[i]) atomicAdd(&hist[i], sh[i]);
 }
 // in-process slabs: dst histogram += src histogram, dst max = max(dst, src)
 __global__ void k_hist_fold(const unsigned *src, const int *src_max, unsigned *dst, int *dst_max) {

@@ -46,13 +46,10 @@ __global__ void k_colgr_flags(Geo g, Soa s, uint8_t *flags, int32_t *lab, int64_
 // Flag-plane BFS init (hard graphs, the default relabel): one dense pass over the records writes the
 // flags, the labels (1 for the seeds T > 0 -- Alg. 3's first level, reading R6 -- else INF), the
 // visited bitmap and the seed list; k_bfs_run<true> then expands from the flags and writes `lab`.
-// Bit 6 of the flags marks vertices holding excess; their number goes to *act_total (the early stop
-// of k_bfs_run<true>).
 __global__ void k_bfs2_init(Geo g, Soa s, uint8_t *flags, int32_t *lab, unsigned *visited, int *lout,
-                            unsigned *cout, unsigned long long *act_total) {
+                            unsigned *cout) {
     constexpr int SPAN = 8;
     SpanAppender<SPAN> ap;
-    unsigned long long nact = 0;
     for (int64_t base = gwarp() * 32 * SPAN; base < g.n; base += nwarps() * 32 * SPAN) {
 #pragma unroll
         for (int j = 0; j < SPAN; j++) {
@@ -63,15 +60,13 @@ __global__ void k_bfs2_init(Geo g, Soa s, uint8_t *flags, int32_t *lab, unsigned
 #if CG_LAYOUT_AOS
                 const int4 *rec = reinterpret_cast<const int4 *>(&s.E[v]);  // E H T D | L0 L1 L2 L3
                 const int4 a = rec[0], b = rec[1];
-                const int E = a.x, T = a.z, D = a.w, L0 = b.x, L1 = b.y, L2 = b.z, L3 = b.w;
+                const int T = a.z, D = a.w, L0 = b.x, L1 = b.y, L2 = b.z, L3 = b.w;
 #else
-                const int E = s.E[v], T = s.T[v], D = s.D[v], L0 = s.L[0][v], L1 = s.L[1][v], L2 = s.L[2][v],
-                          L3 = s.L[3][v];
+                const int T = s.T[v], D = s.D[v], L0 = s.L[0][v], L1 = s.L[1][v], L2 = s.L[2][v], L3 = s.L[3][v];
 #endif
                 seed = T > 0;
-                nact += E > 0;
                 flags[v] = (uint8_t)(seed | (D > 0) << 1 | (L0 > 0) << 2 | (L1 > 0) << 3 | (L2 > 0) << 4 |
-                                     (L3 > 0) << 5 | (E > 0) << 6);
+                                     (L3 > 0) << 5);
                 lab[v] = seed ? 1 : g.INF;
             }
             const unsigned m = __ballot_sync(FULL, seed);
@@ -80,18 +75,6 @@ __global__ void k_bfs2_init(Geo g, Soa s, uint8_t *flags, int32_t *lab, unsigned
         }
         ap.flush(lout, cout);
     }
-    nact = warp_sum_ll((long long)nact);
-    if (lane_id() == 0 && nact) atomicAdd(act_total, nact);
-}
-
-// seeds that hold excess are claimed at label 1 before the levels start
-__global__ void k_bfs2_seeded(BfsState *st, const uint8_t *flags, const int *list) {
-    unsigned long long na = 0;
-    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < st->cnt[0]; i += gridDim.x * blockDim.x)
-        na += (flags[list[i]] >> 6) & 1;
-    na = warp_sum_ll((long long)na);
-    if (lane_id() == 0 && na) atomicAdd(&st->act_claimed, na);
-    if (blockIdx.x == 0 && threadIdx.x == 0) st->claimed = st->cnt[0];
 }
 
 struct ColGrState {
@@ -302,11 +285,8 @@ __global__ void __launch_bounds__(512, (CPC > 4 ? 1 : 2)) k_colgr_run(Geo g, con
 
 // After the fixpoint: the records' H = the labels, and every active vertex (E > 0, H < INF) is
 // listed for the sweeps in index order (replaces k_rebuild_vertices for this relabel).
-// unvisited: the label of vertices the relabel left at INF (INF, or L + 1 after the BFS's early stop,
-// read from *unvisited_from (BfsState.L) when non-null).
 __global__ void k_colgr_rebuild(Geo g, Soa s, const int32_t *__restrict__ lab, int *lout, unsigned *cout, int *vstamp,
-                                int tag, unsigned long long *active, const BfsState *bst) {
-    const int unv = (bst && bst->early == 2) ? bst->L + 1 : g.INF;
+                                int tag, unsigned long long *active) {
     constexpr int SPAN = 8;
     SpanAppender<SPAN> ap;
     unsigned long long myact = 0;
@@ -317,8 +297,7 @@ __global__ void k_colgr_rebuild(Geo g, Soa s, const int32_t *__restrict__ lab, i
             const int64_t v = b0 + lane_id();
             bool a = false;
             if (v < g.n) {
-                const int l = lab[v];
-                const int h = l < g.INF ? l : unv;
+                const int h = lab[v];
                 s.H[v] = h;
                 a = s.E[v] > 0 && h < g.INF;
             }

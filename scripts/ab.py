@@ -1,6 +1,7 @@
 """A/B timing of solver variants (diagnostics): median wall time of build+solve+extract over
 reps, per config.  Variants are env settings applied in subprocesses.
-usage: python scripts/ab.py C3,C4,C5 reps 'NAME:ENV=V,ENV=V' ...
+usage: python scripts/ab.py C3,C4,C5 reps 'NAME:ENV=V,ENV=V' ...   (AB_OPTS={json} -> cg_solve_opts fields;
+pass it inside a variant as AB_OPTS={"gap_every":1} -- no commas inside: use ; between fields)
 """
 import json
 import os
@@ -21,7 +22,7 @@ for name in sys.argv[1].split(","):
     ts, r = [], None
     for rep in range(reps + 1):
         torch.cuda.synchronize(); t = time.perf_counter()
-        r = cg.solve(c, spec.delta, want_mask=False)
+        r = cg.solve(c, spec.delta, want_mask=False, opts=cg.make_opts(**json.loads(os.environ.get("AB_OPTS", "{}"))))
         torch.cuda.synchronize(); dt = time.perf_counter() - t
         if rep:
             ts.append(dt * 1000)
@@ -43,7 +44,7 @@ for var in sys.argv[3:]:
     env = dict(os.environ)
     for kv in filter(None, envs.split(",")):
         k, _, v = kv.partition("=")
-        env[k] = v
+        env[k] = v.replace(";", ",")
     out = subprocess.run([sys.executable, "-c", CHILD, cfgs, reps], env=env, capture_output=True, text=True,
                          timeout=600)
     for line in out.stdout.splitlines():
