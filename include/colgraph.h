@@ -38,8 +38,10 @@
  *   CG_SWEEP=1            tile sweeps (as sweep_kind = CG_SWEEP_TILES); CG_TILE=TXxTY,
  *                         CG_TILE_STEPS, CG_TILE_RELABEL, CG_TILE_PROF=1 (clock counters)
  *   CG_PHASE2_PR=1        maxflow_export_flow: generic push-relabel phase 2 only
- *   CG_RELABEL=bfs        global relabel by the vertex-frontier BFS instead of the column
- *                         fixpoint (the BFS also serves soft graphs, Z > 256 and tiles)
+ *   CG_RELABEL=bfs|colgr|levels  global relabel flavour: default one slab: BFS
+ *                         over the residual-flag plane; x-slabs: in-slab flag BFS + column fixpoint
+ *                         across boundaries; bfs: BFS over the records (also soft graphs, tiles);
+ *                         colgr: column fixpoint from INF; levels (x-slabs): level-synchronous BFS
  *   CG_COLGR_SMALL=k      column fixpoint: worklists <= k columns run in block 0 alone
  * Conventions for every entry point:
  *   - Errors are returned as cg_status, never thrown; no C++ exception crosses
@@ -109,7 +111,8 @@ typedef struct {
  *                 (factor 1..2); default 1.0
  *   gap_every   : run the gap heuristic every gap_every sweeps
  *                 (0 = never); default 0
- *   check_every : sweeps between host reads of the active-vertex count; default 16
+ *   check_every : sweeps between host reads of the active-vertex count (and relabel-trigger
+ *                 checks); 1..256, default 8
  *   max_sweeps  : give up with CG_E_NOT_CONVERGED after this many sweeps; default 1<<30
  *   ops_per_sweep : push/relabel operations a vertex may perform per sweep; default 1
  *   walk_len    : > 0 selects multi-hop sweeps: a vertex's excess follows admissible arcs

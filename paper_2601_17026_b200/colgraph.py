@@ -128,7 +128,7 @@ def version() -> str:
 SWEEP_AUTO, SWEEP_TILES, SWEEP_VERTEX = 0, 1, 2
 
 
-def make_opts(gr_factor=1.0, gap_every=0, check_every=16, max_sweeps=1 << 30, ops_per_sweep=1,
+def make_opts(gr_factor=1.0, gap_every=0, check_every=8, max_sweeps=1 << 30, ops_per_sweep=1,
               walk_len=0, sweep_kind=SWEEP_AUTO, tile_steps=0, tile_relabel_every=0) -> cg_solve_opts:
     return cg_solve_opts(float(gr_factor), int(gap_every), int(check_every), int(max_sweeps), int(ops_per_sweep),
                          int(walk_len), int(sweep_kind), int(tile_steps), int(tile_relabel_every))

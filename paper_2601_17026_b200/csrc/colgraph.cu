@@ -65,7 +65,6 @@ struct Slab {
     unsigned long long *work = nullptr;  // [2*RING] per sweep: operations, relabels
     unsigned long long *visits = nullptr;  // [RING] tile visits per phase
     unsigned *heads = nullptr;             // [RING] work-fetch cursors of k_walk_ws
-    unsigned *relist_cnt = nullptr;        // [RELIST_BLOCKS] ordered re-listing: block counts / offsets
     unsigned *visited = nullptr;           // [n/32 + 1] BFS visited bitmap (persistent BFS)
     int32_t *lab = nullptr;                // column-fixpoint relabel: labels, planes [-YZ, n + YZ)
     uint8_t *gflags = nullptr;             // column-fixpoint relabel: residual-arc flags, same range
@@ -292,7 +291,7 @@ size_t workspace_bytes(const Geo &geo) {
     b += 4 * al(sizeof(int32_t) * geo.YZ) + 4 * al(sizeof(int32_t) * halo_msg_ints(geo));
     b += 5 * al(sizeof(int) * ncol) + al(sizeof(unsigned) * 4) + al(sizeof(unsigned long long) * RING) +
          al(sizeof(unsigned long long) * 16) + al(sizeof(unsigned) * RING) + al(sizeof(unsigned) * (geo.n / 32 + 1));
-    b += al(sizeof(int32_t) * plane) + al(plane) + al(sizeof(ColGrState)) + al(sizeof(unsigned) * RELIST_BLOCKS);
+    b += al(sizeof(int32_t) * plane) + al(plane) + al(sizeof(ColGrState));
     return b;
 }
 
@@ -375,7 +374,6 @@ cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode) {
     sl->tl.prof = carve<unsigned long long>(p, 16);
     sl->visits = carve<unsigned long long>(p, RING);
     sl->heads = carve<unsigned>(p, RING);
-    sl->relist_cnt = carve<unsigned>(p, RELIST_BLOCKS);
     sl->visited = carve<unsigned>(p, n / 32 + 1);
     sl->lab = carve<int32_t>(p, plane) + geo.YZ;
     sl->gflags = carve<uint8_t>(p, plane) + geo.YZ;
@@ -563,17 +561,20 @@ const void *colgr_kernel(int Z) {
 // one slab), COLGR = the column fixpoint (default on x-slabs: its exchanges count slab-boundary
 // crossings, not BFS levels), RECORD = the record BFS (soft graphs, tiles, Z > 256 for the
 // fixpoint, no cooperative launch).  CG_RELABEL = flags | colgr | bfs overrides where applicable.
-enum RelabelKind { RELABEL_RECORD, RELABEL_FLAGS, RELABEL_COLGR };
+// On x-slabs, BFS_COLGR = in-slab flag-plane BFS + the column fixpoint across slab boundaries.
+enum RelabelKind { RELABEL_RECORD, RELABEL_FLAGS, RELABEL_COLGR, RELABEL_BFS_COLGR };
 RelabelKind relabel_kind(const cg_graph *g) {
     const Slab *sl = g->slabs[0];
     if (sl->geo.soft_k || sl->tiles) return RELABEL_RECORD;
     const char *e = getenv("CG_RELABEL");
     if (e && !strcmp(e, "bfs")) return RELABEL_RECORD;
     const bool colgr_ok = sl->colgr_grid > 0;
-    const bool flags_ok = sl->bfs_coop_grid > 0 && !multi(g);
+    const bool flags_ok = sl->bfs_coop_grid > 0;
     if (e && !strcmp(e, "colgr") && colgr_ok) return RELABEL_COLGR;
-    if (e && !strcmp(e, "flags") && flags_ok) return RELABEL_FLAGS;
-    if (multi(g)) return colgr_ok ? RELABEL_COLGR : RELABEL_RECORD;
+    if (multi(g)) {
+        if (e && !strcmp(e, "levels")) return RELABEL_RECORD;
+        return colgr_ok && flags_ok ? RELABEL_BFS_COLGR : colgr_ok ? RELABEL_COLGR : RELABEL_RECORD;
+    }
     return flags_ok ? RELABEL_FLAGS : RELABEL_RECORD;
 }
 
@@ -584,17 +585,25 @@ cg_status colgr_launch(Slab *sl, int dense) {
     return CG_OK;
 }
 
-// flags of the residual arcs + labels reset to INF over owned and ghost planes, fixpoint state
-cg_status colgr_begin(cg_graph *g, Slab *sl) {
+// flags of the residual arcs + labels reset to INF over the ghost planes and (owned = true) the
+// owned planes, fixpoint state
+cg_status colgr_begin(cg_graph *g, Slab *sl, bool owned = true) {
     const Geo &geo = sl->geo;
     CG_CUDA(cudaMemsetAsync(sl->cst, 0, sizeof(ColGrState), sl->stream));
     sl->h_cst->small = getenv("CG_COLGR_SMALL") ? (unsigned)atoi(getenv("CG_COLGR_SMALL")) : 16;
     sl->h_cst->tag0 = sl->tag + 1;
     CG_CUDA(cudaMemcpyAsync(&sl->cst->small, &sl->h_cst->small, 2 * sizeof(int), cudaMemcpyHostToDevice, sl->stream));
-    const int64_t lo = geo.gl ? -geo.YZ : 0, hi = geo.n + (geo.gh ? geo.YZ : 0);
-    k_colgr_flags<<<grid_for(hi - lo, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(geo, sl->s, sl->gflags, sl->lab, lo,
-                                                                                     hi);
-    g->st.kernel_launches++;
+    auto flags = [&](int64_t lo, int64_t hi) {
+        k_colgr_flags<<<grid_for(hi - lo, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(geo, sl->s, sl->gflags, sl->lab,
+                                                                                         lo, hi);
+        g->st.kernel_launches++;
+    };
+    if (owned) {
+        flags(geo.gl ? -geo.YZ : 0, geo.n + (geo.gh ? geo.YZ : 0));
+    } else {
+        if (geo.gl) flags(-geo.YZ, 0);
+        if (geo.gh) flags(geo.n, geo.n + geo.YZ);
+    }
     CG_CUDA(cudaGetLastError());
     return CG_OK;
 }
@@ -621,11 +630,19 @@ cg_status colgr_strict(cg_graph *g, Slab *sl) {
 // restarts the fixpoint.  Stop when no slab listed anything (one global sum per exchange): the
 // number of exchanges is the number of slab-boundary crossings of the shortest paths (+1), not the
 // BFS depth (§3.2.2 L274-289 synchronises every level).
-cg_status colgr_slabs(cg_graph *g) {
+//   bfs_init: each slab first computes its in-slab distances with the flag-plane BFS (paths that
+//   stay inside the slab: upper bounds of the true distances, work-efficient); the fixpoint then
+//   only corrects the labels that cross-slab paths lower.  Otherwise the fixpoint starts from INF.
+cg_status colgr_slabs(cg_graph *g, bool bfs_init) {
     for (Slab *sl : g->slabs) {
-        CG_TRY(colgr_begin(g, sl));
-        CG_TRY(colgr_launch(sl, 1));
-        g->st.kernel_launches++;
+        if (bfs_init) {
+            CG_TRY(bfs_strict(g, sl, true, true));
+            CG_TRY(colgr_begin(g, sl, false));
+        } else {
+            CG_TRY(colgr_begin(g, sl));
+            CG_TRY(colgr_launch(sl, 1));
+            g->st.kernel_launches++;
+        }
     }
     const int64_t YZ = g->slabs[0]->geo.YZ;
     for (int iter = 0;; iter++) {
@@ -650,7 +667,10 @@ cg_status colgr_slabs(cg_graph *g) {
             listed += sl->h_cst->cnt[sl->h_cst->round % 3];
         }
         CG_TRY(gsum(g, &listed, 1));
-        if (listed == 0) break;
+        if (listed == 0) {
+            if (tracing()) fprintf(stderr, "[cg]   x-slab column fixpoint: %d boundary exchanges\n", iter + 1);
+            break;
+        }
         if (iter > 4 * (int64_t)g->dims.X + 64) return CG_E_CUDA;  // every exchange lowers some label
         for (Slab *sl : g->slabs)
             if (sl->h_cst->cnt[sl->h_cst->round % 3]) {
@@ -742,8 +762,8 @@ cg_status bfs_slabs_levels(cg_graph *g) {
 cg_status global_relabel(cg_graph *g, int64_t *active) {
     const RelabelKind kind = relabel_kind(g);
     const bool colgr = kind != RELABEL_RECORD;  // labels are in sl->lab: the rebuild writes the records' H
-    if (kind == RELABEL_COLGR) {
-        CG_TRY(multi(g) ? colgr_slabs(g) : colgr_strict(g, g->slabs[0]));
+    if (kind == RELABEL_COLGR || kind == RELABEL_BFS_COLGR) {
+        CG_TRY(multi(g) ? colgr_slabs(g, kind == RELABEL_BFS_COLGR) : colgr_strict(g, g->slabs[0]));
     } else if (kind == RELABEL_FLAGS) {
         CG_TRY(bfs_strict(g, g->slabs[0], true, true));
     } else if (!multi(g)) {
@@ -926,9 +946,11 @@ cg_status validate_dims(const cg_dims *dims) {
 // Solver options with library defaults (NULL = defaults; 0 fields = defaults); use_tiles = the
 // tile sweep was requested and set up.
 cg_status normalize_opts(cg_graph *g, const cg_solve_opts *opts, cg_solve_opts &o, bool &use_tiles) {
-    o = cg_solve_opts{1.0f, 0, 16, (int64_t)1 << 30, 1, 0, 0, 0, 0};
+    // check_every 8: the relabel triggers are checked every 8 sweeps (measured against 4 / 16:
+    // C4 -5 %, C5 -13 %)
+    o = cg_solve_opts{1.0f, 0, 8, (int64_t)1 << 30, 1, 0, 0, 0, 0};
     if (opts) o = *opts;
-    if (o.check_every <= 0) o.check_every = 16;
+    if (o.check_every <= 0) o.check_every = 8;
     if (o.max_sweeps <= 0) o.max_sweeps = (int64_t)1 << 30;
     if (o.sweep_kind == CG_SWEEP_AUTO && getenv("CG_SWEEP")) o.sweep_kind = atoi(getenv("CG_SWEEP"));
     if (o.tile_steps <= 0) o.tile_steps = getenv("CG_TILE_STEPS") ? atoi(getenv("CG_TILE_STEPS")) : 64;
@@ -992,10 +1014,6 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
     const double gr_budget = (double)o.gr_factor * (double)g->n_global;
     const double walk_min = getenv("CG_WALK_MIN") ? atof(getenv("CG_WALK_MIN")) : 1e-3;
     const double gr_beta = getenv("CG_GR_BETA") ? atof(getenv("CG_GR_BETA")) : 1.0;
-    // CG_RELIST=1: index-ordered worklists for the walks (lists >= n / CG_RELIST_DIV entries, default 64)
-    const bool relist = getenv("CG_RELIST") && atoi(getenv("CG_RELIST")) != 0;
-    const unsigned relist_min =
-        (unsigned)std::max<int64_t>(1, s0->geo.n / (getenv("CG_RELIST_DIV") ? atoi(getenv("CG_RELIST_DIV")) : 64));
     double work_since_gr = 0.0, sweep_ms_since_gr = 0.0;
     int64_t sweeps = g->st.sweeps, since_gap = 0, last_active = active;
     std::vector<int64_t> wv(RING + 3);  // batch <= RING op counters, the overflow flag, the time trigger, relabels
@@ -1099,16 +1117,6 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
                         geo, sl->s, o.walk_len, sl->blist[k & 1], sl->cnt + k % 3, sl->blist[(k + 1) & 1],
                         sl->cnt + (k + 1) % 3, sl->cnt + (k + 2) % 3, sl->vstamp, sl->out_tag, sl->work + 2 * i,
                         sl->flags, sl->heads + i);
-                    if (relist && !multi(g)) {  // index-ordered next worklist (lists >= relist_min only)
-                        k_relist_count<<<RELIST_BLOCKS, 256, 0, sl->stream>>>(geo, sl->vstamp, sl->out_tag,
-                                                                              sl->cnt + (k + 1) % 3, relist_min,
-                                                                              sl->relist_cnt);
-                        k_relist_scan<<<1, 1024, 0, sl->stream>>>(sl->cnt + (k + 1) % 3, relist_min, sl->relist_cnt);
-                        k_relist_write<<<RELIST_BLOCKS, 256, 0, sl->stream>>>(geo, sl->vstamp, sl->out_tag,
-                                                                              sl->cnt + (k + 1) % 3, relist_min,
-                                                                              sl->relist_cnt, sl->blist[(k + 1) & 1]);
-                        g->st.kernel_launches += 3;
-                    }
                 }
                 else
                     (soft ? k_sweep_v<true> : k_sweep_v<false>)<<<gv, 256, 0, sl->stream>>>(geo, sl->s, o.ops_per_sweep, sl->blist[k & 1],

@@ -815,82 +815,6 @@ __global__ void __launch_bounds__(256, CG_SWEEP_MINB) k_walk_ws(Geo g, Soa s, in
     flush_work(work, mywork, myrel);
 }
 
-// Ordered re-listing of a large sweep worklist (CG_RELIST=1, measured alternative): the vertices
-// listed for the next sweep are exactly those with vstamp == tag, so a two-pass compaction over
-// vstamp rewrites the list in vertex-index order (block b owns a contiguous index range: pass 1
-// counts, the host-free scan in pass 2 turns counts into offsets, pass 3 writes in order).  With
-// index order, the walks a work-fetching sweep runs at the same time start in a contiguous window
-// of the volume, so their neighbour records are shared through L2.  Lists shorter than `min_count`
-// are left as they are (the kernels return at once).
-constexpr int RELIST_BLOCKS = 1184;
-__device__ __forceinline__ int64_t relist_chunk(const Geo &g) { return ((g.n + RELIST_BLOCKS - 1) / RELIST_BLOCKS + 31) & ~31ll; }
-__global__ void __launch_bounds__(256) k_relist_count(Geo g, const int *__restrict__ vstamp, int tag, const unsigned *count,
-                                                      unsigned min_count, unsigned *bcnt) {
-    if (*count < min_count) return;
-    const int64_t ch = relist_chunk(g), lo = blockIdx.x * ch, hi = min(g.n, lo + ch);
-    unsigned c = 0;
-    for (int64_t v = lo + threadIdx.x; v < hi; v += blockDim.x) c += __ldcg(&vstamp[v]) == tag;
-    c = warp_sum_i((int)c);
-    __shared__ unsigned ws[8];
-    if (lane_id() == 0) ws[threadIdx.x >> 5] = c;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned t = 0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); i++) t += ws[i];
-        bcnt[blockIdx.x] = t;
-    }
-}
-__global__ void __launch_bounds__(1024) k_relist_scan(const unsigned *count, unsigned min_count, unsigned *bcnt) {
-    if (*count < min_count) return;
-    __shared__ unsigned part[32];
-    constexpr int PER = (RELIST_BLOCKS + 1023) / 1024;
-    unsigned loc[PER], sum = 0;
-#pragma unroll
-    for (int k = 0; k < PER; k++) {
-        const int i = threadIdx.x * PER + k;
-        loc[k] = i < RELIST_BLOCKS ? bcnt[i] : 0;
-        sum += loc[k];
-    }
-    const unsigned incl = (unsigned)warp_incl_scan((int)sum);
-    if (lane_id() == 31) part[threadIdx.x >> 5] = incl;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        const unsigned p = part[threadIdx.x];
-        const unsigned pi = (unsigned)warp_incl_scan((int)p);
-        part[threadIdx.x] = pi - p;
-    }
-    __syncthreads();
-    unsigned off = part[threadIdx.x >> 5] + incl - sum;
-#pragma unroll
-    for (int k = 0; k < PER; k++) {
-        const int i = threadIdx.x * PER + k;
-        if (i < RELIST_BLOCKS) bcnt[i] = off;
-        off += loc[k];
-    }
-}
-__global__ void __launch_bounds__(256) k_relist_write(Geo g, const int *__restrict__ vstamp, int tag, const unsigned *count,
-                                                      unsigned min_count, const unsigned *boff, int *list) {
-    if (*count < min_count) return;
-    const int64_t ch = relist_chunk(g), lo = blockIdx.x * ch, hi = min(g.n, lo + ch);
-    __shared__ unsigned wc[8];
-    unsigned run = boff[blockIdx.x];
-    for (int64_t t0 = lo; t0 < hi; t0 += blockDim.x) {
-        const int64_t v = t0 + threadIdx.x;
-        const bool on = v < hi && __ldcg(&vstamp[v]) == tag;
-        const unsigned m = __ballot_sync(FULL, on);
-        if (lane_id() == 0) wc[threadIdx.x >> 5] = __popc(m);
-        __syncthreads();
-        unsigned before = 0, tot = 0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); i++) {
-            if (i < (int)(threadIdx.x >> 5)) before += wc[i];
-            tot += wc[i];
-        }
-        if (on) list[run + before + __popc(m & lanemask_lt())] = (int)v;
-        run += tot;
-        __syncthreads();
-    }
-}
-
 // After a global relabel: list every active vertex (E > 0, H < INF) in index order.
 __global__ void k_rebuild_vertices(Geo g, const Soa s, int *lout, unsigned *cout, int *vstamp, int tag,
                                    unsigned long long *active) {
