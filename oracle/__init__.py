@@ -64,6 +64,10 @@ def _load():
         lib.oracle_colgraph_solve_soft.argtypes = [i32p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                    ctypes.c_int, i32p, ctypes.c_int, ctypes.c_int, ctypes.c_int, i64p,
                                                    i32p, u8p, i32p, i64p]
+        lib.oracle_colgraph_solve_general.restype = ctypes.c_int
+        lib.oracle_colgraph_solve_general.argtypes = [i32p, ctypes.c_int, ctypes.c_int, ctypes.c_int, i32p, i32p,
+                                                      i32p, ctypes.c_int, ctypes.c_int, ctypes.c_int, i64p, i32p, u8p,
+                                                      i32p, i64p]
         lib.oracle_graph_maxflow.restype = ctypes.c_int
         lib.oracle_graph_maxflow.argtypes = [ctypes.c_int, ctypes.c_int, i32p, i32p, i64p, ctypes.c_int,
                                              ctypes.c_int, ctypes.c_int, i64p, u8p, i32p]
@@ -78,11 +82,25 @@ def _ptr(a, ct):
     return a.ctypes.data_as(ctypes.POINTER(ct))
 
 
+def deltas4(delta):
+    """Edge intervals toward (+x, -x, +y, -y): delta is an int (isotropic), (delta_x, delta_y)
+    (anisotropic, NEXT-3) or a 4-tuple (general proper-ordered interval: the pair p, q = p + x
+    satisfies S(q) - S(p) in [-delta[0], delta[1]], likewise y with delta[2], delta[3])."""
+    if isinstance(delta, (tuple, list)):
+        if len(delta) == 2:
+            dx, dy = int(delta[0]), int(delta[1])
+            dy = dx if dy == -1 else dy
+            return (dx, dx, dy, dy)
+        return tuple(int(d) for d in delta)
+    return (int(delta),) * 4
+
+
 def colgraph_solve(c: np.ndarray, delta, input_is_weight: bool = False, algo: str = "dinic",
-                   want_mask: bool = True, penalty=None) -> dict:
-    """Solve the column graph of cost (or weight) volume c[X][Y][Z].  delta: int (isotropic)
-    or (delta_x, delta_y).  penalty: optional convex soft-smoothness penalty [f(1), .., f(K)],
-    K >= max(delta) (NEXT-1: finite arcs of capacity f(k+1) - 2 f(k) + f(k-1)).
+                   want_mask: bool = True, penalty=None, band=None) -> dict:
+    """Solve the column graph of cost (or weight) volume c[X][Y][Z].  delta: see deltas4.
+    penalty: optional convex soft-smoothness penalty [f(1), .., f(K)], K >= max(delta) (NEXT-1:
+    finite arcs of capacity f(k+1) - 2 f(k) + f(k-1)).  band: optional int32 [X, Y, 2] (lo, hi) per
+    column, the narrow band the surface is confined to (NEXT-3; costs only).
 
     Returns dict(status, flow, surface[X,Y] int32, mask[X,Y,Z] uint8 or None,
     checks (bit set), n_arcs).
@@ -95,14 +113,16 @@ def colgraph_solve(c: np.ndarray, delta, input_is_weight: bool = False, algo: st
     mask = np.zeros((X, Y, Z), np.uint8) if want_mask else None
     checks = np.zeros(1, np.int32)
     n_arcs = np.zeros(1, np.int64)
-    dx, dy = (int(delta[0]), int(delta[1])) if isinstance(delta, (tuple, list)) else (int(delta), -1)
+    dl4 = np.array(deltas4(delta), np.int32)
     pen = np.ascontiguousarray(penalty, dtype=np.int32) if penalty is not None else None
-    st = lib.oracle_colgraph_solve_soft(_ptr(c, ctypes.c_int32), X, Y, Z, dx, dy,
-                                   _ptr(pen, ctypes.c_int32) if pen is not None else None,
-                                   len(pen) if pen is not None else 0, int(bool(input_is_weight)),
-                                   ALGOS[algo], _ptr(flow, ctypes.c_int64), _ptr(surface, ctypes.c_int32),
-                                   _ptr(mask, ctypes.c_uint8) if want_mask else None,
-                                   _ptr(checks, ctypes.c_int32), _ptr(n_arcs, ctypes.c_int64))
+    bnd = np.ascontiguousarray(band, dtype=np.int32).reshape(X * Y * 2) if band is not None else None
+    st = lib.oracle_colgraph_solve_general(_ptr(c, ctypes.c_int32), X, Y, Z, _ptr(dl4, ctypes.c_int32),
+                                           _ptr(bnd, ctypes.c_int32) if bnd is not None else None,
+                                           _ptr(pen, ctypes.c_int32) if pen is not None else None,
+                                           len(pen) if pen is not None else 0, int(bool(input_is_weight)),
+                                           ALGOS[algo], _ptr(flow, ctypes.c_int64), _ptr(surface, ctypes.c_int32),
+                                           _ptr(mask, ctypes.c_uint8) if want_mask else None,
+                                           _ptr(checks, ctypes.c_int32), _ptr(n_arcs, ctypes.c_int64))
     return {"status": int(st), "flow": int(flow[0]), "surface": surface, "mask": mask,
             "checks": int(checks[0]), "n_arcs": int(n_arcs[0])}
 

@@ -114,9 +114,28 @@ static void column_weights(const int32_t *c, int64_t Z, int64_t col, int64_t *w)
     for (int64_t z = 1; z < Z; z++) w[z] = (int64_t)cc[z] - (int64_t)cc[z - 1];
 }
 
+/* Narrow band (the graphs are narrow bands around
+ * landmarks): the surface of column col is confined to [lo, hi).  The base rule R1 applies to the
+ * band: w(lo) = c(lo) - (sum_{lo <= z < hi} c(z) + 1), w(z) = c(z) - c(z-1) for lo < z < hi, and
+ * every vertex outside the band has no terminal arc (w = 0).  The infinite down arcs put the
+ * vertices below the band into every source set that contains (col, lo), i.e. every one, and no
+ * arc of the original graph leads into the vertices above the band from below, so the minimal
+ * source set never contains them: S(col) = max{z in S} lies in [lo, hi). */
+static void column_weights_band(const int32_t *c, int64_t Z, int64_t col, int32_t lo, int32_t hi, int64_t *w) {
+    const int32_t *cc = c + col * Z;
+    int64_t sum = 0;
+    for (int64_t z = lo; z < hi; z++) sum += cc[z];
+    for (int64_t z = 0; z < Z; z++) w[z] = 0;
+    w[lo] = (int64_t)cc[lo] - (sum + 1);
+    for (int64_t z = lo + 1; z < hi; z++) w[z] = (int64_t)cc[z] - (int64_t)cc[z - 1];
+}
+
 /* Inter-column arcs (x,y,z) -> (x',y',max(0,z-Delta_d)): the edge interval toward the
- * adjacent column in direction d, Delta_x for the x-neighbours and Delta_y for
- * the y-neighbours (Delta_x = Delta_y is the paper's isotropic case). */
+ * adjacent column in direction d.  dl[d] for d = +x, -x, +y, -y: the arc of p
+ * toward its neighbour q in direction d encodes S(p) - S(q) <= dl[d], so the pair (p, q = p + x)
+ * has S(q) - S(p) in [-dl[+x], dl[-x]] -- a general (possibly asymmetric) proper-ordered edge
+ * interval; dl = {D, D, D, D} is the paper's isotropic case and
+ * {Dx, Dx, Dy, Dy} the anisotropic one. */
 /* Soft smoothness (VCE-weight net surface): a convex
  * penalty f(d) for |S(p) - S(q)| = d adds finite arcs (x,y,z) -> (x',y',z-k), k = 0..Delta_d-1,
  * z-k >= 0, with capacity c_0 = f(1), c_k = f(k+1) - 2f(k) + f(k-1): the arc is cut for
@@ -132,8 +151,8 @@ static int64_t soft_cap(int k) {
     return k == 0 ? f1 : f1 - 2 * f0 + fm;
 }
 
-static void colgraph_arcs(graph_t *g, int pass, const int32_t *in, int X, int Y, int Z, int delta, int delta_y,
-                          int input_is_weight, int64_t *wbuf) {
+static void colgraph_arcs(graph_t *g, int pass, const int32_t *in, int X, int Y, int Z, const int32_t *dl4,
+                          const int32_t *band, int input_is_weight, int64_t *wbuf) {
     const int64_t n = (int64_t)X * Y * Z, s = n, t = n + 1;
     const int dx[4] = {+1, -1, 0, 0}, dy[4] = {0, 0, +1, -1};
     for (int64_t x = 0; x < X; x++)
@@ -141,6 +160,8 @@ static void colgraph_arcs(graph_t *g, int pass, const int32_t *in, int X, int Y,
             int64_t col = x * Y + y;
             if (input_is_weight) {
                 for (int64_t z = 0; z < Z; z++) wbuf[z] = in[col * Z + z];
+            } else if (band) {
+                column_weights_band(in, Z, col, band[2 * col], band[2 * col + 1], wbuf);
             } else {
                 column_weights(in, Z, col, wbuf);
             }
@@ -152,7 +173,7 @@ static void colgraph_arcs(graph_t *g, int pass, const int32_t *in, int X, int Y,
                 for (int d = 0; d < 4; d++) {
                     int64_t x2 = x + dx[d], y2 = y + dy[d];
                     if (x2 < 0 || x2 >= X || y2 < 0 || y2 >= Y) continue;
-                    const int64_t dl = d < 2 ? delta : delta_y;
+                    const int64_t dl = dl4[d];
                     const int64_t zt = z - dl > 0 ? z - dl : 0;
                     add_arc(g, pass, v, (x2 * Y + y2) * Z + zt, OR_INF);
                     for (int64_t k = 0; g_penalty && k < dl && z - k >= 0; k++) {
@@ -344,12 +365,40 @@ int oracle_colgraph_solve(const int32_t *in, int X, int Y, int Z, int delta, int
                                       surface_out, mask_out, checks_out, n_arcs_out);
 }
 
+int oracle_colgraph_solve_general(const int32_t *in, int X, int Y, int Z, const int32_t *dl4, const int32_t *band,
+                                  const int32_t *penalty, int npenalty, int input_is_weight, int algo,
+                                  int64_t *flow_out, int32_t *surface_out, uint8_t *mask_out, int32_t *checks_out,
+                                  int64_t *n_arcs_out);
+
 int oracle_colgraph_solve_soft(const int32_t *in, int X, int Y, int Z, int delta, int delta_y, const int32_t *penalty,
                                int npenalty, int input_is_weight, int algo, int64_t *flow_out, int32_t *surface_out,
                                uint8_t *mask_out, int32_t *checks_out, int64_t *n_arcs_out) {
     if (delta_y == -1) delta_y = delta; /* isotropic */
-    if (!in || X < 1 || Y < 1 || Z < 1 || delta < 0 || delta_y < 0) return OR_E_INVAL;
-    if (penalty && npenalty < (delta > delta_y ? delta : delta_y)) return OR_E_INVAL;
+    const int32_t dl4[4] = {delta, delta, delta_y, delta_y};
+    return oracle_colgraph_solve_general(in, X, Y, Z, dl4, NULL, penalty, npenalty, input_is_weight, algo, flow_out,
+                                         surface_out, mask_out, checks_out, n_arcs_out);
+}
+
+/*
+ * General entry (NEXT-3): dl4[4] = Delta toward +x, -x, +y, -y (see colgraph_arcs); band nullable
+ * int32[2*X*Y] = (lo, hi) per column, 0 <= lo < hi <= Z, costs only (see column_weights_band).
+ */
+int oracle_colgraph_solve_general(const int32_t *in, int X, int Y, int Z, const int32_t *dl4, const int32_t *band,
+                                  const int32_t *penalty, int npenalty, int input_is_weight, int algo,
+                                  int64_t *flow_out, int32_t *surface_out, uint8_t *mask_out, int32_t *checks_out,
+                                  int64_t *n_arcs_out) {
+    if (!in || !dl4 || X < 1 || Y < 1 || Z < 1) return OR_E_INVAL;
+    int dmax = 0;
+    for (int d = 0; d < 4; d++) {
+        if (dl4[d] < 0) return OR_E_INVAL;
+        if (dl4[d] > dmax) dmax = dl4[d];
+    }
+    if (band) {
+        if (input_is_weight) return OR_E_INVAL;
+        for (int64_t col = 0; col < (int64_t)X * Y; col++)
+            if (band[2 * col] < 0 || band[2 * col] >= band[2 * col + 1] || band[2 * col + 1] > Z) return OR_E_INVAL;
+    }
+    if (penalty && npenalty < dmax) return OR_E_INVAL;
     g_penalty = penalty;
     g_npenalty = npenalty;
     if (penalty) /* convex, non-negative capacities */
@@ -362,9 +411,9 @@ int oracle_colgraph_solve_soft(const int32_t *in, int X, int Y, int Z, int delta
     int64_t *wbuf = (int64_t *)malloc((size_t)Z * sizeof(int64_t));
     uint8_t *mark = (uint8_t *)malloc((size_t)n + 2);
     if (!wbuf || !mark || g_alloc(&g, n + 2)) { free(wbuf); free(mark); return OR_E_NOMEM; }
-    colgraph_arcs(&g, 0, in, X, Y, Z, delta, delta_y, input_is_weight, wbuf);
+    colgraph_arcs(&g, 0, in, X, Y, Z, dl4, band, input_is_weight, wbuf);
     if (g_finish_count(&g)) { g_free(&g); free(wbuf); free(mark); return OR_E_NOMEM; }
-    colgraph_arcs(&g, 1, in, X, Y, Z, delta, delta_y, input_is_weight, wbuf);
+    colgraph_arcs(&g, 1, in, X, Y, Z, dl4, band, input_is_weight, wbuf);
     if (n_arcs_out) *n_arcs_out = g.m / 2;
     int64_t flow = run_maxflow(&g, s, t, algo, &err);
     if (err) { g_free(&g); free(wbuf); free(mark); return err; }

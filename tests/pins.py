@@ -15,6 +15,9 @@ reproduce:
   * closed-form cases Delta >= Z-1 (independent columns) and Delta = 0 (flat).
   * soft smoothness (NEXT-1, PAPER.md:42-43 VCE-weight net surface): brute force and line DP
     with the cost sum c(x,y,S) + sum over 4-neighbour pairs of f(|S(p) - S(q)|).
+  * general edge intervals and narrow bands (NEXT-3; PAPER.md:42 proper ordering, PAPER.md:456
+    narrow bands): surfaces with S(q) - S(p) in [-d(+x), d(-x)] for q = p + x (likewise y) and
+    S(p) in [lo(p), hi(p)); k0_band restates the construction constant for the band rule.
   * brute_force_mincut -- all s-t cuts of a small general graph (PAPER.md
     Eq. 6 and Theorem 1), their minimum and the intersection of all minimum
     source sets (the minimal source set).
@@ -37,6 +40,83 @@ def _dxy(delta):
     """delta: int (isotropic) or (delta_x, delta_y) -- the edge interval toward x- and
     y-neighbours."""
     return (int(delta[0]), int(delta[1])) if isinstance(delta, (tuple, list)) else (int(delta), int(delta))
+
+
+def _d4(delta):
+    """(+x, -x, +y, -y) edge intervals: int, (dx, dy) or a 4-tuple."""
+    if isinstance(delta, (tuple, list)) and len(delta) == 4:
+        return tuple(int(d) for d in delta)
+    dx, dy = _dxy(delta)
+    return (dx, dx, dy, dy)
+
+
+def enumerate_surfaces_general(X: int, Y: int, Z: int, delta, band=None) -> np.ndarray:
+    """All feasible top assignments (K, X*Y) under the general interval: for q = p + x,
+    S(p) - S(q) <= d(+x) (p's arc toward +x) and S(q) - S(p) <= d(-x) (q's arc toward -x); the same
+    with y.  band (X, Y, 2): S(p) in [lo, hi)."""
+    dpx, dmx, dpy, dmy = _d4(delta)
+    cur = np.zeros((1, 0), dtype=np.int16)
+    for col in range(X * Y):
+        x, y = divmod(col, Y)
+        lo, hi = (int(band[x, y, 0]), int(band[x, y, 1])) if band is not None else (0, Z)
+        vals = np.arange(lo, hi, dtype=np.int16)
+        K = cur.shape[0]
+        new = np.repeat(cur, len(vals), axis=0)
+        v = np.tile(vals, K).astype(np.int64)
+        ok = np.ones(len(v), dtype=bool)
+        if x > 0:
+            p = new[:, (x - 1) * Y + y].astype(np.int64)
+            ok &= (p - v <= dpx) & (v - p <= dmx)
+        if y > 0:
+            p = new[:, x * Y + y - 1].astype(np.int64)
+            ok &= (p - v <= dpy) & (v - p <= dmy)
+        cur = np.concatenate([new[ok], v[ok, None].astype(np.int16)], axis=1)
+    return cur
+
+
+def brute_force_general(c: np.ndarray, delta, band=None):
+    """(min cost, lowest optimal surface, number of feasible surfaces) under general intervals / bands."""
+    X, Y, Z = c.shape
+    S = enumerate_surfaces_general(X, Y, Z, delta, band)
+    cols = c.reshape(X * Y, Z).astype(np.int64)
+    cost = cols[np.arange(X * Y)[None, :], S.astype(np.int64)].sum(axis=1)
+    best = cost.min()
+    opt = S[cost == best]
+    return int(best), opt.min(axis=0).reshape(X, Y).astype(np.int32), int(len(S))
+
+
+def k0_band(c: np.ndarray, band) -> int:
+    """|f| = min cost + K0 under the band rule: the cut of the closed set {z <= S(p)} is
+    N + sum_{v in S} w(v) (Eq. 6 with source capacities -w, sink capacities w), the band weights
+    telescope to c(p, S(p)) - (sum_{band} c + 1) per column, and N = sum max(0, -w)."""
+    X, Y, Z = c.shape
+    cc = c.astype(np.int64)
+    N, const = 0, 0
+    for x in range(X):
+        for y in range(Y):
+            lo, hi = int(band[x, y, 0]), int(band[x, y, 1])
+            col = cc[x, y, lo:hi]
+            w = np.empty(hi - lo, np.int64)
+            w[0] = col[0] - (col.sum() + 1)
+            w[1:] = col[1:] - col[:-1]
+            N += int(np.maximum(-w, 0).sum())
+            const += int(col.sum() + 1)
+    return N - const
+
+
+def band_consistent(band, delta) -> bool:
+    """The band reading's precondition (R15): for every neighbour pair and direction, the
+    lower and the upper band limits move by no more than the edge interval allows."""
+    dpx, dmx, dpy, dmy = _d4(delta)
+    lo, hi = band[..., 0].astype(np.int64), band[..., 1].astype(np.int64)
+    ok = True
+    if band.shape[0] > 1:
+        dlo, dhi = lo[1:] - lo[:-1], hi[1:] - hi[:-1]
+        ok &= bool(((-dlo <= dpx) & (dlo <= dmx) & (-dhi <= dpx) & (dhi <= dmx)).all())
+    if band.shape[1] > 1:
+        dlo, dhi = lo[:, 1:] - lo[:, :-1], hi[:, 1:] - hi[:, :-1]
+        ok &= bool(((-dlo <= dpy) & (dlo <= dmy) & (-dhi <= dpy) & (dhi <= dmy)).all())
+    return ok
 
 
 def enumerate_surfaces(X: int, Y: int, Z: int, delta, allow_empty: bool = False) -> np.ndarray:

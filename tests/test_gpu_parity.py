@@ -228,14 +228,39 @@ def test_certificate_c2(cg):
 
 
 def test_determinism(cg):
+    """100 solves of C2 (lock-free schedules differ run to run): the value, surface and minimal
+    source set must not (SURVEY.md §4 item 6 stress)."""
     c = V.generate("C2")
-    ref = None
-    for _ in range(5):
+    o = oracle.colgraph_solve(c, 3)
+    key0 = (o["flow"], hashlib.sha256(o["surface"].tobytes()).hexdigest(), hashlib.sha256(o["mask"].tobytes()).hexdigest())
+    works = set()
+    for _ in range(100):
         r = gpu(cg, c, 3)
         key = (r["flow"], hashlib.sha256(r["surface"].tobytes()).hexdigest(),
                hashlib.sha256(r["mask"].tobytes()).hexdigest())
-        ref = ref or key
-        assert key == ref
+        assert key == key0
+        works.add(r["stats"]["work"])
+    assert len(works) > 1  # the schedules really differed
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_certificate_full_size(cg, name):
+    """The O(n) max-preflow certificate (capacities, exact conservation, no residual path from excess
+    to t) on the exported state of a full-size solve in the bench's launch configuration."""
+    spec = V.CONFIGS[name]
+    c = V.generate(name)
+    t = torch.from_numpy(c).cuda()
+    h = cg.colgraph_build(t, spec.delta)
+    try:
+        st, flow, stats = cg.maxflow_solve(h, None)
+        assert st == 0
+        out = torch.empty(8 * c.size, dtype=torch.int32, device="cuda")
+        assert cg.colgraph_export_state(h, out) == 0
+        state = out.cpu().numpy()
+    finally:
+        cg.colgraph_free(h)
+    del t
+    _certificate(c, spec.delta, state)
 
 
 @pytest.mark.parametrize("kw", [dict(gap_every=4), dict(ops_per_sweep=4), dict(gr_factor=0.25),
