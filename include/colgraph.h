@@ -207,6 +207,31 @@ cg_status colgraph_build_slabs_soft(const cg_dims *dims, const int32_t *cost_dev
                                     const int32_t *penalty, int32_t npenalty, int32_t nslabs, const cg_dist *dist,
                                     cg_graph **out);
 
+/* NEXT-3 -- general proper-ordered edge intervals and narrow bands; the most
+ * general builder (also soft smoothness and in-process slabs).
+ *   dl4      : HOST int32[4] (nullable = from dims): the edge interval toward +x, -x, +y, -y.  The
+ *              lateral arc of (x,y,z) toward direction d lands at z - dl4[d], i.e. S(p) - S(q) <=
+ *              dl4[d] for the neighbour q of p in direction d, so the pair (p, q = p + x) has
+ *              S(q) - S(p) in [-dl4[0], dl4[1]] (and y likewise): the edge interval of PAPER.md:42
+ *              per adjacent column, possibly asymmetric.  {D, D, D, D} is colgraph_build's
+ *              isotropic case, {Dx, Dx, Dy, Dy} its anisotropic one.  Each >= 0.
+ *   band_dev : DEVICE int32[2 * X_r * Y] (nullable): (lo, hi) per column of this rank's slab (the
+ *              whole volume with nslabs >= 1), 0 <= lo < hi <= Z: the narrow band the surface of
+ *              that column is confined to (PAPER.md:456, 475 -- the paper's graphs are narrow bands
+ *              around landmarks; reading R15).  The base rule applies inside the band
+ *              (w(lo) = c(lo) - (sum_{lo<=z<hi} c + 1), w(z) = c(z) - c(z-1)); vertices outside get
+ *              no terminal arc, so the infinite down arcs keep the ones below the band in S and
+ *              nothing pulls the ones above it in: S(x,y) lies in [lo, hi) when the bands move by no
+ *              more than the intervals between neighbours.  Storage stays X*Y*Z (no compaction).
+ *              Costs only (input_is_weight = 1 with a band: CG_E_INVAL).  Copied into the handle.
+ *   penalty, npenalty : as colgraph_build_soft (NULL / 0 = hard only; npenalty >= max dl4).
+ *   nslabs   : >= 1 -- in-process x-slabs as colgraph_build_slabs (cost_dev / band_dev whole-volume);
+ *              0 -- one slab per process as colgraph_build (dist.nranks > 1: NCCL ranks).
+ * Errors: as colgraph_build; CG_E_INVAL for a negative interval or an invalid band. */
+cg_status colgraph_build_general(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight,
+                                 const int32_t *dl4, const int32_t *band_dev, const int32_t *penalty, int32_t npenalty,
+                                 int32_t nslabs, const cg_dist *dist, cg_graph **out);
+
 /* Fill id_out (128 bytes) with a fresh ncclUniqueId for colgraph_build's cg_dist.nccl_id
  * (rank 0 calls it and broadcasts the bytes, e.g. with torch.distributed).
  * Errors: CG_E_INVAL (NULL), CG_E_NCCL (libnccl.so.2 not loadable). */

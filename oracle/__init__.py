@@ -38,7 +38,7 @@ CHECK_BITS = {
     "cut_eq_flow": 1 << 5,
 }
 ALL_CHECKS = sum(CHECK_BITS.values())
-ALGOS = {"dinic": 0, "ek": 1}
+ALGOS = {"dinic": 0, "ek": 1, "pr": 2}
 
 
 def build(force: bool = False) -> str:

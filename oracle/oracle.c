@@ -338,15 +338,122 @@ static int check_invariants(const graph_t *g, int64_t s, int64_t t, const uint8_
     return ok;
 }
 
+/*
+ * Push-relabel (Goldberg-Tarjan; §2.1: labels, push, relabel, global
+ * relabeling), textbook FIFO form in two phases so that it ends with a maximum FLOW:
+ *   phase 1: labels d(v) = residual distance to t (exact by a global relabel -- BFS from t over
+ *            reverse residual arcs -- at the start and after every n relabels); a vertex with
+ *            excess and d(v) < n pushes on admissible arcs (residual > 0, d(v) = d(w) + 1), else
+ *            relabels to 1 + min d(w) over residual arcs; ends when no vertex below n is active,
+ *            i.e. with a maximum preflow;
+ *   phase 2: the same with s as the terminal (labels = residual distance to s, by BFS from s over
+ *            reverse residual arcs): every remaining excess returns to s, giving a maximum flow.
+ * Slower to state than Dinitz but its work on column graphs does not grow with the number of
+ * distinct augmenting-path lengths (C5's Dinitz run needs thousands of phases).  The result is
+ * certified like the others (check_invariants: Eq. 2-5, Theorem 1) and pinned by the same tests.
+ */
+/* Exact labels: residual distance to `root` (t in phase 1, s in phase 2); the other terminal
+ * gets n (never a push target: nothing flows into s in phase 1, or into t in phase 2).  In phase 2
+ * excess reaches s only by cancelling flow on an arc s -> u (the reverse slot u -> s, capacity 0),
+ * never over an original arc into s, so no flow enters s (as with augmenting paths). */
+static void pr_global(const graph_t *g, int64_t root, int64_t other, int phase2, int64_t n, int64_t *d,
+                      int32_t *queue) {
+    for (int64_t i = 0; i < g->nn; i++) d[i] = n;  /* n: cannot reach root */
+    int64_t qh = 0, qt = 0;
+    d[root] = 0;
+    queue[qt++] = (int32_t)root;
+    while (qh < qt) {
+        const int64_t v = queue[qh++];
+        for (int64_t a = g->first[v]; a < g->first[v + 1]; a++) {
+            const int64_t u = g->head[a], ua = g->rev[a]; /* arc ua: u -> v */
+            if (u == other || d[u] != n || g->res[ua] <= 0) continue;
+            if (phase2 && v == root && g->cap[ua] > 0) continue;
+            d[u] = d[v] + 1;
+            queue[qt++] = (int32_t)u;
+        }
+    }
+    d[other] = n;
+}
+
+static int pr_phase(graph_t *g, int64_t s, int64_t t, int phase2, int64_t *ex, int64_t *d, int64_t *cur,
+                    int32_t *fifo, uint8_t *inq, int32_t *bfsq) {
+    const int64_t n = g->nn, term = phase2 ? s : t, other = phase2 ? t : s;
+    int64_t qh = 0, qt = 0, work = 0;
+    pr_global(g, term, other, phase2, n, d, bfsq);
+    for (int64_t v = 0; v < n; v++) {
+        cur[v] = g->first[v];
+        inq[v] = 0;
+        if (v != s && v != t && ex[v] > 0 && d[v] < n) { fifo[qt++ % n] = (int32_t)v; inq[v] = 1; }
+    }
+    while (qh != qt) {
+        const int64_t v = fifo[qh++ % n];
+        inq[v] = 0;
+        while (ex[v] > 0 && d[v] < n) {
+            if (cur[v] == g->first[v + 1]) {        /* relabel */
+                int64_t m = 2 * n;
+                for (int64_t a = g->first[v]; a < g->first[v + 1]; a++)
+                    if (g->res[a] > 0 && d[g->head[a]] + 1 < m && !(phase2 && g->head[a] == s && g->cap[a] > 0))
+                        m = d[g->head[a]] + 1;
+                d[v] = m < n ? m : n;
+                cur[v] = g->first[v];
+                if (++work >= n) {                  /* periodic global relabel */
+                    work = 0;
+                    pr_global(g, term, other, phase2, n, d, bfsq);
+                    for (int64_t u = 0; u < n; u++) cur[u] = g->first[u];
+                }
+                continue;
+            }
+            const int64_t a = cur[v], w = g->head[a];
+            if (g->res[a] > 0 && d[v] == d[w] + 1 && !(phase2 && w == s && g->cap[a] > 0)) { /* push */
+                const int64_t f = ex[v] < g->res[a] ? ex[v] : g->res[a];
+                g->res[a] -= f;
+                g->res[g->rev[a]] += f;
+                ex[v] -= f;
+                ex[w] += f;
+                if (w != s && w != t && !inq[w] && d[w] < n) { fifo[qt++ % n] = (int32_t)w; inq[w] = 1; }
+            } else {
+                cur[v]++;
+            }
+        }
+    }
+    return 0;
+}
+
+static int64_t push_relabel(graph_t *g, int64_t s, int64_t t, int *err) {
+    const int64_t n = g->nn;
+    int64_t *ex = (int64_t *)calloc((size_t)n, sizeof(int64_t));
+    int64_t *d = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    int64_t *cur = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    int32_t *fifo = (int32_t *)malloc((size_t)n * sizeof(int32_t));
+    int32_t *bfsq = (int32_t *)malloc((size_t)n * sizeof(int32_t));
+    uint8_t *inq = (uint8_t *)malloc((size_t)n);
+    int64_t flow = 0;
+    if (!ex || !d || !cur || !fifo || !bfsq || !inq) { *err = OR_E_NOMEM; goto done; }
+    for (int64_t a = g->first[s]; a < g->first[s + 1]; a++) { /* saturate the source arcs */
+        const int64_t f = g->res[a];
+        if (f <= 0) continue;
+        g->res[a] -= f;
+        g->res[g->rev[a]] += f;
+        ex[g->head[a]] += f;
+        ex[s] -= f;
+    }
+    pr_phase(g, s, t, 0, ex, d, cur, fifo, inq, bfsq); /* phase 1: maximum preflow */
+    pr_phase(g, s, t, 1, ex, d, cur, fifo, inq, bfsq); /* phase 2: excess back to s */
+    flow = ex[t];
+done:
+    free(ex); free(d); free(cur); free(fifo); free(bfsq); free(inq);
+    return flow;
+}
+
 static int64_t run_maxflow(graph_t *g, int64_t s, int64_t t, int algo, int *err) {
-    return algo == 1 ? edmonds_karp(g, s, t, err) : dinic(g, s, t, err);
+    return algo == 1 ? edmonds_karp(g, s, t, err) : algo == 2 ? push_relabel(g, s, t, err) : dinic(g, s, t, err);
 }
 
 /*
  * Column-graph oracle.
  *   in[X*Y*Z]       int32 costs c[x][y][z] (z fastest), or vertex weights if input_is_weight
  *   delta, delta_y  smoothness toward x- / y-neighbours (delta_y = -1: same as delta)
- *   algo            0 = Dinitz, 1 = Edmonds-Karp
+ *   algo            0 = Dinitz, 1 = Edmonds-Karp, 2 = two-phase FIFO push-relabel
  *   flow_out        |f| (int64)
  *   surface_out     int32[X*Y], max z in S per column, -1 if none (nullable)
  *   mask_out        uint8[X*Y*Z], 1 if the vertex is in the minimal source set (nullable)

@@ -83,6 +83,10 @@ def _load():
                                          P(ctypes.c_void_p)]
     lib.cg_nccl_unique_id.restype = ctypes.c_int
     lib.cg_nccl_unique_id.argtypes = [ctypes.c_void_p]
+    lib.colgraph_build_general.restype = ctypes.c_int
+    lib.colgraph_build_general.argtypes = [P(cg_dims), ctypes.c_void_p, ctypes.c_int32, P(ctypes.c_int32),
+                                           ctypes.c_void_p, P(ctypes.c_int32), ctypes.c_int32, ctypes.c_int32,
+                                           P(cg_dist), P(ctypes.c_void_p)]
     lib.cg_nccl_loopback.restype = ctypes.c_int
     lib.cg_nccl_loopback.argtypes = [ctypes.c_int32]
     lib.maxflow_solve.restype = ctypes.c_int
@@ -112,7 +116,7 @@ def _load():
 
 _lib = _load()
 
-EXPORTED = ["colgraph_build", "colgraph_build_slabs", "colgraph_build_soft", "colgraph_build_slabs_soft", "cg_nccl_unique_id", "cg_nccl_loopback", "maxflow_solve", "mincut_extract_surface",
+EXPORTED = ["colgraph_build", "colgraph_build_slabs", "colgraph_build_soft", "colgraph_build_slabs_soft", "colgraph_build_general", "cg_nccl_unique_id", "cg_nccl_loopback", "maxflow_solve", "mincut_extract_surface",
             "maxflow_export_flow", "colgraph_solve_host",
             "colgraph_export_state", "colgraph_stats", "colgraph_free", "cg_status_str", "cg_slab_range", "cg_version"]
 
@@ -207,6 +211,47 @@ def colgraph_build(cost, delta: int, input_is_weight: bool = False, stream=None,
                              ctypes.byref(h))
     if st != CG_OK:
         raise ColgraphError(st, "colgraph_build")
+    return h
+
+
+def deltas4(delta):
+    """Edge intervals toward (+x, -x, +y, -y) from an int, (delta_x, delta_y) or a 4-tuple."""
+    if isinstance(delta, (tuple, list)):
+        if len(delta) == 4:
+            return tuple(int(d) for d in delta)
+        dx, dy = int(delta[0]), int(delta[1])
+        dy = dx if dy == -1 else dy
+        return (dx, dx, dy, dy)
+    return (int(delta),) * 4
+
+
+def colgraph_build_general(cost, delta, band=None, penalty=None, nslabs: int = 0, input_is_weight: bool = False,
+                           stream=None, rank=0, nranks=1, nccl_id=None, dims=None):
+    """NEXT-3 (include/colgraph.h colgraph_build_general): delta int / (dx, dy) / (d+x, d-x, d+y, d-y);
+    band: CUDA int32 tensor [X_r, Y, 2] (lo, hi) per column or None; penalty: soft smoothness or None;
+    nslabs >= 1: in-process x-slabs; else one slab per process (nranks > 1: NCCL)."""
+    _check_dev_int32(cost, "cost")
+    if band is not None:
+        _check_dev_int32(band, "band")
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(cost.device)
+    d4 = deltas4(delta)
+    if dims is None:
+        X, Y, Z = cost.shape
+        dims = cg_dims(X, Y, Z, d4[0], d4[2])
+    dl = (ctypes.c_int32 * 4)(*d4)
+    pen = (ctypes.c_int32 * len(penalty))(*[int(v) for v in penalty]) if penalty is not None else None
+    h = ctypes.c_void_p()
+    idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
+    st = _lib.colgraph_build_general(ctypes.byref(dims), ctypes.c_void_p(cost.data_ptr()), int(bool(input_is_weight)),
+                                     dl, ctypes.c_void_p(band.data_ptr()) if band is not None else None,
+                                     pen, len(penalty) if penalty is not None else 0, int(nslabs),
+                                     ctypes.byref(_dist(cost.device.index, ctypes.c_void_p(stream.cuda_stream), rank,
+                                                        nranks, ctypes.cast(idbuf, ctypes.c_void_p)
+                                                        if idbuf is not None else None)), ctypes.byref(h))
+    if st != CG_OK:
+        raise ColgraphError(st, "colgraph_build_general")
     return h
 
 
@@ -338,13 +383,15 @@ def cg_slab_range(X: int, Y: int, Z: int, delta: int, rank: int, nranks: int):
 
 
 def solve(cost, delta: int, input_is_weight: bool = False, want_mask: bool = True, opts=None, nslabs: int = 1,
-          penalty=None):
+          penalty=None, band=None):
     """Device-resident convenience: build -> solve -> extract on a CUDA int32 tensor
     (nslabs > 1: the in-process x-slab path).
     Returns dict(status, extract_status, flow, surface (tensor), mask (tensor), stats)."""
     import torch
     X, Y, Z = cost.shape
-    if penalty is not None:
+    if band is not None or (isinstance(delta, (tuple, list)) and len(delta) == 4):
+        h = colgraph_build_general(cost, delta, band, penalty, nslabs if nslabs > 1 else 0, input_is_weight)
+    elif penalty is not None:
         h = colgraph_build_soft(cost, delta, penalty, input_is_weight) if nslabs == 1 else \
             colgraph_build_slabs_soft(cost, delta, penalty, nslabs, input_is_weight)
     else:

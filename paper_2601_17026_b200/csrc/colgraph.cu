@@ -70,6 +70,7 @@ struct Slab {
     uint8_t *gflags = nullptr;             // column-fixpoint relabel: residual-arc flags, same range
     ColGrState *cst = nullptr, *h_cst = nullptr;
     int colgr_grid = 0;                    // > 0: cooperative grid of k_colgr_run
+    int32_t *band = nullptr;               // narrow band (lo, hi) per column (NEXT-3), device copy; null = none
     unsigned long long *u64 = nullptr;   // [0]=N [1]=sumT0 [2]=sumT [3]=active [4]=gap lifted [5]=scratch
     int *flags = nullptr;                // [0]=overflow [1]=maxh [2]=gap [3]=empty
     int32_t *snap[2] = {nullptr, nullptr};   // ghost lateral residual at the last refresh
@@ -291,7 +292,7 @@ size_t workspace_bytes(const Geo &geo) {
     b += 4 * al(sizeof(int32_t) * geo.YZ) + 4 * al(sizeof(int32_t) * halo_msg_ints(geo));
     b += 5 * al(sizeof(int) * ncol) + al(sizeof(unsigned) * 4) + al(sizeof(unsigned long long) * RING) +
          al(sizeof(unsigned long long) * 16) + al(sizeof(unsigned) * RING) + al(sizeof(unsigned) * (geo.n / 32 + 1));
-    b += al(sizeof(int32_t) * plane) + al(plane) + al(sizeof(ColGrState));
+    b += al(sizeof(int32_t) * plane) + al(plane) + al(sizeof(ColGrState)) + al(sizeof(int32_t) * 2 * ncol);
     return b;
 }
 
@@ -303,7 +304,7 @@ void slab_free(Slab *sl) {
 }
 
 // Allocate and initialise a slab, then run a1 (k_build) on its x-range of cost_dev.
-cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode) {
+cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode, const int32_t *band_dev) {
     const Geo &geo = sl->geo;
     cudaStream_t st = sl->stream;
     const int64_t n = geo.n, ncol = (int64_t)geo.X * geo.Y, plane = (int64_t)(geo.X + 2) * geo.YZ;
@@ -378,6 +379,10 @@ cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode) {
     sl->lab = carve<int32_t>(p, plane) + geo.YZ;
     sl->gflags = carve<uint8_t>(p, plane) + geo.YZ;
     sl->cst = carve<ColGrState>(p, 1);
+    {
+        int32_t *bnd = carve<int32_t>(p, 2 * ncol);
+        sl->band = band_dev ? bnd : nullptr;
+    }
     for (int side = 0; side < 2; side++) {
         sl->snap[side] = carve<int32_t>(p, geo.YZ);
         sl->hold[side] = carve<int32_t>(p, geo.YZ);
@@ -386,12 +391,14 @@ cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode) {
     }
     // everything starts at zero (E, T written by k_build; heights set by the first relabel)
     CG_CUDA(cudaMemsetAsync(sl->ws, 0, bytes, st));
-    k_build<<<grid_for(ncol * 32, 256, sl->num_sms * 16), 256, 0, st>>>(geo, cost_dev, weight_mode, sl->s, sl->u64,
+    if (sl->band) CG_CUDA(cudaMemcpyAsync(sl->band, band_dev, sizeof(int32_t) * 2 * ncol, cudaMemcpyDeviceToDevice, st));
+    k_build<<<grid_for(ncol * 32, 256, sl->num_sms * 16), 256, 0, st>>>(geo, cost_dev, weight_mode, sl->band, sl->s, sl->u64,
                                                                         sl->flags);
     CG_CUDA(cudaGetLastError());
     CG_CUDA(cudaMemcpyAsync(sl->h_u64, sl->u64, sizeof(unsigned long long) * 2, cudaMemcpyDeviceToHost, st));
     CG_CUDA(cudaMemcpyAsync(sl->h_flags, sl->flags, sizeof(int), cudaMemcpyDeviceToHost, st));
     CG_CUDA(cudaStreamSynchronize(st));
+    if (sl->h_flags[0] & FLAG_BAD_BAND) return CG_E_INVAL;
     if (sl->h_flags[0] & FLAG_OVERFLOW) return CG_E_OVERFLOW;
     sl->N = (int64_t)sl->h_u64[0];
     sl->sumT0 = (int64_t)sl->h_u64[1];
@@ -916,13 +923,13 @@ bool tile_setup(Slab *sl, int steps, int relabel_every) {
     return true;
 }
 
-Geo make_geo(const cg_dims *dims, int x0, int x1, int nranks_total, bool gl, bool gh, int64_t n_global) {
+Geo make_geo(const cg_dims *dims, const int32_t *dl4, int x0, int x1, int nranks_total, bool gl, bool gh,
+             int64_t n_global) {
     Geo geo{};
     geo.X = x1 - x0;
     geo.Y = dims->Y;
     geo.Z = dims->Z;
-    geo.delta = dims->delta;
-    geo.delta_y = dims->delta_y < 0 ? dims->delta : dims->delta_y;
+    for (int d = 0; d < 4; d++) geo.dl[d] = dl4[d];
     geo.CPC = (dims->Z + 31) / 32;
     geo.gl = gl;
     geo.gh = gh;
@@ -1268,13 +1275,24 @@ void colgraph_free(cg_graph *g) {
 // Common constructor: `nslabs_local` slabs in this process starting at global slab `rank`.
 static cg_status build_common(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight,
                               const cg_dist *dist, int nranks, int rank, int nslabs_local, bool local,
-                              cg_graph **out, const int32_t *penalty = nullptr, int32_t npenalty = 0) {
+                              cg_graph **out, const int32_t *penalty = nullptr, int32_t npenalty = 0,
+                              const int32_t *dl4_in = nullptr, const int32_t *band_dev = nullptr) {
     CG_TRY(validate_dims(dims));
+    // edge intervals toward +x, -x, +y, -y (NEXT-3): from dims unless given
+    int32_t dl4[4];
+    {
+        const int32_t dy = dims->delta_y < 0 ? dims->delta : dims->delta_y;
+        const int32_t def[4] = {dims->delta, dims->delta, dy, dy};
+        for (int d = 0; d < 4; d++) {
+            dl4[d] = dl4_in ? dl4_in[d] : def[d];
+            if (dl4[d] < 0) return CG_E_INVAL;
+        }
+    }
+    if (band_dev && input_is_weight) return CG_E_INVAL;  // bands apply to the cost rule
     // soft smoothness (NEXT-1): capacities c_0 = f(1), c_k = f(k+1) - 2 f(k) + f(k-1) >= 0
     int32_t soft_k = 0, soft_cap[SOFT_KMAX] = {0};
     if (penalty) {
-        const int dy = dims->delta_y < 0 ? dims->delta : dims->delta_y;
-        soft_k = std::max(dims->delta, dy);
+        soft_k = std::max(std::max(dl4[0], dl4[1]), std::max(dl4[2], dl4[3]));
         if (npenalty < soft_k || soft_k > SOFT_KMAX) return CG_E_INVAL;
         for (int k = 0; k < soft_k; k++) {
             const int64_t f1 = penalty[k], f0 = k >= 1 ? penalty[k - 1] : 0, fm = k >= 2 ? penalty[k - 2] : 0;
@@ -1334,13 +1352,15 @@ static cg_status build_common(const cg_dims *dims, const int32_t *cost_dev, int3
         }
         sl->x0 = x0;
         sl->x1 = x1;
-        sl->geo = make_geo(dims, x0, x1, nranks, r > 0, r + 1 < nranks, g->n_global);
+        sl->geo = make_geo(dims, dl4, x0, x1, nranks, r > 0, r + 1 < nranks, g->n_global);
         sl->geo.soft_k = soft_k;
         for (int k = 0; k < SOFT_KMAX; k++) sl->geo.soft_cap[k] = soft_cap[k];
         g->slabs.push_back(sl);
         // LOCAL: cost_dev is the whole volume; NCCL / single: this rank's slab
         const int32_t *src = local ? cost_dev + (int64_t)x0 * sl->geo.YZ : cost_dev;
-        const cg_status s = slab_build(sl, src, input_is_weight ? 1 : 0);
+        // band: whole-volume array in LOCAL mode, this rank's slab otherwise (2 ints per column)
+        const int32_t *bsrc = band_dev ? (local ? band_dev + (int64_t)x0 * dims->Y * 2 : band_dev) : nullptr;
+        const cg_status s = slab_build(sl, src, input_is_weight ? 1 : 0, bsrc);
         if (s != CG_OK) return fail(s);
     }
     int64_t fl = 0;
@@ -1435,6 +1455,20 @@ cg_status colgraph_build_slabs_soft(const cg_dims *dims, const int32_t *cost_dev
     if (!penalty || npenalty < 1 || nslabs < 1) return CG_E_INVAL;
     return debug_check(build_common(dims, cost_dev, input_is_weight, dist, nslabs, 0, nslabs, true, out, penalty,
                                     npenalty));
+}
+
+cg_status colgraph_build_general(const cg_dims *dims, const int32_t *cost_dev, int32_t input_is_weight,
+                                 const int32_t *dl4, const int32_t *band_dev, const int32_t *penalty, int32_t npenalty,
+                                 int32_t nslabs, const cg_dist *dist, cg_graph **out) {
+    if (nslabs < 0 || (penalty && npenalty < 1)) return CG_E_INVAL;
+    if (nslabs >= 1)
+        return debug_check(build_common(dims, cost_dev, input_is_weight, dist, nslabs, 0, nslabs, true, out, penalty,
+                                        npenalty, dl4, band_dev));
+    cg_dist dd{0, 1, nullptr, 0, nullptr};
+    if (dist) dd = *dist;
+    if (dd.nranks < 1 || dd.rank < 0 || dd.rank >= dd.nranks) return CG_E_INVAL;
+    return debug_check(build_common(dims, cost_dev, input_is_weight, &dd, dd.nranks, dd.rank, 1, false, out, penalty,
+                                    npenalty, dl4, band_dev));
 }
 
 cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_value, cg_solve_stats *stats) {
@@ -1573,9 +1607,8 @@ static cg_status maxflow_export_flow_impl(cg_graph *g, const int32_t *cost_dev, 
         // phase 2 (NEXT-2): the terminal becomes s -- T(v) := flow on s->v, the phase-1 sink
         // residuals are parked in tmp.  Vertices with excess cannot reach t (maximum preflow),
         // so no flow into t changes.
-        k_phase2_setup<<<grid_for(ncol * 32, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(geo, src,
-                                                                                           input_is_weight ? 1 : 0,
-                                                                                           sl->s, tmp[i]);
+        k_phase2_setup<<<grid_for(ncol * 32, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(
+            geo, src, input_is_weight ? 1 : 0, sl->band, sl->s, tmp[i]);
         g->st.kernel_launches++;
     }
     CG_CUDA(cudaGetLastError());
@@ -1589,7 +1622,8 @@ static cg_status maxflow_export_flow_impl(cg_graph *g, const int32_t *cost_dev, 
         // x-slabs: a halo exchange after every pass delivers the excess cancelled into ghost
         // vertices (and the consumed ghost residuals) before the owner reaches that level.
         constexpr int SAME_LEVEL_PASSES = 64;
-        const bool flat = g0.delta == 0 || g0.delta_y == 0 || (g0.soft_k > 0 && g0.soft_cap[0] > 0);
+        const bool flat = g0.dl[0] == 0 || g0.dl[1] == 0 || g0.dl[2] == 0 || g0.dl[3] == 0 ||
+                          (g0.soft_k > 0 && g0.soft_cap[0] > 0);
         for (int z = 0; z < g0.Z && r == CG_OK; z++) {
             const bool same_level = z == 0 || flat;
             for (Slab *sl : g->slabs)
@@ -1652,7 +1686,7 @@ static cg_status maxflow_export_flow_impl(cg_graph *g, const int32_t *cost_dev, 
             int32_t *dst = g->local ? flow_dev + (int64_t)sl->x0 * geo.YZ : flow_dev;
             CG_CUDA(cudaMemsetAsync(sl->flags + 3, 0, sizeof(int), sl->stream));
             k_flow_export<<<grid_for(ncol * 32, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(
-                geo, src, input_is_weight ? 1 : 0, sl->s, tmp[i], dst, plane_stride, sl->flags + 3);
+                geo, src, input_is_weight ? 1 : 0, sl->band, sl->s, tmp[i], dst, plane_stride, sl->flags + 3);
             g->st.kernel_launches++;
             CG_CUDA(cudaMemcpyAsync(sl->h_flags + 3, sl->flags + 3, sizeof(int), cudaMemcpyDeviceToHost, sl->stream));
         }

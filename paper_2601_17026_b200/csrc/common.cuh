@@ -16,8 +16,10 @@ namespace cg {
 constexpr unsigned FULL = 0xffffffffu;
 
 struct Geo {
-    int32_t X, Y, Z, delta;  // X = x-planes owned by this slab; delta = Delta_x (toward x-neighbours)
-    int32_t delta_y;         // Delta_y (toward y-neighbours); = delta in the isotropic case
+    int32_t X, Y, Z;         // X = x-planes owned by this slab
+    int32_t dl[4];           // edge interval toward +x, -x, +y, -y: v's lateral arc in direction d lands
+                             // at z - dl[d] (S(v) - S(nbr_d(v)) <= dl[d], NEXT-3); the
+                             // isotropic case has all four equal
     int32_t CPC;             // chunks per column = ceil(Z / 32)
     int32_t gl, gh;          // a ghost plane exists at x = -1 (gl) / x = X (gh): neighbour slab
     int64_t n;               // vertices owned by this slab
@@ -97,7 +99,7 @@ constexpr int64_t NONE = INT64_MIN;  // "no vertex" (ghost vertices of the x = -
 
 __device__ __forceinline__ bool owned(const Geo &g, int64_t v) { return v >= 0 && v < g.n; }
 
-enum { FLAG_OVERFLOW = 1 };
+enum { FLAG_OVERFLOW = 1, FLAG_BAD_BAND = 2 };
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ unsigned lanemask_lt() { return (1u << lane_id()) - 1u; }
@@ -108,8 +110,12 @@ __device__ __forceinline__ int64_t nwarps() { return ((int64_t)gridDim.x * block
 // lateral in-arc of (x,y,z) per direction comes from (nbr, zi(z)).
 __device__ __forceinline__ int zo_of(int z, int delta) { return z == 0 ? 0 : (z > delta ? z - delta : -1); }
 __device__ __forceinline__ int zi_of(int z, int delta, int Z) { return z == 0 ? 0 : (z + delta < Z ? z + delta : -1); }
-// edge interval toward direction d (0:+x 1:-x 2:+y 3:-y): Delta_x or Delta_y (NEXT-3)
-__device__ __forceinline__ int delta_d(const Geo &g, int d) { return d < 2 ? g.delta : g.delta_y; }
+// edge intervals (NEXT-3): dl_out(d) is that of v's own lateral arc toward direction d (0:+x 1:-x
+// 2:+y 3:-y); dl_in(d) that of the arc INTO v from its neighbour in direction d, i.e. the
+// neighbour's arc toward d^1 -- the in-arc of (x,y,z) from direction d leaves (nbr_d, zi(z)) with
+// zi computed from dl_in(d)
+__device__ __forceinline__ int dl_out(const Geo &g, int d) { return g.dl[d]; }
+__device__ __forceinline__ int dl_in(const Geo &g, int d) { return g.dl[d ^ 1]; }
 
 // neighbour column offset (in vertices) in direction d, 0 if the neighbour is outside the slab
 __device__ __forceinline__ int64_t nbr_off(const Geo &g, int x, int y, int d) {

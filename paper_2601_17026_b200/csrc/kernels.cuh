@@ -25,25 +25,49 @@ namespace cg {
 #endif
 
 // ------------------------------------------------------------------ a1: build
-// One warp per column: w(0) = c(0) - (sum_z c + 1), w(z) = c(z) - c(z-1) (R1).
-// E = max(0,-w): source arcs pre-saturated (Goldberg-Tarjan init);
-// T = max(0, w): sink-arc residual.  Totals N = sum E and sum T0 in int64.
-__global__ void k_build(Geo g, const int32_t *__restrict__ in, int weight_mode, Soa s,
-                        unsigned long long *sums /* [0]=N [1]=sum T0 */, int *flags) {
+// Vertex weights of one column (warp-collective): w(0) = c(0) - (sum_z c + 1), w(z) = c(z) - c(z-1)
+// (R1); with a narrow band [lo, hi) (NEXT-3, reading R15) the rule applies to the band
+// (w(lo) = c(lo) - (sum_{lo<=z<hi} c + 1)) and vertices outside it get w = 0; weight mode takes w as
+// given.  k_build, the phase-2 setup and the flow export all recompute w with these two functions.
+struct ColW {
+    int lo, hi;
+    long long colsum;
+    bool bad;  // invalid band (lo < 0, lo >= hi or hi > Z)
+};
+__device__ __forceinline__ ColW col_w_setup(const int32_t *cc, int Z, const int32_t *band, int64_t col, int weight_mode) {
+    ColW w{0, Z, 0, false};
+    if (band) {
+        w.lo = band[2 * col];
+        w.hi = band[2 * col + 1];
+        w.bad = w.lo < 0 || w.lo >= w.hi || w.hi > Z;
+        if (w.bad) w.lo = 0, w.hi = Z;
+    }
+    if (!weight_mode) {
+        long long cs = 0;
+        for (int z = w.lo + lane_id(); z < w.hi; z += 32) cs += cc[z];
+        w.colsum = warp_sum_ll(cs);
+    }
+    return w;
+}
+__device__ __forceinline__ long long col_w(const int32_t *cc, int z, const ColW &w, int weight_mode) {
+    if (weight_mode) return cc[z];
+    if (z < w.lo || z >= w.hi) return 0;
+    return z == w.lo ? (long long)cc[z] - (w.colsum + 1) : (long long)cc[z] - (long long)cc[z - 1];
+}
+
+// One warp per column.  E = max(0,-w): source arcs pre-saturated (Goldberg-Tarjan init,
+// PAPER.md:134); T = max(0, w): sink-arc residual.  Totals N = sum E and sum T0 in int64.
+__global__ void k_build(Geo g, const int32_t *__restrict__ in, int weight_mode, const int32_t *__restrict__ band,
+                        Soa s, unsigned long long *sums /* [0]=N [1]=sum T0 */, int *flags) {
     const int64_t ncol = (int64_t)g.X * g.Y;
     long long accN = 0, accT = 0;
-    bool bad = false;
+    bool bad = false, badband = false;
     for (int64_t col = gwarp(); col < ncol; col += nwarps()) {
         const int32_t *cc = in + col * g.Z;
-        long long colsum = 0;
-        if (!weight_mode) {
-            for (int z = lane_id(); z < g.Z; z += 32) colsum += cc[z];
-            colsum = warp_sum_ll(colsum);
-        }
+        const ColW cw = col_w_setup(cc, g.Z, band, col, weight_mode);
+        badband |= cw.bad;
         for (int z = lane_id(); z < g.Z; z += 32) {
-            long long w;
-            if (weight_mode) w = cc[z];
-            else w = z == 0 ? (long long)cc[0] - (colsum + 1) : (long long)cc[z] - (long long)cc[z - 1];
+            const long long w = col_w(cc, z, cw, weight_mode);
             const bool ok = w <= INT_MAX && w >= -(long long)INT_MAX;
             bad |= !ok;
             const int32_t e = (ok && w < 0) ? (int32_t)(-w) : 0, t = (ok && w > 0) ? (int32_t)w : 0;
@@ -60,31 +84,22 @@ __global__ void k_build(Geo g, const int32_t *__restrict__ in, int weight_mode, 
         if (accT) atomicAdd(&sums[1], (unsigned long long)accT);
     }
     if (bad) atomicOr(flags, FLAG_OVERFLOW);
+    if (badband) atomicOr(flags, FLAG_BAD_BAND);
 }
 
 // ------------------------------------------------------------------ NEXT-2: phase 2 + flow export
-// Vertex weights are recomputed from the caller's input exactly as k_build does (one warp
-// per column) to recover the source / sink capacities E0 = max(0,-w), T0 = max(0,w).
-__device__ __forceinline__ long long column_sum(const int32_t *cc, int Z) {
-    long long colsum = 0;
-    for (int z = lane_id(); z < Z; z += 32) colsum += cc[z];
-    return warp_sum_ll(colsum);
-}
-
-__device__ __forceinline__ long long weight_of(const int32_t *cc, int z, long long colsum, int weight_mode) {
-    if (weight_mode) return cc[z];
-    return z == 0 ? (long long)cc[0] - (colsum + 1) : (long long)cc[z] - (long long)cc[z - 1];
-}
-
+// Vertex weights are recomputed from the caller's input exactly as k_build does (one warp per
+// column) to recover the source / sink capacities E0 = max(0,-w), T0 = max(0,w).
 // tmp = phase-1 sink residual T; T := E0 (flow on the saturated source arc s->v)
-__global__ void k_phase2_setup(Geo g, const int32_t *__restrict__ in, int weight_mode, Soa s, int32_t *tmp) {
+__global__ void k_phase2_setup(Geo g, const int32_t *__restrict__ in, int weight_mode, const int32_t *__restrict__ band,
+                               Soa s, int32_t *tmp) {
     const int64_t ncol = (int64_t)g.X * g.Y;
     for (int64_t col = gwarp(); col < ncol; col += nwarps()) {
         const int32_t *cc = in + col * g.Z;
-        const long long colsum = weight_mode ? 0 : column_sum(cc, g.Z);
+        const ColW cw = col_w_setup(cc, g.Z, band, col, weight_mode);
         for (int z = lane_id(); z < g.Z; z += 32) {
             const int64_t v = col * g.Z + z;
-            const long long w = weight_of(cc, z, colsum, weight_mode);
+            const long long w = col_w(cc, z, cw, weight_mode);
             tmp[v] = s.T[v];
             s.T[v] = w < 0 ? (int32_t)(-w) : 0;
         }
@@ -124,7 +139,7 @@ __global__ void k_return_level(Geo g, Soa s, int z, unsigned *left) {
 #pragma unroll
         for (int d = 0; d < 4 && e > 0; d++) {
             const int64_t o = nbr_off(g, x, y, d);
-            const int zi = zi_of(z, delta_d(g, d), g.Z);
+            const int zi = zi_of(z, dl_in(g, d), g.Z);
             if (!o || zi < 0) continue;
             const int64_t u = col * g.Z + o + zi;  // may be a ghost vertex: the halo delivers E(u)
             cancel(&s.L[d ^ 1][u], &s.E[u]);
@@ -132,7 +147,7 @@ __global__ void k_return_level(Geo g, Soa s, int z, unsigned *left) {
         for (int d = 0; d < 4 && e > 0 && g.soft_k; d++) {  // soft inflows from (nbr, z + k), level >= z
             const int64_t o = nbr_off(g, x, y, d);
             if (!o) continue;
-            const int kmax = min(g.soft_k, delta_d(g, d));
+            const int kmax = min(g.soft_k, dl_in(g, d));  // the neighbour's soft arcs toward d^1
             for (int k = 0; k < kmax && e > 0; k++) {
                 if (z + k >= g.Z) break;
                 const int64_t u = col * g.Z + o + z + k;
@@ -157,7 +172,8 @@ __global__ void k_net_level(Geo g, Soa s, int z) {
         const int x = (int)(col / g.Y), y = (int)(col - (int64_t)x * g.Y);
 #pragma unroll
         for (int d = 0; d < 4; d += 2) {
-            if (zo_of(z, delta_d(g, d)) != z) continue;  // the arc leaves the level
+            // both antiparallel arcs must stay on the level (z = 0, or a zero interval each way)
+            if (zo_of(z, dl_out(g, d)) != z || zo_of(z, dl_in(g, d)) != z) continue;
             const int64_t o = nbr_off(g, x, y, d);
             if (!o || !owned(g, v + o)) continue;
             const int a = s.L[d][v], b = s.L[d ^ 1][v + o];
@@ -169,7 +185,7 @@ __global__ void k_net_level(Geo g, Soa s, int z) {
         }
 #pragma unroll
         for (int d = 0; d < 4; d += 2) {  // soft arcs with k = 0 stay on the level
-            if (!g.soft_k || g.soft_cap[0] <= 0 || delta_d(g, d) < 1) continue;
+            if (!g.soft_k || g.soft_cap[0] <= 0 || dl_out(g, d) < 1 || dl_in(g, d) < 1) continue;
             const int64_t o = nbr_off(g, x, y, d);
             if (!o || !owned(g, v + o)) continue;
             int32_t *fa = soft_flow(g, s, v, d, 0), *fb = soft_flow(g, s, v + o, d ^ 1, 0);
@@ -193,16 +209,16 @@ __global__ void k_count_excess(Geo g, const Soa s, unsigned *count) {
 
 // out planes (int32[7][n]): s->v, v->t, down v->v-1, lateral +x, -x, +y, -y.  Any vertex left
 // with excess sets *bad (the result would not be a flow).
-__global__ void k_flow_export(Geo g, const int32_t *__restrict__ in, int weight_mode, Soa s,
-                              const int32_t *__restrict__ tmp, int32_t *out, int64_t n, int *bad) {
+__global__ void k_flow_export(Geo g, const int32_t *__restrict__ in, int weight_mode, const int32_t *__restrict__ band,
+                              Soa s, const int32_t *__restrict__ tmp, int32_t *out, int64_t n, int *bad) {
     const int64_t ncol = (int64_t)g.X * g.Y;  // n: plane stride of out (whole volume for in-process slabs)
     bool b = false;
     for (int64_t col = gwarp(); col < ncol; col += nwarps()) {
         const int32_t *cc = in + col * g.Z;
-        const long long colsum = weight_mode ? 0 : column_sum(cc, g.Z);
+        const ColW cw = col_w_setup(cc, g.Z, band, col, weight_mode);
         for (int z = lane_id(); z < g.Z; z += 32) {
             const int64_t v = col * g.Z + z;
-            const long long w = weight_of(cc, z, colsum, weight_mode);
+            const long long w = col_w(cc, z, cw, weight_mode);
             const int32_t t0 = w > 0 ? (int32_t)w : 0;
             out[v] = s.T[v];
             out[n + v] = t0 - tmp[v];
@@ -241,7 +257,8 @@ __global__ void k_export(F f, int64_t n, int32_t *out) {
 // read is a lower bound of what the reader may subtract.
 struct OpCtx {
     int64_t v, v0, col;
-    int z, zo[2], zi[2];  // [0]: toward x-neighbours (Delta_x), [1]: y-neighbours (Delta_y)
+    int z, zo[4], zi[4];  // per direction d: target level of v's lateral arc (dl_out) and source
+                          // level of the lateral in-arc (dl_in); -1 = none
     int64_t off[4];  // vertex offset of the neighbour column (0 = none)
 };
 
@@ -270,7 +287,8 @@ constexpr int ARC_SOFT_FWD = 11, ARC_SOFT_REV = 75;
 __device__ __noinline__ void scan_soft(const Geo &g, const Soa &s, const OpCtx &c, int hx, ArcPick &p) {
     for (int d = 0; d < 4; d++) {
         if (!c.off[d]) continue;
-        const int kmax = min(g.soft_k, delta_d(g, d));
+        // forward soft arcs of v toward d: k < dl_out(d); reverse of the neighbour's arcs toward d^1: k < dl_in(d)
+        const int kf = min(g.soft_k, dl_out(g, d)), kr = min(g.soft_k, dl_in(g, d)), kmax = max(kf, kr);
 #if CG_SOFT_GATHER
         // four offsets k at a time: their soft-flow values in one round of loads, then the
         // heights of the targets with residual in another (instead of one dependent chain per arc)
@@ -280,8 +298,8 @@ __device__ __noinline__ void scan_soft(const Geo &g, const Soa &s, const OpCtx &
             for (int j = 0; j < 4; j++) {
                 const int k = k0 + j;
                 const int cap = k < kmax ? g.soft_cap[k] : 0;
-                rf[j] = (cap > 0 && c.z - k >= 0) ? cap - *soft_flow(g, s, c.v, d, k) : 0;
-                rr[j] = (cap > 0 && c.z + k < g.Z) ? *soft_flow(g, s, c.v0 + c.off[d] + c.z + k, d ^ 1, k) : 0;
+                rf[j] = (cap > 0 && k < kf && c.z - k >= 0) ? cap - *soft_flow(g, s, c.v, d, k) : 0;
+                rr[j] = (cap > 0 && k < kr && c.z + k < g.Z) ? *soft_flow(g, s, c.v0 + c.off[d] + c.z + k, d ^ 1, k) : 0;
             }
 #pragma unroll
             for (int j = 0; j < 4; j++) {
@@ -306,7 +324,7 @@ __device__ __noinline__ void scan_soft(const Geo &g, const Soa &s, const OpCtx &
         for (int k = 0; k < kmax; k++) {
             const int cap = g.soft_cap[k];
             if (cap <= 0) continue;
-            if (c.z - k >= 0) {  // forward
+            if (k < kf && c.z - k >= 0) {  // forward
                 const int r = cap - *soft_flow(g, s, c.v, d, k);
                 if (r > 0) {
                     const int64_t t = c.v0 + c.off[d] + c.z - k;
@@ -315,7 +333,7 @@ __device__ __noinline__ void scan_soft(const Geo &g, const Soa &s, const OpCtx &
                     if (p.best < hx) return;
                 }
             }
-            if (c.z + k < g.Z) {  // reverse of the arc of u = (nbr_d, z+k) toward this column
+            if (k < kr && c.z + k < g.Z) {  // reverse of the arc of u = (nbr_d, z+k) toward this column
                 const int64_t u = c.v0 + c.off[d] + c.z + k;
                 const int r = *soft_flow(g, s, u, d ^ 1, k);
                 if (r > 0) {
@@ -370,10 +388,10 @@ __device__ __forceinline__ ArcPick scan_arcs_hard(const Geo &g, const Soa &s, co
     bool oko[4], oki[4];
 #pragma unroll
     for (int d = 0; d < 4; d++) {
-        oko[d] = c.off[d] && c.zo[d >> 1] >= 0;
-        oki[d] = c.off[d] && c.zi[d >> 1] >= 0;
-        to[d] = c.v0 + c.off[d] + c.zo[d >> 1];
-        ti[d] = c.v0 + c.off[d] + c.zi[d >> 1];
+        oko[d] = c.off[d] && c.zo[d] >= 0;
+        oki[d] = c.off[d] && c.zi[d] >= 0;
+        to[d] = c.v0 + c.off[d] + c.zo[d];
+        ti[d] = c.v0 + c.off[d] + c.zi[d];
     }
     // stage 1: the arcs that are usually admissible (t, down, lateral-out), loaded together
     const int tres = s.T[c.v];
@@ -458,8 +476,8 @@ __device__ __forceinline__ ArcPick scan_arcs_hard(const Geo &g, const Soa &s, co
         int h4[4];
 #pragma unroll
         for (int d = 0; d < 4; d++) {
-            const bool ok = c.off[d] && c.zo[d >> 1] >= 0;
-            t4[d] = c.v0 + c.off[d] + c.zo[d >> 1];
+            const bool ok = c.off[d] && c.zo[d] >= 0;
+            t4[d] = c.v0 + c.off[d] + c.zo[d];
             h4[d] = ok ? s.H[t4[d]] : g.INF;
         }
 #if CG_SCAN_LAT_ONE  // all eight lateral records in one round
@@ -467,8 +485,8 @@ __device__ __forceinline__ ArcPick scan_arcs_hard(const Geo &g, const Soa &s, co
         int r4[4], hi4[4];
 #pragma unroll
         for (int d = 0; d < 4; d++) {
-            const bool ok = c.off[d] && c.zi[d >> 1] >= 0;
-            ti4[d] = c.v0 + c.off[d] + c.zi[d >> 1];
+            const bool ok = c.off[d] && c.zi[d] >= 0;
+            ti4[d] = c.v0 + c.off[d] + c.zi[d];
             r4[d] = ok ? s.L[d ^ 1][ti4[d]] : 0;
             hi4[d] = ok ? s.H[ti4[d]] : g.INF;
         }
@@ -482,8 +500,8 @@ __device__ __forceinline__ ArcPick scan_arcs_hard(const Geo &g, const Soa &s, co
         int r4[4], hi4[4];
 #pragma unroll
         for (int d = 0; d < 4; d++) {
-            const bool ok = c.off[d] && c.zi[d >> 1] >= 0;
-            ti4[d] = c.v0 + c.off[d] + c.zi[d >> 1];
+            const bool ok = c.off[d] && c.zi[d] >= 0;
+            ti4[d] = c.v0 + c.off[d] + c.zi[d];
             r4[d] = ok ? s.L[d ^ 1][ti4[d]] : 0;
             hi4[d] = ok ? s.H[ti4[d]] : g.INF;
         }
@@ -494,11 +512,11 @@ __device__ __forceinline__ ArcPick scan_arcs_hard(const Geo &g, const Soa &s, co
         return p;
     }
 #endif
-    if (c.zo[0] >= 0 || c.zo[1] >= 0) {
+    if (c.zo[0] >= 0 || c.zo[1] >= 0 || c.zo[2] >= 0 || c.zo[3] >= 0) {
 #pragma unroll
         for (int d = 0; d < 4; d++) {
-            if (!c.off[d] || c.zo[d >> 1] < 0) continue;
-            const int64_t t = c.v0 + c.off[d] + c.zo[d >> 1];
+            if (!c.off[d] || c.zo[d] < 0) continue;
+            const int64_t t = c.v0 + c.off[d] + c.zo[d];
             const int hh = s.H[t];
             if (hh < p.best) { p.best = hh; p.arc = 2 + d; p.tgt = t; }
             if (p.best < hx) return p;
@@ -514,11 +532,11 @@ __device__ __forceinline__ ArcPick scan_arcs_hard(const Geo &g, const Soa &s, co
         }
     }
 #endif
-    if (c.zi[0] >= 0 || c.zi[1] >= 0) {
+    if (c.zi[0] >= 0 || c.zi[1] >= 0 || c.zi[2] >= 0 || c.zi[3] >= 0) {
 #pragma unroll
         for (int d = 0; d < 4; d++) {
-            if (!c.off[d] || c.zi[d >> 1] < 0) continue;
-            const int64_t u = c.v0 + c.off[d] + c.zi[d >> 1];
+            if (!c.off[d] || c.zi[d] < 0) continue;
+            const int64_t u = c.v0 + c.off[d] + c.zi[d];
             const int r = s.L[d ^ 1][u];
             if (r > 0) {
                 const int hh = s.H[u];
@@ -537,10 +555,11 @@ __device__ __forceinline__ void set_ctx(const Geo &g, OpCtx &c, int64_t v) {
     c.z = (int)(v - c.col * g.Z);
     c.v0 = c.col * g.Z;
     const int x = (int)(c.col / g.Y), y = (int)(c.col - (int64_t)x * g.Y);
-    c.zo[0] = zo_of(c.z, g.delta);
-    c.zo[1] = zo_of(c.z, g.delta_y);
-    c.zi[0] = zi_of(c.z, g.delta, g.Z);
-    c.zi[1] = zi_of(c.z, g.delta_y, g.Z);
+#pragma unroll
+    for (int d = 0; d < 4; d++) {
+        c.zo[d] = zo_of(c.z, dl_out(g, d));
+        c.zi[d] = zi_of(c.z, dl_in(g, d), g.Z);
+    }
 #pragma unroll
     for (int d = 0; d < 4; d++) c.off[d] = nbr_off(g, x, y, d);
 }
@@ -898,7 +917,9 @@ __device__ __noinline__ void bfs_soft_preds(const Geo &g, const Soa &s, int64_t 
     };
     for (int d = 0; d < 4; d++) {
         const int64_t o = has ? nbr_off(g, x, y, d) : 0;
-        const int kmax = min(g.soft_k, delta_d(g, d));
+        // wu's forward arc (d^1, k) into v exists for k < dl_in(d); v's own arc (d, k) for k < dl_out(d)
+        const int kin = min(g.soft_k, dl_in(g, d)), kout = min(g.soft_k, dl_out(g, d));
+        const int kmax = max(kin, kout);
         for (int k = 0; k < kmax; k++) {
             const int cap = g.soft_cap[k];
             bool up = false, dn = false;
@@ -906,10 +927,10 @@ __device__ __noinline__ void bfs_soft_preds(const Geo &g, const Soa &s, int64_t 
             if (o && cap > 0) {
                 // MODE 1 (strict) also claims ghost vertices: the owner learns the label through
                 // the ghost plane; ghosts are never listed here
-                up = z + k < g.Z && (MODE == 1 || owned(g, wu)) && cap - *soft_flow(g, s, wu, d ^ 1, k) > 0 &&
-                     claim(wu) && owned(g, wu);
-                dn = z - k >= 0 && (MODE == 1 || owned(g, wd)) && *soft_flow(g, s, v, d, k) > 0 && claim(wd) &&
-                     owned(g, wd);
+                up = k < kin && z + k < g.Z && (MODE == 1 || owned(g, wu)) &&
+                     cap - *soft_flow(g, s, wu, d ^ 1, k) > 0 && claim(wu) && owned(g, wu);
+                dn = k < kout && z - k >= 0 && (MODE == 1 || owned(g, wd)) && *soft_flow(g, s, v, d, k) > 0 &&
+                     claim(wd) && owned(g, wd);
             }
             warp_append(up, (int)wu, lout, cout);
             warp_append(dn, (int)wd, lout, cout);
@@ -927,8 +948,6 @@ __device__ __forceinline__ void bfs_expand_warp(const Geo &g, const Soa &s, int 
         const int z = (int)(v - col * g.Z);
         const int x = (int)(col / g.Y), y = (int)(col - (int64_t)x * g.Y);
         const int64_t v0 = col * g.Z;
-        const int zox = zo_of(z, g.delta), zix = zi_of(z, g.delta, g.Z);
-        const int zoy = zo_of(z, g.delta_y), ziy = zi_of(z, g.delta_y, g.Z);
         // all candidate predecessors and their labels first (independent loads in flight
         // together), then CAS only the unlabelled ones: one latency chain per vertex
         int w[10];  // vertex indices fit int32 (validate_dims: n + ghosts < 2^31)
@@ -939,7 +958,7 @@ __device__ __forceinline__ void bfs_expand_warp(const Geo &g, const Soa &s, int 
         for (int d = 0; d < 4; d++) {
             const int64_t o = nbr_off(g, x, y, d);
             if (!o) continue;
-            const int zi = d < 2 ? zix : ziy, zo = d < 2 ? zox : zoy;
+            const int zi = zi_of(z, dl_in(g, d), g.Z), zo = zo_of(z, dl_out(g, d));
             if (zi >= 0) { w[2 + d] = (int)(v0 + o + zi); cand |= 1u << (2 + d); }
             if (zo >= 0 && s.L[d][v] > 0) {
                 w[6 + d] = (int)(v0 + o + zo);
@@ -1011,8 +1030,6 @@ __device__ __forceinline__ void bfs_expand_multi(const Geo &g, const Soa &s, int
         const int z = v - col * g.Z;
         const int x = col / g.Y, y = col - x * g.Y;
         const int v0 = col * g.Z;
-        const int zox = zo_of(z, g.delta), zix = zi_of(z, g.delta, g.Z);
-        const int zoy = zo_of(z, g.delta_y), ziy = zi_of(z, g.delta_y, g.Z);
         int D, L[4];
         if (FL) {
             const unsigned f = __ldg(&flags[v]);
@@ -1028,7 +1045,7 @@ __device__ __forceinline__ void bfs_expand_multi(const Geo &g, const Soa &s, int
         for (int d = 0; d < 4; d++) {
             const int o = (int)nbr_off(g, x, y, d);
             if (!o) continue;
-            const int zi = d < 2 ? zix : ziy, zo = d < 2 ? zox : zoy;
+            const int zi = zi_of(z, dl_in(g, d), g.Z), zo = zo_of(z, dl_out(g, d));
             if (zi >= 0 && owned(g, v0 + o + zi)) { w[r][2 + d] = v0 + o + zi; cand[r] |= 1u << (2 + d); }
             if (zo >= 0 && L[d] > 0 && owned(g, v0 + o + zo)) { w[r][6 + d] = v0 + o + zo; cand[r] |= 1u << (6 + d); }
         }
@@ -1538,25 +1555,26 @@ __global__ void __launch_bounds__(256) k_ext_round(Geo g, Soa s, const int *__re
             const int z = zb + lane_id();
 #pragma unroll
             for (int d = 0; d < 4; d++) {
-                const int zi = z <= t ? zi_of(z, delta_d(g, d), g.Z) : -1;
+                const int zi = z <= t ? zi_of(z, dl_in(g, d), g.Z) : -1;
                 if (zi >= 0 && nc[d] != INT64_MIN && s.L[d ^ 1][nc[d] * g.Z + zi] > 0) cd[d] = max(cd[d], zi);
             }
             if (g.soft_k && z <= t)  // soft arcs with residual (NEXT-1)
                 for (int d = 0; d < 4; d++) {
                     if (nc[d] == INT64_MIN) continue;
-                    const int kmax = min(g.soft_k, delta_d(g, d));
-                    for (int k = 0; k < kmax; k++) {
+                    const int kout = min(g.soft_k, dl_out(g, d)), kin = min(g.soft_k, dl_in(g, d));
+                    for (int k = 0; k < max(kout, kin); k++) {
                         const int cap = g.soft_cap[k];
                         if (cap <= 0) continue;
-                        if (z - k >= 0 && cap - *soft_flow(g, s, v0 + z, d, k) > 0) cd[d] = max(cd[d], z - k);
-                        if (z + k < g.Z && *soft_flow(g, s, nc[d] * g.Z + z + k, d ^ 1, k) > 0) cd[d] = max(cd[d], z + k);
+                        if (k < kout && z - k >= 0 && cap - *soft_flow(g, s, v0 + z, d, k) > 0) cd[d] = max(cd[d], z - k);
+                        if (k < kin && z + k < g.Z && *soft_flow(g, s, nc[d] * g.Z + z + k, d ^ 1, k) > 0)
+                            cd[d] = max(cd[d], z + k);
                     }
                 }
         }
         int mark = -1;
 #pragma unroll
         for (int d = 0; d < 4; d++) {
-            const int zout = t > delta_d(g, d) ? t - delta_d(g, d) : 0;
+            const int zout = t > dl_out(g, d) ? t - dl_out(g, d) : 0;
             const int cand = max(warp_max_i(cd[d]), zout);
             if (lane_id() == d && nc[d] != INT64_MIN) {
                 const int old = atomicMax(&top[nc[d]], cand);

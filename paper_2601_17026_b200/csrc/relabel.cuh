@@ -119,8 +119,7 @@ __device__ __forceinline__ bool colgr_update(const Geo &g, const uint8_t *__rest
             unsigned fi[4];
 #pragma unroll
             for (int d = 0; d < 4; d++) {
-                const int dl = d < 2 ? g.delta : g.delta_y;
-                const int zo = zo_of(z, dl), zi = zi_of(z, dl, Z);
+                const int zo = zo_of(z, dl_out(g, d)), zi = zi_of(z, dl_in(g, d), Z);
                 const int64_t u0 = v0 + off[d];
                 lo[d] = off[d] && zo >= 0 ? __ldcg(&lab[u0 + zo]) : INF;
                 li[d] = off[d] && zi >= 0 ? __ldcg(&lab[u0 + zi]) : INF;

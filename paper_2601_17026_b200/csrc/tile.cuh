@@ -214,7 +214,7 @@ __device__ __forceinline__ void local_relabel(const Geo &g, const TileGeo &t, co
                 for (int dd = 0; dd < 4; dd++) {
                     const int nb = cc.nb[dd];
                     if (nb == NB_NONE || nb >= 0) continue;  // halo exits only
-                    const int zo = zo_of(z, delta_d(g, dd)), zi = zi_of(z, delta_d(g, dd), Z);
+                    const int zo = zo_of(z, dl_out(g, dd)), zi = zi_of(z, dl_in(g, dd), Z);
                     if (zo >= 0) {
                         const int hh = op.nH(nb, zo);
                         if (hh < g.INF) b = min(b, hh + 1);
@@ -256,7 +256,7 @@ __device__ __forceinline__ void local_relabel(const Geo &g, const TileGeo &t, co
                 for (int dd = 0; dd < 4; dd++) {
                     const int nb = cc.nb[dd];
                     if (nb < 0) continue;  // tile neighbours only (halo exits are in base)
-                    const int zo = zo_of(z, delta_d(g, dd)), zi = zi_of(z, delta_d(g, dd), Z);
+                    const int zo = zo_of(z, dl_out(g, dd)), zi = zi_of(z, dl_in(g, dd), Z);
                     if (zo >= 0) b = min(b, tsm[m.H + (nb * t.CS + tpos<S>(zo, t.P))] + 1);
                     if (zi >= 0 && tsm[m.L0 + (dd ^ 1) * m.ncs + (nb * t.CS + tpos<S>(zi, t.P))] > 0)
                         b = min(b, tsm[m.H + (nb * t.CS + tpos<S>(zi, t.P))] + 1);
@@ -296,7 +296,7 @@ __device__ __forceinline__ int min_nbr_label(const Geo &g, const TileOps<S> &op,
     for (int d = 0; d < 4; d++) {
         const int nb = cc.nb[d];
         if (nb == NB_NONE) continue;
-        const int zo = zo_of(z, delta_d(g, d)), zi = zi_of(z, delta_d(g, d), g.Z);
+        const int zo = zo_of(z, dl_out(g, d)), zi = zi_of(z, dl_in(g, d), g.Z);
         if (zo >= 0) b = min(b, op.nH(nb, zo));
         if (zi >= 0 && op.nLres(nb, d, zi) > 0) b = min(b, op.nH(nb, zi));
     }
@@ -409,7 +409,7 @@ __device__ __forceinline__ bool push_step(const Geo &g, const TileGeo &t, const 
 #pragma unroll
                 for (int d = 0; d < 4; d++) {
                     const int nb = cc.nb[d];
-                    const int zo = zo_of(z, delta_d(g, d));
+                    const int zo = zo_of(z, dl_out(g, d));
                     if (done || nb == NB_NONE || zo < 0) continue;
                     if (op.nH(nb, zo) < hk) {  // lateral-out (infinite)
                         df = e[k];
@@ -438,7 +438,7 @@ __device__ __forceinline__ bool push_step(const Geo &g, const TileGeo &t, const 
 #pragma unroll
                 for (int d = 0; d < 4; d++) {
                     const int nb = cc.nb[d];
-                    const int zi = zi_of(z, delta_d(g, d), Z);
+                    const int zi = zi_of(z, dl_in(g, d), Z);
                     if (done || nb == NB_NONE || zi < 0) continue;
                     const int r = op.nLres(nb, d, zi);
                     if (r > 0 && op.nH(nb, zi) < hk) {  // lateral-in reverse

@@ -88,20 +88,16 @@ def brute_force_general(c: np.ndarray, delta, band=None):
 def k0_band(c: np.ndarray, band) -> int:
     """|f| = min cost + K0 under the band rule: the cut of the closed set {z <= S(p)} is
     N + sum_{v in S} w(v) (Eq. 6 with source capacities -w, sink capacities w), the band weights
-    telescope to c(p, S(p)) - (sum_{band} c + 1) per column, and N = sum max(0, -w)."""
-    X, Y, Z = c.shape
+    telescope to c(p, S(p)) - (sum_{band} c + 1) per column, and N = sum max(0, -w) =
+    sum_band c + 1 - c(lo) + sum_{lo<z<hi} max(0, c(z-1) - c(z)); so per column
+    K0 = sum_{lo<z<hi} max(0, c(z-1) - c(z)) - c(lo)."""
     cc = c.astype(np.int64)
-    N, const = 0, 0
-    for x in range(X):
-        for y in range(Y):
-            lo, hi = int(band[x, y, 0]), int(band[x, y, 1])
-            col = cc[x, y, lo:hi]
-            w = np.empty(hi - lo, np.int64)
-            w[0] = col[0] - (col.sum() + 1)
-            w[1:] = col[1:] - col[:-1]
-            N += int(np.maximum(-w, 0).sum())
-            const += int(col.sum() + 1)
-    return N - const
+    lo, hi = band[..., 0].astype(np.int64), band[..., 1].astype(np.int64)
+    drops = np.zeros_like(cc)
+    drops[:, :, 1:] = np.maximum(0, cc[:, :, :-1] - cc[:, :, 1:])
+    P = np.cumsum(drops, axis=2)  # P[z] = sum_{1 <= j <= z} drops
+    take = lambda a, i: np.take_along_axis(a, i[..., None], axis=2)[..., 0]  # noqa: E731
+    return int((take(P, hi - 1) - take(P, lo) - take(cc, lo)).sum())
 
 
 def band_consistent(band, delta) -> bool:

@@ -25,14 +25,31 @@ def cg():
     return colgraph
 
 
-def weights(c, weight):
+def weights(c, weight, band=None):
     cc = c.astype(np.int64)
     if weight:
         return cc
     w = np.empty_like(cc)
+    if band is not None:  # narrow band (reading R15): base rule inside [lo, hi), no terminal arc outside
+        w[:] = 0
+        X, Y, _ = c.shape
+        for x in range(X):
+            for y in range(Y):
+                lo, hi = int(band[x, y, 0]), int(band[x, y, 1])
+                w[x, y, lo] = cc[x, y, lo] - (cc[x, y, lo:hi].sum() + 1)
+                w[x, y, lo + 1:hi] = cc[x, y, lo + 1:hi] - cc[x, y, lo:hi - 1]
+        return w
     w[:, :, 0] = cc[:, :, 0] - (cc.sum(axis=2) + 1)
     w[:, :, 1:] = cc[:, :, 1:] - cc[:, :, :-1]
     return w
+
+
+def d4_of(delta):
+    if isinstance(delta, (tuple, list)):
+        if len(delta) == 4:
+            return tuple(int(v) for v in delta)
+        return (int(delta[0]), int(delta[0]), int(delta[1]), int(delta[1]))
+    return (int(delta),) * 4
 
 
 def sl(dx, X):  # (source slice, target slice) along one axis for a shift dx
@@ -44,30 +61,28 @@ def soft_caps(penalty):
     return [f[1]] + [f[k + 1] - 2 * f[k] + f[k - 1] for k in range(1, len(penalty))]
 
 
-def check_flow(c, delta, F, weight=False, penalty=None):
+def check_flow(c, delta, F, weight=False, penalty=None, band=None):
     X, Y, Z = c.shape
     n = X * Y * Z
     fs, ft, fd, *L = [F[i].astype(np.int64) for i in range(7)]
-    dxy0 = tuple(delta) if isinstance(delta, (tuple, list)) else (delta, delta)
-    K = max(dxy0) if penalty is not None else 0  # the library's soft arcs per direction
+    d4 = d4_of(delta)  # edge interval of each vertex's lateral arc toward +x, -x, +y, -y
+    K = max(d4) if penalty is not None else 0  # the library's soft arcs per direction
     caps = soft_caps(penalty)[:K] if K else []
-    w = weights(c, weight)
+    w = weights(c, weight, band)
     E0, T0 = np.maximum(-w, 0), np.maximum(w, 0)
     zs = np.arange(Z)
-    dxy = tuple(delta) if isinstance(delta, (tuple, list)) else (delta, delta)
-    ZO = [np.where(zs == 0, 0, np.where(zs > dl, zs - dl, -1)) for dl in dxy]  # x-, y-neighbours
+    ZO = [np.where(zs == 0, 0, np.where(zs > dl, zs - dl, -1)) for dl in d4]  # per direction
     # Eq. 2: capacities (infinite arcs: non-negative); arcs that do not exist carry nothing
     assert (fs >= 0).all() and (fs <= E0).all()
     assert (ft >= 0).all() and (ft <= T0).all()
     assert (fd >= 0).all() and (fd[:, :, 0] == 0).all()
     for d, (dx, dy) in enumerate(DIRS):
-        valid = ZO[d >> 1] >= 0
+        valid = ZO[d] >= 0
         assert (L[d] >= 0).all() and (L[d][:, :, ~valid] == 0).all()
         if dx == 1: assert (L[d][X - 1] == 0).all()
         if dx == -1: assert (L[d][0] == 0).all()
         if dy == 1: assert (L[d][:, Y - 1] == 0).all()
         if dy == -1: assert (L[d][:, 0] == 0).all()
-    dxy_ = tuple(delta) if isinstance(delta, (tuple, list)) else (delta, delta)
     SF = {}
     for d in range(4 if K else 0):
         for k in range(K):
@@ -75,7 +90,7 @@ def check_flow(c, delta, F, weight=False, penalty=None):
             SF[d, k] = f
             dx, dy = DIRS[d]
             exists = np.zeros((X, Y, Z), bool)
-            if k < dxy_[d >> 1] and caps[k] > 0:
+            if k < d4[d] and caps[k] > 0:
                 xs, _ = sl(dx, X)
                 ys, _ = sl(dy, Y)
                 exists[xs, ys, k:] = True
@@ -85,7 +100,7 @@ def check_flow(c, delta, F, weight=False, penalty=None):
     net = fs - ft - fd
     net[:, :, :-1] += fd[:, :, 1:]
     for d, (dx, dy) in enumerate(DIRS):
-        zo = ZO[d >> 1]
+        zo = ZO[d]
         valid = zo >= 0
         net -= L[d]
         xs, xt = sl(dx, X)
@@ -115,7 +130,7 @@ def check_flow(c, delta, F, weight=False, penalty=None):
     m = fd[:, :, 1:] > 0
     rows.append(idx[:, :, :-1][m]); cols.append(idx[:, :, 1:][m])
     for d, (dx, dy) in enumerate(DIRS):
-        zo = ZO[d >> 1]
+        zo = ZO[d]
         xs, xt = sl(dx, X)
         ys, yt = sl(dy, Y)
         vz = np.flatnonzero(zo >= 0)

@@ -25,13 +25,13 @@ def solve(c, delta, algo="dinic", **kw):
 # ---------------------------------------------------------------- generic max-flow core
 
 @pytest.mark.parametrize("ex", GOLDEN["graph_examples"], ids=lambda e: e["name"])
-@pytest.mark.parametrize("algo", ["dinic", "ek"])
+@pytest.mark.parametrize("algo", ["dinic", "ek", "pr"])
 def test_graph_examples(ex, algo):
     r = oracle.graph_maxflow(ex["nn"], ex["arcs"], ex["s"], ex["t"], algo)
     assert r["status"] == 0 and r["flow"] == ex["flow"] and r["checks"] == oracle.ALL_CHECKS
 
 
-@pytest.mark.parametrize("algo", ["dinic", "ek"])
+@pytest.mark.parametrize("algo", ["dinic", "ek", "pr"])
 def test_graph_random_vs_bruteforce_mincut(algo):
     """Theorem 1: max flow = min cut over all 2^(n-2) cuts; the
     residual-reachable set equals the intersection of all minimum source sets."""
@@ -55,7 +55,7 @@ def test_graph_random_vs_bruteforce_mincut(algo):
 # ---------------------------------------------------------------- column-graph worked examples
 
 @pytest.mark.parametrize("ex", GOLDEN["column_examples"], ids=lambda e: e["name"])
-@pytest.mark.parametrize("algo", ["dinic", "ek"])
+@pytest.mark.parametrize("algo", ["dinic", "ek", "pr"])
 def test_column_examples(ex, algo):
     c = np.array(ex["c"], np.int32)
     r = solve(c, ex["delta"], algo)
@@ -104,7 +104,7 @@ def test_random_tiny_bruteforce():
         X, Y, Z = c.shape
         if X * Y > 9 or Z > 8:  # keep the enumeration small
             c = c[:min(X, 3), :min(Y, 3), :min(Z, 8)]
-        _check_vs_bruteforce(np.ascontiguousarray(c), delta, "dinic" if seed % 2 else "ek")
+        _check_vs_bruteforce(np.ascontiguousarray(c), delta, ("dinic", "ek", "pr")[seed % 3])
 
 
 def test_weight_mode_bruteforce():
@@ -304,3 +304,34 @@ def test_soft_rejects_nonconvex():
     c = np.zeros((2, 2, 4), np.int32)
     assert oracle.colgraph_solve(c, 2, penalty=[5, 6])["status"] == 1   # f(2)-2f(1)+f(0) < 0
     assert oracle.colgraph_solve(c, 3, penalty=[1, 2])["status"] == 1   # too short
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_push_relabel_algorithm_pins(seed):
+    """The oracle's third max-flow algorithm (two-phase FIFO push-relabel, §2.1) on random
+    tiny volumes (brute force), weight mode (brute-force closures) and general intervals + bands."""
+    rng = np.random.default_rng(9000 + seed)
+    c, delta = V.tiny_case(9000 + seed)
+    c = np.ascontiguousarray(c[:3, :3, :8])
+    _check_vs_bruteforce(c, delta, "pr")
+    X, Y, Z = (int(v) for v in rng.integers(1, 4, 3))
+    w = rng.integers(-9, 10, size=(X, Y, Z)).astype(np.int32)
+    dd = int(rng.integers(0, 3))
+    best, lowest = pins.brute_force_weight_closure(w, dd)
+    r = oracle.colgraph_solve(w, dd, input_is_weight=True, algo="pr")
+    assert r["checks"] == oracle.ALL_CHECKS and r["flow"] == best
+    d4 = tuple(int(v) for v in rng.integers(0, 4, 4))
+    best, low, _ = pins.brute_force_general(c, d4)
+    r = oracle.colgraph_solve(c, d4, algo="pr")
+    assert r["checks"] == oracle.ALL_CHECKS and r["flow"] == best + pins.k0(c) and np.array_equal(r["surface"], low)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_push_relabel_agrees_with_dinic(name):
+    from synth import volumes as V2
+    spec = V2.CONFIGS[name]
+    c = V2.generate(name)
+    a = oracle.colgraph_solve(c, spec.delta, algo="pr")
+    b = oracle.colgraph_solve(c, spec.delta, algo="dinic")
+    assert a["checks"] == b["checks"] == oracle.ALL_CHECKS
+    assert a["flow"] == b["flow"] and np.array_equal(a["mask"], b["mask"])
