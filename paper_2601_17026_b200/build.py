@@ -71,5 +71,9 @@ if __name__ == "__main__":
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_prof.so"), defines=("CG_SCAN_PROF=1",)))
     if "--hplane" in sys.argv:
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_hplane.so"), defines=("CG_H_PLANE=1",)))
+    if "--no-precheck" in sys.argv:
+        print(build(force=True, lib=os.path.join(PKG, "libcolgraph_nopre.so"), defines=("CG_BFS_PRECHECK=0",)))
+    if "--bfs-minb2" in sys.argv:
+        print(build(force=True, lib=os.path.join(PKG, "libcolgraph_bfs2.so"), defines=("CG_BFS_RUN_MINB=2",)))
     if "--soa" in sys.argv:
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_soa.so"), defines=("CG_LAYOUT_AOS=0",)))

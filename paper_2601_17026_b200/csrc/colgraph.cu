@@ -510,6 +510,8 @@ cg_status bfs_strict(cg_graph *g, Slab *sl, bool allow_coop = true, bool flag_pl
     sl->h_bst->small = getenv("CG_BFS_SMALL") ? (unsigned)atoi(getenv("CG_BFS_SMALL")) : BFS_RUN_SMALL;
     CG_CUDA(cudaMemcpyAsync(&sl->bst->L, &sl->h_bst->L, sizeof(int), cudaMemcpyHostToDevice, st));
     CG_CUDA(cudaMemcpyAsync(&sl->bst->small, &sl->h_bst->small, sizeof(unsigned), cudaMemcpyHostToDevice, st));
+    sl->h_bst->bar[2] = getenv("CG_BAR_NS") ? (unsigned)atoi(getenv("CG_BAR_NS")) : 0;  // 0: 1024 ns
+    CG_CUDA(cudaMemcpyAsync(&sl->bst->bar[2], &sl->h_bst->bar[2], sizeof(unsigned), cudaMemcpyHostToDevice, st));
     const bool coop = allow_coop && sl->bfs_coop_grid > 0;
     if (flag_plane && !coop) return CG_E_INVAL;
     if (flag_plane)

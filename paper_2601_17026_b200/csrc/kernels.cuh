@@ -248,11 +248,14 @@ __global__ void k_export(F f, int64_t n, int32_t *out) {
 }
 
 // ------------------------------------------------------------------ a3: push-relabel sweep
-// An active vertex (E > 0, H < INF) runs Alg. 2: it scans its residual out-arcs in the
-// fixed order t, down, lateral-out(+x,-x,+y,-y), up, lateral-in-reverse(+x,-x,+y,-y),
-// pushes delta = min(E, r) (r = INF on infinite arcs) on the first admissible arc
-// (neighbour label < own label), or relabels to min label(w)+1 ("newd = min label(w)+1
-// ... only if newd > label(v)") and pushes on that arc.
+// An active vertex (E > 0, H < INF) runs Alg. 2: it scans its residual out-arcs and pushes
+// delta = min(E, r) (r = INF on infinite arcs) on an admissible arc (neighbour label < own label),
+// or relabels to min label(w)+1 ("newd = min label(w)+1 ... only if newd > label(v)").  Default
+// scan (CG_SCAN_COL_GATHER, CG_SCAN_UP_EARLY, CG_SCAN_LAT_GATHER) in three rounds
+// of independent loads: (1) the own column -- t if T > 0, else down, else up (first admissible in
+// that order); (2) the four lateral-out targets, taking the LOWEST-height admissible one; (3) the
+// four lateral-in reverse arcs with residual, again the lowest.  Any admissible arc keeps the
+// algorithm correct; the order only decides which one is used.
 // Lock-free rule: every residual field has one decrementer, so each stale
 // read is a lower bound of what the reader may subtract.
 struct OpCtx {
@@ -267,15 +270,13 @@ struct ArcPick {
     int64_t tgt;
 };
 
-// FIRST admissible arc (label < hx) in the fixed order t, down, lateral-out (+x,-x,+y,-y),
-// up, lateral-in reverse (+x,-x,+y,-y); if none, the lowest residual neighbour (for the
-// relabel).  Candidate fields are loaded in two batches of independent loads -- t, down and
-// lateral-out first, the reverse arcs only if none of those is admissible -- so a hop costs at
-// most two memory round trips instead of a chain of up to 15 dependent ones (ncu: the walk
-// was 84 % long-scoreboard stalls; loading all 15 at once measured slower).
-// CG_SCAN_SERIAL=1 at compile time restores the early-exit scan.
+// An admissible arc (label < hx) -- in the default build the own-column arcs first (t, down, up),
+// then the lowest of the lateral-out targets, then the lowest of the lateral-in reverse arcs (see
+// above); if none, the lowest residual neighbour (for the relabel).  CG_SCAN_SERIAL = 0 at compile
+// time selects a two-stage gather instead (t, down and lateral-out in one batch of independent
+// loads, the reverse arcs in a second; measured within noise).
 #ifndef CG_SCAN_SERIAL
-#define CG_SCAN_SERIAL 1  // measured: the two-stage gather is within noise
+#define CG_SCAN_SERIAL 1
 #endif
 // Soft arcs (NEXT-1) are scanned after every hard arc: arc codes 11 + 16 d + k (forward, v ->
 // (nbr_d, z-k), residual cap_k - F) and 75 + 16 d + k (reverse of (nbr_d, z+k)'s arc in direction
@@ -1050,12 +1051,19 @@ __device__ __forceinline__ void bfs_expand_multi(const Geo &g, const Soa &s, int
             if (zo >= 0 && L[d] > 0 && owned(g, v0 + o + zo)) { w[r][6 + d] = v0 + o + zo; cand[r] |= 1u << (6 + d); }
         }
     }
-    // visited words (L2-resident bitmap): hw = 1 if the candidate is already labelled
+    // visited words (L2-resident bitmap): hw = 1 if the candidate is already labelled.
+    // CG_BFS_PRECHECK = 0 skips this round of loads and lets the atomicOr decide (one L2 round trip
+    // less per level, more atomics).
+#ifndef CG_BFS_PRECHECK
+#define CG_BFS_PRECHECK 1
+#endif
 #pragma unroll
     for (int r = 0; r < R; r++)
 #pragma unroll
         for (int j = 0; j < 10; j++)
-            hw[r][j] = (cand[r] >> j & 1u) ? (int)((__ldcg(&visited[w[r][j] >> 5]) >> (w[r][j] & 31)) & 1u) : 1;
+            hw[r][j] = (cand[r] >> j & 1u)
+                           ? (CG_BFS_PRECHECK ? (int)((__ldcg(&visited[w[r][j] >> 5]) >> (w[r][j] & 31)) & 1u) : 0)
+                           : 1;
     if (!FL && g.soft_k && nl < INF)  // warp-uniform: every lane calls it
         for (int r = 0; r < R; r++) bfs_soft_preds<0>(g, s, vv[r], nl, lout, cout, visited);
     int k = 0;
@@ -1100,7 +1108,7 @@ struct BfsState {
     unsigned cnt[3];       // frontier counters
     unsigned finished;     // blocks done with the current large level
     unsigned long long claimed;  // vertices labelled so far (direction-optimising switch)
-    unsigned bar[2];       // grid barrier of k_bfs_run (arrivals, generation)
+    unsigned bar[3];       // grid barrier of k_bfs_run (arrivals, generation, back-off cap in ns)
     unsigned hist[8];      // levels by frontier size: <=32, <=256, <=2048, <=16K, <=128K, <=1M, more; [7] bottom-up
     unsigned long long cyc[8];  // block-0 clock cycles spent in levels of each bucket ([7]: bottom-up levels)
     unsigned small;             // k_bfs_run: frontiers <= small are run by block 0 alone
@@ -1166,12 +1174,15 @@ __global__ void __launch_bounds__(512, CG_BFS_MINB) k_bfs_step(Geo g, Soa s, int
 // k_bfs_step: small frontiers are run by block 0 alone with block barriers, large ones by
 // the whole grid, top-down or bottom-up.  Must be launched with cudaLaunchCooperativeKernel
 // (all blocks co-resident).
+// bar[2] (nullable 0) caps the pollers' exponential back-off in ns (CG_BAR_NS, default 1024): every
+// poller re-reads the generation at most that often after the release.
 __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks) {
     // sense-free counting barrier: bar[0] = arrivals, bar[1] = generation
     __syncthreads();
     if (threadIdx.x == 0) {
         volatile unsigned *gen = bar + 1;
         const unsigned g0 = *gen;
+        const unsigned cap = bar[2] ? bar[2] : 1024u;
         __threadfence();
         if (atomicAdd(bar, 1u) == nblocks - 1) {
             bar[0] = 0;
@@ -1181,7 +1192,7 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks) {
             unsigned ns = 32;
             while (*gen == g0) {  // back off: ~300 pollers on one line slow the working blocks
                 __nanosleep(ns);
-                ns = min(ns * 2, 1024u);
+                ns = min(ns * 2, cap);
             }
         }
         __threadfence();

@@ -80,7 +80,7 @@ __global__ void k_bfs2_init(Geo g, Soa s, uint8_t *flags, int32_t *lab, unsigned
 struct ColGrState {
     int round;                  // current round (0: every column)
     unsigned cnt[3];            // worklist counters (round r reads cnt[r % 3])
-    unsigned bar[2];            // grid barrier
+    unsigned bar[3];            // grid barrier (arrivals, generation, back-off cap in ns)
     unsigned small;             // worklists <= small run in block 0 alone
     int tag0;                   // colstamp tag of round r's output list = tag0 + r
     unsigned long long updates; // column updates
@@ -297,7 +297,7 @@ __global__ void k_colgr_rebuild(Geo g, Soa s, const int32_t *__restrict__ lab, i
             bool a = false;
             if (v < g.n) {
                 const int h = lab[v];
-                s.H[v] = h;
+                if (s.H[v] != h) s.H[v] = h;  // same sector as E: an unchanged label leaves it clean
                 a = s.E[v] > 0 && h < g.INF;
             }
             if (a) vstamp[v] = tag;

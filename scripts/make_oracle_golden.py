@@ -1,6 +1,7 @@
 """Write tests/golden/oracle_<C>.json (flow, surface/mask sha256) for full-size configs.
 
-Calls only oracle/ and synth/ (never the CUDA path).  Usage: python scripts/make_oracle_golden.py C3 [C4 ...]
+Calls only oracle/ and synth/ (never the CUDA path).
+Usage: python scripts/make_oracle_golden.py C3 [C4 ...]   (ORACLE_ALGO=pr|dinic|ek, default dinic)
 """
 import hashlib
 import json
@@ -21,14 +22,15 @@ for name in sys.argv[1:]:
     sha = V.sha256_volume(c)
     assert sha == V.MANIFEST[name]
     t = time.time()
-    r = oracle.colgraph_solve(c, spec.delta, want_mask=True)
+    algo = os.environ.get("ORACLE_ALGO", "dinic")
+    r = oracle.colgraph_solve(c, spec.delta, want_mask=True, algo=algo)
     dt = time.time() - t
     assert r["status"] == 0 and r["checks"] == oracle.ALL_CHECKS, (r["status"], r["checks"])
     out = {"config": name, "input_sha256": sha, "delta": spec.delta, "flow": r["flow"],
            "surface_sha256": hashlib.sha256(r["surface"].astype("<i4").tobytes()).hexdigest(),
            "mask_sha256": hashlib.sha256(r["mask"].tobytes()).hexdigest(),
            "surface_min": int(r["surface"].min()), "surface_max": int(r["surface"].max()),
-           "n_explicit_arcs": r["n_arcs"], "oracle_seconds": round(dt, 1), "oracle_algo": "dinic",
+           "n_explicit_arcs": r["n_arcs"], "oracle_seconds": round(dt, 1), "oracle_algo": algo,
            "checks": "capacity, antisymmetry, conservation, value, t not in S, cut == flow",
            "written_by": "scripts/make_oracle_golden.py (oracle/ + synth/ only)"}
     with open(os.path.join(ROOT, "tests", "golden", f"oracle_{name}.json"), "w") as f:

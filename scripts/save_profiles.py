@@ -52,7 +52,8 @@ if os.path.exists(os.path.join(OUT, "launches.csv")):
     open(os.path.join(PROF, f"{tag}_launch_summary_c4.txt"), "w").write(s)
     with open(os.path.join(OUT, "launches.csv"), "rb") as f, gzip.open(os.path.join(PROF, f"{tag}_launches_c4.csv.gz"), "wb") as g:
         g.write(f.read())
-for rep, name in [("prof_walk.ncu-rep", "k_walk"), ("prof_bfs.ncu-rep", "k_bfs_run")]:
+for rep, name in [("prof_walk.ncu-rep", "k_walk_ws"), ("prof_bfs.ncu-rep", "k_bfs_run"),
+                  ("prof_passes.ncu-rep", "relabel_passes")]:
     p = os.path.join(OUT, rep)
     if os.path.exists(p):
         avg = ncu_summary(p, name)
@@ -69,12 +70,12 @@ if os.path.exists(st_csv) and os.path.exists(st_log):
             per[r["ID"]] = per.get(r["ID"], 0.0) + float(r["Metric Value"].replace(",", "")) * SCALE[r["Metric Unit"]]
     alg = next(json.loads(l) for l in open(st_log) if l.startswith("{"))
     tot, n = sum(per.values()), len(per)
-    json.dump({"kernel": "k_walk / k_sweep_v (all sweep launches of one C4 solve)",
+    json.dump({"kernel": "k_walk_ws / k_sweep_v (all sweep launches of one C4 solve)",
                "sweep_dram_bytes_per_launch": tot / n,
                "sweep_alg_bytes_per_launch_same_run": alg["sweep_bytes_alg"] / n,
                "traffic_over_alg": tot / alg["sweep_bytes_alg"], "launches": n, "dram_bytes_total": tot,
                "alg_bytes_total": alg["sweep_bytes_alg"],
-               "note": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over EVERY k_walk/k_sweep_v launch of "
+               "note": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over EVERY k_walk_ws/k_sweep_v launch of "
                        "one C4 solve (scripts/gpu_session.sh); the algorithmic bytes are that same solve's "
                        "(profile_one.py), run with the relabel schedule of an unprofiled solve replayed "
                        "(CG_GR_SCHEDULE) so its sweeps match the bench's.",
