@@ -43,6 +43,10 @@
  *                         across boundaries; bfs: BFS over the records (also soft graphs, tiles);
  *                         colgr: column fixpoint from INF; levels (x-slabs): level-synchronous BFS
  *   CG_COLGR_SMALL=k      column fixpoint: worklists <= k columns run in block 0 alone
+ *   CG_BFS_TRUNC=s,k      flag-plane BFS relabels not forced to be exhaustive stop after k
+ *                         consecutive frontiers of <= s vertices; unreached vertices stay at INF
+ *                         until the next exhaustive relabel (the one that decides termination)
+ *   CG_BAR_NS=ns          back-off cap of the persistent kernels' grid barrier (default 1024)
  * Conventions for every entry point:
  *   - Errors are returned as cg_status, never thrown; no C++ exception crosses
  *     this ABI.
@@ -157,6 +161,7 @@ typedef struct {
                                   tiles (64 B per tile vertex + 8 B per halo vertex) per tile visit */
     int64_t tile_visits;       /* tile visits summed over all phases (tile sweeps only) */
     int64_t relabel_ops;       /* sweep operations that were relabels (vertex worklists) */
+    int64_t gr_truncated;      /* global relabels that deferred a thin BFS tail (CG_BFS_TRUNC) */
 } cg_solve_stats;
 
 /* a1 -- build the int32 structure-of-arrays residual graph.

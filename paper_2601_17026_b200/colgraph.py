@@ -58,7 +58,7 @@ class cg_solve_stats(ctypes.Structure):
                 ("ms_sweeps", ctypes.c_double), ("bytes_per_sweep_alg", ctypes.c_double),
                 ("source_capacity", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
                 ("ms_sweep_kernels", ctypes.c_double), ("sweep_bytes_alg", ctypes.c_double),
-                ("tile_visits", ctypes.c_int64), ("relabel_ops", ctypes.c_int64)]
+                ("tile_visits", ctypes.c_int64), ("relabel_ops", ctypes.c_int64), ("gr_truncated", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

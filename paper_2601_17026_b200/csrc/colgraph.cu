@@ -115,6 +115,7 @@ struct cg_graph {
     int64_t n_global = 0;
     bool solved = false;
     bool exported = false;      // phase 2 ran (maxflow_export_flow): the preflow is now a flow
+    unsigned trunc_small = 0, trunc_levels = 0;  // truncated relabels (CG_BFS_TRUNC), 0 = off
     cg_solve_stats st{};
 };
 
@@ -502,7 +503,7 @@ void k_fill_ghost_h(Slab *sl) {
 // Strict level-synchronous BFS of one slab without neighbours (the single-GPU path).  flag_plane:
 // the flag-plane BFS (k_bfs2_init + k_bfs_run<true>, labels in sl->lab; the default for hard
 // graphs), else the record BFS (k_bfs_init + k_bfs_run<false> / k_bfs_step, labels in the records).
-cg_status bfs_strict(cg_graph *g, Slab *sl, bool allow_coop = true, bool flag_plane = false) {
+cg_status bfs_strict(cg_graph *g, Slab *sl, bool allow_coop = true, bool flag_plane = false, bool exhaustive = true) {
     const Geo &geo = sl->geo;
     cudaStream_t st = sl->stream;
     CG_CUDA(cudaMemsetAsync(sl->bst, 0, sizeof(BfsState), st));
@@ -512,6 +513,15 @@ cg_status bfs_strict(cg_graph *g, Slab *sl, bool allow_coop = true, bool flag_pl
     CG_CUDA(cudaMemcpyAsync(&sl->bst->small, &sl->h_bst->small, sizeof(unsigned), cudaMemcpyHostToDevice, st));
     sl->h_bst->bar[2] = getenv("CG_BAR_NS") ? (unsigned)atoi(getenv("CG_BAR_NS")) : 0;  // 0: 1024 ns
     CG_CUDA(cudaMemcpyAsync(&sl->bst->bar[2], &sl->h_bst->bar[2], sizeof(unsigned), cudaMemcpyHostToDevice, st));
+    // truncated relabel (flag-plane BFS, not exhaustive): CG_BFS_TRUNC="small,levels" stops after
+    // `levels` consecutive frontiers of <= `small` vertices
+    sl->h_bst->trunc_small = sl->h_bst->trunc_levels = 0;
+    if (flag_plane && !exhaustive && g->trunc_levels > 0) {
+        sl->h_bst->trunc_small = g->trunc_small;
+        sl->h_bst->trunc_levels = g->trunc_levels;
+    }
+    CG_CUDA(cudaMemcpyAsync(&sl->bst->trunc_small, &sl->h_bst->trunc_small, 2 * sizeof(unsigned),
+                            cudaMemcpyHostToDevice, st));
     const bool coop = allow_coop && sl->bfs_coop_grid > 0;
     if (flag_plane && !coop) return CG_E_INVAL;
     if (flag_plane)
@@ -534,7 +544,7 @@ cg_status bfs_strict(cg_graph *g, Slab *sl, bool allow_coop = true, bool flag_pl
         CG_CUDA(cudaMemcpyAsync(sl->h_bst, sl->bst, sizeof(BfsState), cudaMemcpyDeviceToHost, st));
         CG_CUDA(cudaStreamSynchronize(st));
         L = sl->h_bst->L;
-        if (sl->h_bst->cnt[(L - 1) % 3] != 0) return CG_E_CUDA;
+        if (sl->h_bst->cnt[(L - 1) % 3] != 0 && !sl->h_bst->truncated) return CG_E_CUDA;
         g->st.gr_passes += L - 1;
         return CG_OK;
     }
@@ -768,13 +778,18 @@ cg_status bfs_slabs_levels(cg_graph *g) {
 }
 
 // a2/a5: global relabel + rebuild of every slab's active list; returns the global active count.
-cg_status global_relabel(cg_graph *g, int64_t *active) {
+// exhaustive = false allows the truncated flag-plane BFS (g->trunc_levels > 0); a truncated relabel
+// that leaves no active vertex is redone exhaustively (termination is decided only on an exact one)
+cg_status global_relabel(cg_graph *g, int64_t *active, bool exhaustive = true) {
     const RelabelKind kind = relabel_kind(g);
     const bool colgr = kind != RELABEL_RECORD;  // labels are in sl->lab: the rebuild writes the records' H
+    bool truncated = false;
     if (kind == RELABEL_COLGR || kind == RELABEL_BFS_COLGR) {
         CG_TRY(multi(g) ? colgr_slabs(g, kind == RELABEL_BFS_COLGR) : colgr_strict(g, g->slabs[0]));
     } else if (kind == RELABEL_FLAGS) {
-        CG_TRY(bfs_strict(g, g->slabs[0], true, true));
+        CG_TRY(bfs_strict(g, g->slabs[0], true, true, exhaustive));
+        truncated = g->slabs[0]->h_bst->truncated != 0;
+        g->st.gr_truncated += truncated;
     } else if (!multi(g)) {
         CG_TRY(bfs_strict(g, g->slabs[0]));
     } else {
@@ -811,6 +826,7 @@ cg_status global_relabel(cg_graph *g, int64_t *active) {
     CG_TRY(gsum(g, &act, 1));
     *active = act;
     g->st.global_relabels++;
+    if (truncated && act == 0) return global_relabel(g, active, true);
     return CG_OK;
 }
 
@@ -985,13 +1001,21 @@ cg_status normalize_opts(cg_graph *g, const cg_solve_opts *opts, cg_solve_opts &
 cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &ms_gr) {
     const bool trace = tracing();
     Slab *s0 = g->slabs[0];
+    g->trunc_small = g->trunc_levels = 0;
+    if (const char *e = getenv("CG_BFS_TRUNC")) {  // "small,levels"
+        unsigned a = 0, b = 0;
+        if (sscanf(e, "%u,%u", &a, &b) == 2) {
+            g->trunc_small = a;
+            g->trunc_levels = b;
+        }
+    }
     cudaStream_t st0 = s0->stream;
     double last_gr_ms = 0.0;
     int64_t active = 0;
-    auto timed_gr = [&]() -> cg_status {
+    auto timed_gr = [&](bool exhaustive) -> cg_status {
         const double a = now_ms();
         const int64_t p0 = g->st.gr_passes;
-        const cg_status s = global_relabel(g, &active);
+        const cg_status s = global_relabel(g, &active, exhaustive);
         last_gr_ms = now_ms() - a;
         ms_gr += last_gr_ms;
         if (trace) {
@@ -1019,7 +1043,7 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
         }
         return s;
     };
-    CG_TRY(timed_gr());
+    CG_TRY(timed_gr(true));
     const double gr_budget = (double)o.gr_factor * (double)g->n_global;
     const double walk_min = getenv("CG_WALK_MIN") ? atof(getenv("CG_WALK_MIN")) : 1e-3;
     const double gr_beta = getenv("CG_GR_BETA") ? atof(getenv("CG_GR_BETA")) : 1.0;
@@ -1097,7 +1121,7 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
             CG_CUDA(cudaMemset(sl->tl.prof, 0, sizeof(pf)));
         }
         if (quiescent || work_since_gr >= gr_budget || sweep_ms_since_gr >= gr_beta * std::max(last_gr_ms, 0.05)) {
-            CG_TRY(timed_gr());
+            CG_TRY(timed_gr(true));
             work_since_gr = 0.0;
             sweep_ms_since_gr = 0.0;
         }
@@ -1190,8 +1214,9 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
         if (trigger) {
             fired.push_back(sweeps);
             while (sched_i < sched.size() && sched[sched_i] <= sweeps) sched_i++;
-            // a4: termination is decided only after an exact global relabel
-            CG_TRY(timed_gr());
+            // a4: termination is decided only after an exact global relabel (a quiescent batch asks
+            // for an exhaustive one; a truncated one that leaves nothing active is redone exhaustively)
+            CG_TRY(timed_gr(quiescent));
             last_active = active;
             work_since_gr = 0.0;
             sweep_ms_since_gr = 0.0;

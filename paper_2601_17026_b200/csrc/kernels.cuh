@@ -1113,6 +1113,11 @@ struct BfsState {
     unsigned long long cyc[8];  // block-0 clock cycles spent in levels of each bucket ([7]: bottom-up levels)
     unsigned small;             // k_bfs_run: frontiers <= small are run by block 0 alone
     unsigned long long svert;   // vertices expanded in block-0 (small) levels
+    // truncated relabel (flag-plane BFS, trunc_levels > 0): after trunc_levels consecutive levels
+    // with frontiers <= trunc_small the BFS stops; the vertices it did not reach keep INF ("parked"
+    // until the next exhaustive relabel); truncated = 1 when it stopped early
+    unsigned trunc_small, trunc_levels, truncated;
+    unsigned thin;              // consecutive thin levels, handed from block 0's small-level loop to the grid
 };
 __device__ __forceinline__ int bfs_bucket(unsigned c) {
     return c <= 32 ? 0 : c <= 256 ? 1 : c <= 2048 ? 2 : c <= 16384 ? 3 : c <= 131072 ? 4 : c <= 1048576 ? 5 : 6;
@@ -1213,9 +1218,16 @@ __global__ void __launch_bounds__(512, CG_BFS_RUN_MINB) k_bfs_run(Geo g, Soa s, 
     unsigned *bar = st->bar;
     int L = *(volatile int *)&st->L;
     unsigned long long claimed = *(volatile unsigned long long *)&st->claimed;
+    const unsigned tr_small = st->trunc_small, tr_levels = FL ? st->trunc_levels : 0;
+    unsigned thin = 0;  // consecutive levels with a frontier <= tr_small
     for (int guard = 0; guard <= g.INF + 2; guard++) {
         const unsigned count = *(volatile unsigned *)&st->cnt[(L - 1) % 3];
         if (count == 0) break;
+        thin = count <= tr_small ? thin + 1 : 0;
+        if (tr_levels && thin > tr_levels) {  // the thin tail is deferred (every block sees the same counts)
+            if (blockIdx.x == 0 && threadIdx.x == 0) st->truncated = 1;
+            break;
+        }
         const int i = L - 1;
         if (count <= st->small) {
             // everyone has read this level's counter before block 0 starts recycling counters
@@ -1249,14 +1261,18 @@ __global__ void __launch_bounds__(512, CG_BFS_RUN_MINB) k_bfs_run(Geo g, Soa s, 
                     if (threadIdx.x == 0) st->claimed += c;
                     __syncthreads();
                     if (c == 0 || c > st->small) break;
+                    if (tr_levels && c <= tr_small && thin + 1 > tr_levels) break;  // the grid loop stops
+                    thin = c <= tr_small ? thin + 1 : 0;
                 }
                 if (threadIdx.x == 0) {
                     st->L = L;
+                    st->thin = thin;
                     st->cyc[2] += clock64() - t0;  // small levels, accounted to the <=2K bucket
                 }
             }
             grid_barrier(bar, gridDim.x);
             L = *(volatile int *)&st->L;
+            thin = *(volatile unsigned *)&st->thin;  // every block continues from block 0's count
             claimed = *(volatile unsigned long long *)&st->claimed;
             continue;
         }
