@@ -48,25 +48,34 @@ __global__ void k_colgr_flags(Geo g, Soa s, uint8_t *flags, int32_t *lab, int64_
 // visited bitmap and the seed list; k_bfs_run<true> then expands from the flags and writes `lab`.
 __global__ void k_bfs2_init(Geo g, Soa s, uint8_t *flags, int32_t *lab, unsigned *visited, int *lout,
                             unsigned *cout) {
-    constexpr int SPAN = 8;
+    constexpr int SPAN = 4;
     SpanAppender<SPAN> ap;
     for (int64_t base = gwarp() * 32 * SPAN; base < g.n; base += nwarps() * 32 * SPAN) {
+        // the SPAN records of this lane first (independent loads in flight together), then the flags
+        int T[SPAN], D[SPAN], L[SPAN][4];
+#pragma unroll
+        for (int j = 0; j < SPAN; j++) {
+            const int64_t v = base + 32 * j + lane_id();
+            T[j] = 0;
+            if (v < g.n) {
+#if CG_LAYOUT_AOS
+                const int4 *rec = reinterpret_cast<const int4 *>(&s.E[v]);  // E H T D | L0 L1 L2 L3
+                const int4 a = __ldcs(&rec[0]), b = __ldcs(&rec[1]);        // streamed: not reused here
+                T[j] = a.z; D[j] = a.w; L[j][0] = b.x; L[j][1] = b.y; L[j][2] = b.z; L[j][3] = b.w;
+#else
+                T[j] = s.T[v]; D[j] = s.D[v];
+                for (int d = 0; d < 4; d++) L[j][d] = s.L[d][v];
+#endif
+            }
+        }
 #pragma unroll
         for (int j = 0; j < SPAN; j++) {
             const int64_t b0 = base + 32 * j;
             const int64_t v = b0 + lane_id();
-            bool seed = false;
+            const bool seed = v < g.n && T[j] > 0;
             if (v < g.n) {
-#if CG_LAYOUT_AOS
-                const int4 *rec = reinterpret_cast<const int4 *>(&s.E[v]);  // E H T D | L0 L1 L2 L3
-                const int4 a = rec[0], b = rec[1];
-                const int T = a.z, D = a.w, L0 = b.x, L1 = b.y, L2 = b.z, L3 = b.w;
-#else
-                const int T = s.T[v], D = s.D[v], L0 = s.L[0][v], L1 = s.L[1][v], L2 = s.L[2][v], L3 = s.L[3][v];
-#endif
-                seed = T > 0;
-                flags[v] = (uint8_t)(seed | (D > 0) << 1 | (L0 > 0) << 2 | (L1 > 0) << 3 | (L2 > 0) << 4 |
-                                     (L3 > 0) << 5);
+                flags[v] = (uint8_t)(seed | (D[j] > 0) << 1 | (L[j][0] > 0) << 2 | (L[j][1] > 0) << 3 |
+                                     (L[j][2] > 0) << 4 | (L[j][3] > 0) << 5);
                 lab[v] = seed ? 1 : g.INF;
             }
             const unsigned m = __ballot_sync(FULL, seed);
