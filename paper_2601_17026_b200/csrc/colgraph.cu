@@ -522,6 +522,17 @@ cg_status bfs_strict(cg_graph *g, Slab *sl, bool allow_coop = true, bool flag_pl
     }
     CG_CUDA(cudaMemcpyAsync(&sl->bst->trunc_small, &sl->h_bst->trunc_small, 2 * sizeof(unsigned),
                             cudaMemcpyHostToDevice, st));
+    // bottom-up levels (flag-plane BFS): CG_BFS_BU="div,min"
+    sl->h_bst->bu_div = sl->h_bst->bu_min = 0;
+    if (flag_plane)
+        if (const char *e = getenv("CG_BFS_BU")) {
+            unsigned a = 0, b = 0;
+            if (sscanf(e, "%u,%u", &a, &b) == 2) {
+                sl->h_bst->bu_div = a;
+                sl->h_bst->bu_min = b;
+            }
+        }
+    CG_CUDA(cudaMemcpyAsync(&sl->bst->bu_div, &sl->h_bst->bu_div, 2 * sizeof(unsigned), cudaMemcpyHostToDevice, st));
     const bool coop = allow_coop && sl->bfs_coop_grid > 0;
     if (flag_plane && !coop) return CG_E_INVAL;
     if (flag_plane)
@@ -1032,6 +1043,7 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
             fprintf(stderr, "[cg] GR#%lld levels=%lld active=%lld ms=%.3f (sweeps %lld) flow=%lld\n",
                     (long long)g->st.global_relabels, (long long)(g->st.gr_passes - p0), (long long)active, last_gr_ms,
                     (long long)g->st.sweeps, (long long)-sumT);
+            if (s0->h_bst->bu_levels) fprintf(stderr, "[cg]   bottom-up levels %u\n", s0->h_bst->bu_levels);
             const unsigned *h = s0->h_bst->hist;
             fprintf(stderr, "[cg]   levels by frontier: <=32 %u <=256 %u <=2K %u <=16K %u <=128K %u <=1M %u more %u "
                     "(bottom-up %u)\n", h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
@@ -1046,6 +1058,8 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
     CG_TRY(timed_gr(true));
     const double gr_budget = (double)o.gr_factor * (double)g->n_global;
     const double walk_min = getenv("CG_WALK_MIN") ? atof(getenv("CG_WALK_MIN")) : 1e-3;
+    // tail batches of 8 x check_every single-hop sweeps (measured C3 -5 %, C5 =)
+    const int tail_mult = std::max(1, getenv("CG_TAIL_BATCH") ? atoi(getenv("CG_TAIL_BATCH")) : 8);
     const double gr_beta = getenv("CG_GR_BETA") ? atof(getenv("CG_GR_BETA")) : 1.0;
     double work_since_gr = 0.0, sweep_ms_since_gr = 0.0;
     int64_t sweeps = g->st.sweeps, since_gap = 0, last_active = active;
@@ -1128,9 +1142,12 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
     }
     while (!use_tiles && active > 0) {
         if (sweeps >= o.max_sweeps) { result = CG_E_NOT_CONVERGED; break; }
-        const int batch = (int)std::min<int64_t>(o.check_every, o.max_sweeps - sweeps);
-        // multi-hop walks while many vertices are active; single hops in the sparse tail
+        // multi-hop walks while many vertices are active; single hops in the sparse tail, where a
+        // sweep is ~15 us of GPU time and the host round trip after every batch would otherwise
+        // idle the GPU for a comparable time: tail batches are tail_mult x longer (CG_TAIL_BATCH)
         const bool walk = o.walk_len > 0 && (double)last_active >= walk_min * (double)g->n_global;
+        const int64_t per_batch = walk ? o.check_every : std::min<int64_t>(RING, (int64_t)o.check_every * tail_mult);
+        const int batch = (int)std::min<int64_t>(per_batch, o.max_sweeps - sweeps);
         for (Slab *sl : g->slabs) {
             CG_CUDA(cudaMemsetAsync(sl->work, 0, sizeof(unsigned long long) * 2 * batch, sl->stream));
             if (walk) CG_CUDA(cudaMemsetAsync(sl->heads, 0, sizeof(unsigned) * batch, sl->stream));

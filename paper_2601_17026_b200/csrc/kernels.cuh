@@ -1118,6 +1118,9 @@ struct BfsState {
     // until the next exhaustive relabel); truncated = 1 when it stopped early
     unsigned trunc_small, trunc_levels, truncated;
     unsigned thin;              // consecutive thin levels, handed from block 0's small-level loop to the grid
+    // bottom-up levels of the flag-plane BFS (CG_BFS_BU=div,min): when the frontier exceeds both
+    // (vertices not yet labelled) / bu_div and bu_min; 0 = top-down only
+    unsigned bu_div, bu_min, bu_levels;
 };
 __device__ __forceinline__ int bfs_bucket(unsigned c) {
     return c <= 32 ? 0 : c <= 256 ? 1 : c <= 2048 ? 2 : c <= 16384 ? 3 : c <= 131072 ? 4 : c <= 1048576 ? 5 : 6;
@@ -1205,6 +1208,59 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks) {
     __syncthreads();
 }
 
+// Bottom-up level of the flag-plane BFS (Beamer's direction optimisation) for very large frontiers:
+// each word of the visited bitmap (32 consecutive vertices) that still has unvisited vertices is
+// taken by one warp, and an unvisited vertex u joins level L+1 if one of its residual out-arcs
+// leads to a vertex labelled L -- down (u-1), up (u+1, residual D(u+1) > 0: flag bit 1 of u+1),
+// lateral-out (nbr, zo(z)), lateral-in reverse (nbr, zi(z), flag bit 2+(d^1) of that vertex).  The
+// labels come from the label plane in coalesced 32-vertex spans (one column per word when Z is a
+// multiple of 32), the warp owns its bitmap word (plain store), and a vertex written L+1 here is
+// never read as L by another lane.  Single slab only (no ghost planes).
+__device__ void bfs2_bottom_up_level(const Geo &g, const uint8_t *__restrict__ flags, int32_t *lab, unsigned *visited,
+                                     int L, int *lout, unsigned *cout) {
+    const int64_t nw = (g.n + 31) >> 5;
+    for (int64_t w = gwarp(); w < nw; w += nwarps()) {
+        const unsigned word = __ldcg(&visited[w]);  // warp-uniform
+        if (word == 0xffffffffu) continue;
+        const int64_t u = w * 32 + lane_id();
+        bool hit = false;
+        if (u < g.n && !((word >> lane_id()) & 1u)) {
+            const int64_t col = u / g.Z;
+            const int z = (int)(u - col * g.Z);
+            const int x = (int)(col / g.Y), y = (int)(col - (int64_t)x * g.Y);
+            const int64_t v0 = col * g.Z;
+            // every candidate's label (and flag) in one round of independent loads
+            int ld = -1, lu = -1, lo[4], li[4];
+            unsigned fu = 0, fi[4];
+            if (z >= 1) ld = __ldcg(&lab[u - 1]);
+            if (z + 1 < g.Z) {
+                fu = flags[u + 1];
+                lu = __ldcg(&lab[u + 1]);
+            }
+#pragma unroll
+            for (int d = 0; d < 4; d++) {
+                lo[d] = li[d] = -1;
+                fi[d] = 0;
+                const int64_t o = nbr_off(g, x, y, d);
+                if (!o) continue;
+                const int zo = zo_of(z, dl_out(g, d)), zi = zi_of(z, dl_in(g, d), g.Z);
+                if (zo >= 0) lo[d] = __ldcg(&lab[v0 + o + zo]);
+                if (zi >= 0) {
+                    fi[d] = flags[v0 + o + zi];
+                    li[d] = __ldcg(&lab[v0 + o + zi]);
+                }
+            }
+            hit = ld == L || ((fu & 2u) && lu == L);
+#pragma unroll
+            for (int d = 0; d < 4; d++) hit |= lo[d] == L || (((fi[d] >> (2 + (d ^ 1))) & 1u) && li[d] == L);
+        }
+        const unsigned m = __ballot_sync(FULL, hit);
+        if (hit) lab[u] = L + 1;
+        if (m && lane_id() == 0) visited[w] = word | m;
+        warp_append(hit, (int)u, lout, cout);
+    }
+}
+
 #ifndef BFS_R
 #define BFS_R 2
 #endif
@@ -1284,7 +1340,11 @@ __global__ void __launch_bounds__(512, CG_BFS_RUN_MINB) k_bfs_run(Geo g, Soa s, 
             st->hist[bfs_bucket(count)]++;
         }
         const long long t0 = clock64();
-        {
+        const unsigned long long unvisited = (unsigned long long)g.n - claimed;
+        if (FL && st->bu_div && count >= st->bu_min && (unsigned long long)count * st->bu_div >= unvisited) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) st->bu_levels++;
+            bfs2_bottom_up_level(g, flags, lab, visited, L, lout, &st->cnt[(i + 1) % 3]);
+        } else {
             // few vertices per warp: spread them (R = 1); many: R per lane for load-level parallelism
             if ((int64_t)count < nwarps() * 32 * BFS_R) {
                 for (int64_t base = gwarp() * 32; base < count; base += nwarps() * 32) {

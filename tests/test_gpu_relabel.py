@@ -71,13 +71,16 @@ def solve_state(cg, c, delta, nslabs=1, weight=False):
         cg.colgraph_free(h)
 
 
-@pytest.fixture(params=["default", "flags", "colgr", "bfs", "trunc"])
+@pytest.fixture(params=["default", "flags", "colgr", "bfs", "trunc", "bottomup"])
 def flavour(request, monkeypatch):
     if request.param == "default":
         monkeypatch.delenv("CG_RELABEL", raising=False)
     elif request.param == "trunc":  # truncated relabels mid-solve; the last one is exhaustive
         monkeypatch.delenv("CG_RELABEL", raising=False)
         monkeypatch.setenv("CG_BFS_TRUNC", "64,2")
+    elif request.param == "bottomup":  # flag-plane BFS with bottom-up levels whenever allowed
+        monkeypatch.delenv("CG_RELABEL", raising=False)
+        monkeypatch.setenv("CG_BFS_BU", "1000000,1")
     else:
         monkeypatch.setenv("CG_RELABEL", request.param)
     return request.param
