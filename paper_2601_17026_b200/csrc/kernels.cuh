@@ -1215,7 +1215,7 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks) {
 // lateral-out (nbr, zo(z)), lateral-in reverse (nbr, zi(z), flag bit 2+(d^1) of that vertex).  The
 // labels come from the label plane in coalesced 32-vertex spans (one column per word when Z is a
 // multiple of 32), the warp owns its bitmap word (plain store), and a vertex written L+1 here is
-// never read as L by another lane.  Single slab only (no ghost planes).
+// never read as L by another lane.  Neighbour columns in ghost planes are skipped (in-slab BFS).
 __device__ void bfs2_bottom_up_level(const Geo &g, const uint8_t *__restrict__ flags, int32_t *lab, unsigned *visited,
                                      int L, int *lout, unsigned *cout) {
     const int64_t nw = (g.n + 31) >> 5;
@@ -1242,7 +1242,9 @@ __device__ void bfs2_bottom_up_level(const Geo &g, const uint8_t *__restrict__ f
                 lo[d] = li[d] = -1;
                 fi[d] = 0;
                 const int64_t o = nbr_off(g, x, y, d);
-                if (!o) continue;
+                // paths inside this slab only: a ghost column's labels are not this BFS's (on x-slabs
+                // the boundary fixpoint brings the cross-slab paths in afterwards)
+                if (!o || !owned(g, v0 + o)) continue;
                 const int zo = zo_of(z, dl_out(g, d)), zi = zi_of(z, dl_in(g, d), g.Z);
                 if (zo >= 0) lo[d] = __ldcg(&lab[v0 + o + zo]);
                 if (zi >= 0) {
