@@ -110,6 +110,11 @@ struct cg_graph {
     std::vector<Slab *> slabs;  // slabs owned by this process
     ncclComm_t comm = nullptr;
     int64_t *d_red = nullptr;   // NCCL allreduce buffer
+    // in-process slabs: descriptors + state of the all-slab BFS launch (k_bfs_run_slabs)
+    SlabBfsDesc *d_sdesc = nullptr;
+    MultiBfsState *d_mst = nullptr, *h_mst = nullptr;
+    std::vector<SlabBfsDesc> h_sdesc;
+    int mslab_grid = 0;
     int64_t *h_red = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int64_t n_global = 0;
@@ -660,13 +665,53 @@ cg_status colgr_strict(cg_graph *g, Slab *sl) {
 // restarts the fixpoint.  Stop when no slab listed anything (one global sum per exchange): the
 // number of exchanges is the number of slab-boundary crossings of the shortest paths (+1), not the
 // BFS depth (§3.2.2 L274-289 synchronises every level).
+// In-process slabs: every slab's in-slab flag-plane BFS in ONE cooperative launch (k_bfs_run_slabs).
+cg_status bfs_slabs_flags(cg_graph *g) {
+    const int S = (int)g->slabs.size();
+    Slab *s0 = g->slabs[0];
+    cudaStream_t st = s0->stream;  // in-process slabs share the stream
+    if (!g->d_sdesc) {
+        CG_CUDA(cudaMalloc(&g->d_sdesc, sizeof(SlabBfsDesc) * S));
+        CG_CUDA(cudaMalloc(&g->d_mst, sizeof(MultiBfsState)));
+        CG_CUDA(cudaHostAlloc(&g->h_mst, sizeof(MultiBfsState), cudaHostAllocDefault));
+        g->h_sdesc.resize(S);
+        for (int k = 0; k < S; k++) {
+            Slab *sl = g->slabs[k];
+            g->h_sdesc[k] = SlabBfsDesc{sl->geo, sl->s, {sl->blist[0], sl->blist[1]}, sl->bst->cnt, sl->visited,
+                                        sl->gflags, sl->lab};
+        }
+        CG_CUDA(cudaMemcpy(g->d_sdesc, g->h_sdesc.data(), sizeof(SlabBfsDesc) * S, cudaMemcpyHostToDevice));
+    }
+    for (Slab *sl : g->slabs) {
+        const Geo &geo = sl->geo;
+        CG_CUDA(cudaMemsetAsync(sl->bst, 0, sizeof(BfsState), st));
+        k_bfs2_init<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, st>>>(geo, sl->s, sl->gflags, sl->lab,
+                                                                             sl->visited, sl->blist[0], &sl->bst->cnt[0]);
+        g->st.kernel_launches++;
+    }
+    CG_CUDA(cudaMemsetAsync(g->d_mst, 0, sizeof(MultiBfsState), st));
+    g->h_mst->L = 1;
+    CG_CUDA(cudaMemcpyAsync(&g->d_mst->L, &g->h_mst->L, sizeof(int), cudaMemcpyHostToDevice, st));
+    int Sarg = S;
+    void *args[] = {(void *)&g->d_sdesc, (void *)&Sarg, (void *)&g->d_mst};
+    CG_CUDA(cudaLaunchCooperativeKernel((const void *)k_bfs_run_slabs, g->mslab_grid, 512, args, 0, st));
+    g->st.kernel_launches++;
+    CG_CUDA(cudaMemcpyAsync(g->h_mst, g->d_mst, sizeof(MultiBfsState), cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaStreamSynchronize(st));
+    g->st.gr_passes += g->h_mst->L - 1;
+    return CG_OK;
+}
+
 //   bfs_init: each slab first computes its in-slab distances with the flag-plane BFS (paths that
 //   stay inside the slab: upper bounds of the true distances, work-efficient); the fixpoint then
 //   only corrects the labels that cross-slab paths lower.  Otherwise the fixpoint starts from INF.
 cg_status colgr_slabs(cg_graph *g, bool bfs_init) {
+    const bool all_slabs = bfs_init && g->local && g->mslab_grid > 0 && (int)g->slabs.size() <= MSLAB_MAX &&
+                           !(getenv("CG_SLAB_BFS_EACH") && atoi(getenv("CG_SLAB_BFS_EACH")));
+    if (all_slabs) CG_TRY(bfs_slabs_flags(g));
     for (Slab *sl : g->slabs) {
         if (bfs_init) {
-            CG_TRY(bfs_strict(g, sl, true, true));
+            if (!all_slabs) CG_TRY(bfs_strict(g, sl, true, true));
             CG_TRY(colgr_begin(g, sl, false));
         } else {
             CG_TRY(colgr_begin(g, sl));
@@ -1309,6 +1354,9 @@ void colgraph_free(cg_graph *g) {
         for (Slab *sl : g->slabs) slab_free(sl);
         if (g->comm) comm_release(g->comm);
         if (g->d_red) cudaFree(g->d_red);
+        if (g->d_sdesc) cudaFree(g->d_sdesc);
+        if (g->d_mst) cudaFree(g->d_mst);
+        if (g->h_mst) cudaFreeHost(g->h_mst);
         if (g->h_red) cudaFreeHost(g->h_red);
         if (g->ev0) cudaEventDestroy(g->ev0);
         if (g->ev1) cudaEventDestroy(g->ev1);
@@ -1406,6 +1454,13 @@ static cg_status build_common(const cg_dims *dims, const int32_t *cost_dev, int3
         const int32_t *bsrc = band_dev ? (local ? band_dev + (int64_t)x0 * dims->Y * 2 : band_dev) : nullptr;
         const cg_status s = slab_build(sl, src, input_is_weight ? 1 : 0, bsrc);
         if (s != CG_OK) return fail(s);
+    }
+    if (local && nslabs_local > 1) {  // all-slab BFS launch (k_bfs_run_slabs)
+        int per_sm = 0, coop = 0;
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dd.device);
+        if (coop && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bfs_run_slabs, 512, 0) == cudaSuccess &&
+            per_sm > 0)
+            g->mslab_grid = num_sms;
     }
     int64_t fl = 0;
     for (Slab *sl : g->slabs) fl |= sl->h_flags[0];

@@ -138,6 +138,15 @@ def test_labels_exact_slabs(cg, flavour, ns):
     check(cg, c, 3, nslabs=ns, ctx=f"C2 crop /{ns}")
 
 
+@pytest.mark.parametrize("each", ["0", "1"])
+def test_labels_exact_slabs_bfs_launch(cg, monkeypatch, each):
+    """In-process slabs: the in-slab BFS of all slabs in one launch (default) or one launch per slab."""
+    monkeypatch.delenv("CG_RELABEL", raising=False)
+    monkeypatch.setenv("CG_SLAB_BFS_EACH", each)
+    for ns in (2, 4, 7):
+        check(cg, V.generate("C2")[:56], 3, nslabs=ns, ctx=f"C2 crop /{ns} each={each}")
+
+
 def test_colgr_counts_rounds(cg, monkeypatch):
     """The fixpoint reports its rounds in gr_passes (one launch per relabel on one slab)."""
     monkeypatch.setenv("CG_RELABEL", "colgr")
