@@ -1508,6 +1508,18 @@ static cg_status maxflow_solve_impl(cg_graph *g, const cg_solve_opts *opts, int6
     const bool trace = tracing();
     const double t0 = now_ms();
     Slab *s0 = g->slabs[0];
+    // a1': optional exact per-column pre-cancellation (a valid initial preflow)
+    const size_t pc_smem = (size_t)8 * (g->dims.Z + 1) * sizeof(long long);
+    if (getenv("CG_PRECANCEL") && atoi(getenv("CG_PRECANCEL")) && pc_smem <= 200 * 1024 && !g->slabs[0]->geo.soft_k) {
+        if (pc_smem > 48 * 1024)
+            CG_CUDA(cudaFuncSetAttribute(k_precancel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pc_smem));
+        for (Slab *sl : g->slabs) {
+            k_precancel<<<grid_for((int64_t)sl->geo.X * sl->geo.Y * 32, 256, sl->num_sms * 16), 256, pc_smem,
+                          sl->stream>>>(sl->geo, sl->s, sl->flags);
+            g->st.kernel_launches++;
+        }
+        CG_CUDA(cudaGetLastError());
+    }
     double ms_gr = 0.0;
     const cg_status result = pr_loop(g, o, use_tiles, ms_gr);
     if (result != CG_OK && result != CG_E_NOT_CONVERGED) return result;

@@ -1569,6 +1569,94 @@ __global__ void k_sum_T(Geo g, const Field T, unsigned long long *out) {
     if (lane_id() == 0 && acc) atomicAdd(out, (unsigned long long)acc);
 }
 
+// ------------------------------------------------------------------ a1': column pre-cancellation
+// Exact max-flow of every column in isolation (ignoring lateral arcs), applied as the
+// initial preflow: source excess may only move DOWN a column (infinite down arcs) into
+// sink arcs below it, and the top-down greedy is optimal because the set of sinks a
+// source can feed is nested.  With a(z) = E(z) - T(z) and S(z) = sum_{j>=z} a(j):
+//   carry leaving z downward    c(z) = S(z) - min_{m in [z, Z]} S(m)       (S(Z) = 0)
+//   absorbed at a sink          ab(z) = min(T(z), c(z+1))
+//   flow on the down arc z->z-1 f(z) = min(c(z), sum_{z'<z} ab(z'))  (only what is absorbed below)
+//   new state  T -= ab,  D = f,  E = f(z+1) + E(z) - ab(z) - f(z) >= 0.
+// Not in the paper: an accelerator whose result is a valid preflow, so the maximum flow
+// and the minimal cut are unchanged.  One warp per column, z in chunks of 32.
+__device__ __forceinline__ long long warp_suffix_sum_ll(long long v) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long t = __shfl_down_sync(FULL, v, o);
+        if (lane_id() + o < 32) v += t;
+    }
+    return v;
+}
+__device__ __forceinline__ long long warp_suffix_min_ll(long long v) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long t = __shfl_down_sync(FULL, v, o);
+        if (lane_id() + o < 32) v = min(v, t);
+    }
+    return v;
+}
+__device__ __forceinline__ long long warp_excl_prefix_sum_ll(long long v) {
+    long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long t = __shfl_up_sync(FULL, x, o);
+        if (lane_id() >= o) x += t;
+    }
+    return x - v;
+}
+
+__global__ void __launch_bounds__(256) k_precancel(Geo g, Soa s, int *flags) {
+    extern __shared__ long long sh_c[];  // per warp: Z+1 carries c(z)
+    long long *cz = sh_c + (int64_t)(threadIdx.x >> 5) * (g.Z + 1);
+    const int64_t ncol = (int64_t)g.X * g.Y;
+    const int last_c0 = ((g.Z - 1) >> 5) << 5;
+    bool bad = false;
+    for (int64_t col = gwarp(); col < ncol; col += nwarps()) {
+        const int64_t v0 = col * g.Z;
+        long long sum_above = 0, min_above = 0;  // S over chunks above; min over m above incl. S(Z) = 0
+        if (lane_id() == 0) cz[g.Z] = 0;
+        for (int c0 = last_c0; c0 >= 0; c0 -= 32) {
+            const int z = c0 + lane_id();
+            long long a = 0;
+            if (z < g.Z) a = (long long)s.E[v0 + z] - (long long)s.T[v0 + z];
+            const long long S = warp_suffix_sum_ll(a) + sum_above;
+            const long long m = min(warp_suffix_min_ll(z < g.Z ? S : LLONG_MAX), min_above);
+            if (z < g.Z) cz[z] = S - m;
+            sum_above = __shfl_sync(FULL, S, 0);
+            min_above = __shfl_sync(FULL, m, 0);
+        }
+        __syncwarp();
+        long long ab_below = 0;
+        for (int c0 = 0; c0 < g.Z; c0 += 32) {
+            const int z = c0 + lane_id();
+            const bool ok = z < g.Z;
+            int e = 0, t = 0;
+            long long ab = 0, f = 0;
+            if (ok) {
+                e = s.E[v0 + z];
+                t = s.T[v0 + z];
+                ab = t > 0 ? min((long long)t, cz[z + 1]) : 0;
+            }
+            const long long AB = warp_excl_prefix_sum_ll(ab) + ab_below;
+            if (ok && z >= 1) f = min(cz[z], AB);
+            long long f_up = __shfl_down_sync(FULL, f, 1);
+            const long long ab_total = __shfl_sync(FULL, AB + ab, 31);
+            if (lane_id() == 31) f_up = (z + 1 < g.Z) ? min(cz[z + 1], ab_total) : 0;
+            if (ok) {
+                const long long ne = f_up + (long long)e - ab - f;
+                if (ne < 0 || ne > INT_MAX || f > INT_MAX) bad = true;
+                s.E[v0 + z] = (int32_t)ne;
+                s.T[v0 + z] = t - (int32_t)ab;
+                s.D[v0 + z] = (int32_t)f;
+            }
+            ab_below = ab_total;
+        }
+        __syncwarp();
+    }
+    if (bad) atomicOr(flags, FLAG_OVERFLOW);
+}
+
 // ------------------------------------------------------------------ a7: extraction
 // Minimal source set S = forward residual closure of {v : E(v) > 0} (R5,
 // SURVEY.md V3).  Infinite down arcs make S downward closed per column, so S is
