@@ -162,7 +162,25 @@ typedef struct {
     int64_t tile_visits;       /* tile visits summed over all phases (tile sweeps only) */
     int64_t relabel_ops;       /* sweep operations that were relabels (vertex worklists) */
     int64_t gr_truncated;      /* global relabels that deferred a thin BFS tail (CG_BFS_TRUNC) */
+    /* maxflow_solve_bk only (NEXT-4); zero after maxflow_solve */
+    int64_t bk_stages;         /* merge stages run (one launch each) */
+    int64_t bk_growths;        /* growth steps (an active vertex's arcs scanned once) */
+    int64_t bk_augmentations;  /* augmenting paths */
+    int64_t bk_orphans;        /* orphans processed by the adoption stage */
+    int64_t bk_freed;          /* orphans that found no parent and became free */
+    double ms_bk_last_stages;  /* CUDA-event time of the stages with <= 4 segments (the serial tail) */
 } cg_solve_stats;
+
+/* Options of maxflow_solve_bk (NULL = defaults).
+ *   seg_x, seg_y : columns per first-stage segment along x and y (0 = default 1: measured fastest,
+ *                  larger first segments grow deep trees whose orphans cascade); every segment
+ *                  spans all of Z (§3.1: the volume is split "along the columns and
+ *                  slices", the two dominant dimensions)
+ *   time_limit_ms: give up with CG_E_NOT_CONVERGED when a stage runs longer (0 = 600000) */
+typedef struct {
+    int32_t seg_x, seg_y;
+    int32_t time_limit_ms;
+} cg_bk_opts;
 
 /* a1 -- build the int32 structure-of-arrays residual graph.
  *   cost_dev : device int32[X_r*Y*Z], this rank's x-slab [x][y][z], z fastest;
@@ -261,6 +279,22 @@ cg_status cg_nccl_loopback(int32_t enable);
  * Errors: CG_E_STATE (already solved), CG_E_OVERFLOW, CG_E_CUDA, CG_E_NCCL,
  *         CG_E_NOT_CONVERGED. */
 cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_value, cg_solve_stats *stats);
+
+/* NEXT-4 -- the paper's first parallelisation, parallel Boykov-Kolmogorov with hierarchical
+ * merging (§3.1; BK's growth / augmentation / adoption stages, §2.2),
+ * as a second solver on the same handle: the volume is cut into segments of seg_x x seg_y columns,
+ * BK exhausts the augmenting paths inside every segment in parallel (one warp per segment), then
+ * adjacent segments merge pairwise (alternating x and y) and the search trees grow across the old
+ * boundaries, until one segment covers the volume.  The result is a maximum FLOW whose residual
+ * state the other calls read like maxflow_solve's: mincut_extract_surface gives the same minimal
+ * source set and surface, maxflow_export_flow the flow on every arc.
+ *   flow_value : host int64, receives |f| (Eq. 5).
+ *   opts, stats: nullable.
+ * One slab, hard smoothness only (general intervals and narrow bands included): handles from
+ * colgraph_build_slabs*, NCCL ranks or soft penalties return CG_E_INVAL.
+ * Errors: CG_E_INVAL, CG_E_STATE (already solved), CG_E_OVERFLOW (an arc flow above INT32_MAX),
+ *         CG_E_NOT_CONVERGED (time_limit_ms passed), CG_E_CUDA (incl. an internal tree check). */
+cg_status maxflow_solve_bk(cg_graph *g, const cg_bk_opts *opts, int64_t *flow_value, cg_solve_stats *stats);
 
 /* a7 -- minimal min-cut source set and surface (Theorem 1).
  *   surface_dev : device int32[X_r*Y], S(x,y) = max{z : (x,y,z) in S}, -1 if none.

@@ -58,10 +58,16 @@ class cg_solve_stats(ctypes.Structure):
                 ("ms_sweeps", ctypes.c_double), ("bytes_per_sweep_alg", ctypes.c_double),
                 ("source_capacity", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
                 ("ms_sweep_kernels", ctypes.c_double), ("sweep_bytes_alg", ctypes.c_double),
-                ("tile_visits", ctypes.c_int64), ("relabel_ops", ctypes.c_int64), ("gr_truncated", ctypes.c_int64)]
+                ("tile_visits", ctypes.c_int64), ("relabel_ops", ctypes.c_int64), ("gr_truncated", ctypes.c_int64),
+                ("bk_stages", ctypes.c_int64), ("bk_growths", ctypes.c_int64), ("bk_augmentations", ctypes.c_int64),
+                ("bk_orphans", ctypes.c_int64), ("bk_freed", ctypes.c_int64), ("ms_bk_last_stages", ctypes.c_double)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class cg_bk_opts(ctypes.Structure):
+    _fields_ = [("seg_x", ctypes.c_int32), ("seg_y", ctypes.c_int32), ("time_limit_ms", ctypes.c_int32)]
 
 
 def _load():
@@ -91,6 +97,8 @@ def _load():
     lib.cg_nccl_loopback.argtypes = [ctypes.c_int32]
     lib.maxflow_solve.restype = ctypes.c_int
     lib.maxflow_solve.argtypes = [ctypes.c_void_p, P(cg_solve_opts), P(ctypes.c_int64), P(cg_solve_stats)]
+    lib.maxflow_solve_bk.restype = ctypes.c_int
+    lib.maxflow_solve_bk.argtypes = [ctypes.c_void_p, P(cg_bk_opts), P(ctypes.c_int64), P(cg_solve_stats)]
     lib.mincut_extract_surface.restype = ctypes.c_int
     lib.mincut_extract_surface.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
     lib.colgraph_solve_host.restype = ctypes.c_int
@@ -116,7 +124,7 @@ def _load():
 
 _lib = _load()
 
-EXPORTED = ["colgraph_build", "colgraph_build_slabs", "colgraph_build_soft", "colgraph_build_slabs_soft", "colgraph_build_general", "cg_nccl_unique_id", "cg_nccl_loopback", "maxflow_solve", "mincut_extract_surface",
+EXPORTED = ["colgraph_build", "colgraph_build_slabs", "colgraph_build_soft", "colgraph_build_slabs_soft", "colgraph_build_general", "cg_nccl_unique_id", "cg_nccl_loopback", "maxflow_solve", "maxflow_solve_bk", "mincut_extract_surface",
             "maxflow_export_flow", "colgraph_solve_host",
             "colgraph_export_state", "colgraph_stats", "colgraph_free", "cg_status_str", "cg_slab_range", "cg_version"]
 
@@ -300,6 +308,15 @@ def maxflow_solve(handle, opts: cg_solve_opts | None = None):
     return st, int(flow.value), stats.as_dict()
 
 
+def maxflow_solve_bk(handle, seg_x: int = 0, seg_y: int = 0, time_limit_ms: int = 0):
+    """NEXT-4: parallel BK with hierarchical merging (include/colgraph.h).  Returns (status, |f|, stats)."""
+    flow = ctypes.c_int64(0)
+    stats = cg_solve_stats()
+    o = cg_bk_opts(int(seg_x), int(seg_y), int(time_limit_ms))
+    st = _lib.maxflow_solve_bk(handle, ctypes.byref(o), ctypes.byref(flow), ctypes.byref(stats))
+    return st, int(flow.value), stats.as_dict()
+
+
 def mincut_extract_surface(handle, surface, mask=None) -> int:
     _check_dev_int32(surface, "surface")
     return _lib.mincut_extract_surface(handle, ctypes.c_void_p(surface.data_ptr()),
@@ -383,9 +400,9 @@ def cg_slab_range(X: int, Y: int, Z: int, delta: int, rank: int, nranks: int):
 
 
 def solve(cost, delta: int, input_is_weight: bool = False, want_mask: bool = True, opts=None, nslabs: int = 1,
-          penalty=None, band=None):
+          penalty=None, band=None, bk=None):
     """Device-resident convenience: build -> solve -> extract on a CUDA int32 tensor
-    (nslabs > 1: the in-process x-slab path).
+    (nslabs > 1: the in-process x-slab path; bk = (seg_x, seg_y) or True: maxflow_solve_bk, NEXT-4).
     Returns dict(status, extract_status, flow, surface (tensor), mask (tensor), stats)."""
     import torch
     X, Y, Z = cost.shape
@@ -398,7 +415,11 @@ def solve(cost, delta: int, input_is_weight: bool = False, want_mask: bool = Tru
         h = colgraph_build(cost, delta, input_is_weight) if nslabs == 1 else \
             colgraph_build_slabs(cost, delta, nslabs, input_is_weight)
     try:
-        st, flow, stats = maxflow_solve(h, opts)
+        if bk is not None and bk is not False:
+            sx, sy = (0, 0) if bk is True else bk
+            st, flow, stats = maxflow_solve_bk(h, sx, sy)
+        else:
+            st, flow, stats = maxflow_solve(h, opts)
         surface = torch.empty((X, Y), dtype=torch.int32, device=cost.device)
         mask = torch.empty((X, Y, Z), dtype=torch.uint8, device=cost.device) if want_mask else None
         est = mincut_extract_surface(h, surface, mask) if st == CG_OK else CG_E_STATE

@@ -29,6 +29,7 @@
 #include "nccl_shim.h"
 #include "nccl_loopback.h"
 #include "tile.cuh"
+#include "bk.cuh"
 
 #include <algorithm>
 #include <chrono>
@@ -1597,6 +1598,93 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
     }
 #endif
     return debug_check(maxflow_solve_impl(g, opts, flow_value, stats));
+}
+
+// NEXT-4: parallel BK with hierarchical merging (bk.cuh; §3.1).  The segment
+// schedule: first-stage segments of bx x by columns, then pairwise merges alternating x and y (an
+// axis stops merging once its segments span the volume) until one segment remains.
+static cg_status maxflow_solve_bk_impl(cg_graph *g, const cg_bk_opts *opts, int64_t *flow_value, cg_solve_stats *stats) {
+    if (!g || !flow_value) return CG_E_INVAL;
+    if (g->solved) return CG_E_STATE;
+    if (g->slabs.size() != 1 || multi(g) || g->slabs[0]->geo.soft_k) return CG_E_INVAL;
+    const int bx = opts && opts->seg_x > 0 ? opts->seg_x : 1, by = opts && opts->seg_y > 0 ? opts->seg_y : 1;
+    const int limit_ms = opts && opts->time_limit_ms > 0 ? opts->time_limit_ms : 600000;
+    DeviceGuard dg(g->dist.device);
+    Slab *sl = g->slabs[0];
+    const Geo &geo = sl->geo;
+    cudaStream_t st = sl->stream;
+    const double t0 = now_ms();
+    BkArrays a{sl->blist[0], sl->blist[1], sl->vstamp, sl->lab, sl->u64 + 8, sl->flags + 8, sl->flags};
+    CG_CUDA(cudaMemsetAsync(a.ctr, 0, 4 * sizeof(unsigned long long), st));
+    CG_CUDA(cudaMemsetAsync(sl->flags, 0, 16 * sizeof(int), st));
+    k_bk_init<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, st>>>(geo, sl->s, a);
+    g->st.kernel_launches++;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    CG_CUDA(cudaEventCreate(&e0));
+    CG_CUDA(cudaEventCreate(&e1));
+    bool tail_started = false;
+    int sx = std::min(bx, geo.X), sy = std::min(by, geo.Y), axis = -1, half = 0;
+    bool prefer_x = true;
+    int64_t stages = 0;
+    cg_status result = CG_OK;
+    for (;;) {
+        const int nsx = (geo.X + sx - 1) / sx, nsy = (geo.Y + sy - 1) / sy;
+        if (nsx * nsy <= 4 && !tail_started) {
+            tail_started = true;
+            CG_CUDA(cudaEventRecord(e0, st));
+        }
+        k_bk_stage<<<nsx * nsy, 32, 0, st>>>(geo, sl->s, a, sx, sy, axis, half, (unsigned long long)limit_ms * 1000000ull);
+        k_bk_time_fold<<<1, 1, 0, st>>>(a);
+        g->st.kernel_launches += 2;
+        stages++;
+        CG_CUDA(cudaGetLastError());
+        if (nsx == 1 && nsy == 1) break;
+        // next merge: x and y alternate while both still have more than one segment
+        const bool can_x = nsx > 1, can_y = nsy > 1;
+        if (can_x && (prefer_x || !can_y)) {
+            half = sx, sx *= 2, axis = 0;
+        } else {
+            half = sy, sy *= 2, axis = 1;
+        }
+        prefer_x = !prefer_x;
+    }
+    if (!tail_started) CG_CUDA(cudaEventRecord(e0, st));
+    CG_CUDA(cudaEventRecord(e1, st));
+    // a6: |f| = sum(T0) - sum(T)
+    CG_CUDA(cudaMemsetAsync(sl->u64 + 2, 0, sizeof(unsigned long long), st));
+    k_sum_T<<<sl->num_sms * 8, 256, 0, st>>>(geo, sl->s.T, sl->u64 + 2);
+    g->st.kernel_launches++;
+    CG_CUDA(cudaMemcpyAsync(sl->h_u64, sl->u64, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaMemcpyAsync(sl->h_flags, sl->flags, 16 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CG_CUDA(cudaStreamSynchronize(st));
+    float ms_tail = 0.f;
+    cudaEventElapsedTime(&ms_tail, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    CG_CUDA(cudaGetLastError());
+    const int err = sl->h_flags[10];
+    if (err & 8) result = CG_E_NOT_CONVERGED;
+    else if (err) result = CG_E_CUDA;
+    else if (sl->h_flags[0] & FLAG_OVERFLOW) result = CG_E_OVERFLOW;
+    if (err && getenv("CG_DEBUG")) fprintf(stderr, "colgraph: maxflow_solve_bk error flags %d\n", err);
+    *flow_value = sl->sumT0 - (int64_t)sl->h_u64[2];
+    g->st.bk_stages = stages;
+    g->st.sweeps = stages;
+    g->st.bk_growths = (int64_t)sl->h_u64[8];
+    g->st.work = g->st.bk_growths;
+    g->st.bk_augmentations = (int64_t)sl->h_u64[9];
+    g->st.bk_orphans = (int64_t)sl->h_u64[10];
+    g->st.bk_freed = (int64_t)sl->h_u64[11];
+    g->st.ms_bk_last_stages = ms_tail;
+    g->st.ms_solve = now_ms() - t0;
+    g->st.ms_sweeps = g->st.ms_solve;
+    g->solved = result == CG_OK;
+    if (stats) *stats = g->st;
+    return result;
+}
+
+cg_status maxflow_solve_bk(cg_graph *g, const cg_bk_opts *opts, int64_t *flow_value, cg_solve_stats *stats) {
+    return debug_check(maxflow_solve_bk_impl(g, opts, flow_value, stats));
 }
 
 static cg_status mincut_extract_surface_impl(cg_graph *g, int32_t *surface_dev, uint8_t *mask_dev) {
