@@ -75,5 +75,7 @@ if __name__ == "__main__":
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_nopre.so"), defines=("CG_BFS_PRECHECK=0",)))
     if "--bfs-minb2" in sys.argv:
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_bfs2.so"), defines=("CG_BFS_RUN_MINB=2",)))
+    if "--bfs-serial-atom" in sys.argv:
+        print(build(force=True, lib=os.path.join(PKG, "libcolgraph_bfsser.so"), defines=("CG_BFS_ATOM_BATCH=0",)))
     if "--soa" in sys.argv:
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_soa.so"), defines=("CG_LAYOUT_AOS=0",)))

@@ -1057,6 +1057,9 @@ __device__ __forceinline__ void bfs_expand_multi(const Geo &g, const Soa &s, int
 #ifndef CG_BFS_PRECHECK
 #define CG_BFS_PRECHECK 1
 #endif
+#ifndef CG_BFS_ATOM_BATCH
+#define CG_BFS_ATOM_BATCH 1
+#endif
 #pragma unroll
     for (int r = 0; r < R; r++)
 #pragma unroll
@@ -1067,6 +1070,26 @@ __device__ __forceinline__ void bfs_expand_multi(const Geo &g, const Soa &s, int
     if (!FL && g.soft_k && nl < INF)  // warp-uniform: every lane calls it
         for (int r = 0; r < R; r++) bfs_soft_preds<0>(g, s, vv[r], nl, lout, cout, visited);
     int k = 0;
+#if CG_BFS_ATOM_BATCH
+    // every claim's atomicOr is issued before any label store: a store between two atomics (possibly
+    // aliasing in the compiler's view) would make each atomic wait for the previous one's round trip
+    unsigned old[R][10];
+#pragma unroll
+    for (int r = 0; r < R; r++)
+#pragma unroll
+        for (int j = 0; j < 10; j++)
+            old[r][j] = hw[r][j] ? 0xffffffffu : atomicOr(&visited[w[r][j] >> 5], 1u << (w[r][j] & 31));
+#pragma unroll
+    for (int r = 0; r < R; r++)
+#pragma unroll
+        for (int j = 0; j < 10; j++)
+            if (!((old[r][j] >> (w[r][j] & 31)) & 1u)) {  // claimed: this lane owns w's label
+                if (FL) lab[w[r][j]] = nl;
+                else s.H[w[r][j]] = nl;
+                got[r] |= 1u << j;
+                k++;
+            }
+#else
 #pragma unroll
     for (int r = 0; r < R; r++)
 #pragma unroll
@@ -1080,6 +1103,7 @@ __device__ __forceinline__ void bfs_expand_multi(const Geo &g, const Soa &s, int
                     k++;
                 }
             }
+#endif
     const int incl = warp_incl_scan(k);
     const int total = __shfl_sync(FULL, incl, 31);
     if (total == 0) return;
