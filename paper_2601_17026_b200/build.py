@@ -77,5 +77,9 @@ if __name__ == "__main__":
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_bfs2.so"), defines=("CG_BFS_RUN_MINB=2",)))
     if "--bfs-serial-atom" in sys.argv:
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_bfsser.so"), defines=("CG_BFS_ATOM_BATCH=0",)))
+    if "--bfs-r1b2" in sys.argv:
+        print(build(force=True, lib=os.path.join(PKG, "libcolgraph_bfsr1b2.so"), defines=("BFS_R=1", "CG_BFS_RUN_MINB=2")))
+    if "--no-init-preload" in sys.argv:
+        print(build(force=True, lib=os.path.join(PKG, "libcolgraph_noprel.so"), defines=("CG_INIT_PRELOAD=0",)))
     if "--soa" in sys.argv:
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_soa.so"), defines=("CG_LAYOUT_AOS=0",)))

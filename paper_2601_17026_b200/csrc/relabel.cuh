@@ -23,6 +23,10 @@
 
 #include "kernels.cuh"
 
+#ifndef CG_INIT_PRELOAD
+#define CG_INIT_PRELOAD 1
+#endif
+#define CG_REBUILD_PRELOAD (CG_INIT_PRELOAD && CG_LAYOUT_AOS && !CG_H_PLANE)
 namespace cg {
 
 // flags[v]: bit 0 T(v) > 0 (arc to t), bit 1 D(v) > 0 (residual of the up arc (v-1) -> v),
@@ -49,17 +53,34 @@ __global__ void k_colgr_flags(Geo g, Soa s, uint8_t *flags, int32_t *lab, int64_
 __global__ void k_bfs2_init(Geo g, Soa s, uint8_t *flags, int32_t *lab, unsigned *visited, int *lout,
                             unsigned *cout) {
     // (measured: loading a span's records ahead of the flag writes with streaming loads made this
-    // pass slower, 0.80 -> 1.22 ms at C4 under ncu; the straight loop stays)
+    // pass slower, 0.80 -> 1.22 ms at C4 under ncu; CG_INIT_PRELOAD loads the span's records with
+    // plain loads before any store -- the stores to flags / lab / visited otherwise keep each
+    // record load waiting for the previous iteration's, one DRAM round trip per 32 vertices)
     constexpr int SPAN = 8;
     SpanAppender<SPAN> ap;
     for (int64_t base = gwarp() * 32 * SPAN; base < g.n; base += nwarps() * 32 * SPAN) {
+#if CG_LAYOUT_AOS && CG_INIT_PRELOAD
+        int4 ra[SPAN], rb[SPAN];
+#pragma unroll
+        for (int j = 0; j < SPAN; j++) {
+            const int64_t v = base + 32 * j + lane_id();
+            if (v < g.n) {
+                const int4 *rec = reinterpret_cast<const int4 *>(&s.E[v]);
+                ra[j] = rec[0];
+                rb[j] = rec[1];
+            }
+        }
+#endif
 #pragma unroll
         for (int j = 0; j < SPAN; j++) {
             const int64_t b0 = base + 32 * j;
             const int64_t v = b0 + lane_id();
             bool seed = false;
             if (v < g.n) {
-#if CG_LAYOUT_AOS
+#if CG_LAYOUT_AOS && CG_INIT_PRELOAD
+                const int4 a = ra[j], b = rb[j];
+                const int T = a.z, D = a.w, L0 = b.x, L1 = b.y, L2 = b.z, L3 = b.w;
+#elif CG_LAYOUT_AOS
                 const int4 *rec = reinterpret_cast<const int4 *>(&s.E[v]);  // E H T D | L0 L1 L2 L3
                 const int4 a = rec[0], b = rec[1];
                 const int T = a.z, D = a.w, L0 = b.x, L1 = b.y, L2 = b.z, L3 = b.w;
@@ -351,15 +372,34 @@ __global__ void k_colgr_rebuild(Geo g, Soa s, const int32_t *__restrict__ lab, i
     SpanAppender<SPAN> ap;
     unsigned long long myact = 0;
     for (int64_t base = gwarp() * 32 * SPAN; base < g.n; base += nwarps() * 32 * SPAN) {
+#if CG_REBUILD_PRELOAD
+        int hl[SPAN], hh[SPAN], he[SPAN];  // every load of the span before any store (see k_bfs2_init)
+#pragma unroll
+        for (int j = 0; j < SPAN; j++) {
+            const int64_t v = base + 32 * j + lane_id();
+            if (v < g.n) {
+                hl[j] = lab[v];
+                const int2 eh = *reinterpret_cast<const int2 *>(&s.E[v]);  // E, H (adjacent in the record)
+                he[j] = eh.x;
+                hh[j] = eh.y;
+            }
+        }
+#endif
 #pragma unroll
         for (int j = 0; j < SPAN; j++) {
             const int64_t b0 = base + 32 * j;
             const int64_t v = b0 + lane_id();
             bool a = false;
             if (v < g.n) {
+#if CG_REBUILD_PRELOAD
+                const int h = hl[j];
+                if (hh[j] != h) s.H[v] = h;  // same sector as E: an unchanged label leaves it clean
+                a = he[j] > 0 && h < g.INF;
+#else
                 const int h = lab[v];
                 if (s.H[v] != h) s.H[v] = h;  // same sector as E: an unchanged label leaves it clean
                 a = s.E[v] > 0 && h < g.INF;
+#endif
             }
             if (a) vstamp[v] = tag;
             myact += a;
