@@ -30,7 +30,6 @@
 #include "nccl_loopback.h"
 #include "tile.cuh"
 #include "bk.cuh"
-#include "chunk.cuh"
 
 #include <algorithm>
 #include <chrono>
@@ -1187,37 +1186,17 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
             sweep_ms_since_gr = 0.0;
         }
     }
-    // column-chunk sweeps (chunk.cuh; measured alternative, CG_CHUNK_MIN = fraction of n that must be
-    // active after a relabel for the chunk kind to run until the next relabel; 0 = never)
-    const double chunk_min = getenv("CG_CHUNK_MIN") ? atof(getenv("CG_CHUNK_MIN")) : 0.0;
-    const int chunk_rounds = getenv("CG_CHUNK_ROUNDS") ? atoi(getenv("CG_CHUNK_ROUNDS")) : 32;
-    const bool chunk_ok = chunk_min > 0 && g->slabs.size() == 1 && !multi(g) && !s0->geo.soft_k && CG_LAYOUT_AOS;
-    bool chunk_mode = false;
-    int64_t relabels_seen = -1;
     while (!use_tiles && active > 0) {
         if (sweeps >= o.max_sweeps) { result = CG_E_NOT_CONVERGED; break; }
-        if (chunk_ok && relabels_seen != g->st.global_relabels) {  // a relabel just listed the active vertices
-            relabels_seen = g->st.global_relabels;
-            chunk_mode = (double)active >= chunk_min * (double)g->n_global;
-            if (chunk_mode) {  // list chunks instead
-                Slab *sl = s0;
-                CG_CUDA(cudaMemsetAsync(sl->cnt, 0, 3 * sizeof(unsigned), st0));
-                k_chunk_rebuild<<<grid_for(sl->geo.nchunks, 256, sl->num_sms * 16), 256, 0, st0>>>(
-                    sl->geo, sl->s, sl->blist[0], sl->cnt, sl->vstamp, ++sl->tag);
-                g->st.kernel_launches++;
-                sl->sweep_k = 0;
-            }
-        }
         // multi-hop walks while many vertices are active; single hops in the sparse tail, where a
         // sweep is ~15 us of GPU time and the host round trip after every batch would otherwise
         // idle the GPU for a comparable time: tail batches are tail_mult x longer (CG_TAIL_BATCH)
-        const bool walk = !chunk_mode && o.walk_len > 0 && (double)last_active >= walk_min * (double)g->n_global;
+        const bool walk = o.walk_len > 0 && (double)last_active >= walk_min * (double)g->n_global;
         const int64_t per_batch = walk ? o.check_every : std::min<int64_t>(RING, (int64_t)o.check_every * tail_mult);
         const int batch = (int)std::min<int64_t>(per_batch, o.max_sweeps - sweeps);
         for (Slab *sl : g->slabs) {
             CG_CUDA(cudaMemsetAsync(sl->work, 0, sizeof(unsigned long long) * 2 * batch, sl->stream));
             if (walk) CG_CUDA(cudaMemsetAsync(sl->heads, 0, sizeof(unsigned) * batch, sl->stream));
-            if (chunk_mode) CG_CUDA(cudaMemsetAsync(sl->visits, 0, sizeof(unsigned long long) * batch, sl->stream));
         }
         CG_CUDA(cudaEventRecord(g->ev0, st0));
         for (int i = 0; i < batch; i++) {
@@ -1229,12 +1208,7 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
                 const int k = sl->sweep_k++;
                 sl->out_tag = ++sl->tag;
                 const bool soft = geo.soft_k > 0;
-                if (chunk_mode) {
-                    k_chunk_sweep<<<list_grid(sl, geo.nchunks), 256, 0, sl->stream>>>(
-                        geo, sl->s, chunk_rounds, sl->blist[k & 1], sl->cnt + k % 3, sl->blist[(k + 1) & 1],
-                        sl->cnt + (k + 1) % 3, sl->cnt + (k + 2) % 3, sl->vstamp, sl->out_tag, sl->work + 2 * i,
-                        sl->visits + i, sl->flags);
-                } else if (walk) {  // multi-hop work-fetching walks
+                if (walk) {  // multi-hop work-fetching walks
                     (soft ? k_walk_ws<true> : k_walk_ws<false>)<<<gv, 256, 0, sl->stream>>>(
                         geo, sl->s, o.walk_len, sl->blist[k & 1], sl->cnt + k % 3, sl->blist[(k + 1) & 1],
                         sl->cnt + (k + 1) % 3, sl->cnt + (k + 2) % 3, sl->vstamp, sl->out_tag, sl->work + 2 * i,
@@ -1255,9 +1229,6 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
             CG_CUDA(cudaMemcpyAsync(sl->h_work, sl->work, sizeof(unsigned long long) * 2 * batch, cudaMemcpyDeviceToHost,
                                     sl->stream));
             CG_CUDA(cudaMemcpyAsync(sl->h_flags, sl->flags, sizeof(int), cudaMemcpyDeviceToHost, sl->stream));
-            if (chunk_mode)
-                CG_CUDA(cudaMemcpyAsync(sl->h_visits, sl->visits, sizeof(unsigned long long) * batch,
-                                        cudaMemcpyDeviceToHost, sl->stream));
         }
         int64_t overflow = 0;
         std::fill(wv.begin(), wv.begin() + batch + 3, 0);
@@ -1282,16 +1253,7 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
         if (trace) {
             fprintf(stderr, "[cg] sweeps %lld..%lld ops:", (long long)sweeps, (long long)(sweeps + batch - 1));
             for (int i = 0; i < batch; i += std::max(1, batch / 8)) fprintf(stderr, " %lld", (long long)wv[i]);
-            fprintf(stderr, " | %.3f ms%s\n", ms, chunk_mode ? " (chunks)" : walk ? " (walk)" : "");
-            if (chunk_mode) {
-                unsigned long long vis = 0;
-                for (int i = 0; i < batch; i++) vis += s0->h_visits[i];
-                fprintf(stderr, "[cg]   chunk visits %llu ops %lld relabels %lld\n", vis, (long long)[&] {
-                    int64_t o2 = 0;
-                    for (int i = 0; i < batch; i++) o2 += wv[i];
-                    return o2;
-                }(), (long long)wv[batch + 2]);
-            }
+            fprintf(stderr, " | %.3f ms%s\n", ms, walk ? " (walk)" : "");
         }
         bool quiescent = false;
         last_active = wv[batch - 1];
@@ -1306,14 +1268,7 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
             g->st.work += wv[i];
         }
         g->st.relabel_ops += rel;
-        if (chunk_mode) {  // a chunk visit reads its 32 vertices' state once: 32 B each
-            int64_t vis = 0;
-            for (int i = 0; i < batch; i++) vis += (int64_t)s0->h_visits[i];
-            g->st.tile_visits += vis;
-            g->st.sweep_bytes_alg += 32.0 * 32.0 * (double)vis + 12.0 * (double)(ops - rel) + 4.0 * (double)rel;
-        } else {
-            g->st.sweep_bytes_alg += 32.0 * (double)ops + 12.0 * (double)(ops - rel) + 4.0 * (double)rel;
-        }
+        g->st.sweep_bytes_alg += 32.0 * (double)ops + 12.0 * (double)(ops - rel) + 4.0 * (double)rel;
         sweeps += batch;
         since_gap += batch;
         g->st.sweeps = sweeps;

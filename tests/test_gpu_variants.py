@@ -115,22 +115,3 @@ def test_tiles_full_size(cg, name):
     assert r["flow"] == gold["flow"]
     assert hashlib.sha256(r["surface"].astype("<i4").tobytes()).hexdigest() == gold["surface_sha256"]
     assert hashlib.sha256(r["mask"].tobytes()).hexdigest() == gold["mask_sha256"]
-
-
-@pytest.mark.parametrize("rounds", ["1", "32"])
-def test_chunk_sweeps(cg, env, rounds):
-    """Column-chunk sweeps (chunk.cuh, CG_CHUNK_MIN: chunk kind while >= that fraction of n is
-    active after a relabel): random tiny volumes (ragged chunks, Z not a multiple of 32), C1, C2."""
-    env.setenv("CG_CHUNK_MIN", "1e-9")
-    env.setenv("CG_CHUNK_ROUNDS", rounds)
-    for seed in range(1000, 1300):
-        c, delta = V.tiny_case(seed)
-        assert_same(gpu(cg, c, delta), oracle.colgraph_solve(c, delta), f"seed {seed}")
-    for shape, delta in [((6, 5, 70), 2), ((3, 4, 33), 0), ((5, 5, 100), 7)]:
-        c = V.tiny(700 + sum(shape), *shape, 255)
-        assert_same(gpu(cg, c, delta), oracle.colgraph_solve(c, delta), str(shape))
-    for name, delta in [("C1", 2), ("C2", 3)]:
-        c = V.generate(name)
-        r = gpu(cg, c, delta)
-        assert_same(r, oracle.colgraph_solve(c, delta), name)
-        assert r["stats"]["tile_visits"] > 0  # chunk visits ran
