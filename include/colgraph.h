@@ -169,6 +169,9 @@ typedef struct {
     int64_t bk_orphans;        /* orphans processed by the adoption stage */
     int64_t bk_freed;          /* orphans that found no parent and became free */
     double ms_bk_last_stages;  /* CUDA-event time of the stages with <= 4 segments (the serial tail) */
+    int64_t src_terminated;    /* 1: maxflow_solve ended on the source-side check (a4: the residual
+                                  closure of the vertices with excess reaches no arc into t) instead
+                                  of an exhaustive global relabel */
 } cg_solve_stats;
 
 /* Options of maxflow_solve_bk (NULL = defaults).

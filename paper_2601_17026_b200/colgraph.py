@@ -60,7 +60,8 @@ class cg_solve_stats(ctypes.Structure):
                 ("ms_sweep_kernels", ctypes.c_double), ("sweep_bytes_alg", ctypes.c_double),
                 ("tile_visits", ctypes.c_int64), ("relabel_ops", ctypes.c_int64), ("gr_truncated", ctypes.c_int64),
                 ("bk_stages", ctypes.c_int64), ("bk_growths", ctypes.c_int64), ("bk_augmentations", ctypes.c_int64),
-                ("bk_orphans", ctypes.c_int64), ("bk_freed", ctypes.c_int64), ("ms_bk_last_stages", ctypes.c_double)]
+                ("bk_orphans", ctypes.c_int64), ("bk_freed", ctypes.c_int64), ("ms_bk_last_stages", ctypes.c_double),
+                ("src_terminated", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -121,6 +121,7 @@ struct cg_graph {
     int64_t n_global = 0;
     bool solved = false;
     bool exported = false;      // phase 2 ran (maxflow_export_flow): the preflow is now a flow
+    bool top_ready = false;     // the solve ended on a source-side termination check: top[] is S
     unsigned trunc_small = 0, trunc_levels = 0;  // truncated relabels (CG_BFS_TRUNC), 0 = off
     cg_solve_stats st{};
 };
@@ -1055,6 +1056,66 @@ cg_status normalize_opts(cg_graph *g, const cg_solve_opts *opts, cg_solve_opts &
 
 // a2-a5: exact global relabel, then sweeps until a global relabel finds no active vertex
 // (a maximum preflow).  Shared by maxflow_solve (phase 1) and maxflow_export_flow (phase 2).
+// Forward residual closure of {E > 0} as column tops (the extraction's rounds, one slab), at most
+// max_passes rounds; *converged = the worklist emptied.
+cg_status closure_tops(cg_graph *g, Slab *sl, int max_passes, bool *converged) {
+    const Geo &geo = sl->geo;
+    const int64_t ncol = (int64_t)geo.X * geo.Y;
+    CG_CUDA(cudaMemsetAsync(sl->cnt + 8, 0, 3 * sizeof(unsigned), sl->stream));
+    CG_CUDA(cudaMemsetAsync(sl->top - geo.Y, 0xff, sizeof(int32_t) * (ncol + 2 * geo.Y), sl->stream));
+    sl->ext_k = 0;
+    k_ext_seed<<<grid_for(ncol, 256, sl->num_sms * 16), 256, 0, sl->stream>>>(geo, sl->s, sl->top, sl->proc,
+                                                                             sl->collist[0], sl->cnt + 8,
+                                                                             sl->colstamp, ++sl->tag);
+    g->st.kernel_launches++;
+    *converged = false;
+    const int grid = list_grid(sl, ncol);
+    while (sl->ext_k < max_passes) {
+        for (int b = 0; b < EXT_BATCH; b++) {
+            const int r = sl->ext_k++;
+            k_ext_round<<<grid, 256, 0, sl->stream>>>(geo, sl->s, sl->collist[r & 1], sl->cnt + 8 + r % 3,
+                                                       sl->collist[(r + 1) & 1], sl->cnt + 8 + (r + 1) % 3,
+                                                       sl->cnt + 8 + (r + 2) % 3, sl->top, sl->proc, sl->colstamp,
+                                                       ++sl->tag);
+        }
+        g->st.kernel_launches += EXT_BATCH;
+        g->st.extract_passes += EXT_BATCH;
+        CG_CUDA(cudaGetLastError());
+        CG_CUDA(cudaMemcpyAsync(sl->h_cnt + 8, sl->cnt + 8, 5 * sizeof(unsigned), cudaMemcpyDeviceToHost, sl->stream));
+        CG_CUDA(cudaStreamSynchronize(sl->stream));
+        if (sl->h_cnt[8 + sl->ext_k % 3] == 0) {
+            *converged = true;
+            break;
+        }
+    }
+    return CG_OK;
+}
+
+// a4 by the source side (one slab): when a batch went quiescent, the preflow is maximum iff the
+// residual closure of the vertices with excess holds no vertex with a residual arc into t.  If that
+// closure converges within a few rounds and reaches no such vertex, the solve ends without the
+// exhaustive global relabel (and mincut_extract_surface reuses the tops); otherwise the relabel runs
+// as before.  CG_SRC_TERM=0 disables it; CG_SRC_TERM=k caps the rounds (default 48).
+cg_status source_side_done(cg_graph *g, bool *done) {
+    *done = false;
+    const int cap = getenv("CG_SRC_TERM") ? atoi(getenv("CG_SRC_TERM")) : 48;
+    if (cap <= 0 || g->slabs.size() != 1 || multi(g)) return CG_OK;
+    Slab *sl = g->slabs[0];
+    bool conv = false;
+    CG_TRY(closure_tops(g, sl, cap, &conv));
+    if (!conv) return CG_OK;
+    CG_CUDA(cudaMemsetAsync(sl->flags + 4, 0, sizeof(int), sl->stream));
+    k_ext_check_t<<<list_grid(sl, (int64_t)sl->geo.X * sl->geo.Y), 256, 0, sl->stream>>>(sl->geo, sl->s, sl->top,
+                                                                                      sl->flags + 4);
+    g->st.kernel_launches++;
+    CG_CUDA(cudaMemcpyAsync(sl->h_flags + 4, sl->flags + 4, sizeof(int), cudaMemcpyDeviceToHost, sl->stream));
+    CG_CUDA(cudaStreamSynchronize(sl->stream));
+    *done = sl->h_flags[4] == 0;
+    g->top_ready = *done;
+    g->st.src_terminated = *done;
+    return CG_OK;
+}
+
 cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &ms_gr) {
     const bool trace = tracing();
     Slab *s0 = g->slabs[0];
@@ -1279,6 +1340,17 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
             while (sched_i < sched.size() && sched[sched_i] <= sweeps) sched_i++;
             // a4: termination is decided only after an exact global relabel (a quiescent batch asks
             // for an exhaustive one; a truncated one that leaves nothing active is redone exhaustively)
+            bool done = false;
+            if (quiescent) {
+                const double a = now_ms();
+                CG_TRY(source_side_done(g, &done));
+                if (trace) fprintf(stderr, "[cg] source-side termination check: %s (%.3f ms)\n", done ? "max" : "no",
+                                   now_ms() - a);
+            }
+            if (done) {
+                active = 0;
+                break;
+            }
             CG_TRY(timed_gr(quiescent));
             last_active = active;
             work_since_gr = 0.0;
@@ -1693,6 +1765,7 @@ static cg_status mincut_extract_surface_impl(cg_graph *g, int32_t *surface_dev, 
     DeviceGuard dg(g->dist.device);
     const double t0 = now_ms();
     for (Slab *sl : g->slabs) {
+        if (g->top_ready) break;  // the solve's termination check left the tops of S
         const Geo &geo = sl->geo;
         const int64_t ncol = (int64_t)geo.X * geo.Y;
         CG_CUDA(cudaMemsetAsync(sl->cnt + 8, 0, 3 * sizeof(unsigned), sl->stream));
@@ -1702,7 +1775,7 @@ static cg_status mincut_extract_surface_impl(cg_graph *g, int32_t *surface_dev, 
             geo, sl->s, sl->top, sl->proc, sl->collist[0], sl->cnt + 8, sl->colstamp, ++sl->tag);
         g->st.kernel_launches++;
     }
-    for (int outer = 0;; outer++) {
+    for (int outer = 0; !g->top_ready; outer++) {
         if (multi(g)) {  // exchange column tops (proposals for ghosts, boundary tops)
             for (Slab *sl : g->slabs) {
                 const Geo &geo = sl->geo;

@@ -1787,6 +1787,22 @@ __global__ void __launch_bounds__(256) k_ext_round(Geo g, Soa s, const int *__re
     }
 }
 
+// a4 by the source side: after the closure rounds, is there a vertex in S = {z <= top(x,y)} with a
+// residual arc into t (T > 0)?  None <=> no vertex with excess can reach t <=> the preflow is
+// maximum (Theorem 1).  Warp per column.
+__global__ void k_ext_check_t(Geo g, const Soa s, const int32_t *__restrict__ top, int *hit) {
+    const int64_t ncol = (int64_t)g.X * g.Y;
+    for (int64_t col = gwarp(); col < ncol; col += nwarps()) {
+        const int t = top[col];
+        bool h = false;
+        for (int z = lane_id(); z <= t; z += 32) h |= s.T[col * g.Z + z] > 0;
+        if (__any_sync(FULL, h)) {
+            if (lane_id() == 0) atomicOr(hit, 1);
+            return;
+        }
+    }
+}
+
 // Top halo: [0] this slab's proposals for the ghost columns, [1] its boundary tops.
 __global__ void k_top_halo_pack(Geo g, const int32_t *top, int side, int32_t *send) {
     const int64_t ncol = (int64_t)g.X * g.Y;

@@ -243,6 +243,30 @@ def test_determinism(cg):
     assert len(works) > 1  # the schedules really differed
 
 
+def test_source_side_termination(cg, monkeypatch):
+    """a4 by the source side: a quiescent solve may end when the residual closure of the vertices with
+    excess reaches no arc into t (csrc/colgraph.cu source_side_done) instead of on an exhaustive
+    relabel; the extraction then reuses that closure.  Both ways give the oracle's result, and the
+    check does end solves (src_terminated) -- also when capped to one batch of rounds."""
+    ended = 0
+    for cap in ("48", "16", "0"):
+        monkeypatch.setenv("CG_SRC_TERM", cap)
+        for seed in range(1000, 1200):
+            c, delta = V.tiny_case(seed)
+            r = gpu(cg, c, delta)
+            assert_same(r, oracle.colgraph_solve(c, delta), f"cap {cap} seed {seed}")
+            if cap == "0":
+                assert r["stats"]["src_terminated"] == 0
+            else:
+                ended += r["stats"]["src_terminated"]
+        for name, delta in (("C1", 2), ("C2", 3)):
+            c = V.generate(name)
+            r = gpu(cg, c, delta)
+            assert_same(r, oracle.colgraph_solve(c, delta), f"cap {cap} {name}")
+            ended += r["stats"]["src_terminated"] if cap != "0" else 0
+    assert ended > 100
+
+
 @pytest.mark.parametrize("name", ["C3", "C4"])
 def test_certificate_full_size(cg, name):
     """The O(n) max-preflow certificate (capacities, exact conservation, no residual path from excess

@@ -1,6 +1,7 @@
 """a2/a5 global relabel: the labels the library leaves are the exact BFS distances to t.
 
-maxflow_solve ends with an exact global relabel (a4), so the heights in the exported state are the
+maxflow_solve ends with an exact global relabel (a4; the source-side termination check is switched off
+here with CG_SRC_TERM=0), so the heights in the exported state are the
 residual-graph distances d(v) to t of the final preflow (§2.1, Alg. 3;
 INF = n + 1 for vertices that cannot reach t, reading R8).  The reference here is independent of
 the library: the residual graph is rebuilt from the exported flows with scipy and searched from t
@@ -73,6 +74,8 @@ def solve_state(cg, c, delta, nslabs=1, weight=False):
 
 @pytest.fixture(params=["default", "flags", "colgr", "bfs", "trunc", "bottomup"])
 def flavour(request, monkeypatch):
+    # the labels are exact after an exhaustive relabel: end every solve on one (no source-side check)
+    monkeypatch.setenv("CG_SRC_TERM", "0")
     if request.param == "default":
         monkeypatch.delenv("CG_RELABEL", raising=False)
     elif request.param == "trunc":  # truncated relabels mid-solve; the last one is exhaustive
