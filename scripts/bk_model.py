@@ -1,5 +1,6 @@
 """Sequential Python model of k_bk_stage (csrc/bk.cuh), lane loops written out, for debugging the
-algorithm on a CPU box: python scripts/bk_model.py [ncases].  Compares with the oracle."""
+algorithm on a CPU box: python scripts/bk_model.py [ncases] compares it with the oracle (so does
+tests/test_bk_model.py).  Not product code: the library never calls it."""
 import os
 import sys
 
@@ -7,7 +8,6 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-import oracle  # noqa: E402
 from synth import volumes as V  # noqa: E402
 
 FREE, S, T = 0, 1, 2
@@ -320,6 +320,7 @@ def solve(c, delta, bx, by):
 
 
 if __name__ == "__main__":
+    import oracle  # the check below only (test infrastructure)
     rng = np.random.default_rng(1)
     ncase = int(sys.argv[1]) if len(sys.argv) > 1 else 200
     for seed in range(3000, 3000 + ncase):
