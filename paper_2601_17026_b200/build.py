@@ -81,5 +81,7 @@ if __name__ == "__main__":
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_bfsr1b2.so"), defines=("BFS_R=1", "CG_BFS_RUN_MINB=2")))
     if "--no-init-preload" in sys.argv:
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_noprel.so"), defines=("CG_INIT_PRELOAD=0",)))
+    if "--no-fastdiv" in sys.argv:
+        print(build(force=True, lib=os.path.join(PKG, "libcolgraph_nofdiv.so"), defines=("CG_FASTDIV=0",)))
     if "--soa" in sys.argv:
         print(build(force=True, lib=os.path.join(PKG, "libcolgraph_soa.so"), defines=("CG_LAYOUT_AOS=0",)))

@@ -1013,6 +1013,8 @@ Geo make_geo(const cg_dims *dims, const int32_t *dl4, int x0, int x1, int nranks
     geo.YZ = (int64_t)dims->Y * dims->Z;
     geo.nchunks = (int64_t)geo.X * geo.Y * geo.CPC;
     geo.INF = (int32_t)(n_global + 1);
+    fastdiv_params((uint32_t)geo.Z, geo.mZ, geo.shZ);
+    fastdiv_params((uint32_t)geo.Y, geo.mY, geo.shY);
     (void)nranks_total;
     return geo;
 }

@@ -30,7 +30,28 @@ struct Geo {
     // k < Delta_d, capacity soft_cap[k] = f(k+1) - 2 f(k) + f(k-1); 0 = hard constraint only
     int32_t soft_k;
     int32_t soft_cap[16];
+    // division by Z and by Y without the division routine (set_fastdiv): q = n * m >> sh for
+    // 0 <= n < 2^31 (Granlund-Montgomery: m = ceil(2^(31+l) / d), l = ceil(log2 d), sh = 31 + l)
+    uint64_t mZ, mY;
+    int32_t shZ, shY;
 };
+inline void fastdiv_params(uint32_t d, uint64_t &m, int32_t &sh) {
+    int l = 0;
+    while ((1ull << l) < d) l++;
+    m = ((1ull << (31 + l)) + d - 1) / d;
+    sh = 31 + l;
+}
+#ifndef CG_FASTDIV
+#define CG_FASTDIV 1
+#endif
+#if CG_FASTDIV
+#define CG_DIVZ(g, n) fdiv((uint32_t)(n), (g).mZ, (g).shZ)
+#define CG_DIVY(g, n) fdiv((uint32_t)(n), (g).mY, (g).shY)
+#else
+#define CG_DIVZ(g, n) ((uint32_t)(n) / (uint32_t)(g).Z)
+#define CG_DIVY(g, n) ((uint32_t)(n) / (uint32_t)(g).Y)
+#endif
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, uint64_t m, int sh) { return (uint32_t)(((uint64_t)n * m) >> sh); }
 constexpr int SOFT_KMAX = 16;
 
 // Residual state: 8 int32 fields per vertex -- E excess, H height, T sink residual, D flow

@@ -550,12 +550,13 @@ __device__ __forceinline__ ArcPick scan_arcs_hard(const Geo &g, const Soa &s, co
 #endif
 }
 
-__device__ __forceinline__ void set_ctx(const Geo &g, OpCtx &c, int64_t v) {
+__device__ __forceinline__ void set_ctx(const Geo &g, OpCtx &c, int64_t v) {  // v owned (>= 0)
     c.v = v;
-    c.col = v / g.Z;
-    c.z = (int)(v - c.col * g.Z);
+    const uint32_t col = CG_DIVZ(g, v);
+    c.col = col;
+    c.z = (int)((uint32_t)v - col * (uint32_t)g.Z);
     c.v0 = c.col * g.Z;
-    const int x = (int)(c.col / g.Y), y = (int)(c.col - (int64_t)x * g.Y);
+    const int x = (int)CG_DIVY(g, col), y = (int)(col - (uint32_t)x * (uint32_t)g.Y);
 #pragma unroll
     for (int d = 0; d < 4; d++) {
         c.zo[d] = zo_of(c.z, dl_out(g, d));
@@ -1027,9 +1028,9 @@ __device__ __forceinline__ void bfs_expand_multi(const Geo &g, const Soa &s, int
         got[r] = 0;
         const int v = vv[r];
         if (v < 0 || nl >= INF) continue;
-        const int col = v / g.Z;
+        const int col = (int)CG_DIVZ(g, v);
         const int z = v - col * g.Z;
-        const int x = col / g.Y, y = col - x * g.Y;
+        const int x = (int)CG_DIVY(g, col), y = col - x * g.Y;
         const int v0 = col * g.Z;
         int D, L[4];
         if (FL) {
