@@ -47,6 +47,14 @@
  *                         consecutive frontiers of <= s vertices; unreached vertices stay at INF
  *                         until the next exhaustive relabel (the one that decides termination)
  *   CG_BAR_NS=ns          back-off cap of the persistent kernels' grid barrier (default 1024)
+ *   CG_BFS_BU=div,min     flag-plane BFS: bottom-up levels when the frontier >= unvisited / div
+ *                         and >= min (measured alternative; off)
+ *   CG_TAIL_BATCH=k       single-hop tail: k x check_every sweeps between host reads (default 8)
+ *   CG_SRC_TERM=k         a4 source-side check: closure rounds cap (default 48; 0 = always end
+ *                         on an exhaustive relabel)
+ *   CG_PRECANCEL=1        exact per-column pre-cancellation before the first relabel (measured
+ *                         alternative; off)
+ *   CG_SLAB_BFS_EACH=1    in-process x-slabs: one in-slab BFS launch per slab instead of one for all
  * Conventions for every entry point:
  *   - Errors are returned as cg_status, never thrown; no C++ exception crosses
  *     this ABI.
