@@ -292,7 +292,7 @@ cg_status cg_nccl_loopback(int32_t enable);
 cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_value, cg_solve_stats *stats);
 
 /* NEXT-4 -- the paper's first parallelisation, parallel Boykov-Kolmogorov with hierarchical
- * merging (PAPER.md §3.1 L247-250; BK's growth / augmentation / adoption stages, §2.2 L205-208),
+ * merging (PAPER.md §3.1 L225-228; BK's growth / augmentation / adoption stages, §2.2 L198-199),
  * as a second solver on the same handle: the volume is cut into segments of seg_x x seg_y columns,
  * BK exhausts the augmenting paths inside every segment in parallel (one warp per segment), then
  * adjacent segments merge pairwise (alternating x and y) and the search trees grow across the old

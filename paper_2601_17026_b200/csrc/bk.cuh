@@ -1,24 +1,24 @@
 // bk.cuh -- NEXT-4: parallel Boykov-Kolmogorov with hierarchical merging.
 //
-// PAPER.md §3.1 (L247-250): "we extended Liu and Sun's parallel BK algorithm to 3D by first
+// PAPER.md §3.1 (L225-228): "we extended Liu and Sun's parallel BK algorithm to 3D by first
 // segmenting the structured graph into smaller segments of uniform size ... splitting across the
 // two most dominant dimensions ... In the first stage of the algorithm, the source and the sink
 // search trees are expanded to exhaust all the paths within the small segments.  When no further
 // paths are found in the small segments, they are hierarchically merged into larger segments by
 // combining adjacent segments into larger segments containing twice the number of nodes ... any
 // new capacity carrying path has to include the nodes along the segment boundaries."  The BK stages
-// themselves (growth, augmentation, adoption of orphans, PAPER.md §2.2 L205-208) follow Boykov &
+// themselves (growth, augmentation, adoption of orphans, PAPER.md §2.2 L198-199) follow Boykov &
 // Kolmogorov as the paper summarises them.
 //
 // B200 mapping: one warp per segment (segments are disjoint, so a warp owns every vertex and every
 // arc it touches during a stage: no atomics, no locks -- "since the segments are logically separated
-// and the paths are restricted to these segments, we do not use any kind of locking", L250).  A
+// and the paths are restricted to these segments, we do not use any kind of locking", L228).  A
 // growth step scans the (at most 10) neighbours of the current active vertex with one lane per arc;
 // an adoption scans the orphan's neighbours the same way and walks every candidate's origin in its
 // own lane; augmentation walks the two tree paths serially (lane 0).  One launch per merge stage;
 // segments are bx x by columns (full Z) and merge pairwise, alternating x and y, until one segment
 // covers the volume.  The last stages run on few warps: the serial tail the paper measured ("capped
-// at a meager 3x", L243) is inherent to the scheme and is what the measurement shows.
+// at a meager 3x", L216) is inherent to the scheme and is what the measurement shows.
 //
 // State: the residual record of the push-relabel path (E = residual of the source arc -- the
 // build pre-saturates source arcs, so the excess IS that residual --, T = residual of the sink

@@ -1674,7 +1674,7 @@ cg_status maxflow_solve(cg_graph *g, const cg_solve_opts *opts, int64_t *flow_va
     return debug_check(maxflow_solve_impl(g, opts, flow_value, stats));
 }
 
-// NEXT-4: parallel BK with hierarchical merging (bk.cuh; PAPER.md §3.1 L247-250).  The segment
+// NEXT-4: parallel BK with hierarchical merging (bk.cuh; PAPER.md §3.1 L225-228).  The segment
 // schedule: first-stage segments of bx x by columns, then pairwise merges alternating x and y (an
 // axis stops merging once its segments span the volume) until one segment remains.
 static cg_status maxflow_solve_bk_impl(cg_graph *g, const cg_bk_opts *opts, int64_t *flow_value, cg_solve_stats *stats) {

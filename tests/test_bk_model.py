@@ -1,7 +1,7 @@
 """NEXT-4 host logic without a GPU: the sequential model of the parallel-BK kernel
 (scripts/bk_model.py: the same segment schedule -- 1 x 1 .. b x b first segments, pairwise merges
 alternating x and y -- and the same growth / augmentation / adoption steps as csrc/bk.cuh, lanes
-written as loops) reaches the oracle's max-flow value on tiny volumes (PAPER.md §3.1 L247-250)."""
+written as loops) reaches the oracle's max-flow value on tiny volumes (PAPER.md §3.1 L225-228)."""
 import os
 import sys
 

@@ -1,5 +1,5 @@
 """GPU parity for NEXT-4: parallel Boykov-Kolmogorov with hierarchical merging
-(PAPER.md §3.1 L247-250), maxflow_solve_bk, against the CPU oracle bit-exactly -- flow value,
+(PAPER.md §3.1 L225-228), maxflow_solve_bk, against the CPU oracle bit-exactly -- flow value,
 minimal source set (mask) and surface -- on random tiny volumes with random first-stage segment
 sizes (1 x 1 columns up to larger than the volume, so zero to many merge stages, ragged edge
 segments), general intervals and narrow bands, weight mode, C1/C2 and the C3 golden; the residual
