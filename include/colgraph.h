@@ -49,6 +49,10 @@
  *   CG_BAR_NS=ns          back-off cap of the persistent kernels' grid barrier (default 1024)
  *   CG_BFS_BU=div,min     flag-plane BFS: bottom-up levels when the frontier >= unvisited / div
  *                         and >= min (measured alternative; off)
+ *   CG_BFS_DENSE=k        flag-plane BFS on one slab with Z % 32 == 0 (intervals < 32): levels
+ *                         whose frontier has >= k vertices run as dense bit-plane shifts over
+ *                         32-z words (from level 1 on, until the first smaller frontier); default
+ *                         n / 256, 0 = off
  *   CG_TAIL_BATCH=k       single-hop tail: k x check_every sweeps between host reads (default 8)
  *   CG_SRC_TERM=k         a4 source-side check: closure rounds cap (default 48; 0 = always end
  *                         on an exhaustive relabel)

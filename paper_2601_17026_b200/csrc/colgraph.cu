@@ -67,6 +67,7 @@ struct Slab {
     unsigned long long *visits = nullptr;  // [RING] tile visits per phase
     unsigned *heads = nullptr;             // [RING] work-fetch cursors of k_walk_ws
     unsigned *visited = nullptr;           // [n/32 + 1] BFS visited bitmap (persistent BFS)
+    unsigned *dbits = nullptr;             // [7][n/32 + 1] dense BFS levels: Dm, Lm0..3, F0, F1 bit planes
     int32_t *lab = nullptr;                // column-fixpoint relabel: labels, planes [-YZ, n + YZ)
     uint8_t *gflags = nullptr;             // column-fixpoint relabel: residual-arc flags, same range
     ColGrState *cst = nullptr, *h_cst = nullptr;
@@ -299,7 +300,8 @@ size_t workspace_bytes(const Geo &geo) {
          al(sizeof(int) * 16);
     b += 4 * al(sizeof(int32_t) * geo.YZ) + 4 * al(sizeof(int32_t) * halo_msg_ints(geo));
     b += 5 * al(sizeof(int) * ncol) + al(sizeof(unsigned) * 4) + al(sizeof(unsigned long long) * RING) +
-         al(sizeof(unsigned long long) * 16) + al(sizeof(unsigned) * RING) + al(sizeof(unsigned) * (geo.n / 32 + 1));
+         al(sizeof(unsigned long long) * 16) + al(sizeof(unsigned) * RING) + al(sizeof(unsigned) * (geo.n / 32 + 1)) +
+         al(sizeof(unsigned) * 7 * (geo.n / 32 + 1));
     b += al(sizeof(int32_t) * plane) + al(plane) + al(sizeof(ColGrState)) + al(sizeof(int32_t) * 2 * ncol);
     return b;
 }
@@ -384,6 +386,7 @@ cg_status slab_build(Slab *sl, const int32_t *cost_dev, int weight_mode, const i
     sl->visits = carve<unsigned long long>(p, RING);
     sl->heads = carve<unsigned>(p, RING);
     sl->visited = carve<unsigned>(p, n / 32 + 1);
+    sl->dbits = carve<unsigned>(p, 7 * (n / 32 + 1));
     sl->lab = carve<int32_t>(p, plane) + geo.YZ;
     sl->gflags = carve<uint8_t>(p, plane) + geo.YZ;
     sl->cst = carve<ColGrState>(p, 1);
@@ -542,9 +545,21 @@ cg_status bfs_strict(cg_graph *g, Slab *sl, bool allow_coop = true, bool flag_pl
     CG_CUDA(cudaMemcpyAsync(&sl->bst->bu_div, &sl->h_bst->bu_div, 2 * sizeof(unsigned), cudaMemcpyHostToDevice, st));
     const bool coop = allow_coop && sl->bfs_coop_grid > 0;
     if (flag_plane && !coop) return CG_E_INVAL;
+    // dense bit-plane levels for the large frontiers (one slab without ghost planes, Z % 32 == 0 so a
+    // bitmap word is 32 z of one column, intervals < 32): CG_BFS_DENSE = frontier threshold in
+    // vertices (0: off; default n / 256)
+    unsigned dense_min = 0;
+    if (flag_plane && !geo.gl && !geo.gh && geo.Z % 32 == 0 && geo.dl[0] < 32 && geo.dl[1] < 32 && geo.dl[2] < 32 &&
+        geo.dl[3] < 32) {
+        const char *e = getenv("CG_BFS_DENSE");
+        const long long dm = e ? atoll(e) : std::max<long long>(1, geo.n / 256);
+        dense_min = (unsigned)std::max<long long>(0, std::min<long long>(dm, 0xffffffffll));
+    }
+    unsigned *dbits = dense_min ? sl->dbits : nullptr;
     if (flag_plane)
         k_bfs2_init<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, st>>>(geo, sl->s, sl->gflags, sl->lab,
-                                                                             sl->visited, sl->blist[0], &sl->bst->cnt[0]);
+                                                                             sl->visited, sl->blist[0], &sl->bst->cnt[0],
+                                                                             dbits);
     else
         k_bfs_init<<<grid_for(geo.n, 256, sl->num_sms * 16), 256, 0, st>>>(geo, sl->s, sl->blist[0], &sl->bst->cnt[0],
                                                                             coop ? sl->visited : nullptr);
@@ -554,8 +569,9 @@ cg_status bfs_strict(cg_graph *g, Slab *sl, bool allow_coop = true, bool flag_pl
     if (coop) {  // every level in one cooperative launch (k_bfs_run)
         const uint8_t *fl = flag_plane ? sl->gflags : nullptr;
         int32_t *lb = flag_plane ? sl->lab : nullptr;
-        void *args[] = {(void *)&sl->geo, (void *)&sl->s, (void *)&sl->blist[0], (void *)&sl->blist[1],
-                        (void *)&sl->bst, (void *)&sl->visited, (void *)&fl, (void *)&lb};
+        void *args[] = {(void *)&sl->geo, (void *)&sl->s,       (void *)&sl->blist[0], (void *)&sl->blist[1],
+                        (void *)&sl->bst, (void *)&sl->visited, (void *)&fl,          (void *)&lb,
+                        (void *)&dbits,   (void *)&dense_min};
         CG_CUDA(cudaLaunchCooperativeKernel(flag_plane ? (const void *)k_bfs_run<true> : (const void *)k_bfs_run<false>,
                                             sl->bfs_coop_grid, 512, args, 0, st));
         g->st.kernel_launches++;
@@ -1153,6 +1169,7 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
                     (long long)g->st.global_relabels, (long long)(g->st.gr_passes - p0), (long long)active, last_gr_ms,
                     (long long)g->st.sweeps, (long long)-sumT);
             if (s0->h_bst->bu_levels) fprintf(stderr, "[cg]   bottom-up levels %u\n", s0->h_bst->bu_levels);
+            if (s0->h_bst->dense_levels) fprintf(stderr, "[cg]   dense levels %u\n", s0->h_bst->dense_levels);
             const unsigned *h = s0->h_bst->hist;
             fprintf(stderr, "[cg]   levels by frontier: <=32 %u <=256 %u <=2K %u <=16K %u <=128K %u <=1M %u more %u "
                     "(bottom-up %u)\n", h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);

@@ -1146,6 +1146,7 @@ struct BfsState {
     // bottom-up levels of the flag-plane BFS (CG_BFS_BU=div,min): when the frontier exceeds both
     // (vertices not yet labelled) / bu_div and bu_min; 0 = top-down only
     unsigned bu_div, bu_min, bu_levels;
+    unsigned conv, dense_levels;  // dense bit-plane levels: list-conversion cursor, levels run dense
 };
 __device__ __forceinline__ int bfs_bucket(unsigned c) {
     return c <= 32 ? 0 : c <= 256 ? 1 : c <= 2048 ? 2 : c <= 16384 ? 3 : c <= 131072 ? 4 : c <= 1048576 ? 5 : 6;
@@ -1288,6 +1289,137 @@ __device__ void bfs2_bottom_up_level(const Geo &g, const uint8_t *__restrict__ f
     }
 }
 
+// Dense bit-plane level of the flag-plane BFS (the large early levels of a relabel; hard graphs on one
+// slab with Z % 32 == 0, so a 32-bit word is 32 consecutive z of ONE column).  The same predecessor
+// sets as bfs_expand_multi, written as shifts of the frontier's bit words instead of per-vertex
+// neighbour lists (the columns' z order makes every arc family a shift):
+//   down arc (v+1) -> v, infinite           : u = v + 1                      -> F << 1
+//   up arc (v-1) -> v, residual iff D(v) > 0 : u = v - 1                      -> (F & Dm) >> 1
+//   lateral arc of u = (nbr_d(v), zi(z)) -> v, infinite: u.z = z + dl_in(d) (z >= 1), 0 (z = 0)
+//   reverse of v's lateral arc, residual iff L_d(v) > 0: u = (nbr_d(v), zo(z)): u.z = z - dl_out(d)
+//                                            (z > dl_out(d)), 0 (z = 0)
+// Seen from u's column, v's column is nbr_{d^1}(u's column).  N = preds(F) & ~visited; each lane owns
+// one word of the visited bitmap and of the next frontier bitmap (plain stores, no atomics), and the
+// warp writes the labels of its 32 words in coalesced 128-B rows.  The frontier bitmaps are
+// double-buffered (Fn is fully rewritten, zeros included).  dl < 32 (checked on the host).
+__device__ __forceinline__ unsigned shl_w(unsigned a, unsigned am1, int s) { return s ? (a << s) | (am1 >> (32 - s)) : a; }
+__device__ __forceinline__ unsigned shr_w(unsigned a, unsigned ap1, int s) { return s ? (a >> s) | (ap1 << (32 - s)) : a; }
+
+#ifndef CG_DENSE_R
+#define CG_DENSE_R 1
+#endif
+__device__ void bfs_dense_level(const Geo &g, const unsigned *__restrict__ Dm, const unsigned *__restrict__ Lm,
+                                int64_t NW, const unsigned *F, unsigned *Fn, unsigned *visited, int32_t *lab, int nl,
+                                unsigned *cout) {
+    constexpr int R = CG_DENSE_R;  // words per lane, every load of the R words issued before any use
+                                   // (measured: R = 1 / 2 / 3 equal or worse)
+    const int WPC = g.Z >> 5;
+    const int64_t nw = g.n >> 5;
+    unsigned tot = 0;
+    for (int64_t base = gwarp() * 32 * R; base < nw; base += nwarps() * 32 * R) {
+        unsigned vis[R], f0[R], fm[R], fp[R], d0[R], dp[R], a0[R][4], am[R][4], ap[R][4], l0[R][4], lp[R][4];
+        int kk[R];
+        unsigned on[R];  // bit d: the neighbour column toward d^1 exists
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const int64_t w = base + r * 32 + lane_id();
+            on[r] = 0;
+            kk[r] = 0;
+            vis[r] = 0xffffffffu;
+            f0[r] = fm[r] = fp[r] = d0[r] = dp[r] = 0;
+#pragma unroll
+            for (int d = 0; d < 4; d++) a0[r][d] = am[r][d] = ap[r][d] = l0[r][d] = lp[r][d] = 0;
+            if (w >= nw) continue;
+            const uint32_t col = CG_DIVZ(g, (uint32_t)w * 32u);  // 32-bit indices, as in bfs_expand_multi
+            const int k = (int)((uint32_t)w - col * (uint32_t)WPC);
+            kk[r] = k;
+            const int x = (int)CG_DIVY(g, col), y = (int)(col - (uint32_t)x * (uint32_t)g.Y);
+            const bool hasm = k > 0, hasp = k + 1 < WPC;
+            vis[r] = __ldcg(&visited[w]);
+            f0[r] = __ldcg(&F[w]);
+            if (hasm) fm[r] = __ldcg(&F[w - 1]);
+            if (hasp) fp[r] = __ldcg(&F[w + 1]);
+            d0[r] = __ldg(&Dm[w]);
+            if (hasp) dp[r] = __ldg(&Dm[w + 1]);
+#pragma unroll
+            for (int d = 0; d < 4; d++) {
+                const int64_t o = nbr_off(g, x, y, d ^ 1);  // v's column, seen from u's
+                if (!o) continue;
+                on[r] |= 1u << d;
+                const int64_t wv = w + o / 32;
+                a0[r][d] = __ldcg(&F[wv]);
+                if (hasm) am[r][d] = __ldcg(&F[wv - 1]);
+                if (hasp) ap[r][d] = __ldcg(&F[wv + 1]);
+                l0[r][d] = __ldg(&Lm[d * NW + wv]);
+                if (hasp) lp[r][d] = __ldg(&Lm[d * NW + wv + 1]);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const int64_t w = base + r * 32 + lane_id();
+            unsigned N = shl_w(f0[r], fm[r], 1) | shr_w(f0[r] & d0[r], fp[r] & dp[r], 1);
+            const bool first = kk[r] == 0;
+#pragma unroll
+            for (int d = 0; d < 4; d++) {
+                if (!((on[r] >> d) & 1u)) continue;
+                const int si = dl_in(g, d), so = dl_out(g, d);
+                // infinite lateral arcs into v: from v.z >= 1 shifted up by si; v.z = 0 -> u.z = 0
+                unsigned t = shl_w(a0[r][d], am[r][d], si);
+                if (first) t = (t & ~(1u << si)) | (a0[r][d] & 1u);
+                N |= t;
+                // reverse lateral arcs (L_d(v) > 0): v.z > so shifted down by so; v.z = 0 -> u.z = 0
+                unsigned g0 = a0[r][d] & l0[r][d];
+                if (first) {
+                    N |= g0 & 1u;
+                    g0 &= so >= 31 ? 0u : ~((2u << so) - 1u);
+                }
+                N |= shr_w(g0, ap[r][d] & lp[r][d], so);
+            }
+            N &= ~vis[r];
+            if (w < nw) {
+                if (N) visited[w] = vis[r] | N;
+                Fn[w] = N;
+            }
+            tot += __popc(N);
+            unsigned m = __ballot_sync(FULL, N != 0);
+            const int64_t wb = base + r * 32;
+            while (m) {  // labels of the new vertices, one coalesced row per word
+                const int j = __ffs(m) - 1;
+                m &= m - 1;
+                const unsigned Nj = __shfl_sync(FULL, N, j);
+                if ((Nj >> lane_id()) & 1u) lab[(wb + j) * 32 + lane_id()] = nl;
+            }
+        }
+    }
+    tot = (unsigned)warp_sum_ll((long long)tot);
+    if (lane_id() == 0 && tot) atomicAdd(cout, tot);
+}
+
+// List the vertices of a frontier bitmap (the switch from dense to list levels), 32 words per warp.
+__device__ void bfs_dense_list(const Geo &g, const unsigned *F, int *lout, unsigned *cout) {
+    const int64_t nw = g.n >> 5;
+    for (int64_t base = gwarp() * 32; base < nw; base += nwarps() * 32) {
+        const int64_t w = base + lane_id();
+        const unsigned N = w < nw ? __ldcg(&F[w]) : 0u;
+        const int c = __popc(N);
+        const int incl = warp_incl_scan(c);
+        const int total = __shfl_sync(FULL, incl, 31);
+        if (!total) continue;
+        unsigned b = 0;
+        if (lane_id() == 31) b = atomicAdd(cout, (unsigned)total);
+        b = __shfl_sync(FULL, b, 31);
+        unsigned pos = b;
+        unsigned m = __ballot_sync(FULL, N != 0);
+        while (m) {
+            const int j = __ffs(m) - 1;
+            m &= m - 1;
+            const unsigned Nj = __shfl_sync(FULL, N, j);
+            if ((Nj >> lane_id()) & 1u) lout[pos + __popc(Nj & lanemask_lt())] = (int)((base + j) * 32 + lane_id());
+            pos += __popc(Nj);
+        }
+    }
+}
+
 #ifndef BFS_R
 #define BFS_R 2
 #endif
@@ -1297,12 +1429,18 @@ __device__ void bfs2_bottom_up_level(const Geo &g, const uint8_t *__restrict__ f
 template <bool FL>
 __global__ void __launch_bounds__(512, CG_BFS_RUN_MINB) k_bfs_run(Geo g, Soa s, int *list0, int *list1, BfsState *st,
                                                                   unsigned *visited, const uint8_t *flags,
-                                                                  int32_t *lab) {
+                                                                  int32_t *lab, unsigned *dbits, unsigned dense_min) {
     unsigned *bar = st->bar;
     int L = *(volatile int *)&st->L;
     unsigned long long claimed = *(volatile unsigned long long *)&st->claimed;
     const unsigned tr_small = st->trunc_small, tr_levels = FL ? st->trunc_levels : 0;
     unsigned thin = 0;  // consecutive levels with a frontier <= tr_small
+    // dense bit-plane levels (bfs_dense_level) while the frontier has >= dense_min vertices, from level 1
+    // on: dbits = [Dm | Lm0..3 | F0 | F1], NW words each (k_bfs2_init wrote Dm, Lm and F0 = the seeds)
+    bool dense = FL && dbits && dense_min && L == 1;
+    bool dense_ran = false;
+    int fcur = 0;
+    const int64_t NW = g.n / 32 + 1;
     for (int guard = 0; guard <= g.INF + 2; guard++) {
         const unsigned count = *(volatile unsigned *)&st->cnt[(L - 1) % 3];
         if (count == 0) break;
@@ -1312,6 +1450,31 @@ __global__ void __launch_bounds__(512, CG_BFS_RUN_MINB) k_bfs_run(Geo g, Soa s, 
             break;
         }
         const int i = L - 1;
+        if (dense) {
+            unsigned *F = dbits + (5 + fcur) * NW;
+            if (count >= dense_min) {
+                if (blockIdx.x == 0 && threadIdx.x == 0) {
+                    st->cnt[(i + 2) % 3] = 0;
+                    st->hist[bfs_bucket(count)]++;
+                    st->dense_levels++;
+                }
+                const long long t0 = clock64();
+                bfs_dense_level(g, dbits, dbits + NW, NW, F, dbits + (6 - fcur) * NW, visited, lab, L + 1,
+                                &st->cnt[(i + 1) % 3]);
+                grid_barrier(bar, gridDim.x);
+                if (blockIdx.x == 0 && threadIdx.x == 0) st->cyc[bfs_bucket(count)] += clock64() - t0;
+                fcur ^= 1;
+                dense_ran = true;
+                ++L;
+                claimed += *(volatile unsigned *)&st->cnt[(L - 1) % 3];
+                continue;
+            }
+            dense = false;
+            if (dense_ran) {  // this level's frontier exists only as the bitmap F: list it
+                bfs_dense_list(g, F, (i & 1) ? list1 : list0, &st->conv);
+                grid_barrier(bar, gridDim.x);
+            }
+        }
         if (count <= st->small) {
             // everyone has read this level's counter before block 0 starts recycling counters
             grid_barrier(bar, gridDim.x);

@@ -51,7 +51,10 @@ __global__ void k_colgr_flags(Geo g, Soa s, uint8_t *flags, int32_t *lab, int64_
 // flags, the labels (1 for the seeds T > 0 -- Alg. 3's first level, reading R6 -- else INF), the
 // visited bitmap and the seed list; k_bfs_run<true> then expands from the flags and writes `lab`.
 __global__ void k_bfs2_init(Geo g, Soa s, uint8_t *flags, int32_t *lab, unsigned *visited, int *lout,
-                            unsigned *cout) {
+                            unsigned *cout, unsigned *dbits = nullptr) {
+    // dbits (dense bit-plane levels, k_bfs_run): the residual bits as 32-vertex words -- Dm (D > 0),
+    // Lm[d] (L_d > 0) -- and the seed frontier F0, NW words per plane
+    const int64_t NW = g.n / 32 + 1;
     // (measured: loading a span's records ahead of the flag writes with streaming loads made this
     // pass slower, 0.80 -> 1.22 ms at C4 under ncu; CG_INIT_PRELOAD loads the span's records with
     // plain loads before any store -- the stores to flags / lab / visited otherwise keep each
@@ -76,6 +79,7 @@ __global__ void k_bfs2_init(Geo g, Soa s, uint8_t *flags, int32_t *lab, unsigned
             const int64_t b0 = base + 32 * j;
             const int64_t v = b0 + lane_id();
             bool seed = false;
+            unsigned bits = 0;  // bit 1: D > 0, bits 2+d: L_d > 0
             if (v < g.n) {
 #if CG_LAYOUT_AOS && CG_INIT_PRELOAD
                 const int4 a = ra[j], b = rb[j];
@@ -88,12 +92,26 @@ __global__ void k_bfs2_init(Geo g, Soa s, uint8_t *flags, int32_t *lab, unsigned
                 const int T = s.T[v], D = s.D[v], L0 = s.L[0][v], L1 = s.L[1][v], L2 = s.L[2][v], L3 = s.L[3][v];
 #endif
                 seed = T > 0;
-                flags[v] = (uint8_t)(seed | (D > 0) << 1 | (L0 > 0) << 2 | (L1 > 0) << 3 | (L2 > 0) << 4 |
-                                     (L3 > 0) << 5);
+                bits = (D > 0) << 1 | (L0 > 0) << 2 | (L1 > 0) << 3 | (L2 > 0) << 4 | (L3 > 0) << 5;
+                flags[v] = (uint8_t)(seed | bits);
                 lab[v] = seed ? 1 : g.INF;
             }
             const unsigned m = __ballot_sync(FULL, seed);
             if (lane_id() == 0 && b0 < g.n) visited[b0 >> 5] = m;
+            if (dbits) {
+                const unsigned md = __ballot_sync(FULL, bits & 2u), m0 = __ballot_sync(FULL, bits & 4u),
+                               m1 = __ballot_sync(FULL, bits & 8u), m2 = __ballot_sync(FULL, bits & 16u),
+                               m3 = __ballot_sync(FULL, bits & 32u);
+                if (lane_id() == 0 && b0 < g.n) {
+                    const int64_t w = b0 >> 5;
+                    dbits[w] = md;
+                    dbits[NW + w] = m0;
+                    dbits[2 * NW + w] = m1;
+                    dbits[3 * NW + w] = m2;
+                    dbits[4 * NW + w] = m3;
+                    dbits[5 * NW + w] = m;
+                }
+            }
             ap.add(m, b0);
         }
         ap.flush(lout, cout);

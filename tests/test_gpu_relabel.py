@@ -72,7 +72,7 @@ def solve_state(cg, c, delta, nslabs=1, weight=False):
         cg.colgraph_free(h)
 
 
-@pytest.fixture(params=["default", "flags", "colgr", "bfs", "trunc", "bottomup"])
+@pytest.fixture(params=["default", "flags", "colgr", "bfs", "trunc", "bottomup", "dense_all", "dense_off"])
 def flavour(request, monkeypatch):
     # the labels are exact after an exhaustive relabel: end every solve on one (no source-side check)
     monkeypatch.setenv("CG_SRC_TERM", "0")
@@ -81,6 +81,9 @@ def flavour(request, monkeypatch):
     elif request.param == "trunc":  # truncated relabels mid-solve; the last one is exhaustive
         monkeypatch.delenv("CG_RELABEL", raising=False)
         monkeypatch.setenv("CG_BFS_TRUNC", "64,2")
+    elif request.param in ("dense_all", "dense_off"):  # dense bit-plane levels for every level / never
+        monkeypatch.delenv("CG_RELABEL", raising=False)
+        monkeypatch.setenv("CG_BFS_DENSE", "1" if request.param == "dense_all" else "0")
     elif request.param == "bottomup":  # flag-plane BFS with bottom-up levels whenever allowed
         monkeypatch.delenv("CG_RELABEL", raising=False)
         monkeypatch.setenv("CG_BFS_BU", "1000000,1")
@@ -156,3 +159,20 @@ def test_colgr_counts_rounds(cg, monkeypatch):
     c = V.generate("C2")
     _, stats = solve_state(cg, c, 3)
     assert stats["gr_passes"] >= stats["global_relabels"] > 0
+
+
+@pytest.mark.parametrize("dense", ["1", "5", "40", "0"])
+def test_labels_exact_dense_levels(cg, monkeypatch, dense):
+    """Dense bit-plane BFS levels (kernels.cuh bfs_dense_level; one slab, Z % 32 == 0): columns of one
+    to four 32-z words, intervals 0..31 on either axis (and 32, which the host routes to the list
+    levels), thresholds from "every level" to "never"; the labels equal the scipy distances."""
+    monkeypatch.delenv("CG_RELABEL", raising=False)
+    monkeypatch.setenv("CG_SRC_TERM", "0")
+    monkeypatch.setenv("CG_BFS_DENSE", dense)
+    rng = np.random.default_rng(31)
+    for k in range(40):
+        X, Y, Z = int(rng.integers(1, 7)), int(rng.integers(1, 7)), 32 * int(rng.integers(1, 5))
+        cmax = int(rng.choice([3, 9, 255]))
+        c = rng.integers(0, cmax + 1, size=(X, Y, Z)).astype(np.int32)
+        dl = (int(rng.choice([0, 1, 2, 4, 7, 31, 32])), int(rng.choice([0, 1, 3, 16, 31])))
+        check(cg, c, dl if k % 2 else dl[0], ctx=f"d{k} {X}x{Y}x{Z} {dl}")
