@@ -1308,6 +1308,9 @@ __device__ __forceinline__ unsigned shr_w(unsigned a, unsigned ap1, int s) { ret
 #ifndef CG_DENSE_R
 #define CG_DENSE_R 1
 #endif
+#ifndef CG_DENSE_ROWS_ALL  // words with new vertices from which the label rows are written unrolled
+#define CG_DENSE_ROWS_ALL 12
+#endif
 __device__ void bfs_dense_level(const Geo &g, const unsigned *__restrict__ Dm, const unsigned *__restrict__ Lm,
                                 int64_t NW, const unsigned *F, unsigned *Fn, unsigned *visited, int32_t *lab, int nl,
                                 unsigned *cout) {
@@ -1382,12 +1385,22 @@ __device__ void bfs_dense_level(const Geo &g, const unsigned *__restrict__ Dm, c
             }
             tot += __popc(N);
             unsigned m = __ballot_sync(FULL, N != 0);
-            const int64_t wb = base + r * 32;
-            while (m) {  // labels of the new vertices, one coalesced row per word
-                const int j = __ffs(m) - 1;
-                m &= m - 1;
-                const unsigned Nj = __shfl_sync(FULL, N, j);
-                if ((Nj >> lane_id()) & 1u) lab[(wb + j) * 32 + lane_id()] = nl;
+            // labels of the new vertices, one coalesced row per word; streaming stores (evict-first in
+            // L2: the label plane is 4 B/vertex and must not push the bit planes out of L2)
+            int32_t *row = lab + (base + r * 32) * 32 + lane_id();
+            if (__popc(m) >= CG_DENSE_ROWS_ALL) {
+#pragma unroll
+                for (int j = 0; j < 32; j++) {
+                    const unsigned Nj = __shfl_sync(FULL, N, j);
+                    if ((Nj >> lane_id()) & 1u) __stcs(row + j * 32, nl);
+                }
+            } else {
+                while (m) {
+                    const int j = __ffs(m) - 1;
+                    m &= m - 1;
+                    const unsigned Nj = __shfl_sync(FULL, N, j);
+                    if ((Nj >> lane_id()) & 1u) __stcs(row + j * 32, nl);
+                }
             }
         }
     }
