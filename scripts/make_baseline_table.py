@@ -42,7 +42,7 @@ oracle (single-threaded Dinitz) runs at {bench['cpu_baseline']['value']:.3f} Mno
 Roofline (SURVEY.md §8(d) algorithmic bytes: 32 B per vertex visit + 12 B per push + 4 B per
 relabel for the sweeps, 28 B per vertex per global relabel):
 - sweeps (`k_walk_ws` / `k_sweep_v`, {100 * rf['share_of_step']:.0f} % of the step): {rf['achieved']:.0f} GB/s =
-  **{100 * rf['frac']:.1f} % of the measured 6,457 GB/s copy peak**; ncu (`profiles/{T}_ncu_k_walk_ws.json`,
+  **{100 * rf['frac']:.1f} % of the measured {rf['peak']:,.0f} GB/s copy peak**; ncu (`profiles/{T}_ncu_k_walk_ws.json`,
   early launches): {float(wk[0]['gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed [%]']):.0f} % of DRAM peak, L2 hit
   {float(wk[0]['lts__t_sector_hit_rate.pct [%]']):.0f} %, {float(wk[0]['smsp__thread_inst_executed_per_inst_executed.ratio']):.1f} active threads per warp instruction; over every sweep
   launch of a solve DRAM traffic is {tr['traffic_over_alg']:.1f}x the algorithmic bytes (`profiles/traffic.json`);
