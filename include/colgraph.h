@@ -43,9 +43,12 @@
  *                         across boundaries; bfs: BFS over the records (also soft graphs, tiles);
  *                         colgr: column fixpoint from INF; levels (x-slabs): level-synchronous BFS
  *   CG_COLGR_SMALL=k      column fixpoint: worklists <= k columns run in block 0 alone
- *   CG_BFS_TRUNC=s,k      flag-plane BFS relabels not forced to be exhaustive stop after k
- *                         consecutive frontiers of <= s vertices; unreached vertices stay at INF
- *                         until the next exhaustive relabel (the one that decides termination)
+ *   CG_BFS_TRUNC=s,k[,0]  truncated relabels (default 65536,32; 0,0 = off): a flag-plane BFS relabel that
+ *                         is not forced to be exhaustive stops after k consecutive frontiers of <= s
+ *                         vertices; unreached vertices stay at INF (inactive) until the next exhaustive
+ *                         relabel.  A quiescent batch always gets an exhaustive relabel (the one that
+ *                         decides termination) and ends truncation for the rest of the solve; a third
+ *                         field 0 keeps truncating after it
  *   CG_BAR_NS=ns          back-off cap of the persistent kernels' grid barrier (default 1024)
  *   CG_BFS_BU=div,min     flag-plane BFS: bottom-up levels when the frontier >= unvisited / div
  *                         and >= min (measured alternative; off)

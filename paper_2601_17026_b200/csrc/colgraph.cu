@@ -124,6 +124,7 @@ struct cg_graph {
     bool exported = false;      // phase 2 ran (maxflow_export_flow): the preflow is now a flow
     bool top_ready = false;     // the solve ended on a source-side termination check: top[] is S
     unsigned trunc_small = 0, trunc_levels = 0;  // truncated relabels (CG_BFS_TRUNC), 0 = off
+    bool trunc_until_quiescent = true;           // truncation ends with the first quiescent batch of a solve
     cg_solve_stats st{};
 };
 
@@ -900,7 +901,10 @@ cg_status global_relabel(cg_graph *g, int64_t *active, bool exhaustive = true) {
     CG_TRY(gsum(g, &act, 1));
     *active = act;
     g->st.global_relabels++;
-    if (truncated && act == 0) return global_relabel(g, active, true);
+    if (truncated && act == 0) {
+        if (g->trunc_until_quiescent) g->trunc_levels = 0;
+        return global_relabel(g, active, true);
+    }
     return CG_OK;
 }
 
@@ -1137,12 +1141,21 @@ cg_status source_side_done(cg_graph *g, bool *done) {
 cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &ms_gr) {
     const bool trace = tracing();
     Slab *s0 = g->slabs[0];
-    g->trunc_small = g->trunc_levels = 0;
-    if (const char *e = getenv("CG_BFS_TRUNC")) {  // "small,levels"
-        unsigned a = 0, b = 0;
-        if (sscanf(e, "%u,%u", &a, &b) == 2) {
+    // truncated relabels (default 65536,32 since round 2): a relabel that is not forced to be
+    // exhaustive stops after trunc_levels consecutive frontiers of <= trunc_small vertices and leaves the
+    // deferred deep tail at INF -- parked, i.e. inactive -- so the sweeps stop moving excess that is hundreds
+    // of arcs from t while nearer excess still drains.  Truncation ends with the first quiescent batch: from
+    // then on the flow still to deliver sits in that tail and a truncated relabel would park it again
+    // (measured on C3).  CG_BFS_TRUNC="small,levels[,0]": 0,0 = off; a third field 0 keeps truncating.
+    g->trunc_small = 65536;
+    g->trunc_levels = 32;
+    g->trunc_until_quiescent = true;
+    if (const char *e = getenv("CG_BFS_TRUNC")) {
+        unsigned a = 0, b = 0, c = 1;
+        if (sscanf(e, "%u,%u,%u", &a, &b, &c) >= 2) {
             g->trunc_small = a;
             g->trunc_levels = b;
+            g->trunc_until_quiescent = c != 0;
         }
     }
     cudaStream_t st0 = s0->stream;
@@ -1370,6 +1383,7 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
                 active = 0;
                 break;
             }
+            if (quiescent && g->trunc_until_quiescent) g->trunc_levels = 0;
             CG_TRY(timed_gr(quiescent));
             last_active = active;
             work_since_gr = 0.0;

@@ -72,7 +72,8 @@ def solve_state(cg, c, delta, nslabs=1, weight=False):
         cg.colgraph_free(h)
 
 
-@pytest.fixture(params=["default", "flags", "colgr", "bfs", "trunc", "bottomup", "dense_all", "dense_off"])
+@pytest.fixture(params=["default", "flags", "colgr", "bfs", "trunc", "trunc_sticky", "trunc_off", "bottomup", "dense_all",
+                        "dense_off"])
 def flavour(request, monkeypatch):
     # the labels are exact after an exhaustive relabel: end every solve on one (no source-side check)
     monkeypatch.setenv("CG_SRC_TERM", "0")
@@ -81,6 +82,12 @@ def flavour(request, monkeypatch):
     elif request.param == "trunc":  # truncated relabels mid-solve; the last one is exhaustive
         monkeypatch.delenv("CG_RELABEL", raising=False)
         monkeypatch.setenv("CG_BFS_TRUNC", "64,2")
+    elif request.param == "trunc_sticky":  # truncation also after the first quiescent batch (third field 0)
+        monkeypatch.delenv("CG_RELABEL", raising=False)
+        monkeypatch.setenv("CG_BFS_TRUNC", "64,2,0")
+    elif request.param == "trunc_off":  # every relabel exhaustive (the default truncates: 65536,32)
+        monkeypatch.delenv("CG_RELABEL", raising=False)
+        monkeypatch.setenv("CG_BFS_TRUNC", "0,0")
     elif request.param in ("dense_all", "dense_off"):  # dense bit-plane levels for every level / never
         monkeypatch.delenv("CG_RELABEL", raising=False)
         monkeypatch.setenv("CG_BFS_DENSE", "1" if request.param == "dense_all" else "0")
