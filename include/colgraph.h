@@ -49,6 +49,9 @@
  *                         relabel.  A quiescent batch always gets an exhaustive relabel (the one that
  *                         decides termination) and ends truncation for the rest of the solve; a third
  *                         field 0 keeps truncating after it
+ *   CG_ADAPT_BATCH=m      walk batches end when the cost-balance relabel trigger is due (sized from the
+ *                         previous batch's average sweep time), at least m sweeps, at most check_every
+ *                         (default 2; 0 = fixed batches of check_every sweeps; single-process jobs only)
  *   CG_BAR_NS=ns          back-off cap of the persistent kernels' grid barrier (default 1024)
  *   CG_BFS_BU=div,min     flag-plane BFS: bottom-up levels when the frontier >= unvisited / div
  *                         and >= min (measured alternative; off)

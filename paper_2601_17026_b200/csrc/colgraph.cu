@@ -1279,13 +1279,25 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
             sweep_ms_since_gr = 0.0;
         }
     }
+    double walk_sweep_ms = 0.0;  // average sweep time of the last walk batch
+    const int adapt_min = getenv("CG_ADAPT_BATCH") ? atoi(getenv("CG_ADAPT_BATCH")) : 2;
     while (!use_tiles && active > 0) {
         if (sweeps >= o.max_sweeps) { result = CG_E_NOT_CONVERGED; break; }
         // multi-hop walks while many vertices are active; single hops in the sparse tail, where a
         // sweep is ~15 us of GPU time and the host round trip after every batch would otherwise
         // idle the GPU for a comparable time: tail batches are tail_mult x longer (CG_TAIL_BATCH)
         const bool walk = o.walk_len > 0 && (double)last_active >= walk_min * (double)g->n_global;
-        const int64_t per_batch = walk ? o.check_every : std::min<int64_t>(RING, (int64_t)o.check_every * tail_mult);
+        int64_t per_batch = walk ? o.check_every : std::min<int64_t>(RING, (int64_t)o.check_every * tail_mult);
+        // a walk batch ends when the cost-balance trigger is due: with sweeps of ~1 ms and relabels of
+        // 2-3 ms (C4) a fixed batch of check_every = 8 sweeps overshoots the trigger by 3x; sized from the
+        // previous batch's average sweep time, at least adapt_min sweeps (CG_ADAPT_BATCH).
+        // One process only: the batch length sizes a collective, and this estimate is a local clock
+        if (walk && adapt_min > 0 && g->nranks == 1 && walk_sweep_ms > 0.0) {
+            const double due = gr_beta * std::max(last_gr_ms, 0.05) - sweep_ms_since_gr;
+            per_batch = std::max<int64_t>(adapt_min, std::min<int64_t>(o.check_every, (int64_t)std::ceil(due / walk_sweep_ms)));
+        }
+        if (walk && sched_i < sched.size() && sched[sched_i] > sweeps)  // replayed schedule: end the batch where it fired
+            per_batch = std::min<int64_t>(per_batch > 0 ? o.check_every : 1, sched[sched_i] - sweeps);
         const int batch = (int)std::min<int64_t>(per_batch, o.max_sweeps - sweeps);
         for (Slab *sl : g->slabs) {
             CG_CUDA(cudaMemsetAsync(sl->work, 0, sizeof(unsigned long long) * 2 * batch, sl->stream));
@@ -1337,6 +1349,7 @@ cg_status pr_loop(cg_graph *g, const cg_solve_opts &o, bool use_tiles, double &m
         cudaEventElapsedTime(&ms, g->ev0, g->ev1);
         g->st.ms_sweep_kernels += ms;
         sweep_ms_since_gr += ms;
+        if (walk) walk_sweep_ms = ms / batch;
         wv[batch] = overflow;
         // the time-based relabel trigger is a local measurement: ranks agree on it through the
         // same allreduce as the sweep counters (one collective per batch)

@@ -90,7 +90,8 @@ def test_tiles_rejects_tall_columns(cg):
                                  {"CG_COLGR_SMALL": "100000"}, {"CG_GR_SCHEDULE": "1,2,3,5,8,13,21,34"},
                                  {"CG_GR_BETA": "1000"}, {"CG_OPS": "4"},
                                  {"CG_BFS_TRUNC": "64,2"}, {"CG_BFS_TRUNC": "100000000,1"}, {"CG_BFS_TRUNC": "0,0"},
-                                 {"CG_BFS_TRUNC": "64,2,0"}, {"CG_BFS_TRUNC": "16,1"},
+                                 {"CG_BFS_TRUNC": "64,2,0"}, {"CG_BFS_TRUNC": "16,1"}, {"CG_ADAPT_BATCH": "0"},
+                                 {"CG_ADAPT_BATCH": "1"}, {"CG_ADAPT_BATCH": "5"},
                                  {"CG_BFS_BU": "1000000,1"}, {"CG_BFS_BU": "2,64"}, {"CG_PRECANCEL": "1"},
                                  {"CG_BFS_DENSE": "1"}, {"CG_BFS_DENSE": "0"}])
 def test_schedule_variants(cg, env, var):
